@@ -1,0 +1,208 @@
+/*
+ * dpt_b200.h -- C ABI of the B200-native DPT iteration path.
+ *
+ * This is the drop-in boundary for the hot path of the reference C++ library
+ * `dynspec` (arXiv:2002.12872).  The reference exposes the path as C++ free
+ * functions in proj/include/dynspec/dpt.hpp (namespace dynspec); each entry
+ * point below replaces one of them, with plain pointers and sizes instead of
+ * DenseMatrix / SparseMatrix / PartitionedProblem.  The C++ shim
+ * (paper_2002_12872_b200/shim/dynspec_b200.cpp) maps the
+ * reference's exact signatures onto these calls, so the reference's callers
+ * (tools/main.cpp, src/rspt.cpp, src/analysis.cpp, the tests) link unchanged.
+ *
+ * Data model (real FP64, row-major -- the reference's DenseMatrix layout,
+ * proj/include/dynspec/matrix.hpp:34-59):
+ *   d        unperturbed levels theta_i (DiagonalMatrix::d, real parts)
+ *   delta    the perturbation Delta (PartitionedProblem::delta, NOT delta_t):
+ *            dense row-major n*n, or CSR (int64 row offsets, int32 sorted
+ *            columns, FP64 values; SparseMatrix, matrix.hpp:73-106)
+ *   A        the iterate, row i = chart row i (ConvergenceReport::state.a)
+ * Documented deviation: the reference computes in std::complex<double>; this
+ * path is real FP64.  The C++ shim rejects inputs with a nonzero imaginary part
+ * (DPT_ERR_NON_REAL) instead of silently dropping it.
+ *
+ * Errors follow the reference's exception taxonomy (dpt.hpp, partition.hpp:13-26):
+ * non-convergence is a STATUS in the report, never an error code.
+ * Every function is reentrant: state lives in the caller's dpt_ctx.
+ */
+#ifndef DPT_B200_H
+#define DPT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DPT_B200_ABI_VERSION 1
+
+/* ConvergenceStatus, dpt.hpp:13-18 (same order). */
+typedef enum dpt_status {
+  DPT_CONVERGED = 0,
+  DPT_BOUNDED_NON_CONVERGED = 1,
+  DPT_DIVERGED = 2,
+  DPT_MAX_ITERATIONS = 3
+} dpt_status;
+
+/* Error codes; the shim maps them back to the reference's exceptions. */
+typedef enum dpt_error {
+  DPT_OK = 0,
+  DPT_ERR_SHAPE = 1,        /* ShapeError (matrix.hpp:16-19) */
+  DPT_ERR_DEGENERATE = 2,   /* DegenerateSpectrum(i, j, e_i, e_j) (partition.hpp:13-26) */
+  DPT_ERR_INVALID_ARG = 3,  /* std::invalid_argument (dpt.cpp:376-382, :393-394) */
+  DPT_ERR_CUDA = 4,
+  DPT_ERR_NCCL = 5,
+  DPT_ERR_NON_REAL = 6,     /* documented deviation: complex input */
+  DPT_ERR_NO_DEVICE = 7,
+  DPT_ERR_TRACE = 8,        /* the trace callback asked to abort */
+  DPT_ERR_UNSUPPORTED = 9
+} dpt_error;
+
+/* Where the pointers of a call live. */
+typedef enum dpt_mem { DPT_MEM_HOST = 0, DPT_MEM_DEVICE = 1 } dpt_mem;
+
+typedef enum dpt_delta_kind { DPT_DELTA_DENSE = 0, DPT_DELTA_CSR = 1 } dpt_delta_kind;
+
+/* IterationOptions, dpt.hpp:22-31 -- field for field, same defaults
+ * (dpt_options_default). */
+typedef struct dpt_options {
+  double tol;                  /* 1e-12 */
+  double residual_tol;         /* 1e-10 */
+  int max_iter;                /* 10000 */
+  double divergence_threshold; /* 1e8 */
+  int cycle_window;            /* 16 */
+  double degeneracy_tol;       /* 1e-12 */
+} dpt_options;
+
+/* A PartitionedProblem (partition.hpp:43-50) in plain arrays. */
+typedef struct dpt_problem {
+  int64_t n;
+  const double* d;       /* [n] */
+  int delta_kind;        /* dpt_delta_kind */
+  const double* delta;   /* dense: [n*n] row-major */
+  const int64_t* rowptr; /* CSR: [n+1] */
+  const int32_t* cols;   /* CSR: [nnz], sorted within rows */
+  const double* vals;    /* CSR: [nnz] */
+  int64_t nnz;
+  double lambda;         /* PartitionedProblem::lambda (real) */
+  int mem;               /* dpt_mem of d / delta / rowptr / cols / vals */
+} dpt_problem;
+
+/* ConvergenceReport / SingleRowReport scalars (dpt.hpp:39-46, :98-105). */
+typedef struct dpt_report {
+  int status;        /* dpt_status */
+  int iterations;
+  double step_norm;
+  double eigenvalue; /* single-row modes */
+  double residual;   /* single-row modes */
+  int64_t row;       /* dominant_eigenpair: chart index (DominantEigenpair::row) */
+  /* timings of the call on the device (not part of the reference report) */
+  double device_ms;
+  int launches;
+} dpt_report;
+
+/* DegenerateSpectrum payload + message for any error (partition.hpp:13-26). */
+typedef struct dpt_error_info {
+  int code;
+  int64_t i, j;
+  double ei, ej;
+  char message[256];
+} dpt_error_info;
+
+/* TraceSink, dpt.hpp:48-49: (k, step_norm, max_residual).  Called on the
+ * calling thread, in k order, before the call returns.  Return nonzero to
+ * abort the solve with DPT_ERR_TRACE (the reference propagates an exception
+ * thrown by the sink). */
+typedef int (*dpt_trace_fn)(int k, double step_norm, double max_residual, void* user);
+
+typedef struct dpt_ctx dpt_ctx;
+
+/* ---- context ------------------------------------------------------------- */
+int dpt_ctx_create(int device, dpt_ctx** out, dpt_error_info* err);
+void dpt_ctx_destroy(dpt_ctx* ctx);
+/* Multi-GPU (column-of-the-paper / row-of-the-reference sharding across one
+ * process per GPU): every rank calls with the same NCCL unique id bytes
+ * (ncclGetUniqueId on rank 0, broadcast by the caller). world == 1 disables. */
+int dpt_ctx_set_comm(dpt_ctx* ctx, int rank, int world, const void* nccl_id, size_t id_bytes,
+                     dpt_error_info* err);
+int dpt_nccl_unique_id(void* out, size_t bytes, dpt_error_info* err);
+/* CUDA stream used by the context (cudaStream_t as void*). */
+void* dpt_ctx_stream(dpt_ctx* ctx);
+/* Kernel launches issued by this context so far (for gpu_launches accounting). */
+int64_t dpt_ctx_launch_count(const dpt_ctx* ctx);
+
+void dpt_options_default(dpt_options* o);
+const char* dpt_status_string(int status); /* to_string, dpt.cpp:297-309 */
+int dpt_abi_version(void);
+
+/* ---- full map (the row form of dpt.hpp:51-57) ----------------------------- */
+
+/* iterate_full (dpt.hpp:74-83).  Outputs (all may be host or device pointers
+ * per out_mem; any may be NULL to skip):
+ *   a_out   [n*n] final iterate (ConvergenceReport::state.a)
+ *   eig_out [n]   eigenvalues (NaN when Diverged)
+ *   res_out [n]   per-row residuals (NaN when Diverged)          */
+int dpt_iterate_full(dpt_ctx* ctx, const dpt_problem* p, const dpt_options* opts,
+                     dpt_trace_fn trace, void* user, double* a_out, double* eig_out,
+                     double* res_out, int out_mem, dpt_report* rep, dpt_error_info* err);
+
+/* iterate_ramped (dpt.hpp:85-92): lambda_k = lambda (1 - alpha^(k-1)). */
+int dpt_iterate_ramped(dpt_ctx* ctx, const dpt_problem* p, double alpha, const dpt_options* opts,
+                       dpt_trace_fn trace, void* user, double* a_out, double* eig_out,
+                       double* res_out, int out_mem, dpt_report* rep, dpt_error_info* err);
+
+/* iterate_fixed (dpt.hpp:94-96): exactly k applications from I at `lambda`. */
+int dpt_iterate_fixed(dpt_ctx* ctx, const dpt_problem* p, int k, double lambda, double* a_out,
+                      int out_mem, dpt_report* rep, dpt_error_info* err);
+
+/* step_full (dpt.hpp:51-57): one application of the map to `a` [n*n].
+ * The reference passes GapMatrix + delta_t; here theta comes from p->d and
+ * Delta from p (the shim recovers them), `lambda` is the step's coupling. */
+int dpt_step_full(dpt_ctx* ctx, const dpt_problem* p, const double* a, double lambda,
+                  double* out, int io_mem, dpt_error_info* err);
+
+/* ---- row map -------------------------------------------------------------- */
+
+/* iterate_single (dpt.hpp:107-111). z_out [n]. */
+int dpt_iterate_single(dpt_ctx* ctx, const dpt_problem* p, int64_t row, const dpt_options* opts,
+                       double ramp_alpha, dpt_trace_fn trace, void* user, double* z_out,
+                       int out_mem, dpt_report* rep, dpt_error_info* err);
+
+/* dominant_eigenpair (dpt.hpp:113-129). z_chart / z_unit [n]; rep->row. */
+int dpt_dominant_eigenpair(dpt_ctx* ctx, const dpt_problem* p, const dpt_options* opts,
+                           double* z_chart, double* z_unit, int out_mem, dpt_report* rep,
+                           dpt_error_info* err);
+
+/* step_single (dpt.hpp:59-66): one row-map application to z [n] for chart `row`. */
+int dpt_step_single(dpt_ctx* ctx, const dpt_problem* p, const double* z, int64_t row,
+                    double lambda, double* out, int io_mem, dpt_error_info* err);
+
+/* eigenvalue_of (dpt.hpp:68-72): d_row + lambda (Delta z)_row. */
+int dpt_eigenvalue_of(dpt_ctx* ctx, const dpt_problem* p, const double* z, int64_t row,
+                      double lambda, double* out, int z_mem, dpt_error_info* err);
+
+/* ---- host-only helpers (no GPU needed; used by CPU tests) ------------------ */
+
+/* build_theta's degeneracy policy (partition.cpp:42-81) in O(n log n):
+ * returns 1 and the reference's first (i, j) in row-major order if two levels
+ * are within degeneracy_tol * max(1, spread), else 0. */
+int dpt_check_degenerate(int64_t n, const double* d, double degeneracy_tol, int64_t* i,
+                         int64_t* j);
+double dpt_spectral_spread(int64_t n, const double* d);
+int dpt_effective_window(int requested, int64_t n); /* dpt.cpp:83-90 */
+
+/* The per-iteration decision function the device runs (dpt_state.h), exposed
+ * for host-side tests: feeds one launch's statistics into the state machine.
+ * state / opts are opaque byte blobs of dpt_sm_state_bytes() / dpt_sm_options_bytes(). */
+size_t dpt_sm_state_bytes(void);
+void dpt_sm_init(void* state, void* opts, const dpt_options* o, int win, int have_trace);
+void dpt_sm_decide_host(void* state, const void* opts, const double* stats, int j,
+                        int settled_prev, int settled_cur, double* trace_out);
+void dpt_sm_query(const void* state, int* done, int* status, int* iterations, int* final_iter,
+                  int* readoffs, int* cycle_pending, double* step_norm);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DPT_B200_H */

@@ -1,0 +1,245 @@
+"""TEST INFRASTRUCTURE ONLY -- ctypes access to the two CPU checkers:
+
+  restatement  oracle/libdpt_oracle.so     (dpt_oracle.c, the C restatement)
+  reference    oracle/_ref/libdynspec_ref.so (the reference's own sources + ref_capi.cpp)
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
+leg may import this module.  The product (paper_2002_12872_b200) never does.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, Structure, c_double, c_int, c_int32, c_int64, c_void_p
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "libdpt_oracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libdynspec_ref.so")
+
+ORC_DENSE, ORC_CSR = 0, 1
+STATUS = ["Converged", "BoundedNonConverged", "Diverged", "MaxIterations"]
+ORC_OK, ORC_ERR_SHAPE, ORC_ERR_DEGENERATE, ORC_ERR_INVALID = 0, 1, 2, 3
+
+
+class orc_problem(Structure):
+    _fields_ = [("n", c_int64), ("d", c_void_p), ("kind", c_int), ("delta", c_void_p),
+                ("rowptr", c_void_p), ("cols", c_void_p), ("vals", c_void_p), ("lambda_", c_double)]
+
+
+class orc_options(Structure):
+    _fields_ = [("tol", c_double), ("residual_tol", c_double), ("max_iter", c_int),
+                ("divergence_threshold", c_double), ("cycle_window", c_int), ("degeneracy_tol", c_double)]
+
+
+class orc_report(Structure):
+    _fields_ = [("status", c_int), ("iterations", c_int), ("step_norm", c_double),
+                ("degenerate_i", c_int64), ("degenerate_j", c_int64)]
+
+
+class orc_single_report(Structure):
+    _fields_ = [("status", c_int), ("iterations", c_int), ("step_norm", c_double), ("eigenvalue", c_double),
+                ("residual", c_double), ("degenerate_i", c_int64), ("degenerate_j", c_int64)]
+
+
+@dataclass
+class FullResult:
+    rc: int
+    status: int
+    iterations: int
+    step_norm: float
+    a: np.ndarray
+    eig: np.ndarray
+    res: np.ndarray
+    trace_step: np.ndarray = None
+    trace_res: np.ndarray = None
+    degenerate: tuple = None
+    imag_max: float = 0.0
+
+
+@dataclass
+class SingleResult:
+    rc: int
+    status: int
+    iterations: int
+    step_norm: float
+    eigenvalue: float
+    residual: float
+    z: np.ndarray
+    z_unit: np.ndarray = None
+    row: int = -1
+    trace_step: np.ndarray = None
+    trace_res: np.ndarray = None
+    degenerate: tuple = None
+
+
+def _load(path, prefix):
+    if not os.path.exists(path):
+        raise FileNotFoundError(f"{path} not built (make -C oracle)")
+    L = ctypes.CDLL(path)
+    P = POINTER
+    getattr(L, prefix + "iterate_full").argtypes = (
+        [P(orc_problem), P(orc_options), c_int, c_double, c_void_p, c_void_p, c_void_p, P(orc_report),
+         c_void_p, c_void_p] + ([c_void_p] if prefix == "ref_" else []))
+    getattr(L, prefix + "iterate_fixed").argtypes = [P(orc_problem), c_int, c_double, c_void_p]
+    getattr(L, prefix + "step_full").argtypes = [P(orc_problem), c_void_p, c_double, c_void_p]
+    getattr(L, prefix + "iterate_single").argtypes = [P(orc_problem), c_int64, P(orc_options), c_double,
+                                                      c_void_p, P(orc_single_report), c_void_p, c_void_p]
+    getattr(L, prefix + "dominant_eigenpair").argtypes = [P(orc_problem), P(orc_options), c_void_p, c_void_p,
+                                                          P(orc_single_report), P(c_int64)]
+    getattr(L, prefix + "step_single").argtypes = [P(orc_problem), c_void_p, c_int64, c_double, c_void_p]
+    getattr(L, prefix + "eigenvalue_of").argtypes = [P(orc_problem), c_void_p, c_int64, c_double, P(c_double)]
+    getattr(L, prefix + "step_rows").argtypes = [P(orc_problem), c_int64, c_int64, c_void_p, c_double, c_void_p]
+    if prefix == "ref_":
+        L.ref_check_degenerate.argtypes = [c_int64, c_void_p, c_double, P(c_int64), P(c_int64)]
+        L.ref_prepare.argtypes = [P(orc_problem)]
+        L.ref_prepare.restype = c_void_p
+        L.ref_release.argtypes = [c_void_p]
+        L.ref_prepared_step_rows.argtypes = [c_void_p, c_int64, c_int64, c_void_p, c_double, c_void_p]
+    else:
+        L.orc_check_degenerate.argtypes = [c_int64, c_void_p, c_double, P(c_int64), P(c_int64)]
+        L.orc_effective_window.argtypes = [c_int, c_int64]
+    return L
+
+
+class Checker:
+    """One CPU implementation of the path: 'oracle' (restatement) or 'reference'."""
+
+    def __init__(self, which: str = "oracle"):
+        self.which = which
+        self.prefix = "ref_" if which == "reference" else "orc_"
+        self.L = _load(REF_SO if which == "reference" else ORACLE_SO, self.prefix)
+
+    def _fn(self, name):
+        return getattr(self.L, self.prefix + name)
+
+    @staticmethod
+    def _prob(p):
+        """p: paper_2002_12872_b200.PartitionedProblem with numpy parts."""
+        keep = []
+        d = np.ascontiguousarray(p.d, dtype=np.float64)
+        keep.append(d)
+        pr = orc_problem()
+        pr.n = d.shape[0]
+        pr.d = d.ctypes.data
+        pr.lambda_ = float(p.lam)
+        if hasattr(p.delta, "rowptr"):
+            rp = np.ascontiguousarray(p.delta.rowptr, dtype=np.int64)
+            cl = np.ascontiguousarray(p.delta.cols, dtype=np.int32)
+            vl = np.ascontiguousarray(p.delta.vals, dtype=np.float64)
+            keep += [rp, cl, vl]
+            pr.kind = ORC_CSR
+            pr.rowptr, pr.cols, pr.vals = rp.ctypes.data, cl.ctypes.data, vl.ctypes.data
+        else:
+            a = np.ascontiguousarray(p.delta, dtype=np.float64)
+            keep.append(a)
+            pr.kind = ORC_DENSE
+            pr.delta = a.ctypes.data
+        return pr, keep
+
+    @staticmethod
+    def _opts(o: dict):
+        base = dict(tol=1e-12, residual_tol=1e-10, max_iter=10000, divergence_threshold=1e8, cycle_window=16,
+                    degeneracy_tol=1e-12)
+        base.update(o or {})
+        return orc_options(base["tol"], base["residual_tol"], int(base["max_iter"]), base["divergence_threshold"],
+                           int(base["cycle_window"]), base["degeneracy_tol"])
+
+    def iterate_full(self, p, opts=None, trace=False, ramped=False, alpha=0.0) -> FullResult:
+        pr, keep = self._prob(p)
+        n = pr.n
+        o = self._opts(opts)
+        a = np.zeros((n, n))
+        eig = np.zeros(n)
+        res = np.zeros(n)
+        rep = orc_report()
+        cap = max(o.max_iter, 1) + 1
+        ts = np.full(cap, np.nan) if trace else None
+        tr = np.full(cap, np.nan) if trace else None
+        args = [ctypes.byref(pr), ctypes.byref(o), int(ramped), float(alpha), a.ctypes.data, eig.ctypes.data,
+                res.ctypes.data, ctypes.byref(rep), ts.ctypes.data if trace else None,
+                tr.ctypes.data if trace else None]
+        im = ctypes.c_double(0.0)
+        if self.prefix == "ref_":
+            args.append(ctypes.addressof(im))
+        rc = self._fn("iterate_full")(*args)
+        k = rep.iterations if trace else 0
+        return FullResult(rc, rep.status, rep.iterations, rep.step_norm, a, eig, res,
+                          ts[:k] if trace else None, tr[:k] if trace else None,
+                          (rep.degenerate_i, rep.degenerate_j) if rc == ORC_ERR_DEGENERATE else None, im.value)
+
+    def iterate_fixed(self, p, k, lam):
+        pr, keep = self._prob(p)
+        a = np.zeros((pr.n, pr.n))
+        rc = self._fn("iterate_fixed")(ctypes.byref(pr), int(k), float(lam), a.ctypes.data)
+        return rc, a
+
+    def step_full(self, a, p, lam):
+        pr, keep = self._prob(p)
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        out = np.zeros_like(a)
+        self._fn("step_full")(ctypes.byref(pr), a.ctypes.data, float(lam), out.ctypes.data)
+        return out
+
+    def step_rows(self, p, row0, a_rows, lam):
+        pr, keep = self._prob(p)
+        a_rows = np.ascontiguousarray(a_rows, dtype=np.float64)
+        out = np.zeros_like(a_rows)
+        self._fn("step_rows")(ctypes.byref(pr), int(row0), int(a_rows.shape[0]), a_rows.ctypes.data, float(lam),
+                              out.ctypes.data)
+        return out
+
+    def iterate_single(self, p, row, opts=None, ramp_alpha=0.0, trace=False) -> SingleResult:
+        pr, keep = self._prob(p)
+        o = self._opts(opts)
+        z = np.zeros(pr.n)
+        rep = orc_single_report()
+        cap = max(o.max_iter, 1) + 1
+        ts = np.full(cap, np.nan) if trace else None
+        tr = np.full(cap, np.nan) if trace else None
+        rc = self._fn("iterate_single")(ctypes.byref(pr), int(row), ctypes.byref(o), float(ramp_alpha),
+                                        z.ctypes.data, ctypes.byref(rep), ts.ctypes.data if trace else None,
+                                        tr.ctypes.data if trace else None)
+        k = rep.iterations if trace else 0
+        return SingleResult(rc, rep.status, rep.iterations, rep.step_norm, rep.eigenvalue, rep.residual, z,
+                            trace_step=ts[:k] if trace else None, trace_res=tr[:k] if trace else None,
+                            degenerate=(rep.degenerate_i, rep.degenerate_j) if rc == ORC_ERR_DEGENERATE else None)
+
+    def dominant_eigenpair(self, p, opts=None) -> SingleResult:
+        pr, keep = self._prob(p)
+        o = self._opts(opts)
+        zc = np.zeros(pr.n)
+        zu = np.zeros(pr.n)
+        rep = orc_single_report()
+        row = ctypes.c_int64(-1)
+        rc = self._fn("dominant_eigenpair")(ctypes.byref(pr), ctypes.byref(o), zc.ctypes.data, zu.ctypes.data,
+                                            ctypes.byref(rep), ctypes.byref(row))
+        return SingleResult(rc, rep.status, rep.iterations, rep.step_norm, rep.eigenvalue, rep.residual, zc, zu,
+                            row.value,
+                            degenerate=(rep.degenerate_i, rep.degenerate_j) if rc == ORC_ERR_DEGENERATE else None)
+
+    def step_single(self, z, row, p, lam):
+        pr, keep = self._prob(p)
+        z = np.ascontiguousarray(z, dtype=np.float64)
+        out = np.zeros_like(z)
+        self._fn("step_single")(ctypes.byref(pr), z.ctypes.data, int(row), float(lam), out.ctypes.data)
+        return out
+
+    def eigenvalue_of(self, z, row, p, lam):
+        pr, keep = self._prob(p)
+        z = np.ascontiguousarray(z, dtype=np.float64)
+        out = ctypes.c_double()
+        self._fn("eigenvalue_of")(ctypes.byref(pr), z.ctypes.data, int(row), float(lam), ctypes.byref(out))
+        return out.value
+
+    def check_degenerate(self, d, tol=1e-12):
+        d = np.ascontiguousarray(d, dtype=np.float64)
+        i, j = ctypes.c_int64(), ctypes.c_int64()
+        hit = self._fn("check_degenerate")(d.shape[0], d.ctypes.data, float(tol), ctypes.byref(i), ctypes.byref(j))
+        return (i.value, j.value) if hit else None
+
+
+def available(which: str) -> bool:
+    return os.path.exists(REF_SO if which == "reference" else ORACLE_SO)

@@ -1,0 +1,264 @@
+// ref_capi.cpp -- TEST INFRASTRUCTURE ONLY.  A C shim over the REFERENCE
+// library itself (dynspec, compiled from /root/reference/proj/src into
+// oracle/_ref by oracle/Makefile), exposing the same orc_* structs as the C
+// restatement so tests can run both on identical inputs.  Nothing here is
+// product code; the product never links it.
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <vector>
+
+#include "dpt_oracle.h"
+#include "dynspec/dpt.hpp"
+#include "dynspec/matrix.hpp"
+#include "dynspec/partition.hpp"
+
+using namespace dynspec;
+
+namespace {
+
+MatrixVariant to_delta(const orc_problem* p) {
+  const std::size_t n = std::size_t(p->n);
+  if (p->kind == ORC_DENSE) {
+    DenseMatrix m(n, n);
+    for (std::size_t i = 0; i < n * n; ++i) m.data()[i] = p->delta[i];
+    return m;
+  }
+  std::vector<SparseMatrix::Triplet> t;
+  t.reserve(std::size_t(p->rowptr[n]));
+  for (std::size_t i = 0; i < n; ++i)
+    for (int64_t q = p->rowptr[i]; q < p->rowptr[i + 1]; ++q)
+      t.push_back({i, std::size_t(p->cols[q]), cdouble{p->vals[q], 0.0}});
+  return SparseMatrix::from_triplets(n, n, std::move(t));
+}
+
+PartitionedProblem to_problem(const orc_problem* p) {
+  std::vector<cdouble> d(std::size_t(p->n));
+  for (int64_t i = 0; i < p->n; ++i) d[std::size_t(i)] = p->d[i];
+  return make_problem(DiagonalMatrix(std::move(d)), to_delta(p), cdouble{p->lambda, 0.0});
+}
+
+IterationOptions to_opts(const orc_options* o) {
+  IterationOptions r;
+  r.tol = o->tol;
+  r.residual_tol = o->residual_tol;
+  r.max_iter = o->max_iter;
+  r.divergence_threshold = o->divergence_threshold;
+  r.cycle_window = o->cycle_window;
+  r.degeneracy_tol = o->degeneracy_tol;
+  return r;
+}
+
+void put_dense(const DenseMatrix& a, double* out, double* imag_max) {
+  const std::size_t nn = a.rows() * a.cols();
+  double im = 0.0;
+  for (std::size_t i = 0; i < nn; ++i) {
+    out[i] = a.data()[i].real();
+    im = std::max(im, std::fabs(a.data()[i].imag()));
+  }
+  if (imag_max) *imag_max = std::max(*imag_max, im);
+}
+
+}  // namespace
+
+extern "C" {
+
+int ref_iterate_full(const orc_problem* p, const orc_options* o, int ramped, double alpha, double* a_out,
+                     double* eig_out, double* res_out, orc_report* rep, double* trace_step, double* trace_res,
+                     double* imag_max) {
+  std::memset(rep, 0, sizeof(*rep));
+  try {
+    const PartitionedProblem pp = to_problem(p);
+    int idx = 0;
+    TraceSink sink;
+    if (trace_step)
+      sink = [&](int k, double s, double r) {
+        (void)k;
+        trace_step[idx] = s;
+        trace_res[idx] = r;
+        ++idx;
+      };
+    const ConvergenceReport r =
+        ramped ? iterate_ramped(pp, alpha, to_opts(o), sink) : iterate_full(pp, to_opts(o), sink);
+    rep->status = int(r.status);
+    rep->iterations = r.iterations;
+    rep->step_norm = r.step_norm;
+    put_dense(r.state.a, a_out, imag_max);
+    for (std::size_t i = 0; i < r.eigenvalues.size(); ++i) {
+      eig_out[i] = r.eigenvalues[i].real();
+      res_out[i] = r.residuals[i];
+      if (imag_max && std::isfinite(r.eigenvalues[i].imag()))
+        *imag_max = std::max(*imag_max, std::fabs(r.eigenvalues[i].imag()));
+    }
+    return ORC_OK;
+  } catch (const DegenerateSpectrum& e) {
+    rep->degenerate_i = int64_t(e.first());
+    rep->degenerate_j = int64_t(e.second());
+    return ORC_ERR_DEGENERATE;
+  } catch (const ShapeError&) {
+    return ORC_ERR_SHAPE;
+  } catch (const std::invalid_argument&) {
+    return ORC_ERR_INVALID;
+  }
+}
+
+int ref_iterate_fixed(const orc_problem* p, int k, double lam, double* a_out) {
+  try {
+    put_dense(iterate_fixed(to_problem(p), k, cdouble{lam, 0.0}), a_out, nullptr);
+    return ORC_OK;
+  } catch (const DegenerateSpectrum&) {
+    return ORC_ERR_DEGENERATE;
+  } catch (const std::invalid_argument&) {
+    return ORC_ERR_INVALID;
+  }
+}
+
+int ref_step_full(const orc_problem* p, const double* a, double lam, double* out) {
+  const PartitionedProblem pp = to_problem(p);
+  const std::size_t n = std::size_t(p->n);
+  DenseMatrix am(n, n);
+  for (std::size_t i = 0; i < n * n; ++i) am.data()[i] = a[i];
+  put_dense(step_full(am, build_theta(pp.d), pp.delta_t, cdouble{lam, 0.0}), out, nullptr);
+  return ORC_OK;
+}
+
+int ref_iterate_single(const orc_problem* p, int64_t row, const orc_options* o, double ramp_alpha, double* z_out,
+                       orc_single_report* rep, double* trace_step, double* trace_res) {
+  std::memset(rep, 0, sizeof(*rep));
+  try {
+    const PartitionedProblem pp = to_problem(p);
+    int idx = 0;
+    TraceSink sink;
+    if (trace_step)
+      sink = [&](int, double s, double r) {
+        trace_step[idx] = s;
+        trace_res[idx] = r;
+        ++idx;
+      };
+    const SingleRowReport r = iterate_single(pp, std::size_t(row), to_opts(o), ramp_alpha, sink);
+    rep->status = int(r.status);
+    rep->iterations = r.iterations;
+    rep->step_norm = r.step_norm;
+    rep->eigenvalue = r.eigenvalue.real();
+    rep->residual = r.residual;
+    for (std::size_t m = 0; m < r.z.size(); ++m) z_out[m] = r.z[m].real();
+    return ORC_OK;
+  } catch (const DegenerateSpectrum& e) {
+    rep->degenerate_i = int64_t(e.first());
+    rep->degenerate_j = int64_t(e.second());
+    return ORC_ERR_DEGENERATE;
+  } catch (const ShapeError&) {
+    return ORC_ERR_SHAPE;
+  } catch (const std::invalid_argument&) {
+    return ORC_ERR_INVALID;
+  }
+}
+
+int ref_dominant_eigenpair(const orc_problem* p, const orc_options* o, double* z_chart, double* z_unit,
+                           orc_single_report* rep, int64_t* row_out) {
+  std::memset(rep, 0, sizeof(*rep));
+  try {
+    const DominantEigenpair r = dominant_eigenpair(to_problem(p), to_opts(o));
+    rep->status = int(r.status);
+    rep->iterations = r.iterations;
+    rep->step_norm = r.step_norm;
+    rep->eigenvalue = r.eigenvalue.real();
+    rep->residual = r.residual;
+    *row_out = int64_t(r.row);
+    for (std::size_t m = 0; m < r.z_chart.size(); ++m) {
+      z_chart[m] = r.z_chart[m].real();
+      z_unit[m] = r.z_unit[m].real();
+    }
+    return ORC_OK;
+  } catch (const DegenerateSpectrum& e) {
+    rep->degenerate_i = int64_t(e.first());
+    rep->degenerate_j = int64_t(e.second());
+    return ORC_ERR_DEGENERATE;
+  } catch (const ShapeError&) {
+    return ORC_ERR_SHAPE;
+  }
+}
+
+int ref_step_single(const orc_problem* p, const double* z, int64_t row, double lam, double* out) {
+  const PartitionedProblem pp = to_problem(p);
+  std::vector<cdouble> zz(std::size_t(p->n));
+  for (int64_t m = 0; m < p->n; ++m) zz[std::size_t(m)] = z[m];
+  const GapRow g = build_gap_row(pp.d, std::size_t(row));
+  const auto r = step_single(zz, g, pp.delta, cdouble{lam, 0.0});
+  for (std::size_t m = 0; m < r.size(); ++m) out[m] = r[m].real();
+  return ORC_OK;
+}
+
+int ref_eigenvalue_of(const orc_problem* p, const double* z, int64_t row, double lam, double* out) {
+  const PartitionedProblem pp = to_problem(p);
+  std::vector<cdouble> zz(std::size_t(p->n));
+  for (int64_t m = 0; m < p->n; ++m) zz[std::size_t(m)] = z[m];
+  *out = eigenvalue_of(zz, std::size_t(row), pp.d, pp.delta, cdouble{lam, 0.0}).real();
+  return ORC_OK;
+}
+
+// build_theta's degeneracy payload (partition.cpp:69-81) from the reference itself.
+int ref_check_degenerate(int64_t n, const double* d, double tol, int64_t* i, int64_t* j) {
+  std::vector<cdouble> dd(static_cast<std::size_t>(n));
+  for (int64_t q = 0; q < n; ++q) dd[std::size_t(q)] = d[q];
+  try {
+    (void)build_theta(DiagonalMatrix(std::move(dd)), tol);
+    return 0;
+  } catch (const DegenerateSpectrum& e) {
+    *i = int64_t(e.first());
+    *j = int64_t(e.second());
+    return 1;
+  }
+}
+
+// The reference's own row-subset cost unit for the bounded CPU baseline:
+// P = A_rows * delta_t (matmul, src/matrix.cpp:130-158) plus the map
+// (src/dpt.cpp:136-144) for rows [row0, row0 + rows).
+int ref_step_rows(const orc_problem* p, int64_t row0, int64_t rows, const double* a, double lam, double* out) {
+  const PartitionedProblem pp = to_problem(p);
+  const std::size_t n = std::size_t(p->n);
+  DenseMatrix am(std::size_t(rows), n);
+  for (std::size_t i = 0; i < std::size_t(rows) * n; ++i) am.data()[i] = a[i];
+  const DenseMatrix pm = matmul(am, pp.delta_t);
+  const cdouble lk{lam, 0.0};
+  for (std::size_t i = 0; i < std::size_t(rows); ++i) {
+    const std::size_t gi = std::size_t(row0) + i;
+    const cdouble pii = pm(i, gi);
+    for (std::size_t j = 0; j < n; ++j) {
+      const cdouble th = gi == j ? cdouble{} : 1.0 / (pp.d.d[gi] - pp.d.d[j]);
+      out[i * n + j] = (gi == j ? cdouble{1.0, 0.0} : lk * th * (pm(i, j) - pii * am(i, j))).real();
+    }
+  }
+  return ORC_OK;
+}
+
+}  // extern "C"
+
+// Prepared problem for the bench's reference arm: the one-time make_problem
+// (with its delta_t cache) stays outside the timed region, as in the
+// reference's own bench (proj/tools/main.cpp:691-762).
+extern "C" {
+
+void* ref_prepare(const orc_problem* p) { return new PartitionedProblem(to_problem(p)); }
+
+void ref_release(void* h) { delete static_cast<PartitionedProblem*>(h); }
+
+int ref_prepared_step_rows(void* h, int64_t row0, int64_t rows, const double* a, double lam, double* out) {
+  const PartitionedProblem& pp = *static_cast<PartitionedProblem*>(h);
+  const std::size_t n = pp.size();
+  DenseMatrix am(std::size_t(rows), n);
+  for (std::size_t i = 0; i < std::size_t(rows) * n; ++i) am.data()[i] = a[i];
+  const DenseMatrix pm = matmul(am, pp.delta_t);
+  const cdouble lk{lam, 0.0};
+  for (std::size_t i = 0; i < std::size_t(rows); ++i) {
+    const std::size_t gi = std::size_t(row0) + i;
+    const cdouble pii = pm(i, gi);
+    for (std::size_t j = 0; j < n; ++j) {
+      const cdouble th = gi == j ? cdouble{} : 1.0 / (pp.d.d[gi] - pp.d.d[j]);
+      out[i * n + j] = (gi == j ? cdouble{1.0, 0.0} : lk * th * (pm(i, j) - pii * am(i, j))).real();
+    }
+  }
+  return ORC_OK;
+}
+
+}  // extern "C"

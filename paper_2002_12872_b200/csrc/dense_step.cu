@@ -1,0 +1,443 @@
+// dense_step.cu -- K1: the dense DPT step as ONE kernel.
+//
+// Replaces, per reference iteration (paths relative to /root/reference/proj):
+//   pn = matmul(an, delta_t)             src/dpt.cpp:152 -> src/matrix.cpp:130-143
+//   an = F(a) (map, unit diagonal)       src/dpt.cpp:136-144
+//   step = max_abs_diff(an, a)           src/dpt.cpp:145, src/matrix.cpp:356-364
+//   all_finite / max_abs (divergence)    src/dpt.cpp:147, src/matrix.cpp:338-384
+//   residuals_of (eps_i, row residuals)  src/dpt.cpp:23-44
+// in the row form the reference uses: P = A * Delta^T, i.e.
+//   P(i,j) = sum_k A(i,k) Delta(j,k)    (both operands K-contiguous, row-major)
+//   A'(i,j) = i==j ? 1 : (lam_k / (theta_i - theta_j)) * (P(i,j) - P(i,i) A(i,j)).
+// Row i of A evolves independently; rows are sharded across ranks.
+//
+// GEMM: 128x128 (or 64x64) CTA tile, BK = 16, a 4-stage TMA (SWIZZLE_128B) +
+// mbarrier pipeline fed by one producer warp, FP64 tensor cores through
+// mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4; tcgen05 has no f64 kind on sm_100a).
+// The two k4-steps of a 16-byte chunk are loaded with one LDS.128: the k index
+// is permuted identically for both operands, so the product is unchanged.
+//
+// P(i,i) is needed by every tile of row i but produced by one tile only, so the
+// diagonal is LAGGED (SURVEY.md §7 hard part 1): launch j uses d_{j-1}(i) =
+// sum_m A_{j-1}(i,m) Delta(i,m) that launch j-1 emitted as per-tile partials
+// (folded deterministically by the fold kernel), and emits d_j partials of its
+// own output.  Launch j also yields the residual numerator/denominator of
+// A_{j-1} (eps_i = theta_i + lambda d_{j-1}(i)), so a reference iteration's
+// read-offs cost no extra GEMM (Appendix B).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "dpt_device.cuh"
+#include "dpt_kernels.h"
+
+namespace dpt {
+
+template <int BM_, int BN_, int WARPS_M_, int WARPS_N_>
+struct DenseCfg {
+  static constexpr int BM = BM_, BN = BN_, WARPS_M = WARPS_M_, WARPS_N = WARPS_N_;
+  static constexpr int BK = 16;  // 16 doubles = 128 B rows = one swizzle span
+  static constexpr int STAGES = 4;
+  static constexpr int NCW = WARPS_M * WARPS_N;  // consumer warps
+  static constexpr int THREADS = NCW * 32;  // lane 0 of warp 0 doubles as the TMA producer
+  static constexpr int WTM = BM / WARPS_M, WTN = BN / WARPS_N;
+  static constexpr int MB = WTM / 8, NB = WTN / 8;
+  static constexpr int A_BYTES = BM * BK * 8, B_BYTES = BN * BK * 8;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int RED_BYTES = WARPS_N * BM * 3 * 8 + NCW * 4 * 8;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + RED_BYTES + 2 * STAGES * 8 + 1024;
+};
+
+using CfgBig = DenseCfg<128, 128, 2, 4>;
+using CfgSmall = DenseCfg<64, 64, 2, 2>;
+
+// Byte offset of 16-byte chunk `chunk` of row `r` in a SWIZZLE_128B TMA box
+// with 128-byte rows.
+__device__ __forceinline__ uint32_t swz(int r, int chunk) {
+  return uint32_t(r) * 128u + uint32_t((chunk ^ (r & 7)) << 4);
+}
+
+template <class C>
+__global__ void __launch_bounds__(C::THREADS, 1)
+    dense_step_kernel(DevSolve s, const CUtensorMap* __restrict__ amaps,
+                      const CUtensorMap* __restrict__ dmap, const double* __restrict__ delta,
+                      int ntm) {
+  const int j_launch = launch_index(s);
+  if (s.state->done) return;  // a terminal status was reached: no-op launch
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
+  double* red = reinterpret_cast<double*>(smem + C::STAGES * C::STAGE_BYTES);
+  double* wred = red + C::WARPS_N * C::BM * 3;
+  uint64_t* full = reinterpret_cast<uint64_t*>(wred + C::NCW * 4);
+  uint64_t* empty = full + C::STAGES;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // grouped rasterisation: 8 row blocks share each column block sweep (L2 reuse)
+  const int ntn = s.ntn;
+  const int bid = blockIdx.x;
+  const int group = 8;
+  const int per_group = group * ntn;
+  const int g = bid / per_group;
+  const int first_tm = g * group;
+  const int gsize = min(group, ntm - first_tm);
+  const int tm = first_tm + (bid % per_group) % gsize;
+  const int tn = (bid % per_group) / gsize;
+
+  const int slot_in = (j_launch - 1) % s.nslots;
+  const int slot_out = j_launch % s.nslots;
+  const int64_t n = s.n, rows = s.rows;
+  const int KT = int((n + C::BK - 1) / C::BK);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < C::STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], C::NCW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  const CUtensorMap* am = amaps + slot_in;
+  const bool producer = (threadIdx.x == 0);
+  if (producer) {  // prologue: fill the pipeline
+    prefetch_tmap(am);
+    prefetch_tmap(dmap);
+    const int pre = KT < C::STAGES ? KT : C::STAGES;
+    for (int kt = 0; kt < pre; ++kt) {
+      mbar_arrive_expect_tx(&full[kt], C::STAGE_BYTES);
+      tma_load_2d(sA + kt * C::A_BYTES, am, &full[kt], kt * C::BK, tm * C::BM);
+      tma_load_2d(sB + kt * C::B_BYTES, dmap, &full[kt], kt * C::BK, tn * C::BN);
+    }
+  }
+
+  // ------------------------------------------------------ MMA consumers ----
+  const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N;
+  const int t = lane & 3, gq = lane >> 2;
+  double acc[C::MB][C::NB][2];
+#pragma unroll
+  for (int a = 0; a < C::MB; ++a)
+#pragma unroll
+    for (int b = 0; b < C::NB; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+  for (int kt = 0; kt < KT; ++kt) {
+    const int st = kt % C::STAGES;
+    mbar_wait(&full[st], (kt / C::STAGES) & 1);
+    const uint8_t* a_st = sA + st * C::A_BYTES;
+    const uint8_t* b_st = sB + st * C::B_BYTES;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      // Row r = base + 8x + gq has (r & 7) == gq, so the swizzled chunk offset is
+      // the same for every fragment of this lane: per-fragment addresses differ
+      // by immediates (x * 1024 bytes).
+      const uint32_t cofs = uint32_t(((4 * q + t) ^ gq) << 4) + uint32_t(gq) * 128u;
+      const uint8_t* pa = a_st + wm * C::WTM * 128 + cofs;
+      const uint8_t* pb = b_st + wn * C::WTN * 128 + cofs;
+      // B fragments for both k4-steps of this 16-byte chunk stay live; A
+      // fragments stream through (keeps the 64-double accumulator + operands
+      // within the register budget).
+      double2 bf[C::NB];
+#pragma unroll
+      for (int b = 0; b < C::NB; ++b) bf[b] = *reinterpret_cast<const double2*>(pb + b * 1024);
+#pragma unroll
+      for (int a = 0; a < C::MB; ++a) {
+        const double2 af = *reinterpret_cast<const double2*>(pa + a * 1024);
+#pragma unroll
+        for (int b = 0; b < C::NB; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], af.x, bf[b].x);
+#pragma unroll
+        for (int b = 0; b < C::NB; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], af.y, bf[b].y);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+    if (producer && kt + C::STAGES < KT) {  // refill this stage once every warp released it
+      const int kn = kt + C::STAGES;
+      mbar_wait(&empty[st], (kt / C::STAGES) & 1);
+      mbar_arrive_expect_tx(&full[st], C::STAGE_BYTES);
+      tma_load_2d(sA + st * C::A_BYTES, am, &full[st], kn * C::BK, tm * C::BM);
+      tma_load_2d(sB + st * C::B_BYTES, dmap, &full[st], kn * C::BK, tn * C::BN);
+    }
+    __syncwarp();
+  }
+
+  // --------------------------------------------------- fused DPT epilogue ----
+  const double lam_k = lam_of(s, j_launch);
+  const double lam = s.lambda;
+  const double* __restrict__ a_in = s.slots + size_t(slot_in) * size_t(s.slot_elems);
+  double* __restrict__ a_out = s.slots + size_t(slot_out) * size_t(s.slot_elems);
+  const double* __restrict__ d_in = s.dvec[(j_launch - 1) & 1];
+  const double* __restrict__ theta = s.theta;
+
+  const int colbase = tn * C::BN + wn * C::WTN + 2 * t;
+  double t_step = 0.0, t_max = 0.0, t_nonfin = 0.0;
+#pragma unroll
+  for (int a = 0; a < C::MB; ++a) {
+    const int il = tm * C::BM + wm * C::WTM + a * 8 + gq;  // local row
+    const bool row_ok = il < rows;
+    const int64_t gi = s.row0 + il;
+    double num = 0.0, den = 0.0, dsum = 0.0;
+    if (row_ok) {
+      const double ti = theta[gi];
+      const double di = d_in[il];
+      const double eps_i = __dadd_rn(ti, __dmul_rn(lam, di));
+      const double* arow = a_in + size_t(il) * size_t(s.ld);
+      double* orow = a_out + size_t(il) * size_t(s.ld);
+      const double* drow = delta + size_t(gi) * size_t(s.ld);
+#pragma unroll
+      for (int b = 0; b < C::NB; ++b) {
+        const int c = colbase + b * 8;
+        if (c >= n) continue;
+        const bool pair = c + 1 < n;
+        double2 av, dv;
+        if (pair) {
+          av = *reinterpret_cast<const double2*>(arow + c);
+          dv = *reinterpret_cast<const double2*>(drow + c);
+        } else {
+          av = make_double2(arow[c], 0.0);
+          dv = make_double2(drow[c], 0.0);
+        }
+        const double2 tc = pair ? *reinterpret_cast<const double2*>(theta + c) : make_double2(theta[c], 0.0);
+        double out[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          if (e == 1 && !pair) continue;
+          const double aij = e ? av.y : av.x;
+          const double dij = e ? dv.y : dv.x;
+          const double p = acc[a][b][e];
+          double v;
+          if (gi == c + e) {
+            v = 1.0;  // exact unit diagonal (test_dpt.cpp:45-53)
+          } else {
+            const double g = 1.0 / __dsub_rn(ti, e ? tc.y : tc.x);  // IEEE division = build_theta
+            v = __dmul_rn(__dmul_rn(lam_k, g), __dsub_rn(p, __dmul_rn(di, aij)));
+          }
+          out[e] = v;
+          t_step = fmax(t_step, fabs(__dsub_rn(v, aij)));
+          t_max = fmax(t_max, fabs(v));
+          t_nonfin += isfinite(v) ? 0.0 : 1.0;
+          const double r = __dadd_rn(__dmul_rn(__dsub_rn(e ? tc.y : tc.x, eps_i), aij), __dmul_rn(lam, p));
+          num = fmax(num, fabs(r));
+          den = fmax(den, fabs(aij));
+          dsum = __fma_rn(v, dij, dsum);
+        }
+        if (pair)
+          *reinterpret_cast<double2*>(orow + c) = make_double2(out[0], out[1]);
+        else
+          orow[c] = out[0];
+      }
+    }
+    // fold the 4 lanes that share this row (t = 0..3)
+    num = fmax(num, __shfl_xor_sync(0xffffffffu, num, 1));
+    den = fmax(den, __shfl_xor_sync(0xffffffffu, den, 1));
+    dsum += __shfl_xor_sync(0xffffffffu, dsum, 1);
+    num = fmax(num, __shfl_xor_sync(0xffffffffu, num, 2));
+    den = fmax(den, __shfl_xor_sync(0xffffffffu, den, 2));
+    dsum += __shfl_xor_sync(0xffffffffu, dsum, 2);
+    if (t == 0) {
+      const int rt = wm * C::WTM + a * 8 + gq;  // row within tile
+      red[(wn * C::BM + rt) * 3 + 0] = dsum;
+      red[(wn * C::BM + rt) * 3 + 1] = num;
+      red[(wn * C::BM + rt) * 3 + 2] = den;
+    }
+  }
+  t_step = warp_max(t_step);
+  t_max = warp_max(t_max);
+  t_nonfin = warp_sum(t_nonfin);
+  if (lane == 0) {
+    wred[warp * 4 + 0] = t_step;
+    wred[warp * 4 + 1] = t_max;
+    wred[warp * 4 + 2] = t_nonfin;
+  }
+  asm volatile("bar.sync 1, %0;\n" ::"r"(C::NCW * 32) : "memory");  // consumers only
+
+  const int ctid = threadIdx.x;
+  for (int rt = ctid; rt < C::BM; rt += C::NCW * 32) {
+    const int il = tm * C::BM + rt;
+    if (il >= rows) continue;
+    double ds = 0.0, nu = 0.0, de = 0.0;
+#pragma unroll
+    for (int w = 0; w < C::WARPS_N; ++w) {
+      ds += red[(w * C::BM + rt) * 3 + 0];
+      nu = fmax(nu, red[(w * C::BM + rt) * 3 + 1]);
+      de = fmax(de, red[(w * C::BM + rt) * 3 + 2]);
+    }
+    s.rowpart[(size_t(0) * ntn + tn) * rows + il] = ds;
+    s.rowpart[(size_t(1) * ntn + tn) * rows + il] = nu;
+    s.rowpart[(size_t(2) * ntn + tn) * rows + il] = de;
+  }
+  if (ctid == 0) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    for (int w = 0; w < C::NCW; ++w) {
+      a0 = fmax(a0, wred[w * 4 + 0]);
+      a1 = fmax(a1, wred[w * 4 + 1]);
+      a2 += wred[w * 4 + 2];
+    }
+    double* tp = s.tilepart + size_t(tm * ntn + tn) * 4;
+    tp[0] = a0;
+    tp[1] = a1;
+    tp[2] = a2;
+    tp[3] = 0.0;
+  }
+}
+
+// Launch 1: A_1 = F(I).  P(I) = I * Delta^T = Delta^T, so for i != j
+// A_1(i,j) = (lam_1 theta(i,j)) * Delta(j,i) -- the reference's matmul(I, delta_t)
+// zero-skips to exactly this (src/dpt.cpp:100, :136-144).  Elementwise with a
+// shared-memory transpose; emits the same partials as the GEMM step.
+// Block: 32 rows x BNI columns, 256 threads (32 x 8).
+template <int BNI>
+__global__ void __launch_bounds__(256) dense_init_kernel(DevSolve s, const double* __restrict__ delta) {
+  if (s.state->done) return;
+  __shared__ double sT[32][33];
+  __shared__ double wr[8][3];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t n = s.n, rows = s.rows;
+  const int tn = blockIdx.x;
+  const int tmb = blockIdx.y;  // 32-row block (local rows)
+  const int64_t il0 = int64_t(tmb) * 32;
+  const double lam1 = lam_of(s, 1);
+  double* __restrict__ a_out = s.slots + size_t(1 % s.nslots) * size_t(s.slot_elems);
+  double dsum[4] = {0.0, 0.0, 0.0, 0.0};
+  double t_step = 0.0, t_max = 0.0, t_nonfin = 0.0;
+  for (int sub = 0; sub < BNI / 32; ++sub) {
+    const int64_t j0 = int64_t(tn) * BNI + sub * 32;
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {  // sT[jj][ii] = Delta(j0 + jj, gi0 + ii)
+      const int64_t jj = j0 + ty + 8 * r;
+      const int64_t gi = s.row0 + il0 + tx;
+      sT[ty + 8 * r][tx] = (jj < n && il0 + tx < rows) ? delta[size_t(jj) * size_t(s.ld) + size_t(gi)] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int64_t il = il0 + ty + 8 * r;
+      const int64_t gi = s.row0 + il;
+      const int64_t c = j0 + tx;
+      if (il >= rows || c >= n) continue;
+      double v;
+      if (gi == c) {
+        v = 1.0;
+      } else {
+        const double g = 1.0 / __dsub_rn(s.theta[gi], s.theta[c]);
+        v = __dmul_rn(__dmul_rn(lam1, g), sT[tx][ty + 8 * r]);
+      }
+      a_out[size_t(il) * size_t(s.ld) + size_t(c)] = v;
+      const double prev = (gi == c) ? 1.0 : 0.0;
+      t_step = fmax(t_step, fabs(__dsub_rn(v, prev)));
+      t_max = fmax(t_max, fabs(v));
+      t_nonfin += isfinite(v) ? 0.0 : 1.0;
+      dsum[r] = __fma_rn(v, delta[size_t(gi) * size_t(s.ld) + size_t(c)], dsum[r]);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const double v = warp_sum(dsum[r]);
+    const int64_t il = il0 + ty + 8 * r;
+    if (tx == 0 && il < rows) {
+      s.rowpart[(size_t(0) * s.ntn + tn) * rows + il] = v;
+      s.rowpart[(size_t(1) * s.ntn + tn) * rows + il] = 0.0;
+      s.rowpart[(size_t(2) * s.ntn + tn) * rows + il] = 0.0;
+    }
+  }
+  t_step = warp_max(t_step);
+  t_max = warp_max(t_max);
+  t_nonfin = warp_sum(t_nonfin);
+  if (tx == 0) {
+    wr[ty][0] = t_step;
+    wr[ty][1] = t_max;
+    wr[ty][2] = t_nonfin;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    for (int w = 0; w < 8; ++w) {
+      a0 = fmax(a0, wr[w][0]);
+      a1 = fmax(a1, wr[w][1]);
+      a2 += wr[w][2];
+    }
+    double* tp = s.tilepart + size_t(tmb * gridDim.x + tn) * 4;
+    tp[0] = a0;
+    tp[1] = a1;
+    tp[2] = a2;
+    tp[3] = 0.0;
+  }
+}
+
+// ------------------------------------------------------------- host side ----
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// Row-major [dim1 x dim0] doubles with leading dimension ld, box [box1 x 16], 128B swizzle.
+int make_tmap_rowmajor(CUtensorMap* out, const double* base, int64_t dim0, int64_t dim1, int64_t ld,
+                       int box1) {
+  auto enc = get_encode();
+  if (!enc) return -1;
+  cuuint64_t dims[2] = {cuuint64_t(dim0), cuuint64_t(dim1)};
+  cuuint64_t strides[1] = {cuuint64_t(ld) * sizeof(double)};
+  cuuint32_t box[2] = {16u, cuuint32_t(box1)};
+  cuuint32_t estr[2] = {1u, 1u};
+  CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box,
+                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : int(r);
+}
+
+int dense_tile_n(int big) { return big ? CfgBig::BN : CfgSmall::BN; }
+int dense_tile_m(int big) { return big ? CfgBig::BM : CfgSmall::BM; }
+
+cudaError_t launch_dense_step(const DevSolve& s, const CUtensorMap* amaps, const CUtensorMap* dmap,
+                              const double* delta, int big, cudaStream_t st) {
+  if (big) {
+    using C = CfgBig;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(dense_step_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+      attr = true;
+    }
+    const int ntm = int((s.rows + C::BM - 1) / C::BM);
+    dense_step_kernel<C><<<ntm * s.ntn, C::THREADS, C::SMEM, st>>>(s, amaps, dmap, delta, ntm);
+  } else {
+    using C = CfgSmall;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(dense_step_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+      attr = true;
+    }
+    const int ntm = int((s.rows + C::BM - 1) / C::BM);
+    dense_step_kernel<C><<<ntm * s.ntn, C::THREADS, C::SMEM, st>>>(s, amaps, dmap, delta, ntm);
+  }
+  return cudaGetLastError();
+}
+
+int dense_step_ntiles(int64_t rows, int ntn, int big) {
+  const int bm = big ? CfgBig::BM : CfgSmall::BM;
+  return int((rows + bm - 1) / bm) * ntn;
+}
+
+int dense_init_ntiles(int64_t rows, int ntn) { return int((rows + 31) / 32) * ntn; }
+
+cudaError_t launch_dense_init(const DevSolve& s, const double* delta, int big, cudaStream_t st) {
+  dim3 grid(s.ntn, unsigned((s.rows + 31) / 32));
+  if (big)
+    dense_init_kernel<CfgBig::BN><<<grid, 256, 0, st>>>(s, delta);
+  else
+    dense_init_kernel<CfgSmall::BN><<<grid, 256, 0, st>>>(s, delta);
+  return cudaGetLastError();
+}
+
+}  // namespace dpt

@@ -1,0 +1,119 @@
+// dpt_device.cuh -- device-side plumbing shared by the DPT kernels:
+// the per-solve device workspace descriptor, PTX wrappers (mbarrier, TMA,
+// DMMA) and deterministic warp reductions.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "dpt_state.h"
+
+namespace dpt {
+
+// Everything a launch needs that may change from iteration to iteration is
+// read from device memory (the state / tables below), so one captured CUDA
+// graph of K iterations can be replayed unchanged.
+struct DevSolve {
+  int64_t n;            // global problem size (columns of A, length of theta)
+  int64_t row0, rows;   // this rank's row shard [row0, row0 + rows)
+  int64_t ld;           // leading dimension (doubles) of A slots and dense Delta rows: n rounded up to even
+  int nslots;           // ring of iterates A_m in slot m % nslots
+  int64_t slot_elems;   // doubles per slot (>= rows * ld; equal on every rank for the gather)
+  int ntn;              // column partial blocks per row (rowpart leading dim)
+  double lambda;        // p.lambda (read-offs always use it, dpt.cpp:23-44)
+  const double* theta;  // [n] unperturbed levels (device)
+  const double* lam_table;  // [max_iter + 2] lambda_k (ramped schedule) or null
+  const int* settled_table; // [max_iter + 2] settled(k) or null (=1)
+  double* slots;        // nslots * rows * n, row-major per slot (row-local)
+  double* dvec[2];      // d_m(i) = P(A_m)(i,i) for local rows, m % 2
+  double* eps;          // [rows] read-offs of the latest folded iterate
+  double* res;          // [rows]
+  double* rowpart;      // [3][ntn][rows] (sum d, max num, max den)
+  double* tilepart;     // [ntiles][4] (max step, max |A|, nonfinite count, spare)
+  int ntiles;
+  double* blockpart;    // fold partials [fold_blocks][8]
+  double* stats;        // [DPT_NSTATS] after (optional) cross-rank max
+  dpt_sm_state* state;
+  dpt_sm_options opts;
+  double* trace;        // [3 * (max_iter + 1)] (k, step, max_res) log
+  unsigned int* counter;  // last-block election for the folds
+  double* cyclepart;    // [fold_blocks][DPT_MAX_WINDOW]
+  int fixed_mode;       // iterate_fixed: no decisions, step every launch
+};
+
+__device__ __forceinline__ int launch_index(const DevSolve& s) { return s.state->j + 1; }
+
+__device__ __forceinline__ double lam_of(const DevSolve& s, int j) {
+  return s.lam_table ? s.lam_table[j] : s.lambda;
+}
+
+// ---------------------------------------------------------------- PTX ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// 2-D TMA tile load (global -> shared), completion on an mbarrier.
+__device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, uint64_t* bar, int c0,
+                                            int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];\n" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void prefetch_tmap(const void* tmap) {
+  asm volatile("prefetch.tensormap [%0];\n" ::"l"(tmap) : "memory");
+}
+
+// D(8x8) += A(8x4, row) * B(4x8, col), FP64 tensor core (SASS DMMA.8x8x4).
+// Fragments: a = A[lane>>2][lane&3], b = B[lane&3][lane>>2],
+// d = {D[lane>>2][2(lane&3)], D[lane>>2][2(lane&3)+1]}.
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// ------------------------------------------------------- reductions ----
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+}  // namespace dpt

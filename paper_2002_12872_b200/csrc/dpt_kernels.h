@@ -1,0 +1,50 @@
+// dpt_kernels.h -- internal launch API of the CUDA kernels (host side).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "dpt_device.cuh"
+
+namespace dpt {
+
+// dense_step.cu (K1)
+int make_tmap_rowmajor(CUtensorMap* out, const double* base, int64_t dim0, int64_t dim1, int64_t ld,
+                       int box1);
+int dense_tile_n(int big);
+int dense_tile_m(int big);
+int dense_step_ntiles(int64_t rows, int ntn, int big);
+int dense_init_ntiles(int64_t rows, int ntn);
+cudaError_t launch_dense_step(const DevSolve& s, const CUtensorMap* amaps, const CUtensorMap* dmap,
+                              const double* delta, int big, cudaStream_t st);
+cudaError_t launch_dense_init(const DevSolve& s, const double* delta, int big, cudaStream_t st);
+
+// sparse_step.cu (K2: CSR full map; K3: CSR / dense row map)
+struct DevCsr {
+  const int64_t* rowptr;  // [n+1]
+  const int32_t* cols;    // [nnz]
+  const double* vals;     // [nnz]
+  int64_t nnz;
+};
+int csr_step_ntiles(int64_t rows, int64_t n);
+int csr_ntn(int64_t n);
+cudaError_t launch_csr_step(const DevSolve& s, const DevCsr& d, cudaStream_t st);
+
+// row map (single vector): z slots are [nslots][n]
+int single_ntn(int64_t n);
+int single_ntiles(int64_t n);
+cudaError_t launch_single_step(const DevSolve& s, const DevCsr& d, const double* dense, int64_t row,
+                               const double* g, cudaStream_t st);
+
+// fold.cu (K4)
+int fold_blocks(int64_t rows);
+cudaError_t launch_fold(const DevSolve& s, int ntiles_this, cudaStream_t st);
+cudaError_t launch_decide(const DevSolve& s, cudaStream_t st);
+cudaError_t launch_cycle(const DevSolve& s, int64_t elems, cudaStream_t st);
+cudaError_t launch_identity(const DevSolve& s, cudaStream_t st);
+cudaError_t launch_unit(const double* z, double* out, int64_t n, cudaStream_t st);
+cudaError_t launch_rowdot(const DevSolve& s, const double* delta, const DevCsr* csr, cudaStream_t st);
+cudaError_t launch_set_diag_delta(const DevSolve& s, const double* delta, const DevCsr* csr,
+                                  cudaStream_t st);
+
+}  // namespace dpt

@@ -1,0 +1,1144 @@
+// solver.cu -- host driver of the DPT iteration and the C ABI (include/dpt_b200.h).
+//
+// The reference's loops run_full / run_single (proj/src/dpt.cpp:92-192,
+// :194-293) become a stream of device work per iteration:
+//     step kernel (K1 dense / K2 CSR / K3 row map)
+//  -> fold (K4a)  [-> ncclAllReduce(max) of the stats when sharded]
+//  -> decide (K4b, the reference's decision order, dpt_state.h)
+//  -> cycle test (only when the window is on)
+// Every kernel reads the launch index from the device state, so the host can
+// enqueue a CHUNK of iterations without looking at results; launches after a
+// terminal decision are no-ops.  The host syncs once per chunk, replays the
+// trace log to the TraceSink in k order, and stops.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cmath>
+#include <limits>
+#include <memory>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/dpt_b200.h"
+#include "dpt_kernels.h"
+#include "dpt_state.h"
+
+// ------------------------------------------------------------- NCCL (dlopen) --
+// NCCL is bound at run time so the library loads on a CPU-only host and in a
+// process where torch already mapped its own libnccl.so.2.
+typedef struct ncclComm* ncclComm_t;
+typedef struct {
+  char internal[128];
+} ncclUniqueId;
+typedef int (*nccl_get_unique_id_fn)(ncclUniqueId*);
+typedef int (*nccl_comm_init_rank_fn)(ncclComm_t*, int, ncclUniqueId, int);
+typedef int (*nccl_all_reduce_fn)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t);
+typedef int (*nccl_all_gather_fn)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t);
+typedef int (*nccl_comm_destroy_fn)(ncclComm_t);
+struct NcclApi {
+  void* h = nullptr;
+  nccl_get_unique_id_fn get_unique_id = nullptr;
+  nccl_comm_init_rank_fn comm_init_rank = nullptr;
+  nccl_all_reduce_fn all_reduce = nullptr;
+  nccl_all_gather_fn all_gather = nullptr;
+  nccl_comm_destroy_fn comm_destroy = nullptr;
+};
+static NcclApi* nccl_api() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    api.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (api.h) {
+      api.get_unique_id = (nccl_get_unique_id_fn)dlsym(api.h, "ncclGetUniqueId");
+      api.comm_init_rank = (nccl_comm_init_rank_fn)dlsym(api.h, "ncclCommInitRank");
+      api.all_reduce = (nccl_all_reduce_fn)dlsym(api.h, "ncclAllReduce");
+      api.all_gather = (nccl_all_gather_fn)dlsym(api.h, "ncclAllGather");
+      api.comm_destroy = (nccl_comm_destroy_fn)dlsym(api.h, "ncclCommDestroy");
+    }
+  }
+  return api.all_reduce ? &api : nullptr;
+}
+static const int kNcclFloat64 = 8, kNcclMax = 2;
+
+struct dpt_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int rank = 0, world = 1;
+  ncclComm_t comm = nullptr;
+  int64_t launches = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+namespace {
+
+using namespace dpt;
+
+struct Fail {
+  int code;
+};
+
+void set_err(dpt_error_info* e, int code, const std::string& msg) {
+  if (!e) return;
+  e->code = code;
+  snprintf(e->message, sizeof(e->message), "%s", msg.c_str());
+}
+
+bool debug_sync() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DPT_DEBUG_SYNC");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+// CK: check a CUDA call; with DPT_DEBUG_SYNC=1 every launch is also synchronised
+// so a device fault is attributed to the kernel that raised it.
+#define CK(expr)                                                                        \
+  do {                                                                                  \
+    cudaError_t _e = (expr);                                                            \
+    if (_e == cudaSuccess && debug_sync()) _e = cudaDeviceSynchronize();                \
+    if (_e != cudaSuccess) {                                                            \
+      set_err(err, DPT_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));   \
+      throw Fail{DPT_ERR_CUDA};                                                         \
+    }                                                                                   \
+  } while (0)
+
+// RAII device buffer
+struct DBuf {
+  void* p = nullptr;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() {
+    if (p) cudaFree(p);
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+void dalloc(DBuf& b, size_t bytes, dpt_error_info* err) {
+  if (bytes == 0) bytes = 16;
+  cudaError_t e = cudaMalloc(&b.p, bytes);
+  if (e != cudaSuccess) {
+    set_err(err, DPT_ERR_CUDA, std::string("cudaMalloc(") + std::to_string(bytes) + "): " + cudaGetErrorString(e));
+    throw Fail{DPT_ERR_CUDA};
+  }
+}
+
+// ------------------------------------------------------------ gap policy ----
+double spread_of(int64_t n, const double* d) {  // spectral_spread, partition.cpp:42-53
+  if (n == 0) return 0.0;
+  double lo = d[0], hi = d[0];
+  for (int64_t i = 0; i < n; ++i) {
+    lo = std::min(lo, d[i]);
+    hi = std::max(hi, d[i]);
+  }
+  return std::hypot(hi - lo, 0.0);
+}
+
+double threshold_of(int64_t n, const double* d, double tol) {  // degeneracy_threshold, :57-59
+  return tol * std::max(1.0, spread_of(n, d));
+}
+
+// build_theta's scan (partition.cpp:69-81) -- the first (i, j) in row-major
+// order with |d_i - d_j| <= thresh -- in O(n log n): rounding of d_i - d_j is
+// monotone in d_j, so the partners of i form a contiguous run of the sorted
+// order around i, and i has a partner iff a sorted neighbour is within thresh.
+bool find_degenerate(int64_t n, const double* d, double tol, int64_t* bi, int64_t* bj) {
+  if (n < 2) return false;
+  const double thresh = threshold_of(n, d, tol);
+  std::vector<int64_t> ord(static_cast<size_t>(n));
+  std::iota(ord.begin(), ord.end(), int64_t(0));
+  std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) {
+    const bool na = std::isnan(d[a]), nb = std::isnan(d[b]);
+    if (na != nb) return nb;  // NaNs last
+    if (na) return a < b;
+    return d[a] < d[b];
+  });
+  std::vector<int64_t> pos(static_cast<size_t>(n));
+  for (int64_t q = 0; q < n; ++q) pos[size_t(ord[size_t(q)])] = q;
+  auto close = [&](int64_t a, int64_t b) { return std::fabs(d[a] - d[b]) <= thresh; };
+  for (int64_t i = 0; i < n; ++i) {
+    const int64_t q = pos[size_t(i)];
+    const bool has = (q > 0 && close(i, ord[size_t(q - 1)])) || (q + 1 < n && close(i, ord[size_t(q + 1)]));
+    if (!has) continue;
+    int64_t best = std::numeric_limits<int64_t>::max();
+    for (int64_t r = q - 1; r >= 0 && close(i, ord[size_t(r)]); --r) best = std::min(best, ord[size_t(r)]);
+    for (int64_t r = q + 1; r < n && close(i, ord[size_t(r)]); ++r) best = std::min(best, ord[size_t(r)]);
+    *bi = i;
+    *bj = best;
+    return true;
+  }
+  return false;
+}
+
+// build_gap_row's check for one chart row (partition.cpp:83-96): first m.
+bool find_degenerate_row(int64_t n, const double* d, int64_t row, double tol, int64_t* bj) {
+  const double thresh = threshold_of(n, d, tol);
+  for (int64_t m = 0; m < n; ++m) {
+    if (m == row) continue;
+    if (std::fabs(d[row] - d[m]) <= thresh) {
+      *bj = m;
+      return true;
+    }
+  }
+  return false;
+}
+
+int effective_window(int requested, int64_t n) {  // dpt.cpp:83-90
+  if (requested <= 0) return 0;
+  const double entries = double(n) * double(n);
+  const double cap = 4.0e6 / std::max(entries, 1.0);
+  int win = requested;
+  if (cap < win) win = int(cap);
+  return win < 2 ? 0 : win;
+}
+
+void degenerate_error(dpt_error_info* err, int64_t i, int64_t j, const double* d) {
+  if (err) {
+    err->i = i;
+    err->j = j;
+    err->ei = d[i];
+    err->ej = d[j];
+  }
+  set_err(err, DPT_ERR_DEGENERATE,
+          "degenerate spectrum: levels " + std::to_string(i) + " and " + std::to_string(j) +
+              " coincide within tolerance");
+  throw Fail{DPT_ERR_DEGENERATE};
+}
+
+// ------------------------------------------------------ device problem ----
+struct DevProblem {
+  int64_t n = 0, ld = 0, nnz = 0;
+  int kind = DPT_DELTA_DENSE;
+  std::vector<double> d_host;  // theta on the host (gap policy)
+  DBuf theta, delta, rowptr, cols, vals;
+  DBuf dmap;  // CUtensorMap for dense Delta
+  bool big = true;
+  DevCsr csr() const { return DevCsr{rowptr.as<int64_t>(), cols.as<int32_t>(), vals.as<double>(), nnz}; }
+};
+
+void validate(const dpt_problem* p, dpt_error_info* err) {
+  if (!p || p->n < 0) {
+    set_err(err, DPT_ERR_SHAPE, "problem: bad size");
+    throw Fail{DPT_ERR_SHAPE};
+  }
+  if (p->n > 0 && !p->d) {
+    set_err(err, DPT_ERR_SHAPE, "problem: missing levels");
+    throw Fail{DPT_ERR_SHAPE};
+  }
+  if (p->delta_kind == DPT_DELTA_DENSE) {
+    if (p->n > 0 && !p->delta) {
+      set_err(err, DPT_ERR_SHAPE, "problem: missing dense delta");
+      throw Fail{DPT_ERR_SHAPE};
+    }
+  } else if (p->delta_kind == DPT_DELTA_CSR) {
+    if (!p->rowptr || (p->nnz > 0 && (!p->cols || !p->vals))) {
+      set_err(err, DPT_ERR_SHAPE, "problem: missing CSR arrays");
+      throw Fail{DPT_ERR_SHAPE};
+    }
+  } else {
+    set_err(err, DPT_ERR_INVALID_ARG, "problem: unknown delta kind");
+    throw Fail{DPT_ERR_INVALID_ARG};
+  }
+}
+
+void upload(DevProblem& dp, dpt_ctx* ctx, const dpt_problem* p, dpt_error_info* err) {
+  validate(p, err);
+  const int64_t n = p->n;
+  dp.n = n;
+  dp.ld = (n + 1) & ~int64_t(1);
+  dp.kind = p->delta_kind;
+  const cudaMemcpyKind k = p->mem == DPT_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  cudaStream_t st = ctx->stream;
+  dp.d_host.resize(size_t(n));
+  if (n) CK(cudaMemcpy(dp.d_host.data(), p->d, size_t(n) * 8, p->mem == DPT_MEM_DEVICE ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost));
+  dalloc(dp.theta, size_t(n) * 8, err);
+  if (n) CK(cudaMemcpyAsync(dp.theta.p, dp.d_host.data(), size_t(n) * 8, cudaMemcpyHostToDevice, st));
+  if (p->delta_kind == DPT_DELTA_DENSE) {
+    dalloc(dp.delta, size_t(n) * size_t(dp.ld) * 8 + 64, err);
+    if (n) {
+      if (dp.ld == n)
+        CK(cudaMemcpyAsync(dp.delta.p, p->delta, size_t(n) * size_t(n) * 8, k, st));
+      else
+        CK(cudaMemcpy2DAsync(dp.delta.p, size_t(dp.ld) * 8, p->delta, size_t(n) * 8, size_t(n) * 8, size_t(n), k, st));
+    }
+  } else {
+    int64_t nnz = p->nnz;
+    if (p->mem == DPT_MEM_HOST) {
+      nnz = p->rowptr[n];
+    } else {
+      CK(cudaMemcpy(&nnz, p->rowptr + n, 8, cudaMemcpyDeviceToHost));
+    }
+    dp.nnz = nnz;
+    dalloc(dp.rowptr, size_t(n + 1) * 8, err);
+    dalloc(dp.cols, size_t(nnz) * 4, err);
+    dalloc(dp.vals, size_t(nnz) * 8, err);
+    CK(cudaMemcpyAsync(dp.rowptr.p, p->rowptr, size_t(n + 1) * 8, k, st));
+    if (nnz) {
+      CK(cudaMemcpyAsync(dp.cols.p, p->cols, size_t(nnz) * 4, k, st));
+      CK(cudaMemcpyAsync(dp.vals.p, p->vals, size_t(nnz) * 8, k, st));
+    }
+  }
+}
+
+// ----------------------------------------------------------- workspace ----
+struct Work {
+  DevSolve s{};
+  DBuf slots, dvec, eps, res, rowpart, tilepart, blockpart, stats, state, trace, counter, cyclepart,
+      amaps, lam_table, settled_table;
+  int ntiles_step = 0;
+  int max_trace = 0;
+  dpt_sm_state* h_state = nullptr;  // pinned
+  double* h_trace = nullptr;        // pinned
+  ~Work() {
+    if (h_state) cudaFreeHost(h_state);
+    if (h_trace) cudaFreeHost(h_trace);
+  }
+};
+
+enum Mode { MODE_DENSE_FULL, MODE_CSR_FULL, MODE_SINGLE };
+
+void make_work(Work& w, dpt_ctx* ctx, DevProblem& dp, Mode mode, int64_t row0, int64_t rows,
+               int64_t rows_alloc, int nslots,
+               int max_iter, const std::vector<double>* lam_tab, const std::vector<int>* set_tab,
+               const dpt_sm_options& so, double lambda, int fixed_mode, dpt_error_info* err) {
+  DevSolve& s = w.s;
+  s.n = dp.n;
+  s.ld = dp.ld;
+  s.row0 = row0;
+  s.rows = rows;
+  s.nslots = nslots;
+  s.lambda = lambda;
+  s.opts = so;
+  s.fixed_mode = fixed_mode;
+  int ntiles_aux = 1;
+  if (mode == MODE_DENSE_FULL) {
+    dp.big = dp.n >= 2048;
+    s.ntn = int((dp.n + dense_tile_n(dp.big) - 1) / dense_tile_n(dp.big));
+    w.ntiles_step = dense_step_ntiles(rows, s.ntn, dp.big);
+    ntiles_aux = dense_init_ntiles(rows, s.ntn);
+  } else if (mode == MODE_CSR_FULL) {
+    s.ntn = csr_ntn(dp.n);
+    w.ntiles_step = csr_step_ntiles(rows, dp.n);
+  } else {
+    s.ntn = single_ntn(dp.n);
+    w.ntiles_step = single_ntiles(dp.n);
+  }
+  s.ntiles = std::max(w.ntiles_step, ntiles_aux);
+  const size_t slot_elems = size_t(std::max<int64_t>(rows_alloc, 1)) * size_t(dp.ld);
+  s.slot_elems = int64_t(slot_elems);
+  dalloc(w.slots, size_t(nslots) * slot_elems * 8 + 64, err);
+  dalloc(w.dvec, size_t(2) * size_t(rows) * 8, err);
+  dalloc(w.eps, size_t(std::max<int64_t>(rows_alloc, 1)) * 8, err);
+  dalloc(w.res, size_t(std::max<int64_t>(rows_alloc, 1)) * 8, err);
+  dalloc(w.rowpart, size_t(3) * size_t(s.ntn) * size_t(rows) * 8, err);
+  dalloc(w.tilepart, size_t(s.ntiles) * 4 * 8, err);
+  dalloc(w.blockpart, size_t(fold_blocks(rows) + 512) * 8 * 8, err);
+  dalloc(w.stats, DPT_NSTATS * 8, err);
+  dalloc(w.state, sizeof(dpt_sm_state), err);
+  w.max_trace = (max_iter > 0 ? max_iter : 0) + 2;
+  dalloc(w.trace, size_t(w.max_trace) * 3 * 8, err);
+  dalloc(w.counter, 16, err);
+  dalloc(w.cyclepart, size_t(512) * DPT_MAX_WINDOW * 8, err);
+  s.theta = dp.theta.as<double>();
+  s.slots = w.slots.as<double>();
+  s.dvec[0] = w.dvec.as<double>();
+  s.dvec[1] = w.dvec.as<double>() + rows;
+  s.eps = w.eps.as<double>();
+  s.res = w.res.as<double>();
+  s.rowpart = w.rowpart.as<double>();
+  s.tilepart = w.tilepart.as<double>();
+  s.blockpart = w.blockpart.as<double>();
+  s.stats = w.stats.as<double>();
+  s.state = w.state.as<dpt_sm_state>();
+  s.trace = w.trace.as<double>();
+  s.counter = w.counter.as<unsigned int>();
+  s.cyclepart = w.cyclepart.as<double>();
+  cudaStream_t st = ctx->stream;
+  CK(cudaMemsetAsync(w.counter.p, 0, 16, st));
+  CK(cudaMemsetAsync(w.state.p, 0, sizeof(dpt_sm_state), st));
+  CK(cudaMemsetAsync(w.dvec.p, 0, size_t(2) * size_t(rows) * 8, st));
+  std::vector<double> ones(DPT_NSTATS, 1.0);
+  CK(cudaMemcpyAsync(w.stats.p, ones.data(), DPT_NSTATS * 8, cudaMemcpyHostToDevice, st));
+  if (lam_tab) {
+    dalloc(w.lam_table, lam_tab->size() * 8, err);
+    CK(cudaMemcpyAsync(w.lam_table.p, lam_tab->data(), lam_tab->size() * 8, cudaMemcpyHostToDevice, st));
+    s.lam_table = w.lam_table.as<double>();
+  }
+  if (set_tab) {
+    dalloc(w.settled_table, set_tab->size() * 4, err);
+    CK(cudaMemcpyAsync(w.settled_table.p, set_tab->data(), set_tab->size() * 4, cudaMemcpyHostToDevice, st));
+    s.settled_table = w.settled_table.as<int>();
+  }
+  if (mode == MODE_DENSE_FULL && dp.n > 0) {
+    // tensor maps: one per ring slot (A) + one for Delta; kept in device memory
+    const int box = dense_tile_m(dp.big);
+    std::vector<CUtensorMap> maps(static_cast<size_t>(nslots));
+    for (int q = 0; q < nslots; ++q) {
+      if (make_tmap_rowmajor(&maps[size_t(q)], s.slots + size_t(q) * slot_elems, dp.n, rows, dp.ld, box) != 0) {
+        set_err(err, DPT_ERR_CUDA, "cuTensorMapEncodeTiled failed for an iterate slot");
+        throw Fail{DPT_ERR_CUDA};
+      }
+    }
+    dalloc(w.amaps, sizeof(CUtensorMap) * size_t(nslots), err);
+    CK(cudaMemcpyAsync(w.amaps.p, maps.data(), sizeof(CUtensorMap) * size_t(nslots), cudaMemcpyHostToDevice, st));
+    if (!dp.dmap.p) {
+      CUtensorMap dm;
+      if (make_tmap_rowmajor(&dm, dp.delta.as<double>(), dp.n, dp.n, dp.ld, dense_tile_n(dp.big)) != 0) {
+        set_err(err, DPT_ERR_CUDA, "cuTensorMapEncodeTiled failed for Delta");
+        throw Fail{DPT_ERR_CUDA};
+      }
+      dalloc(dp.dmap, sizeof(CUtensorMap), err);
+      CK(cudaMemcpyAsync(dp.dmap.p, &dm, sizeof(CUtensorMap), cudaMemcpyHostToDevice, st));
+    }
+  }
+  CK(cudaMallocHost(reinterpret_cast<void**>(&w.h_state), sizeof(dpt_sm_state)));
+  CK(cudaMallocHost(reinterpret_cast<void**>(&w.h_trace), size_t(w.max_trace) * 3 * 8));
+}
+
+void allreduce_stats(dpt_ctx* ctx, Work& w, dpt_error_info* err) {
+  if (ctx->world <= 1) return;
+  NcclApi* api = nccl_api();
+  if (!api || api->all_reduce(w.s.stats, w.s.stats, DPT_NSTATS, kNcclFloat64, kNcclMax, ctx->comm, ctx->stream) != 0) {
+    set_err(err, DPT_ERR_NCCL, "ncclAllReduce(max) of the iteration statistics failed");
+    throw Fail{DPT_ERR_NCCL};
+  }
+}
+
+// One iteration's device work after the step kernel.
+void post_step(dpt_ctx* ctx, Work& w, int ntiles, int64_t cycle_elems, dpt_error_info* err) {
+  CK(launch_fold(w.s, ntiles, ctx->stream));
+  allreduce_stats(ctx, w, err);
+  CK(launch_decide(w.s, ctx->stream));
+  ctx->launches += 2;
+  if (w.s.opts.win > 0 && !w.s.fixed_mode) {
+    CK(launch_cycle(w.s, cycle_elems, ctx->stream));
+    ctx->launches += 1;
+  }
+}
+
+void step_launch(dpt_ctx* ctx, Work& w, DevProblem& dp, Mode mode, int64_t row, dpt_error_info* err) {
+  if (mode == MODE_DENSE_FULL)
+    CK(launch_dense_step(w.s, w.amaps.as<CUtensorMap>(), dp.dmap.as<CUtensorMap>(), dp.delta.as<double>(),
+                         dp.big, ctx->stream));
+  else if (mode == MODE_CSR_FULL)
+    CK(launch_csr_step(w.s, dp.csr(), ctx->stream));
+  else
+    CK(launch_single_step(w.s, dp.csr(), dp.kind == DPT_DELTA_DENSE ? dp.delta.as<double>() : nullptr, row,
+                          nullptr, ctx->stream));
+  ctx->launches += 1;
+}
+
+// Runs launches 1 .. until the state machine terminates (or `total` launches).
+// Launch 1 is the special init (dense) or the generic step from slot 0.
+void drive(dpt_ctx* ctx, Work& w, DevProblem& dp, Mode mode, int64_t row, int total, bool first_is_init,
+           dpt_trace_fn trace, void* user, dpt_error_info* err) {
+  cudaStream_t st = ctx->stream;
+  const int64_t cycle_elems = (mode == MODE_SINGLE) ? dp.n : w.s.rows * dp.n;
+  int issued = 0;
+  if (first_is_init) {
+    CK(launch_dense_init(w.s, dp.delta.as<double>(), dp.big, st));
+    ctx->launches += 1;
+    post_step(ctx, w, dense_init_ntiles(w.s.rows, w.s.ntn), cycle_elems, err);
+    issued = 1;
+  }
+  int chunk = 4;
+  int traced = 0;
+  while (true) {
+    const int todo = std::min(chunk, total - issued);
+    for (int c = 0; c < todo; ++c) {
+      step_launch(ctx, w, dp, mode, row, err);
+      post_step(ctx, w, w.ntiles_step, cycle_elems, err);
+    }
+    issued += todo;
+    CK(cudaMemcpyAsync(w.h_state, w.s.state, sizeof(dpt_sm_state), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (trace && w.h_state->trace_len > traced) {
+      const int nt = w.h_state->trace_len;
+      CK(cudaMemcpy(w.h_trace, w.s.trace, size_t(nt) * 3 * 8, cudaMemcpyDeviceToHost));
+      for (int q = traced; q < nt; ++q) {
+        if (trace(int(w.h_trace[3 * q]), w.h_trace[3 * q + 1], w.h_trace[3 * q + 2], user) != 0) {
+          set_err(err, DPT_ERR_TRACE, "trace sink aborted the iteration");
+          throw Fail{DPT_ERR_TRACE};
+        }
+      }
+      traced = nt;
+    }
+    if (w.h_state->done || issued >= total) break;
+    chunk = std::min(chunk * 2, 64);
+  }
+}
+
+void copy_out(double* dst, const double* src, size_t count, int out_mem, cudaStream_t st, dpt_error_info* err) {
+  if (!dst || count == 0) return;
+  CK(cudaMemcpyAsync(dst, src, count * 8, out_mem == DPT_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
+}
+
+void copy_slot_out(double* dst, const Work& w, const DevProblem& dp, int slot, int out_mem, cudaStream_t st,
+                   dpt_error_info* err) {
+  if (!dst || dp.n == 0) return;
+  const double* src = w.s.slots + size_t(slot) * size_t(w.s.slot_elems);
+  const cudaMemcpyKind k = out_mem == DPT_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  if (dp.ld == dp.n)
+    CK(cudaMemcpyAsync(dst, src, size_t(w.s.rows) * size_t(dp.n) * 8, k, st));
+  else
+    CK(cudaMemcpy2DAsync(dst, size_t(dp.n) * 8, src, size_t(dp.ld) * 8, size_t(dp.n) * 8, size_t(w.s.rows), k, st));
+}
+
+void fill_nan(double* dst, size_t count, int out_mem, cudaStream_t st, dpt_error_info* err) {
+  if (!dst || count == 0) return;
+  std::vector<double> nan(count, std::numeric_limits<double>::quiet_NaN());
+  if (out_mem == DPT_MEM_DEVICE) {
+    CK(cudaMemcpyAsync(dst, nan.data(), count * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+  } else {
+    memcpy(dst, nan.data(), count * 8);
+  }
+}
+
+
+struct Guard {
+  dpt_ctx* ctx;
+  int old = -1;
+  explicit Guard(dpt_ctx* c) : ctx(c) {
+    cudaGetDevice(&old);
+    cudaSetDevice(c->device);
+  }
+  ~Guard() {
+    if (old >= 0) cudaSetDevice(old);
+  }
+};
+
+// Rank r owns rows [r*per, min(n, (r+1)*per)) of A (the paper's columns).
+void shard_rows(const dpt_ctx* ctx, int64_t n, int64_t* row0, int64_t* rows) {
+  const int64_t per = (n + ctx->world - 1) / ctx->world;
+  *row0 = std::min<int64_t>(n, per * ctx->rank);
+  *rows = std::min<int64_t>(n, *row0 + per) - *row0;
+}
+
+// Upload a caller iterate (rows x n, row-major) into ring slot `slot`.
+void put_slot(Work& w, const DevProblem& dp, int slot, const double* a, int mem, cudaStream_t st,
+              dpt_error_info* err) {
+  double* dst = w.s.slots + size_t(slot) * size_t(w.s.slot_elems);
+  const cudaMemcpyKind k = mem == DPT_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  CK(cudaMemsetAsync(dst, 0, size_t(w.s.rows) * size_t(dp.ld) * 8, st));
+  if (dp.ld == dp.n)
+    CK(cudaMemcpyAsync(dst, a, size_t(w.s.rows) * size_t(dp.n) * 8, k, st));
+  else
+    CK(cudaMemcpy2DAsync(dst, size_t(dp.ld) * 8, a, size_t(dp.n) * 8, size_t(dp.n) * 8, size_t(w.s.rows), k, st));
+  CK(cudaStreamSynchronize(st));  // `a` may be pageable host memory owned by the caller
+}
+
+// A_0 = I in slot 0 and d_0 = diag(Delta) = P(I)(i,i).
+void put_identity(dpt_ctx* ctx, Work& w, DevProblem& dp, dpt_error_info* err) {
+  CK(launch_identity(w.s, ctx->stream));
+  DevCsr c = dp.csr();
+  if (dp.kind == DPT_DELTA_DENSE)
+    CK(launch_set_diag_delta(w.s, dp.delta.as<double>(), nullptr, ctx->stream));
+  else
+    CK(launch_set_diag_delta(w.s, nullptr, &c, ctx->stream));
+  ctx->launches += 2;
+}
+
+void gather_rows(dpt_ctx* ctx, const Work& w, const DevProblem& dp, int slot, double* dst, int out_mem,
+                 dpt_error_info* err) {
+  if (!dst) return;
+  cudaStream_t st = ctx->stream;
+  if (ctx->world <= 1) {
+    copy_slot_out(dst, w, dp, slot, out_mem, st, err);
+    return;
+  }
+  // C2: the final eigenvector gather (one ncclAllGather of the row shards)
+  NcclApi* api = nccl_api();
+  DBuf all;
+  dalloc(all, size_t(ctx->world) * size_t(w.s.slot_elems) * 8, err);
+  const double* src = w.s.slots + size_t(slot) * size_t(w.s.slot_elems);
+  if (!api || api->all_gather(src, all.p, size_t(w.s.slot_elems), kNcclFloat64, ctx->comm, st) != 0) {
+    set_err(err, DPT_ERR_NCCL, "ncclAllGather of the iterate shards failed");
+    throw Fail{DPT_ERR_NCCL};
+  }
+  const cudaMemcpyKind k = out_mem == DPT_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  CK(cudaMemcpy2DAsync(dst, size_t(dp.n) * 8, all.p, size_t(dp.ld) * 8, size_t(dp.n) * 8, size_t(dp.n), k, st));
+  CK(cudaStreamSynchronize(st));
+}
+
+void gather_vec(dpt_ctx* ctx, const Work& w, const double* src, double* dst, int out_mem, int64_t n,
+                dpt_error_info* err) {
+  if (!dst) return;
+  cudaStream_t st = ctx->stream;
+  const int64_t per = w.s.slot_elems / w.s.ld;
+  DBuf all;
+  dalloc(all, size_t(ctx->world) * size_t(per) * 8, err);
+  NcclApi* api = nccl_api();
+  if (!api || api->all_gather(src, all.p, size_t(per), kNcclFloat64, ctx->comm, st) != 0) {
+    set_err(err, DPT_ERR_NCCL, "ncclAllGather of the read-offs failed");
+    throw Fail{DPT_ERR_NCCL};
+  }
+  copy_out(dst, all.as<double>(), size_t(n), out_mem, st, err);
+  CK(cudaStreamSynchronize(st));
+}
+
+dpt_options opts_or_default(const dpt_options* o) {
+  dpt_options r;
+  if (o)
+    r = *o;
+  else
+    dpt_options_default(&r);
+  return r;
+}
+
+std::vector<double> host_levels(const dpt_problem* p, dpt_error_info* err) {
+  std::vector<double> dh(size_t(p->n));
+  if (p->n)
+    CK(cudaMemcpy(dh.data(), p->d, size_t(p->n) * 8,
+                  p->mem == DPT_MEM_DEVICE ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost));
+  return dh;
+}
+
+void fill_report(dpt_ctx* ctx, dpt_report* rep, int status, int iters, double step) {
+  if (!rep) return;
+  memset(rep, 0, sizeof(*rep));
+  rep->status = status;
+  rep->iterations = iters;
+  rep->step_norm = step;
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+  rep->device_ms = ms;
+  rep->launches = int(ctx->launches);
+}
+
+// ---------------------------------------------------------------- run_full --
+// run_full (dpt.cpp:92-192); fixed_k >= 0 selects iterate_fixed (:381-387).
+int run_full(dpt_ctx* ctx, const dpt_problem* p, const dpt_options* opts_in, bool ramped, double alpha,
+             int fixed_k, double fixed_lambda, dpt_trace_fn trace, void* user, double* a_out,
+             double* eig_out, double* res_out, int out_mem, dpt_report* rep, dpt_error_info* err) {
+  const dpt_options o = opts_or_default(opts_in);
+  Guard g(ctx);
+  validate(p, err);
+  const int64_t n = p->n;
+  const bool fixed = fixed_k >= 0;
+  if (n > 0 && n < ctx->world) {
+    set_err(err, DPT_ERR_SHAPE, "sharded solve needs n >= world size");
+    throw Fail{DPT_ERR_SHAPE};
+  }
+  std::vector<double> dh = host_levels(p, err);
+  int64_t bi, bj;
+  // iterate_fixed builds theta with the default tolerance (dpt.cpp:383)
+  if (find_degenerate(n, dh.data(), fixed ? 1e-12 : o.degeneracy_tol, &bi, &bj)) degenerate_error(err, bi, bj, dh.data());
+  DevProblem dp;
+  upload(dp, ctx, p, err);
+  const Mode mode = p->delta_kind == DPT_DELTA_DENSE ? MODE_DENSE_FULL : MODE_CSR_FULL;
+  const int win = fixed ? 0 : effective_window(o.cycle_window, n);
+  const int nslots = win > 0 ? win + 1 : 2;
+  int64_t row0, rows;
+  shard_rows(ctx, n, &row0, &rows);
+  const int64_t per = (n + ctx->world - 1) / ctx->world;
+  const int max_iter = fixed ? fixed_k : o.max_iter;
+  const int total = fixed ? fixed_k : std::max(max_iter, 0) + 1;  // iterations + the read-off launch
+  const double lam = fixed ? fixed_lambda : p->lambda;
+  std::vector<double> lam_tab;
+  std::vector<int> set_tab;
+  if (ramped) {
+    lam_tab.resize(size_t(total) + 2);
+    set_tab.resize(size_t(total) + 2);
+    for (size_t k = 0; k < lam_tab.size(); ++k) {
+      const double lk = k == 0 ? 0.0 : lam * (1.0 - std::pow(alpha, double(int(k) - 1)));  // dpt.cpp:131-132
+      lam_tab[k] = lk;
+      set_tab[k] = std::fabs(lk - lam) <= o.tol * std::fabs(lam) ? 1 : 0;  // :133-134
+    }
+    set_tab[0] = 1;
+  }
+  dpt_sm_options so{};
+  so.tol = o.tol;
+  so.residual_tol = o.residual_tol;
+  so.divergence_threshold = o.divergence_threshold;
+  so.max_iter = max_iter;
+  so.win = win;
+  so.have_trace = trace ? 1 : 0;
+  Work w;
+  make_work(w, ctx, dp, mode, row0, rows, per, nslots, max_iter, ramped ? &lam_tab : nullptr,
+            ramped ? &set_tab : nullptr, so, lam, fixed ? 1 : 0, err);
+  cudaStream_t st = ctx->stream;
+  CK(cudaEventRecord(ctx->ev0, st));
+  int final_iter = 0, status = DPT_MAX_ITERATIONS, iters = max_iter, readoffs = 1;
+  double step = 0.0;
+  const bool dense = mode == MODE_DENSE_FULL;
+  if (n == 0) {
+    readoffs = 0;
+  } else if (fixed) {
+    if (fixed_k == 0) {
+      put_identity(ctx, w, dp, err);
+    } else {
+      if (!dense) put_identity(ctx, w, dp, err);
+      drive(ctx, w, dp, mode, 0, total, dense, nullptr, nullptr, err);
+    }
+    final_iter = fixed_k;
+    readoffs = 0;
+  } else if (max_iter <= 0) {
+    // the loop never runs: MaxIterations with the read-offs of A_0 = I (dpt.cpp:189-191)
+    put_identity(ctx, w, dp, err);
+    w.s.fixed_mode = 1;
+    step_launch(ctx, w, dp, mode, 0, err);
+    post_step(ctx, w, w.ntiles_step, 0, err);
+    final_iter = 0;
+  } else {
+    if (!dense || win > 0) put_identity(ctx, w, dp, err);  // A_0 = I (CSR start / window entry)
+    drive(ctx, w, dp, mode, 0, total, dense, trace, user, err);
+    if (!w.h_state->done) {
+      set_err(err, DPT_ERR_CUDA, "internal: iteration budget consumed without a terminal status");
+      throw Fail{DPT_ERR_CUDA};
+    }
+    status = w.h_state->status;
+    iters = w.h_state->iterations;
+    final_iter = w.h_state->final_iter;
+    readoffs = w.h_state->readoffs;
+    step = w.h_state->step_norm;
+  }
+  CK(cudaEventRecord(ctx->ev1, st));
+  if (n > 0) {
+    gather_rows(ctx, w, dp, final_iter % nslots, a_out, out_mem, err);
+    if (readoffs) {
+      if (ctx->world > 1) {
+        gather_vec(ctx, w, w.s.eps, eig_out, out_mem, n, err);
+        gather_vec(ctx, w, w.s.res, res_out, out_mem, n, err);
+      } else {
+        copy_out(eig_out, w.s.eps, size_t(n), out_mem, st, err);
+        copy_out(res_out, w.s.res, size_t(n), out_mem, st, err);
+      }
+    } else {
+      fill_nan(eig_out, size_t(n), out_mem, st, err);
+      fill_nan(res_out, size_t(n), out_mem, st, err);
+    }
+  }
+  CK(cudaStreamSynchronize(st));
+  fill_report(ctx, rep, status, iters, step);
+  return DPT_OK;
+}
+
+// step_full (dpt.cpp:311-327): F(a) for a caller iterate.
+int run_step_full(dpt_ctx* ctx, const dpt_problem* p, const double* a, double lambda, double* out, int io_mem,
+                  dpt_error_info* err) {
+  Guard g(ctx);
+  validate(p, err);
+  if (ctx->world > 1) {
+    set_err(err, DPT_ERR_UNSUPPORTED, "step_full is a single-device call");
+    throw Fail{DPT_ERR_UNSUPPORTED};
+  }
+  const int64_t n = p->n;
+  if (n == 0) return DPT_OK;
+  std::vector<double> dh = host_levels(p, err);
+  DevProblem dp;
+  upload(dp, ctx, p, err);
+  const Mode mode = p->delta_kind == DPT_DELTA_DENSE ? MODE_DENSE_FULL : MODE_CSR_FULL;
+  dpt_sm_options so{};
+  so.max_iter = 1;
+  Work w;
+  make_work(w, ctx, dp, mode, 0, n, n, 2, 1, nullptr, nullptr, so, lambda, 1, err);
+  put_slot(w, dp, 0, a, io_mem, ctx->stream, err);
+  DevCsr c = dp.csr();
+  CK(launch_rowdot(w.s, dp.kind == DPT_DELTA_DENSE ? dp.delta.as<double>() : nullptr, dp.kind == DPT_DELTA_CSR ? &c : nullptr, ctx->stream));
+  step_launch(ctx, w, dp, mode, 0, err);
+  post_step(ctx, w, w.ntiles_step, 0, err);
+  copy_slot_out(out, w, dp, 1, io_mem, ctx->stream, err);
+  CK(cudaStreamSynchronize(ctx->stream));
+  return DPT_OK;
+}
+
+// ---------------------------------------------------------------- run_single --
+// run_single (dpt.cpp:194-293) for chart row `row`; fixed >= 0: step_single /
+// eigenvalue_of (one launch from the caller's z).
+int run_single(dpt_ctx* ctx, const dpt_problem* p, int64_t row, const dpt_options* opts_in, double ramp_alpha,
+               dpt_trace_fn trace, void* user, double* z_out, int out_mem, dpt_report* rep,
+               const double* z_in, int z_mem, double fixed_lambda, double* eig_fixed, double* z_unit,
+               dpt_error_info* err) {
+  const dpt_options o = opts_or_default(opts_in);
+  Guard g(ctx);
+  validate(p, err);
+  const int64_t n = p->n;
+  const bool fixed = z_in != nullptr;
+  const bool ramped = ramp_alpha > 0.0;
+  DevProblem dp;
+  upload(dp, ctx, p, err);
+  const int win = fixed ? 0 : (o.cycle_window >= 2 ? std::min(o.cycle_window, DPT_MAX_WINDOW) : 0);  // dpt.cpp:207
+  const int nslots = win > 0 ? win + 1 : 2;
+  const int max_iter = fixed ? 1 : o.max_iter;
+  const int total = fixed ? 1 : std::max(max_iter, 0) + 1;
+  const double lam = fixed ? fixed_lambda : p->lambda;
+  std::vector<double> lam_tab;
+  std::vector<int> set_tab;
+  if (ramped && !fixed) {
+    lam_tab.resize(size_t(total) + 2);
+    set_tab.resize(size_t(total) + 2);
+    for (size_t k = 0; k < lam_tab.size(); ++k) {
+      const double lk = k == 0 ? 0.0 : lam * (1.0 - std::pow(ramp_alpha, double(int(k) - 1)));
+      lam_tab[k] = lk;
+      set_tab[k] = std::fabs(lk - lam) <= o.tol * std::fabs(lam) ? 1 : 0;
+    }
+    set_tab[0] = 1;
+  }
+  dpt_sm_options so{};
+  so.tol = o.tol;
+  so.residual_tol = o.residual_tol;
+  so.divergence_threshold = o.divergence_threshold;
+  so.max_iter = max_iter;
+  so.win = win;
+  so.have_trace = trace ? 1 : 0;
+  Work w;
+  make_work(w, ctx, dp, MODE_SINGLE, row, 1, 1, nslots, max_iter, ramped && !fixed ? &lam_tab : nullptr,
+            ramped && !fixed ? &set_tab : nullptr, so, lam, fixed ? 1 : 0, err);
+  cudaStream_t st = ctx->stream;
+  CK(cudaEventRecord(ctx->ev0, st));
+  int final_iter = 0, status = DPT_MAX_ITERATIONS, iters = max_iter, readoffs = 1;
+  double step = 0.0;
+  if (fixed) {
+    put_slot(w, dp, 0, z_in, z_mem, st, err);
+    step_launch(ctx, w, dp, MODE_SINGLE, row, err);
+    post_step(ctx, w, w.ntiles_step, 0, err);
+    final_iter = 1;
+  } else if (max_iter <= 0) {
+    CK(launch_identity(w.s, st));  // z = e_row
+    w.s.fixed_mode = 1;
+    step_launch(ctx, w, dp, MODE_SINGLE, row, err);
+    post_step(ctx, w, w.ntiles_step, 0, err);
+    final_iter = 0;
+  } else {
+    CK(launch_identity(w.s, st));  // z = e_row (rows == 1, row0 == row)
+    drive(ctx, w, dp, MODE_SINGLE, row, total, false, trace, user, err);
+    if (!w.h_state->done) {
+      set_err(err, DPT_ERR_CUDA, "internal: iteration budget consumed without a terminal status");
+      throw Fail{DPT_ERR_CUDA};
+    }
+    status = w.h_state->status;
+    iters = w.h_state->iterations;
+    final_iter = w.h_state->final_iter;
+    readoffs = w.h_state->readoffs;
+    step = w.h_state->step_norm;
+  }
+  CK(cudaEventRecord(ctx->ev1, st));
+  if (n > 0 && z_out) copy_slot_out(z_out, w, dp, final_iter % nslots, out_mem, st, err);
+  if (n > 0 && z_unit) {  // dominant_eigenpair's z_unit = z / ||z||_2 (dpt.cpp:432-436)
+    DBuf tmp;
+    dalloc(tmp, size_t(n) * 8, err);
+    CK(launch_unit(w.s.slots + size_t(final_iter % nslots) * size_t(w.s.slot_elems), tmp.as<double>(), n, st));
+    copy_out(z_unit, tmp.as<double>(), size_t(n), out_mem, st, err);
+    CK(cudaStreamSynchronize(st));
+  }
+  double eig = std::numeric_limits<double>::quiet_NaN(), res = eig;
+  if (readoffs) {
+    CK(cudaMemcpyAsync(&eig, w.s.eps, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&res, w.s.res, 8, cudaMemcpyDeviceToHost, st));
+  }
+  CK(cudaStreamSynchronize(st));
+  if (eig_fixed) *eig_fixed = eig;
+  fill_report(ctx, rep, status, iters, step);
+  if (rep) {
+    rep->eigenvalue = eig;
+    rep->residual = res;
+    rep->row = row;
+  }
+  return DPT_OK;
+}
+
+
+}  // namespace
+
+// ================================================================ C ABI ====
+#define DPT_API_BEGIN \
+  if (err) memset(err, 0, sizeof(*err)); \
+  try {
+#define DPT_API_END                                                  \
+  }                                                                  \
+  catch (const Fail& f) {                                            \
+    return f.code;                                                   \
+  }                                                                  \
+  catch (const std::exception& e) {                                  \
+    set_err(err, DPT_ERR_CUDA, std::string("exception: ") + e.what()); \
+    return DPT_ERR_CUDA;                                             \
+  }
+
+extern "C" {
+
+void dpt_options_default(dpt_options* o) {  // IterationOptions defaults, dpt.hpp:22-31
+  o->tol = 1e-12;
+  o->residual_tol = 1e-10;
+  o->max_iter = 10000;
+  o->divergence_threshold = 1e8;
+  o->cycle_window = 16;
+  o->degeneracy_tol = 1e-12;
+}
+
+const char* dpt_status_string(int s) {  // to_string, dpt.cpp:297-309
+  switch (s) {
+    case DPT_CONVERGED:
+      return "Converged";
+    case DPT_BOUNDED_NON_CONVERGED:
+      return "BoundedNonConverged";
+    case DPT_DIVERGED:
+      return "Diverged";
+    case DPT_MAX_ITERATIONS:
+      return "MaxIterations";
+  }
+  return "Unknown";
+}
+
+int dpt_abi_version(void) { return DPT_B200_ABI_VERSION; }
+
+int dpt_ctx_create(int device, dpt_ctx** out, dpt_error_info* err) {
+  DPT_API_BEGIN
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    set_err(err, DPT_ERR_NO_DEVICE, "no CUDA device visible: the DPT path has no CPU fallback");
+    return DPT_ERR_NO_DEVICE;
+  }
+  if (device < 0 || device >= count) {
+    set_err(err, DPT_ERR_INVALID_ARG, "device ordinal out of range");
+    return DPT_ERR_INVALID_ARG;
+  }
+  std::unique_ptr<dpt_ctx> c(new dpt_ctx());
+  c->device = device;
+  Guard g(c.get());
+  CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  CK(cudaEventCreate(&c->ev0));
+  CK(cudaEventCreate(&c->ev1));
+  *out = c.release();
+  return DPT_OK;
+  DPT_API_END
+}
+
+void dpt_ctx_destroy(dpt_ctx* ctx) {
+  if (!ctx) return;
+  {
+    Guard g(ctx);
+    if (ctx->comm && nccl_api() && nccl_api()->comm_destroy) nccl_api()->comm_destroy(ctx->comm);
+    if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+    if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  }
+  delete ctx;
+}
+
+int dpt_nccl_unique_id(void* out, size_t bytes, dpt_error_info* err) {
+  DPT_API_BEGIN
+  NcclApi* api = nccl_api();
+  if (!api || bytes < sizeof(ncclUniqueId)) {
+    set_err(err, DPT_ERR_NCCL, "libnccl.so.2 not loadable or id buffer too small");
+    return DPT_ERR_NCCL;
+  }
+  ncclUniqueId id;
+  if (api->get_unique_id(&id) != 0) {
+    set_err(err, DPT_ERR_NCCL, "ncclGetUniqueId failed");
+    return DPT_ERR_NCCL;
+  }
+  memcpy(out, &id, sizeof(id));
+  return DPT_OK;
+  DPT_API_END
+}
+
+int dpt_ctx_set_comm(dpt_ctx* ctx, int rank, int world, const void* id, size_t bytes, dpt_error_info* err) {
+  DPT_API_BEGIN
+  if (world <= 1) {
+    ctx->rank = 0;
+    ctx->world = 1;
+    return DPT_OK;
+  }
+  NcclApi* api = nccl_api();
+  if (!api || bytes < sizeof(ncclUniqueId) || rank < 0 || rank >= world) {
+    set_err(err, DPT_ERR_NCCL, "bad communicator arguments or libnccl.so.2 missing");
+    return DPT_ERR_NCCL;
+  }
+  Guard g(ctx);
+  ncclUniqueId uid;
+  memcpy(&uid, id, sizeof(uid));
+  if (api->comm_init_rank(&ctx->comm, world, uid, rank) != 0) {
+    set_err(err, DPT_ERR_NCCL, "ncclCommInitRank failed");
+    return DPT_ERR_NCCL;
+  }
+  ctx->rank = rank;
+  ctx->world = world;
+  return DPT_OK;
+  DPT_API_END
+}
+
+void* dpt_ctx_stream(dpt_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+int64_t dpt_ctx_launch_count(const dpt_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int dpt_iterate_full(dpt_ctx* ctx, const dpt_problem* p, const dpt_options* opts, dpt_trace_fn trace, void* user,
+                     double* a_out, double* eig_out, double* res_out, int out_mem, dpt_report* rep,
+                     dpt_error_info* err) {
+  DPT_API_BEGIN
+  return run_full(ctx, p, opts, false, 0.0, -1, 0.0, trace, user, a_out, eig_out, res_out, out_mem, rep, err);
+  DPT_API_END
+}
+
+int dpt_iterate_ramped(dpt_ctx* ctx, const dpt_problem* p, double alpha, const dpt_options* opts,
+                       dpt_trace_fn trace, void* user, double* a_out, double* eig_out, double* res_out,
+                       int out_mem, dpt_report* rep, dpt_error_info* err) {
+  DPT_API_BEGIN
+  if (!(alpha >= 0.0) || alpha >= 1.0) {  // dpt.cpp:376-377
+    set_err(err, DPT_ERR_INVALID_ARG, "iterate_ramped: alpha must lie in [0, 1)");
+    return DPT_ERR_INVALID_ARG;
+  }
+  return run_full(ctx, p, opts, true, alpha, -1, 0.0, trace, user, a_out, eig_out, res_out, out_mem, rep, err);
+  DPT_API_END
+}
+
+int dpt_iterate_fixed(dpt_ctx* ctx, const dpt_problem* p, int k, double lambda, double* a_out, int out_mem,
+                      dpt_report* rep, dpt_error_info* err) {
+  DPT_API_BEGIN
+  if (k < 0) {  // dpt.cpp:382
+    set_err(err, DPT_ERR_INVALID_ARG, "iterate_fixed: negative step count");
+    return DPT_ERR_INVALID_ARG;
+  }
+  return run_full(ctx, p, nullptr, false, 0.0, k, lambda, nullptr, nullptr, a_out, nullptr, nullptr, out_mem, rep,
+                  err);
+  DPT_API_END
+}
+
+int dpt_step_full(dpt_ctx* ctx, const dpt_problem* p, const double* a, double lambda, double* out, int io_mem,
+                  dpt_error_info* err) {
+  DPT_API_BEGIN
+  return run_step_full(ctx, p, a, lambda, out, io_mem, err);
+  DPT_API_END
+}
+
+int dpt_iterate_single(dpt_ctx* ctx, const dpt_problem* p, int64_t row, const dpt_options* opts,
+                       double ramp_alpha, dpt_trace_fn trace, void* user, double* z_out, int out_mem,
+                       dpt_report* rep, dpt_error_info* err) {
+  DPT_API_BEGIN
+  validate(p, err);
+  if (row < 0 || row >= p->n) {  // dpt.cpp:392
+    set_err(err, DPT_ERR_SHAPE, "iterate_single: row out of range");
+    return DPT_ERR_SHAPE;
+  }
+  if (!(ramp_alpha >= 0.0) || ramp_alpha >= 1.0) {  // dpt.cpp:393-394
+    set_err(err, DPT_ERR_INVALID_ARG, "iterate_single: ramp alpha must lie in [0, 1)");
+    return DPT_ERR_INVALID_ARG;
+  }
+  const dpt_options o = opts_or_default(opts);
+  std::vector<double> dh = host_levels(p, err);
+  int64_t bj;
+  if (find_degenerate_row(p->n, dh.data(), row, o.degeneracy_tol, &bj)) degenerate_error(err, row, bj, dh.data());
+  return run_single(ctx, p, row, &o, ramp_alpha, trace, user, z_out, out_mem, rep, nullptr, 0, 0.0, nullptr,
+                    nullptr, err);
+  DPT_API_END
+}
+
+int dpt_dominant_eigenpair(dpt_ctx* ctx, const dpt_problem* p, const dpt_options* opts, double* z_chart,
+                           double* z_unit, int out_mem, dpt_report* rep, dpt_error_info* err) {
+  DPT_API_BEGIN
+  validate(p, err);
+  const int64_t n = p->n;
+  if (n == 0) {  // dpt.cpp:402
+    set_err(err, DPT_ERR_SHAPE, "dominant_eigenpair: empty problem");
+    return DPT_ERR_SHAPE;
+  }
+  const dpt_options o = opts_or_default(opts);
+  std::vector<double> d = host_levels(p, err);
+  int64_t best = 0;  // first argmax of Re d (dpt.cpp:404-406)
+  for (int64_t i = 1; i < n; ++i)
+    if (d[size_t(i)] > d[size_t(best)]) best = i;
+  if (n > 1) {  // runner-up ambiguity (dpt.cpp:408-419)
+    int64_t runner = best == 0 ? 1 : 0;
+    for (int64_t i = 0; i < n; ++i) {
+      if (i == best) continue;
+      if (d[size_t(i)] > d[size_t(runner)]) runner = i;
+    }
+    const double thr = threshold_of(n, d.data(), o.degeneracy_tol);
+    if (d[size_t(best)] - d[size_t(runner)] < thr) {
+      if (err) {
+        err->i = best;
+        err->j = runner;
+        err->ei = d[size_t(best)];
+        err->ej = d[size_t(runner)];
+      }
+      set_err(err, DPT_ERR_DEGENERATE, "dominant_eigenpair: ambiguous dominant level");
+      return DPT_ERR_DEGENERATE;
+    }
+  }
+  int64_t bj;
+  if (find_degenerate_row(n, d.data(), best, o.degeneracy_tol, &bj)) degenerate_error(err, best, bj, d.data());
+  return run_single(ctx, p, best, &o, 0.0, nullptr, nullptr, z_chart, out_mem, rep, nullptr, 0, 0.0, nullptr,
+                    z_unit, err);
+  DPT_API_END
+}
+
+int dpt_step_single(dpt_ctx* ctx, const dpt_problem* p, const double* z, int64_t row, double lambda, double* out,
+                    int io_mem, dpt_error_info* err) {
+  DPT_API_BEGIN
+  validate(p, err);
+  if (row < 0 || row >= p->n) {
+    set_err(err, DPT_ERR_SHAPE, "step_single: dimension mismatch");
+    return DPT_ERR_SHAPE;
+  }
+  return run_single(ctx, p, row, nullptr, 0.0, nullptr, nullptr, out, io_mem, nullptr, z, io_mem, lambda, nullptr,
+                    nullptr, err);
+  DPT_API_END
+}
+
+int dpt_eigenvalue_of(dpt_ctx* ctx, const dpt_problem* p, const double* z, int64_t row, double lambda, double* out,
+                      int z_mem, dpt_error_info* err) {
+  DPT_API_BEGIN
+  validate(p, err);
+  if (row < 0 || row >= p->n) {  // dpt.cpp:361-362
+    set_err(err, DPT_ERR_SHAPE, "eigenvalue_of: dimension mismatch");
+    return DPT_ERR_SHAPE;
+  }
+  return run_single(ctx, p, row, nullptr, 0.0, nullptr, nullptr, nullptr, z_mem, nullptr, z, z_mem, lambda, out,
+                    nullptr, err);
+  DPT_API_END
+}
+
+int dpt_check_degenerate(int64_t n, const double* d, double tol, int64_t* i, int64_t* j) {
+  return find_degenerate(n, d, tol, i, j) ? 1 : 0;
+}
+
+double dpt_spectral_spread(int64_t n, const double* d) { return spread_of(n, d); }
+
+int dpt_effective_window(int requested, int64_t n) { return effective_window(requested, n); }
+
+size_t dpt_sm_state_bytes(void) { return sizeof(dpt_sm_state) + sizeof(dpt_sm_options); }
+
+void dpt_sm_init(void* state, void* opts, const dpt_options* o, int win, int have_trace) {
+  memset(state, 0, sizeof(dpt_sm_state));
+  dpt_sm_options* so = static_cast<dpt_sm_options*>(opts);
+  memset(so, 0, sizeof(*so));
+  so->tol = o->tol;
+  so->residual_tol = o->residual_tol;
+  so->divergence_threshold = o->divergence_threshold;
+  so->max_iter = o->max_iter;
+  so->win = win;
+  so->have_trace = have_trace;
+}
+
+void dpt_sm_decide_host(void* state, const void* opts, const double* stats, int j, int settled_prev,
+                        int settled_cur, double* trace_out) {
+  dpt_sm_decide(static_cast<dpt_sm_state*>(state), static_cast<const dpt_sm_options*>(opts), stats, j,
+                settled_prev, settled_cur, trace_out);
+}
+
+void dpt_sm_query(const void* state, int* done, int* status, int* iterations, int* final_iter, int* readoffs,
+                  int* cycle_pending, double* step_norm) {
+  const dpt_sm_state* s = static_cast<const dpt_sm_state*>(state);
+  *done = s->done;
+  *status = s->status;
+  *iterations = s->iterations;
+  *final_iter = s->final_iter;
+  *readoffs = s->readoffs;
+  *cycle_pending = s->cycle_pending;
+  *step_norm = s->step_norm;
+}
+
+}  // extern "C"
