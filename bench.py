@@ -1,0 +1,346 @@
+#!/usr/bin/env python
+"""bench.py -- DPT iteration throughput on B200 (BASELINE.json metric).
+
+Workload (N=1): BASELINE.json configs[1] -- dense unsymmetric full
+diagonalisation, n = 4096, FP64, seed 1, lambda = 0.5/sqrt(n) (SURVEY.md §8(d)
+recipe, synthetic).  Under reference semantics it terminates Diverged at k = 4,
+so, as BASELINE.md prescribes, throughput is timed over a fixed number of map
+applications (iterate_fixed semantics, dpt.hpp:94-96): one STEP = one DPT
+iteration = one fused K1 launch (P = A Delta^T GEMM + map + residual + step
+norm epilogue) + the fold/decision kernels.  Metric unit: iterations / s.
+
+  value   device-resident: inputs in HBM, CUDA events on the solver's stream
+          around exactly K steps, max over ranks.
+  e2e     the public API a user calls (paper_2002_12872_b200.iterate_full) on
+          pinned host arrays: H2D of theta + Delta, the solve to its terminal
+          status, D2H of A / eigenvalues / residuals; iterations / wall second.
+  roofline  the dense step kernel alone (events around each launch): 2 n^2 rows
+          FLOP per launch / average launch time, against the FP64 tensor-core
+          peak measured in this run (DMMA probe; MEASURED_PEAKS.json has no FP64).
+  cpu_baseline  the reference's own implementation (oracle/_ref, compiled from
+          /root/reference/proj/src) on a bounded row sample, all host threads.
+
+--impl reference times only the reference arm (rank 0; other ranks exit 0).
+N > 1 (torchrun): rows of A sharded over ranks (strong scaling of the same
+n = 4096 solve), per-iteration NCCL max-allreduce of the step statistics.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_DEFAULT = 4096
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--n", type=int, default=N_DEFAULT, help="override n (testing only)")
+    ap.add_argument("--e2e-calls", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def workload_config(n, world):
+    return {
+        "workload": f"BASELINE configs[1]: dense unsymmetric DPT full diagonalisation, n={n}, FP64, seed 1, "
+                    "theta ~ sorted U(0,n) with adjacent gaps >= 1e-3, Delta N(0,1) off-diagonal, "
+                    "lambda=0.5/sqrt(n); step = one map application (iterate_fixed semantics)",
+        "n": n,
+        "lambda": 0.5 / math.sqrt(n),
+        "flop_per_step": 2.0 * n ** 3,
+        "l2": "inputs larger than L2: A_k 128 MiB + Delta 128 MiB per step vs 126 MB L2 (no flush needed)",
+        "parallelism": f"rows of A sharded over {world} rank(s), NCCL max-allreduce per iteration" if world > 1
+        else "single GPU",
+    }
+
+
+def make_inputs(n, pinned=False):
+    from paper_2002_12872_b200 import problems as pr
+    p, o, desc = pr.config("c2", n)
+    if pinned:
+        import torch
+        d = torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
+        a = torch.empty((n, n), dtype=torch.float64, pin_memory=True).numpy()
+        d[:] = p.d
+        a[:] = p.delta
+        p.d, p.delta = d, a
+    return p, o
+
+
+# ------------------------------------------------------------------ clocks ----
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "50",
+                 "-i", str(self.device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------- reference arm ----
+def reference_sample(p, a_rows_src, threads, rows_per_thread, lam):
+    """Times the reference's own step (matmul with delta_t + map, proj/src/
+    matrix.cpp:130-143, dpt.cpp:136-144) on threads x rows_per_thread rows.
+    Returns (wall seconds, rows)."""
+    from oracle.bind import Checker
+    import ctypes
+    R = Checker("reference")
+    pr, keep = R._prob(p)
+    h = R.L.ref_prepare(ctypes.byref(pr))
+    try:
+        rows = threads * rows_per_thread
+        a = np.ascontiguousarray(a_rows_src[:rows])
+        out = np.empty_like(a)
+        n = p.d.shape[0]
+
+        def work(t):
+            r0 = t * rows_per_thread
+            R.L.ref_prepared_step_rows(h, r0, rows_per_thread, a[r0:].ctypes.data, lam, out[r0:].ctypes.data)
+
+        ths = [threading.Thread(target=work, args=(t,)) for t in range(threads)]
+        t0 = time.perf_counter()
+        for th in ths:
+            th.start()
+        for th in ths:
+            th.join()
+        return time.perf_counter() - t0, rows, out
+    finally:
+        R.L.ref_release(h)
+
+
+def first_iterate_rows(p, rows):
+    """Dense rows of A_1 = F(I) (the reference's matmul zero-skips I, so a dense
+    iterate is needed for a representative sample): A_1(i,j) = lam theta(i,j) Delta(j,i)."""
+    d, D, lam = p.d, p.delta, p.lam
+    out = np.empty((rows, d.shape[0]))
+    for i in range(rows):
+        with np.errstate(divide="ignore"):
+            g = 1.0 / (d[i] - d)
+        g[i] = 0.0
+        out[i] = (lam * g) * D[:, i]
+        out[i, i] = 1.0
+    return out
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from oracle.bind import available
+    n = args.n
+    cfg = workload_config(n, 1)
+    if not available("reference"):
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libdynspec_ref.so not built"}))
+        return 0
+    p, _ = make_inputs(n)
+    threads = os.cpu_count() or 1
+    rpt = 4
+    a_rows = first_iterate_rows(p, threads * rpt)
+    for _ in range(max(args.warmup, 0)):
+        reference_sample(p, a_rows, threads, rpt, p.lam)
+    secs = []
+    for _ in range(args.steps):
+        s, rows, _ = reference_sample(p, a_rows, threads, rpt, p.lam)
+        secs.append(s)
+    t = float(np.mean(secs))
+    it_s = (threads * rpt / n) / t
+    sample = (f"{threads * rpt} of {n} rows of one c2 iteration per step (reference matmul(A_rows, delta_t) "
+              f"+ map, complex<double> as in the reference), {threads} threads x {rpt} rows; "
+              "iterations/s = sampled fraction / wall time")
+    print(json.dumps({
+        "impl": "reference", "metric": "DPT iterations/s (dense n=4096 FP64 step)", "value": it_s,
+        "unit": "iter/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 / it_s, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64 (complex<double>)", "data": "synthetic", "config": cfg,
+        "cpu_baseline": {"value": it_s, "unit": "iter/s", "cores": threads, "kind": "reference", "sample": sample},
+        "e2e": {"value": it_s, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+    return 0
+
+
+# ------------------------------------------------------------ B200 arm ----
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+    import paper_2002_12872_b200 as P
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n = args.n
+    ctx = P.Context(local)
+    if world > 1:
+        uid = [P.Context.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx.set_comm(rank, world, uid[0])
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    p, opts = make_inputs(n)
+    stream = torch.cuda.ExternalStream(ctx.stream_ptr)
+    plan = P.Plan(p, ctx=ctx)
+    plan.begin()
+    plan.steps(max(args.warmup, 3))
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)  # let the sampler attach before the timed region
+    launches0 = ctx.launches
+    barrier()
+    ev0.record(stream)
+    plan.steps(args.steps)
+    ev1.record(stream)
+    ev1.synchronize()
+    barrier()
+    launches = ctx.launches - launches0
+    ms_total = max_over_ranks(ev0.elapsed_time(ev1))
+    clk = clocks.stop()
+    ms_per_step = ms_total / args.steps
+    value = 1e3 / ms_per_step  # whole-job iterations per second (all ranks advance the same iteration)
+
+    # roofline: the dense step kernel alone, events on its own stream
+    kernel_steps = min(args.steps, 50)
+    kms = plan.steps(kernel_steps, time_kernel=True) / kernel_steps
+    rows_local = (n + world - 1) // world
+    flop_launch = 2.0 * rows_local * n * n
+    achieved = flop_launch / (kms * 1e-3) / 1e12
+    peak = P.fp64_peak_tflops(local)
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("dense_step_n4096", {}).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    plan.close()
+
+    # e2e: the public API on pinned host arrays, solve to the terminal status
+    e2e = None
+    if rank == 0 or world > 1:
+        pe, oe = make_inputs(n, pinned=True)
+        io = P.IterationOptions(**oe)
+        r = P.iterate_full(pe, io, ctx=ctx)  # warm-up (allocator, JIT-free)
+        barrier()
+        t0 = time.perf_counter()
+        iters = 0
+        for _ in range(args.e2e_calls):
+            r = P.iterate_full(pe, io, ctx=ctx)
+            iters += r.iterations
+        barrier()
+        wall = max_over_ranks(time.perf_counter() - t0)
+        e2e = {"value": iters / wall, "unit": "iter/s",
+               "h2d_bytes_per_step": int((n * n + n) * 8 / max(r.iterations, 1)),
+               "d2h_bytes_per_step": int((n * n + 2 * n) * 8 / max(r.iterations, 1)),
+               "call": f"iterate_full(c2) from pinned host arrays -> {P.to_string(r.status)} at k={r.iterations}, "
+                       f"{wall / args.e2e_calls * 1e3:.2f} ms per call (upload, solve, download)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            from oracle.bind import available
+            if available("reference"):
+                threads = os.cpu_count() or 1
+                rpt = 8
+                a_rows = first_iterate_rows(p, threads * rpt)
+                s, rows, _ = reference_sample(p, a_rows, threads, rpt, p.lam)
+                cpu = {"value": (rows / n) / s, "unit": "iter/s", "cores": threads, "kind": "reference",
+                       "sample": f"{rows} of {n} rows of one c2 iteration (reference matmul(A_rows, delta_t) + map, "
+                                 f"complex<double>), {threads} threads; iter/s = fraction / wall"}
+        except Exception as e:  # the baseline is reported, never required
+            cpu = {"value": None, "unit": "iter/s", "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": "DPT iterations/s (dense n=4096 FP64 step)", "value": value, "unit": "iter/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (SURVEY.md §8(d) recipe, seeded)", "config": workload_config(n, world),
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "dense_step_kernel (K1)", "kernel_ms": kms,
+                         "peak_source": "FP64 DMMA probe measured in this run (MEASURED_PEAKS.json has no FP64 entry)"},
+            "e2e": e2e, "cpu_baseline": cpu, "clocks": clk, "gpu_launches": int(launches),
+            "tflops_per_step": 2.0 * n ** 3 / (ms_per_step * 1e-3) / 1e12,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

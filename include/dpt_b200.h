@@ -182,6 +182,27 @@ int dpt_step_single(dpt_ctx* ctx, const dpt_problem* p, const double* z, int64_t
 int dpt_eigenvalue_of(dpt_ctx* ctx, const dpt_problem* p, const double* z, int64_t row,
                       double lambda, double* out, int z_mem, dpt_error_info* err);
 
+/* ---- plans: a problem kept resident in HBM ------------------------------------ */
+/* For repeated calls on one perturbation (the reference's scan_domain / bench
+ * loops call the solver many times on the same Delta) and for device-resident
+ * throughput measurement.  single != 0 selects the row map for chart `row`. */
+typedef struct dpt_plan dpt_plan;
+int dpt_plan_create(dpt_ctx* ctx, const dpt_problem* p, int single, int64_t row, double lambda,
+                    dpt_plan** out, dpt_error_info* err);
+void dpt_plan_destroy(dpt_plan* plan);
+/* restart from A_0 = I (z_0 = e_row) and apply the first step */
+int dpt_plan_begin(dpt_plan* plan, dpt_error_info* err);
+/* k more applications of the map (iterate_fixed semantics); kernel_ms (may be
+ * NULL) receives the summed device time of the step kernels alone */
+int dpt_plan_steps(dpt_plan* plan, int k, double* kernel_ms, dpt_error_info* err);
+int dpt_plan_read(dpt_plan* plan, double* out, int out_mem, dpt_error_info* err);
+/* stats of the latest step: {max|A_j - A_j-1|, max|A_j|, #nonfinite, max residual of A_j-1} */
+int dpt_plan_stats(dpt_plan* plan, double* out4, dpt_error_info* err);
+
+/* Measured FP64 tensor-core (DMMA) throughput of `device` in TFLOP/s: the
+ * roofline denominator for the dense step (MEASURED_PEAKS.json has no FP64). */
+int dpt_probe_fp64_peak(int device, double* tflops, dpt_error_info* err);
+
 /* ---- host-only helpers (no GPU needed; used by CPU tests) ------------------ */
 
 /* build_theta's degeneracy policy (partition.cpp:42-81) in O(n log n):

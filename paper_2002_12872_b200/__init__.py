@@ -2,7 +2,7 @@
 solver API over hand-written sm_100a CUDA kernels (libdpt_b200.so)."""
 from .dpt import (ConvergenceReport, ConvergenceStatus, Context, CsrMatrix, DegenerateSpectrum,
                   DeviceError, DominantEigenpair, EigenIterate, IterationOptions, NoDeviceError,
-                  PartitionedProblem, ShapeError, SingleRowReport, TraceAborted, check_degenerate,
+                  PartitionedProblem, Plan, ShapeError, fp64_peak_tflops, SingleRowReport, TraceAborted, check_degenerate,
                   default_context, dominant_eigenpair, effective_window, eigenvalue_of, iterate_fixed,
                   iterate_full, iterate_ramped, iterate_single, spectral_spread, step_full, step_single,
                   to_string)

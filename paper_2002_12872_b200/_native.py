@@ -89,6 +89,13 @@ def lib() -> ctypes.CDLL:
                                       P(dpt_error_info)]
         L.dpt_eigenvalue_of.argtypes = [c_void_p, P(dpt_problem), c_void_p, I64, D, P(c_double),
                                         c_int, P(dpt_error_info)]
+        L.dpt_plan_create.argtypes = [c_void_p, P(dpt_problem), c_int, I64, D, P(c_void_p), P(dpt_error_info)]
+        L.dpt_plan_destroy.argtypes = [c_void_p]
+        L.dpt_plan_begin.argtypes = [c_void_p, P(dpt_error_info)]
+        L.dpt_plan_steps.argtypes = [c_void_p, c_int, P(c_double), P(dpt_error_info)]
+        L.dpt_plan_read.argtypes = [c_void_p, c_void_p, c_int, P(dpt_error_info)]
+        L.dpt_plan_stats.argtypes = [c_void_p, c_void_p, P(dpt_error_info)]
+        L.dpt_probe_fp64_peak.argtypes = [c_int, P(c_double), P(dpt_error_info)]
         L.dpt_check_degenerate.argtypes = [I64, c_void_p, D, P(c_int64), P(c_int64)]
         L.dpt_spectral_spread.argtypes = [I64, c_void_p]
         L.dpt_spectral_spread.restype = D

@@ -1142,3 +1142,144 @@ void dpt_sm_query(const void* state, int* done, int* status, int* iterations, in
 }
 
 }  // extern "C"
+
+// ============================================================ plans ====
+// A plan keeps a problem resident in HBM with its workspace, for repeated
+// solves / fixed-step throughput runs (the bench's device-resident `value`).
+struct dpt_plan {
+  dpt_ctx* ctx = nullptr;
+  DevProblem dp;
+  Work w;
+  Mode mode = MODE_DENSE_FULL;
+  int64_t row = 0;
+  int nslots = 2;
+  int issued = 0;
+  cudaEvent_t k0 = nullptr, k1 = nullptr;
+  ~dpt_plan() {
+    if (k0) cudaEventDestroy(k0);
+    if (k1) cudaEventDestroy(k1);
+  }
+};
+
+extern "C" {
+
+int dpt_plan_create(dpt_ctx* ctx, const dpt_problem* p, int single, int64_t row, double lambda, dpt_plan** out,
+                    dpt_error_info* err) {
+  DPT_API_BEGIN
+  Guard g(ctx);
+  validate(p, err);
+  std::unique_ptr<dpt_plan> pl(new dpt_plan());
+  pl->ctx = ctx;
+  upload(pl->dp, ctx, p, err);
+  const int64_t n = p->n;
+  if (n == 0) {
+    set_err(err, DPT_ERR_SHAPE, "plan: empty problem");
+    return DPT_ERR_SHAPE;
+  }
+  pl->mode = single ? MODE_SINGLE : (p->delta_kind == DPT_DELTA_DENSE ? MODE_DENSE_FULL : MODE_CSR_FULL);
+  pl->row = row;
+  dpt_sm_options so{};
+  so.max_iter = 1 << 30;
+  if (single) {
+    if (row < 0 || row >= n) {
+      set_err(err, DPT_ERR_SHAPE, "plan: row out of range");
+      return DPT_ERR_SHAPE;
+    }
+    make_work(pl->w, ctx, pl->dp, MODE_SINGLE, row, 1, 1, 2, 0, nullptr, nullptr, so, lambda, 1, err);
+  } else {
+    int64_t row0, rows;
+    shard_rows(ctx, n, &row0, &rows);
+    const int64_t per = (n + ctx->world - 1) / ctx->world;
+    make_work(pl->w, ctx, pl->dp, pl->mode, row0, rows, per, 2, 0, nullptr, nullptr, so, lambda, 1, err);
+  }
+  CK(cudaEventCreate(&pl->k0));
+  CK(cudaEventCreate(&pl->k1));
+  CK(cudaStreamSynchronize(ctx->stream));
+  *out = pl.release();
+  return DPT_OK;
+  DPT_API_END
+}
+
+void dpt_plan_destroy(dpt_plan* pl) {
+  if (!pl) return;
+  Guard g(pl->ctx);
+  delete pl;
+}
+
+// Restart from A_0 = I (or e_row) and run launch 1: afterwards the plan holds A_1.
+int dpt_plan_begin(dpt_plan* pl, dpt_error_info* err) {
+  DPT_API_BEGIN
+  Guard g(pl->ctx);
+  dpt_ctx* ctx = pl->ctx;
+  Work& w = pl->w;
+  cudaStream_t st = ctx->stream;
+  CK(cudaMemsetAsync(w.s.state, 0, sizeof(dpt_sm_state), st));
+  CK(cudaMemsetAsync(w.s.counter, 0, 16, st));
+  if (pl->mode == MODE_DENSE_FULL) {
+    CK(launch_dense_init(w.s, pl->dp.delta.as<double>(), pl->dp.big, st));
+    ctx->launches += 1;
+    post_step(ctx, w, dense_init_ntiles(w.s.rows, w.s.ntn), 0, err);
+  } else {
+    if (pl->mode == MODE_SINGLE)
+      CK(launch_identity(w.s, st));
+    else
+      put_identity(ctx, w, pl->dp, err);
+    step_launch(ctx, w, pl->dp, pl->mode, pl->row, err);
+    post_step(ctx, w, w.ntiles_step, 0, err);
+  }
+  pl->issued = 1;
+  return DPT_OK;
+  DPT_API_END
+}
+
+// Enqueue k more fixed steps (iterate_fixed semantics: no gates).  With
+// kernel_ms != NULL each step kernel is bracketed by CUDA events on the
+// context stream and the summed kernel time is returned (synchronises).
+int dpt_plan_steps(dpt_plan* pl, int k, double* kernel_ms, dpt_error_info* err) {
+  DPT_API_BEGIN
+  Guard g(pl->ctx);
+  dpt_ctx* ctx = pl->ctx;
+  Work& w = pl->w;
+  double tot = 0.0;
+  for (int i = 0; i < k; ++i) {
+    if (kernel_ms) CK(cudaEventRecord(pl->k0, ctx->stream));
+    step_launch(ctx, w, pl->dp, pl->mode, pl->row, err);
+    if (kernel_ms) CK(cudaEventRecord(pl->k1, ctx->stream));
+    post_step(ctx, w, w.ntiles_step, 0, err);
+    if (kernel_ms) {
+      CK(cudaEventSynchronize(pl->k1));
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, pl->k0, pl->k1));
+      tot += ms;
+    }
+  }
+  pl->issued += k;
+  if (kernel_ms) *kernel_ms = tot;
+  return DPT_OK;
+  DPT_API_END
+}
+
+// Copy the current iterate (A_issued or z_issued) out.
+int dpt_plan_read(dpt_plan* pl, double* out, int out_mem, dpt_error_info* err) {
+  DPT_API_BEGIN
+  Guard g(pl->ctx);
+  if (pl->mode == MODE_SINGLE || pl->ctx->world <= 1)
+    copy_slot_out(out, pl->w, pl->dp, pl->issued % 2, out_mem, pl->ctx->stream, err);
+  else
+    gather_rows(pl->ctx, pl->w, pl->dp, pl->issued % 2, out, out_mem, err);
+  CK(cudaStreamSynchronize(pl->ctx->stream));
+  return DPT_OK;
+  DPT_API_END
+}
+
+// Statistics of the latest launch (step, max|A|, nonfinite, max residual of the previous iterate).
+int dpt_plan_stats(dpt_plan* pl, double* out4, dpt_error_info* err) {
+  DPT_API_BEGIN
+  Guard g(pl->ctx);
+  CK(cudaMemcpyAsync(out4, pl->w.s.stats, 4 * sizeof(double), cudaMemcpyDeviceToHost, pl->ctx->stream));
+  CK(cudaStreamSynchronize(pl->ctx->stream));
+  return DPT_OK;
+  DPT_API_END
+}
+
+}  // extern "C"

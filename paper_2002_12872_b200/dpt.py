@@ -465,6 +465,66 @@ def eigenvalue_of(z, row: int, p: PartitionedProblem, lam: float, ctx: Context =
     return out.value
 
 
+class Plan:
+    """A problem kept resident in HBM with its workspace (dpt_plan_*): repeated
+    fixed-step runs of the full map (single=False) or the row map for `row`."""
+
+    def __init__(self, p: PartitionedProblem, lam: float = None, single: bool = False, row: int = 0,
+                 ctx: Context = None):
+        self.ctx = ctx or default_context()
+        self._m = _Marshal(p)
+        self.n = self._m.n
+        self.single = single
+        h, err = ctypes.c_void_p(), N.dpt_error_info()
+        _raise(N.lib().dpt_plan_create(self.ctx.handle, ctypes.byref(self._m.prob), int(single), int(row),
+                                       float(p.lam if lam is None else lam), ctypes.byref(h),
+                                       ctypes.byref(err)), err)
+        self.handle = h
+
+    def begin(self):
+        err = N.dpt_error_info()
+        _raise(N.lib().dpt_plan_begin(self.handle, ctypes.byref(err)), err)
+
+    def steps(self, k: int, time_kernel: bool = False):
+        """Enqueue k map applications; with time_kernel, return the summed step-kernel ms."""
+        err = N.dpt_error_info()
+        ms = ctypes.c_double(0.0)
+        _raise(N.lib().dpt_plan_steps(self.handle, int(k), ctypes.byref(ms) if time_kernel else None,
+                                      ctypes.byref(err)), err)
+        return ms.value if time_kernel else None
+
+    def read(self):
+        shape = (self.n,) if self.single else (self.n, self.n)
+        out = np.empty(shape)
+        err = N.dpt_error_info()
+        _raise(N.lib().dpt_plan_read(self.handle, out.ctypes.data, N.DPT_MEM_HOST, ctypes.byref(err)), err)
+        return out
+
+    def stats(self):
+        out = np.empty(4)
+        err = N.dpt_error_info()
+        _raise(N.lib().dpt_plan_stats(self.handle, out.ctypes.data, ctypes.byref(err)), err)
+        return out
+
+    def close(self):
+        if getattr(self, "handle", None):
+            N.lib().dpt_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def fp64_peak_tflops(device: int = 0) -> float:
+    """Measured DMMA (FP64 tensor core) throughput of the device, TFLOP/s."""
+    v, err = ctypes.c_double(0.0), N.dpt_error_info()
+    _raise(N.lib().dpt_probe_fp64_peak(int(device), ctypes.byref(v), ctypes.byref(err)), err)
+    return v.value
+
+
 # ------------------------------------------------------------ host helpers ----
 def check_degenerate(d, tol: float = 1e-12):
     """build_theta's degeneracy policy: None or the reference's first (i, j)."""

@@ -1,0 +1,64 @@
+"""Generates tests/golden/*.npz from the REFERENCE implementation itself
+(oracle/_ref/libdynspec_ref.so = /root/reference/proj/src compiled by
+oracle/Makefile).  Run in the build container (where /root/reference exists):
+
+    make -C oracle && python tests/golden/make_golden.py
+
+The fixtures are small (n <= 96) so they travel with the repo; the tests check
+both the C restatement and the CUDA path against them.
+"""
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+
+from oracle.bind import Checker  # noqa: E402
+from paper_2002_12872_b200 import problems as pr  # noqa: E402
+from paper_2002_12872_b200.dpt import PartitionedProblem  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def cases():
+    out = []
+    for name, n in [("c1", 48), ("c1", 96), ("c2", 64), ("c2b", 80), ("c3", 96)]:
+        p, o, _ = pr.config(name, n)
+        out.append((f"{name}_n{n}", p, o))
+    t, a = pr.random_uniform(7, 17)
+    out.append(("random_uniform_n7_lam0.03", PartitionedProblem(t, a, 0.03), {}))
+    t, a = pr.oscillator(24)
+    out.append(("oscillator_n24_lam0.5", PartitionedProblem(t, a, 0.5), {}))
+    out.append(("two_by_two_lam0.88", pr.two_by_two(0.88), {}))
+    return out
+
+
+def main():
+    R = Checker("reference")
+    for name, p, o in cases():
+        r = R.iterate_full(p, o, trace=True)
+        rec = dict(d=p.d, lam=p.lam, status=r.status, iterations=r.iterations, step_norm=r.step_norm, a=r.a,
+                   eig=r.eig, res=r.res, trace_step=r.trace_step, trace_res=r.trace_res,
+                   opts=np.array([o.get("tol", 1e-12), o.get("max_iter", 10000)]))
+        if hasattr(p.delta, "rowptr"):
+            rec.update(rowptr=p.delta.rowptr, cols=p.delta.cols, vals=p.delta.vals)
+        else:
+            rec.update(delta=p.delta)
+        a2 = R.iterate_fixed(p, 2, p.lam)[1]
+        rec.update(fixed2=a2)
+        np.savez_compressed(os.path.join(OUT, f"full_{name}.npz"), **rec)
+        print(name, r.status, r.iterations)
+    for name, n in [("c4", 2048), ("c4b", 4096)]:
+        p, o, _ = pr.config(name, n)
+        r = R.dominant_eigenpair(p, o)
+        np.savez_compressed(os.path.join(OUT, f"dominant_{name}_n{n}.npz"), d=p.d, lam=p.lam,
+                            rowptr=p.delta.rowptr, cols=p.delta.cols, vals=p.delta.vals, status=r.status,
+                            iterations=r.iterations, eigenvalue=r.eigenvalue, residual=r.residual, z=r.z,
+                            z_unit=r.z_unit, row=r.row, step_norm=r.step_norm)
+        print(name, n, r.status, r.iterations)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,65 @@
+"""Shared helpers for the parity tests."""
+import glob
+import os
+
+import numpy as np
+
+from paper_2002_12872_b200.dpt import CsrMatrix, PartitionedProblem
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+# Parity bar (BASELINE.json north_star): eigenvalues within 1e-10 relative,
+# eigenvectors within 1e-9 max-abs, iterations within +-1, same status.
+EIG_RTOL = 1e-10
+VEC_ATOL = 1e-9
+
+
+def load_full(path):
+    z = np.load(path)
+    if "delta" in z.files:
+        delta = z["delta"]
+    else:
+        delta = CsrMatrix(int(z["d"].shape[0]), z["rowptr"], z["cols"], z["vals"])
+    p = PartitionedProblem(z["d"], delta, float(z["lam"]))
+    opts = dict(tol=float(z["opts"][0]), max_iter=int(z["opts"][1]))
+    return p, opts, z
+
+
+def load_dominant(path):
+    z = np.load(path)
+    p = PartitionedProblem(z["d"], CsrMatrix(int(z["d"].shape[0]), z["rowptr"], z["cols"], z["vals"]),
+                           float(z["lam"]))
+    return p, z
+
+
+def full_fixtures():
+    return sorted(glob.glob(os.path.join(GOLDEN, "full_*.npz")))
+
+
+def dominant_fixtures():
+    return sorted(glob.glob(os.path.join(GOLDEN, "dominant_*.npz")))
+
+
+def eig_rel_err(got, want):
+    got, want = np.asarray(got), np.asarray(want)
+    fin = np.isfinite(want)
+    if not fin.any():
+        return 0.0
+    return float(np.max(np.abs(got[fin] - want[fin]) / np.maximum(1.0, np.abs(want[fin]))))
+
+
+def assert_full_parity(g, status, iterations, a, eig, res, exact_iters=False):
+    """g: paper_2002_12872_b200 ConvergenceReport; the rest from a checker."""
+    assert int(g.status) == int(status), (int(g.status), int(status))
+    if exact_iters:
+        assert g.iterations == iterations
+    else:
+        assert abs(g.iterations - iterations) <= 1, (g.iterations, iterations)
+    if int(status) == 2:  # Diverged: NaN read-offs, state carries the escaping iterate
+        assert np.all(np.isnan(g.eigenvalues)) and np.all(np.isnan(g.residuals))
+        return
+    if g.iterations == iterations:
+        assert eig_rel_err(g.eigenvalues, eig) < EIG_RTOL
+        assert float(np.max(np.abs(g.state.a - a))) < VEC_ATOL
+        ok = np.isfinite(res)
+        assert np.allclose(g.residuals[ok], res[ok], rtol=1e-3, atol=1e-13)
