@@ -283,7 +283,7 @@ def main():
     prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get("dense_step_n4096", {}).get("dram_bytes_per_launch")
+            traffic = json.load(open(prof)).get("latest:prof_dense_c2", {}).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
     plan.close()

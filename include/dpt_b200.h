@@ -162,6 +162,17 @@ int dpt_iterate_fixed(dpt_ctx* ctx, const dpt_problem* p, int k, double lambda, 
 int dpt_step_full(dpt_ctx* ctx, const dpt_problem* p, const double* a, double lambda,
                   double* out, int io_mem, dpt_error_info* err);
 
+/* step_full with the caller's GapMatrix theta (n*n row-major, zero diagonal):
+ * the reference's exact signature (dpt.hpp:56-57) passes theta, not levels;
+ * p->d is then ignored by the map. */
+int dpt_step_full_gap(dpt_ctx* ctx, const dpt_problem* p, const double* a, const double* gap,
+                      double lambda, double* out, int io_mem, dpt_error_info* err);
+
+/* Read-offs of a caller iterate: eig_i = d_i + lambda P(i,i), residual rows
+ * (residuals_of, dpt.cpp:23-44) with P = a Delta^T.  [n] outputs. */
+int dpt_readoffs(dpt_ctx* ctx, const dpt_problem* p, const double* a, double* eig_out, double* res_out,
+                 int io_mem, dpt_error_info* err);
+
 /* ---- row map -------------------------------------------------------------- */
 
 /* iterate_single (dpt.hpp:107-111). z_out [n]. */
@@ -177,6 +188,11 @@ int dpt_dominant_eigenpair(dpt_ctx* ctx, const dpt_problem* p, const dpt_options
 /* step_single (dpt.hpp:59-66): one row-map application to z [n] for chart `row`. */
 int dpt_step_single(dpt_ctx* ctx, const dpt_problem* p, const double* z, int64_t row,
                     double lambda, double* out, int io_mem, dpt_error_info* err);
+
+/* step_single with the caller's GapRow (dpt.hpp:62-63): gap_row [n], zero at `row`. */
+int dpt_step_single_gap(dpt_ctx* ctx, const dpt_problem* p, const double* z, int64_t row,
+                        const double* gap_row, double lambda, double* out, int io_mem,
+                        dpt_error_info* err);
 
 /* eigenvalue_of (dpt.hpp:68-72): d_row + lambda (Delta z)_row. */
 int dpt_eigenvalue_of(dpt_ctx* ctx, const dpt_problem* p, const double* z, int64_t row,

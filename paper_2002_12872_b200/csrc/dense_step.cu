@@ -211,7 +211,8 @@ __global__ void __launch_bounds__(C::THREADS, 1)
           if (gi == c + e) {
             v = 1.0;  // exact unit diagonal (test_dpt.cpp:45-53)
           } else {
-            const double g = 1.0 / __dsub_rn(ti, e ? tc.y : tc.x);  // IEEE division = build_theta
+            const double g = s.gapmat ? s.gapmat[size_t(il) * size_t(s.ld) + size_t(c + e)]
+                                      : 1.0 / __dsub_rn(ti, e ? tc.y : tc.x);  // IEEE division = build_theta
             v = __dmul_rn(__dmul_rn(lam_k, g), __dsub_rn(p, __dmul_rn(di, aij)));
           }
           out[e] = v;

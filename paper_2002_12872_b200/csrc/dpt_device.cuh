@@ -21,6 +21,8 @@ struct DevSolve {
   int ntn;              // column partial blocks per row (rowpart leading dim)
   double lambda;        // p.lambda (read-offs always use it, dpt.cpp:23-44)
   const double* theta;  // [n] unperturbed levels (device)
+  const double* gapmat; // optional explicit gap matrix (step_full / step_single with a caller
+                        // GapMatrix / GapRow): row-major [rows x ld] (full) or [n] (row map)
   const double* lam_table;  // [max_iter + 2] lambda_k (ramped schedule) or null
   const int* settled_table; // [max_iter + 2] settled(k) or null (=1)
   double* slots;        // nslots * rows * n, row-major per slot (row-local)

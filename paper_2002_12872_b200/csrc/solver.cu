@@ -727,9 +727,12 @@ int run_full(dpt_ctx* ctx, const dpt_problem* p, const dpt_options* opts_in, boo
   return DPT_OK;
 }
 
-// step_full (dpt.cpp:311-327): F(a) for a caller iterate.
-int run_step_full(dpt_ctx* ctx, const dpt_problem* p, const double* a, double lambda, double* out, int io_mem,
-                  dpt_error_info* err) {
+// step_full (dpt.cpp:311-327): F(a) for a caller iterate; with `gap` the
+// caller's GapMatrix (n x n, row-major) replaces theta-generated gaps.  With
+// eig_out / res_out the read-offs of `a` itself (residuals_of, dpt.cpp:23-44)
+// are returned as well (homotopy_solve's final report).
+int run_step_full(dpt_ctx* ctx, const dpt_problem* p, const double* a, const double* gap, double lambda,
+                  double* out, int io_mem, double* eig_out, double* res_out, dpt_error_info* err) {
   Guard g(ctx);
   validate(p, err);
   if (ctx->world > 1) {
@@ -738,7 +741,6 @@ int run_step_full(dpt_ctx* ctx, const dpt_problem* p, const double* a, double la
   }
   const int64_t n = p->n;
   if (n == 0) return DPT_OK;
-  std::vector<double> dh = host_levels(p, err);
   DevProblem dp;
   upload(dp, ctx, p, err);
   const Mode mode = p->delta_kind == DPT_DELTA_DENSE ? MODE_DENSE_FULL : MODE_CSR_FULL;
@@ -746,12 +748,21 @@ int run_step_full(dpt_ctx* ctx, const dpt_problem* p, const double* a, double la
   so.max_iter = 1;
   Work w;
   make_work(w, ctx, dp, mode, 0, n, n, 2, 1, nullptr, nullptr, so, lambda, 1, err);
+  DBuf gbuf;
+  if (gap) {
+    dalloc(gbuf, size_t(n) * size_t(dp.ld) * 8, err);
+    const cudaMemcpyKind k = io_mem == DPT_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    CK(cudaMemcpy2DAsync(gbuf.p, size_t(dp.ld) * 8, gap, size_t(n) * 8, size_t(n) * 8, size_t(n), k, ctx->stream));
+    w.s.gapmat = gbuf.as<double>();
+  }
   put_slot(w, dp, 0, a, io_mem, ctx->stream, err);
   DevCsr c = dp.csr();
   CK(launch_rowdot(w.s, dp.kind == DPT_DELTA_DENSE ? dp.delta.as<double>() : nullptr, dp.kind == DPT_DELTA_CSR ? &c : nullptr, ctx->stream));
   step_launch(ctx, w, dp, mode, 0, err);
   post_step(ctx, w, w.ntiles_step, 0, err);
-  copy_slot_out(out, w, dp, 1, io_mem, ctx->stream, err);
+  if (out) copy_slot_out(out, w, dp, 1, io_mem, ctx->stream, err);
+  copy_out(eig_out, w.s.eps, size_t(n), io_mem, ctx->stream, err);
+  copy_out(res_out, w.s.res, size_t(n), io_mem, ctx->stream, err);
   CK(cudaStreamSynchronize(ctx->stream));
   return DPT_OK;
 }
@@ -762,7 +773,7 @@ int run_step_full(dpt_ctx* ctx, const dpt_problem* p, const double* a, double la
 int run_single(dpt_ctx* ctx, const dpt_problem* p, int64_t row, const dpt_options* opts_in, double ramp_alpha,
                dpt_trace_fn trace, void* user, double* z_out, int out_mem, dpt_report* rep,
                const double* z_in, int z_mem, double fixed_lambda, double* eig_fixed, double* z_unit,
-               dpt_error_info* err) {
+               dpt_error_info* err, const double* gap_row = nullptr) {
   const dpt_options o = opts_or_default(opts_in);
   Guard g(ctx);
   validate(p, err);
@@ -802,6 +813,13 @@ int run_single(dpt_ctx* ctx, const dpt_problem* p, int64_t row, const dpt_option
   CK(cudaEventRecord(ctx->ev0, st));
   int final_iter = 0, status = DPT_MAX_ITERATIONS, iters = max_iter, readoffs = 1;
   double step = 0.0;
+  DBuf gbuf;
+  if (gap_row) {
+    dalloc(gbuf, size_t(n) * 8, err);
+    CK(cudaMemcpyAsync(gbuf.p, gap_row, size_t(n) * 8,
+                       z_mem == DPT_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    w.s.gapmat = gbuf.as<double>();
+  }
   if (fixed) {
     put_slot(w, dp, 0, z_in, z_mem, st, err);
     step_launch(ctx, w, dp, MODE_SINGLE, row, err);
@@ -1010,7 +1028,38 @@ int dpt_iterate_fixed(dpt_ctx* ctx, const dpt_problem* p, int k, double lambda, 
 int dpt_step_full(dpt_ctx* ctx, const dpt_problem* p, const double* a, double lambda, double* out, int io_mem,
                   dpt_error_info* err) {
   DPT_API_BEGIN
-  return run_step_full(ctx, p, a, lambda, out, io_mem, err);
+  return run_step_full(ctx, p, a, nullptr, lambda, out, io_mem, nullptr, nullptr, err);
+  DPT_API_END
+}
+
+int dpt_step_full_gap(dpt_ctx* ctx, const dpt_problem* p, const double* a, const double* gap, double lambda,
+                      double* out, int io_mem, dpt_error_info* err) {
+  DPT_API_BEGIN
+  if (!gap) {
+    set_err(err, DPT_ERR_INVALID_ARG, "step_full_gap: missing gap matrix");
+    return DPT_ERR_INVALID_ARG;
+  }
+  return run_step_full(ctx, p, a, gap, lambda, out, io_mem, nullptr, nullptr, err);
+  DPT_API_END
+}
+
+int dpt_readoffs(dpt_ctx* ctx, const dpt_problem* p, const double* a, double* eig_out, double* res_out,
+                 int io_mem, dpt_error_info* err) {
+  DPT_API_BEGIN
+  return run_step_full(ctx, p, a, nullptr, p ? p->lambda : 0.0, nullptr, io_mem, eig_out, res_out, err);
+  DPT_API_END
+}
+
+int dpt_step_single_gap(dpt_ctx* ctx, const dpt_problem* p, const double* z, int64_t row, const double* gap_row,
+                        double lambda, double* out, int io_mem, dpt_error_info* err) {
+  DPT_API_BEGIN
+  validate(p, err);
+  if (row < 0 || row >= p->n || !gap_row) {
+    set_err(err, DPT_ERR_SHAPE, "step_single: dimension mismatch");
+    return DPT_ERR_SHAPE;
+  }
+  return run_single(ctx, p, row, nullptr, 0.0, nullptr, nullptr, out, io_mem, nullptr, z, io_mem, lambda, nullptr,
+                    nullptr, err, gap_row);
   DPT_API_END
 }
 

@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(kCsrThreads) csr_step_kernel(DevSolve s, DevCs
       if (gi == j) {
         v = 1.0;
       } else {
-        const double g = 1.0 / __dsub_rn(ti[r], tj);
+        const double g = s.gapmat ? s.gapmat[size_t(il0 + r) * size_t(ld) + size_t(j)] : 1.0 / __dsub_rn(ti[r], tj);
         v = __dmul_rn(__dmul_rn(lam_k, g), __dsub_rn(p[r], __dmul_rn(di[r], aij)));
       }
       a_out[size_t(il0 + r) * size_t(ld) + size_t(j)] = v;
@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(kSingleThreads)
     if (m == row) {
       v = 1.0;
     } else {
-      const double g = 1.0 / __dsub_rn(trow, tm);  // build_gap_row, partition.cpp:83-96
+      const double g = s.gapmat ? s.gapmat[m] : 1.0 / __dsub_rn(trow, tm);  // build_gap_row, partition.cpp:83-96
       v = __dmul_rn(__dmul_rn(lam_k, g), __dsub_rn(w, __dmul_rn(wr, zm)));
     }
     zo[m] = v;

@@ -1,0 +1,126 @@
+// drive.cpp -- integration driver for the drop-in boundary.
+//
+// Written only against the reference's PUBLIC headers (dynspec/*.hpp) and
+// exercising the reference's own callers of the hot path unchanged:
+// compare_orders / truncation_agreement (src/rspt.cpp) and scan_domain /
+// bifurcation_scan (src/analysis.cpp, multi-threaded), plus every dpt.hpp
+// entry point.  tests/cpp/Makefile links it twice:
+//   drive_ref   with the reference's src/dpt.cpp       (CPU, the oracle)
+//   drive_b200  with paper_2002_12872_b200/shim/dynspec_b200.cpp + libdpt_b200.so
+// and tests/test_gpu_shim.py compares the two outputs line by line.
+#include <cmath>
+#include <complex>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "dynspec/analysis.hpp"
+#include "dynspec/dpt.hpp"
+#include "dynspec/partition.hpp"
+#include "dynspec/rspt.hpp"
+
+using namespace dynspec;
+
+static void put(const std::string& key, double v) { std::printf("%s %.17g\n", key.c_str(), v); }
+
+static void put_vec(const std::string& key, const std::vector<cdouble>& v) {
+  for (std::size_t i = 0; i < v.size(); ++i) put(key + "[" + std::to_string(i) + "]", v[i].real());
+}
+
+static void put_mat(const std::string& key, const DenseMatrix& a) {
+  for (std::size_t i = 0; i < a.rows(); ++i)
+    for (std::size_t j = 0; j < a.cols(); ++j)
+      put(key + "[" + std::to_string(i) + "," + std::to_string(j) + "]", a(i, j).real());
+}
+
+static void put_report(const std::string& key, const ConvergenceReport& r) {
+  std::printf("%s.status %s\n", key.c_str(), to_string(r.status).c_str());
+  put(key + ".iterations", r.iterations);
+  if (r.status != ConvergenceStatus::Diverged) {
+    put_vec(key + ".eig", r.eigenvalues);
+    put_mat(key + ".a", r.state.a);
+  }
+}
+
+int main() {
+  // 1. iterate_full / ramped / fixed on the reference fixtures
+  put_report("two_by_two", iterate_full(build_two_by_two(cdouble{0.3, 0.0})));
+  put_report("two_by_two_bounded", iterate_full(build_two_by_two(cdouble{0.88, 0.0})));
+  put_report("two_by_two_diverged", iterate_full(build_two_by_two(cdouble{2.0, 0.0})));
+  auto ru = build_random_uniform(9, 17);
+  ru.lambda = cdouble{0.03, 0.0};
+  put_report("random_uniform", iterate_full(ru));
+  put_report("random_uniform_ramped", iterate_ramped(ru, 0.5));
+  int traced = 0;
+  iterate_full(ru, {}, [&](int k, double, double) { traced = k; });
+  put("random_uniform.trace_last_k", traced);
+  put_mat("random_uniform.fixed3", iterate_fixed(ru, 3, cdouble{0.03, 0.0}));
+  auto osc = build_oscillator(24);
+  osc.lambda = cdouble{0.5, 0.0};
+  put_report("oscillator", iterate_full(osc));
+
+  // 2. one-step maps and read-offs with the reference's own GapMatrix / GapRow
+  const GapMatrix theta = build_theta(ru.d);
+  DenseMatrix a = DenseMatrix::identity(9);
+  for (int k = 0; k < 4; ++k) a = step_full(a, theta, ru.delta_t, ru.lambda);
+  put_mat("step_full4", a);
+  std::vector<cdouble> z(9, cdouble{});
+  z[4] = 1.0;
+  for (int k = 0; k < 4; ++k) z = step_single(z, 4, theta, ru.delta, ru.lambda);
+  put_vec("step_single4", z);
+  put_vec("step_single_gaprow", step_single(z, build_gap_row(ru.d, 4), ru.delta, ru.lambda));
+  put("eigenvalue_of", eigenvalue_of(z, 4, ru.d, ru.delta, ru.lambda).real());
+
+  // 3. row map
+  const auto sr = iterate_single(ru, 2);
+  std::printf("single.status %s\n", to_string(sr.status).c_str());
+  put("single.iterations", sr.iterations);
+  put("single.eig", sr.eigenvalue.real());
+  put_vec("single.z", sr.z);
+  const auto er = build_er_perturbed_oscillator(2000, 42, cdouble{0.01, 0.0});
+  const auto dom = dominant_eigenpair(er);
+  std::printf("dominant.status %s\n", to_string(dom.status).c_str());
+  put("dominant.row", double(dom.row));
+  put("dominant.iterations", dom.iterations);
+  put("dominant.eig", dom.eigenvalue.real());
+  put("dominant.z_unit[1999]", dom.z_unit[1999].real());
+  put("dominant.z_unit[1990]", dom.z_unit[1990].real());
+
+  // 4. the reference's own callers (src/rspt.cpp, src/analysis.cpp), unchanged
+  auto three = build_three_by_three(cdouble{1.0, 0.0});
+  const OrderComparison cmp = compare_orders(three, cdouble{0.1, 0.0}, 1e-10);
+  put("compare.k_d", cmp.k_d);
+  put("compare.k_rs", cmp.k_rs);
+  put("compare.d_converged", cmp.d_converged);
+  put("compare.rs_converged", cmp.rs_converged);
+  put("truncation_agreement", truncation_agreement(three, 4, cdouble{0.05, 0.0}));
+  ScanGrid grid;
+  grid.re_min = 0.0;
+  grid.re_max = 1.2;
+  grid.im_min = 0.0;
+  grid.im_max = 0.0;
+  grid.res_re = 13;
+  grid.res_im = 1;
+  IterationOptions sopts;
+  sopts.max_iter = 400;
+  const DomainGrid full = scan_domain(build_two_by_two(cdouble{1.0, 0.0}), grid, {}, sopts, 4);
+  for (std::size_t c = 0; c < full.classes.size(); ++c) {
+    put("scan_full.class[" + std::to_string(c) + "]", double(int(full.classes[c])));
+    put("scan_full.iters[" + std::to_string(c) + "]", full.iterations[c]);
+  }
+  ScanMode single_mode;
+  single_mode.kind = ScanMode::Kind::SingleRow;
+  single_mode.row = 1;
+  const DomainGrid sg = scan_domain(three, grid, single_mode, sopts, 3);
+  for (std::size_t c = 0; c < sg.classes.size(); ++c)
+    put("scan_single.class[" + std::to_string(c) + "]", double(int(sg.classes[c])));
+  const auto bif = bifurcation_scan(build_two_by_two(cdouble{1.0, 0.0}), 0, 1, 0.8, 0.95, 4, 200, 2);
+  for (std::size_t s = 0; s < bif.size(); ++s)
+    for (std::size_t v = 0; v < bif[s].values.size(); ++v)
+      put("bif[" + std::to_string(s) + "," + std::to_string(v) + "]", bif[s].values[v].real());
+
+  // 5. staged continuation (homotopy_solve, dpt.hpp:145-152)
+  put_report("homotopy", homotopy_solve(ru, 3));
+  std::printf("done 1\n");
+  return 0;
+}
