@@ -265,9 +265,9 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       nu = fmax(nu, red[(w * C::BM + rt) * 3 + 1]);
       de = fmax(de, red[(w * C::BM + rt) * 3 + 2]);
     }
-    s.rowpart[(size_t(0) * ntn + tn) * rows + il] = ds;
-    s.rowpart[(size_t(1) * ntn + tn) * rows + il] = nu;
-    s.rowpart[(size_t(2) * ntn + tn) * rows + il] = de;
+    s.rowpart[rp_index(0, il, tn, rows, ntn)] = ds;
+    s.rowpart[rp_index(1, il, tn, rows, ntn)] = nu;
+    s.rowpart[rp_index(2, il, tn, rows, ntn)] = de;
   }
   if (ctid == 0) {
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
@@ -339,9 +339,9 @@ __global__ void __launch_bounds__(256) dense_init_kernel(DevSolve s, const doubl
     const double v = warp_sum(dsum[r]);
     const int64_t il = il0 + ty + 8 * r;
     if (tx == 0 && il < rows) {
-      s.rowpart[(size_t(0) * s.ntn + tn) * rows + il] = v;
-      s.rowpart[(size_t(1) * s.ntn + tn) * rows + il] = 0.0;
-      s.rowpart[(size_t(2) * s.ntn + tn) * rows + il] = 0.0;
+      s.rowpart[rp_index(0, il, tn, rows, s.ntn)] = v;
+      s.rowpart[rp_index(1, il, tn, rows, s.ntn)] = 0.0;
+      s.rowpart[rp_index(2, il, tn, rows, s.ntn)] = 0.0;
     }
   }
   t_step = warp_max(t_step);

@@ -29,7 +29,7 @@ struct DevSolve {
   double* dvec[2];      // d_m(i) = P(A_m)(i,i) for local rows, m % 2
   double* eps;          // [rows] read-offs of the latest folded iterate
   double* res;          // [rows]
-  double* rowpart;      // [3][ntn][rows] (sum d, max num, max den)
+  double* rowpart;      // [3][rows][ntn] (sum d, max num, max den), see rp_index
   double* tilepart;     // [ntiles][4] (max step, max |A|, nonfinite count, spare)
   int ntiles;
   double* blockpart;    // fold partials [fold_blocks][8]
@@ -40,9 +40,16 @@ struct DevSolve {
   unsigned int* counter;  // last-block election for the folds
   double* cyclepart;    // [fold_blocks][DPT_MAX_WINDOW]
   int fixed_mode;       // iterate_fixed: no decisions, step every launch
+  int fuse_decide;      // single rank: the fold's last block also runs the decision
 };
 
 __device__ __forceinline__ int launch_index(const DevSolve& s) { return s.state->j + 1; }
+
+// rowpart layout [3][rows][ntn]: a row's column-block partials are contiguous
+// so the fold reads them coalesced.  k: 0 = sum d, 1 = max num, 2 = max den.
+__device__ __forceinline__ size_t rp_index(int k, int64_t row, int tn, int64_t rows, int ntn) {
+  return (size_t(k) * size_t(rows) + size_t(row)) * size_t(ntn) + size_t(tn);
+}
 
 __device__ __forceinline__ double lam_of(const DevSolve& s, int j) {
   return s.lam_table ? s.lam_table[j] : s.lambda;

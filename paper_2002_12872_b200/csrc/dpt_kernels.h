@@ -31,10 +31,11 @@ int csr_ntn(int64_t n);
 cudaError_t launch_csr_step(const DevSolve& s, const DevCsr& d, cudaStream_t st);
 
 // row map (single vector): z slots are [nslots][n]
-int single_ntn(int64_t n);
-int single_ntiles(int64_t n);
-cudaError_t launch_single_step(const DevSolve& s, const DevCsr& d, const double* dense, int64_t row,
-                               const double* g, cudaStream_t st);
+int single_mode(int dense, int uniform16);
+int single_ntn(int64_t n, int mode);
+int single_ntiles(int64_t n, int mode);
+cudaError_t launch_single_step(const DevSolve& s, const DevCsr& d, const double* dense, int64_t row, int mode,
+                               cudaStream_t st);
 
 // fold.cu (K4)
 int fold_blocks(int64_t rows);

@@ -22,7 +22,8 @@ constexpr int kFoldThreads = 256;
 constexpr int kFoldMaxBlocks = 296;  // 2 x 148 SMs
 
 int fold_blocks(int64_t rows) {
-  int64_t b = (rows + kFoldThreads - 1) / kFoldThreads;
+  if (rows < 32) return int(rows < 1 ? 1 : rows);  // block per row
+  int64_t b = (rows + (kFoldThreads / 32) - 1) / (kFoldThreads / 32);  // warp per row
   if (b > kFoldMaxBlocks) b = kFoldMaxBlocks;
   if (b < 1) b = 1;
   return int(b);
@@ -52,6 +53,50 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
   return r;
 }
 
+// Row fold of one row: column-block partials are summed (d) / maxed (num, den)
+// by `width` cooperating lanes in a fixed tree, so the result is deterministic.
+__device__ __forceinline__ void fold_row_store(const DevSolve& s, int64_t i, double d, double num, double den,
+                                               const double* dprev, double* dnext) {
+  const double r = num / fmax(den, 1e-300);  // kTinyDen, dpt.cpp:18, :40
+  s.eps[i] = __dadd_rn(s.theta[s.row0 + i], __dmul_rn(s.lambda, dprev[i]));
+  s.res[i] = r;
+  dnext[i] = d;
+}
+
+__device__ void decide_now(const DevSolve& s);
+
+// Sample-first part of the cycle test, run by one block right after the
+// decision: if the first entries already differ by >= tol from every window
+// entry, within_tol is false for all of them and the cycle kernel has nothing
+// to do (exact early-out, dpt.cpp:60-79).
+__device__ void cycle_sample_precheck(const DevSolve& s, double* sh) {
+  dpt_sm_state* st = s.state;
+  if (st->done || !st->cycle_pending) return;
+  const int j = st->j;
+  int npast = j - 1;
+  if (npast > s.opts.win - 1) npast = s.opts.win - 1;
+  const int64_t n = s.n, ld = s.ld;
+  const int64_t elems = s.rows * n;
+  const int64_t ns = elems < int64_t(blockDim.x) ? elems : int64_t(blockDim.x);
+  const double* cur = s.slots + size_t(j % s.nslots) * size_t(s.slot_elems);
+  int any = 0;
+  for (int p = 0; p < npast; ++p) {
+    const double* past = s.slots + size_t((j - 2 - p) % s.nslots) * size_t(s.slot_elems);
+    double m = 0.0;
+    const int64_t e = threadIdx.x;
+    if (e < ns) {
+      const int64_t r = e / n, c = e % n;
+      m = fabs(cur[r * ld + c] - past[r * ld + c]);
+    }
+    m = block_max(m, sh);
+    if (threadIdx.x == 0 && m < s.opts.tol) any = 1;
+  }
+  if (threadIdx.x == 0 && !any) {
+    st->cycle_pending = 0;  // refuted for every entry: the stats keep "not within"
+    for (int p = 0; p < DPT_MAX_WINDOW; ++p) s.stats[DPT_STATS_CYCLE0 + p] = 1.0;
+  }
+}
+
 __global__ void __launch_bounds__(kFoldThreads) fold_kernel(DevSolve s, int ntiles_this) {
   if (s.state->done) return;
   const int j = launch_index(s);
@@ -61,20 +106,44 @@ __global__ void __launch_bounds__(kFoldThreads) fold_kernel(DevSolve s, int ntil
   const int ntn = s.ntn;
   const double* dprev = s.dvec[(j - 1) & 1];
   double* dnext = s.dvec[j & 1];
+  const int lane = threadIdx.x & 31;
   double rmax = 0.0;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < rows;
-       i += int64_t(gridDim.x) * blockDim.x) {
-    double d = 0.0, num = 0.0, den = 0.0;
-    for (int tn = 0; tn < ntn; ++tn) {
-      d += s.rowpart[(size_t(0) * ntn + tn) * rows + i];
-      num = fmax(num, s.rowpart[(size_t(1) * ntn + tn) * rows + i]);
-      den = fmax(den, s.rowpart[(size_t(2) * ntn + tn) * rows + i]);
+  if (rows >= 32) {
+    // warp per row, lanes stride over the column blocks (coalesced: [rows][ntn])
+    const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+    for (int64_t i = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); i < rows; i += warps) {
+      double d = 0.0, num = 0.0, den = 0.0;
+      for (int tn = lane; tn < ntn; tn += 32) {
+        d += s.rowpart[rp_index(0, i, tn, rows, ntn)];
+        num = fmax(num, s.rowpart[rp_index(1, i, tn, rows, ntn)]);
+        den = fmax(den, s.rowpart[rp_index(2, i, tn, rows, ntn)]);
+      }
+      d = warp_sum(d);
+      num = warp_max(num);
+      den = warp_max(den);
+      if (lane == 0) {
+        fold_row_store(s, i, d, num, den, dprev, dnext);
+        rmax = fmax(rmax, s.res[i]);
+      }
     }
-    const double r = num / fmax(den, 1e-300);  // kTinyDen, dpt.cpp:18, :40
-    s.eps[i] = __dadd_rn(s.theta[s.row0 + i], __dmul_rn(s.lambda, dprev[i]));
-    s.res[i] = r;
-    dnext[i] = d;
-    rmax = fmax(rmax, r);
+  } else {
+    // few rows (the row map has one): block per row, threads over the blocks
+    for (int64_t i = blockIdx.x; i < rows; i += gridDim.x) {
+      double d = 0.0, num = 0.0, den = 0.0;
+      for (int tn = threadIdx.x; tn < ntn; tn += blockDim.x) {
+        d += s.rowpart[rp_index(0, i, tn, rows, ntn)];
+        num = fmax(num, s.rowpart[rp_index(1, i, tn, rows, ntn)]);
+        den = fmax(den, s.rowpart[rp_index(2, i, tn, rows, ntn)]);
+      }
+      d = block_sum(d, sh);
+      num = block_max(num, sh);
+      den = block_max(den, sh);
+      if (threadIdx.x == 0) {
+        fold_row_store(s, i, d, num, den, dprev, dnext);
+        rmax = fmax(rmax, s.res[i]);
+      }
+      __syncthreads();
+    }
   }
   double a0 = 0.0, a1 = 0.0, a2 = 0.0;
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < ntiles_this; t += gridDim.x * blockDim.x) {
@@ -97,7 +166,8 @@ __global__ void __launch_bounds__(kFoldThreads) fold_kernel(DevSolve s, int ntil
     last = (prev == gridDim.x - 1);
   }
   __syncthreads();
-  if (last && threadIdx.x == 0) {
+  if (!last) return;
+  if (threadIdx.x == 0) {
     __threadfence();
     double r0 = 0.0, r1 = 0.0, r2 = 0.0, r3 = 0.0;
     for (unsigned b = 0; b < gridDim.x; ++b) {
@@ -112,11 +182,15 @@ __global__ void __launch_bounds__(kFoldThreads) fold_kernel(DevSolve s, int ntil
     s.stats[2] = r2;
     s.stats[3] = r3;
     *s.counter = 0u;
+    if (s.fuse_decide) decide_now(s);  // single rank: no cross-rank max in between
+  }
+  if (s.fuse_decide) {
+    __syncthreads();
+    cycle_sample_precheck(s, sh);
   }
 }
 
-__global__ void decide_kernel(DevSolve s) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__device__ void decide_now(const DevSolve& s) {
   dpt_sm_state* st = s.state;
   if (st->done) return;
   const int j = st->j + 1;
@@ -127,6 +201,11 @@ __global__ void decide_kernel(DevSolve s) {
   const int sp = s.settled_table ? s.settled_table[j - 1] : 1;
   const int sc = s.settled_table ? s.settled_table[j] : 1;
   dpt_sm_decide(st, &s.opts, s.stats, j, sp, sc, s.trace);
+}
+
+__global__ void decide_kernel(DevSolve s) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  decide_now(s);
 }
 
 // Tests A_j (slot j % nslots) against A_{j-2-p}, p < npast.

@@ -226,6 +226,7 @@ struct DevProblem {
   DBuf theta, delta, rowptr, cols, vals;
   DBuf dmap;  // CUtensorMap for dense Delta
   bool big = true;
+  int uniform16 = 0;  // CSR with exactly 16 nonzeros per row (K3 fast path)
   DevCsr csr() const { return DevCsr{rowptr.as<int64_t>(), cols.as<int32_t>(), vals.as<double>(), nnz}; }
 };
 
@@ -282,6 +283,14 @@ void upload(DevProblem& dp, dpt_ctx* ctx, const dpt_problem* p, dpt_error_info* 
       CK(cudaMemcpy(&nnz, p->rowptr + n, 8, cudaMemcpyDeviceToHost));
     }
     dp.nnz = nnz;
+    {
+      std::vector<int64_t> rp(size_t(n + 1));
+      CK(cudaMemcpy(rp.data(), p->rowptr, size_t(n + 1) * 8,
+                    p->mem == DPT_MEM_DEVICE ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost));
+      bool u = n > 0;
+      for (int64_t i = 0; i <= n && u; ++i) u = rp[size_t(i)] == 16 * i;
+      dp.uniform16 = u ? 1 : 0;
+    }
     dalloc(dp.rowptr, size_t(n + 1) * 8, err);
     dalloc(dp.cols, size_t(nnz) * 4, err);
     dalloc(dp.vals, size_t(nnz) * 8, err);
@@ -323,6 +332,7 @@ void make_work(Work& w, dpt_ctx* ctx, DevProblem& dp, Mode mode, int64_t row0, i
   s.lambda = lambda;
   s.opts = so;
   s.fixed_mode = fixed_mode;
+  s.fuse_decide = ctx->world <= 1 ? 1 : 0;
   int ntiles_aux = 1;
   if (mode == MODE_DENSE_FULL) {
     dp.big = dp.n >= 2048;
@@ -333,8 +343,9 @@ void make_work(Work& w, dpt_ctx* ctx, DevProblem& dp, Mode mode, int64_t row0, i
     s.ntn = csr_ntn(dp.n);
     w.ntiles_step = csr_step_ntiles(rows, dp.n);
   } else {
-    s.ntn = single_ntn(dp.n);
-    w.ntiles_step = single_ntiles(dp.n);
+    const int sm = single_mode(dp.kind == DPT_DELTA_DENSE, dp.uniform16);
+    s.ntn = single_ntn(dp.n, sm);
+    w.ntiles_step = single_ntiles(dp.n, sm);
   }
   s.ntiles = std::max(w.ntiles_step, ntiles_aux);
   const size_t slot_elems = size_t(std::max<int64_t>(rows_alloc, 1)) * size_t(dp.ld);
@@ -404,7 +415,7 @@ void make_work(Work& w, dpt_ctx* ctx, DevProblem& dp, Mode mode, int64_t row0, i
       CK(cudaMemcpyAsync(dp.dmap.p, &dm, sizeof(CUtensorMap), cudaMemcpyHostToDevice, st));
     }
   }
-  CK(cudaMallocHost(reinterpret_cast<void**>(&w.h_state), sizeof(dpt_sm_state)));
+  CK(cudaMallocHost(reinterpret_cast<void**>(&w.h_state), 2 * sizeof(dpt_sm_state)));
   CK(cudaMallocHost(reinterpret_cast<void**>(&w.h_trace), size_t(w.max_trace) * 3 * 8));
 }
 
@@ -420,9 +431,12 @@ void allreduce_stats(dpt_ctx* ctx, Work& w, dpt_error_info* err) {
 // One iteration's device work after the step kernel.
 void post_step(dpt_ctx* ctx, Work& w, int ntiles, int64_t cycle_elems, dpt_error_info* err) {
   CK(launch_fold(w.s, ntiles, ctx->stream));
-  allreduce_stats(ctx, w, err);
-  CK(launch_decide(w.s, ctx->stream));
-  ctx->launches += 2;
+  ctx->launches += 1;
+  if (!w.s.fuse_decide) {  // sharded: cross-rank max of the statistics, then the decision
+    allreduce_stats(ctx, w, err);
+    CK(launch_decide(w.s, ctx->stream));
+    ctx->launches += 1;
+  }
   if (w.s.opts.win > 0 && !w.s.fixed_mode) {
     CK(launch_cycle(w.s, cycle_elems, ctx->stream));
     ctx->launches += 1;
@@ -437,12 +451,15 @@ void step_launch(dpt_ctx* ctx, Work& w, DevProblem& dp, Mode mode, int64_t row, 
     CK(launch_csr_step(w.s, dp.csr(), ctx->stream));
   else
     CK(launch_single_step(w.s, dp.csr(), dp.kind == DPT_DELTA_DENSE ? dp.delta.as<double>() : nullptr, row,
-                          nullptr, ctx->stream));
+                          single_mode(dp.kind == DPT_DELTA_DENSE, dp.uniform16), ctx->stream));
   ctx->launches += 1;
 }
 
 // Runs launches 1 .. until the state machine terminates (or `total` launches).
 // Launch 1 is the special init (dense) or the generic step from slot 0.
+// Chunks are double-buffered: chunk c+1 is enqueued before the host waits for
+// chunk c's state snapshot, so the GPU never idles on the host's decision;
+// launches queued after a terminal decision are no-ops.
 void drive(dpt_ctx* ctx, Work& w, DevProblem& dp, Mode mode, int64_t row, int total, bool first_is_init,
            dpt_trace_fn trace, void* user, dpt_error_info* err) {
   cudaStream_t st = ctx->stream;
@@ -454,19 +471,24 @@ void drive(dpt_ctx* ctx, Work& w, DevProblem& dp, Mode mode, int64_t row, int to
     post_step(ctx, w, dense_init_ntiles(w.s.rows, w.s.ntn), cycle_elems, err);
     issued = 1;
   }
-  int chunk = 4;
-  int traced = 0;
-  while (true) {
-    const int todo = std::min(chunk, total - issued);
-    for (int c = 0; c < todo; ++c) {
-      step_launch(ctx, w, dp, mode, row, err);
-      post_step(ctx, w, w.ntiles_step, cycle_elems, err);
+  dpt_sm_state* snap = w.h_state;  // [2] pinned snapshots, one per chunk in flight
+  cudaEvent_t ev[2];
+  CK(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+  struct EvGuard {
+    cudaEvent_t* e;
+    ~EvGuard() {
+      cudaEventDestroy(e[0]);
+      cudaEventDestroy(e[1]);
     }
-    issued += todo;
-    CK(cudaMemcpyAsync(w.h_state, w.s.state, sizeof(dpt_sm_state), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    if (trace && w.h_state->trace_len > traced) {
-      const int nt = w.h_state->trace_len;
+  } eg{ev};
+  int chunk = 4, traced = 0, c = 0;
+  bool pending = false;
+  auto consume = [&](int slot) {
+    CK(cudaEventSynchronize(ev[slot]));
+    const dpt_sm_state& h = snap[slot];
+    if (trace && h.trace_len > traced) {
+      const int nt = h.trace_len;
       CK(cudaMemcpy(w.h_trace, w.s.trace, size_t(nt) * 3 * 8, cudaMemcpyDeviceToHost));
       for (int q = traced; q < nt; ++q) {
         if (trace(int(w.h_trace[3 * q]), w.h_trace[3 * q + 1], w.h_trace[3 * q + 2], user) != 0) {
@@ -476,8 +498,39 @@ void drive(dpt_ctx* ctx, Work& w, DevProblem& dp, Mode mode, int64_t row, int to
       }
       traced = nt;
     }
-    if (w.h_state->done || issued >= total) break;
+    return h.done != 0;
+  };
+  bool done = false;
+  while (issued < total && !done) {
+    const int todo = std::min(chunk, total - issued);
+    for (int k = 0; k < todo; ++k) {
+      step_launch(ctx, w, dp, mode, row, err);
+      post_step(ctx, w, w.ntiles_step, cycle_elems, err);
+    }
+    issued += todo;
+    const int slot = c & 1;
+    CK(cudaMemcpyAsync(&snap[slot], w.s.state, sizeof(dpt_sm_state), cudaMemcpyDeviceToHost, st));
+    CK(cudaEventRecord(ev[slot], st));
+    if (pending) done = consume(slot ^ 1);
+    pending = true;
+    ++c;
     chunk = std::min(chunk * 2, 64);
+  }
+  if (pending && !done) done = consume((c - 1) & 1);
+  CK(cudaStreamSynchronize(st));
+  *w.h_state = snap[(c - 1) & 1];
+  // the final snapshot is authoritative (later chunks were no-ops once done)
+  if (!w.h_state->done) {
+    CK(cudaMemcpy(w.h_state, w.s.state, sizeof(dpt_sm_state), cudaMemcpyDeviceToHost));
+  }
+  if (trace && w.h_state->trace_len > traced) {
+    const int nt = w.h_state->trace_len;
+    CK(cudaMemcpy(w.h_trace, w.s.trace, size_t(nt) * 3 * 8, cudaMemcpyDeviceToHost));
+    for (int q = traced; q < nt; ++q)
+      if (trace(int(w.h_trace[3 * q]), w.h_trace[3 * q + 1], w.h_trace[3 * q + 2], user) != 0) {
+        set_err(err, DPT_ERR_TRACE, "trace sink aborted the iteration");
+        throw Fail{DPT_ERR_TRACE};
+      }
   }
 }
 

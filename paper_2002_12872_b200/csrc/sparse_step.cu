@@ -42,12 +42,62 @@ int csr_step_ntiles(int64_t rows, int64_t n) {
   return int((rows + R - 1) / R);
 }
 
+// One CSR row of Delta dotted with R rows of A, by a 16-lane group: lanes take
+// nonzeros sub, sub+16, ... (up to 64 in registers, the rest in a tail loop),
+// then an xor-shuffle tree.  The fixed lane/round order makes the value
+// identical wherever it is recomputed (this launch's P(i,j) and the next
+// launch's P(i,i) = d(i)).
+constexpr int kGroup = 16;
+constexpr int kRounds = 4;
+
+template <int R>
+struct CsrCol {
+  int32_t c[kRounds];
+  double v[kRounds];
+  int64_t pb, pe;
+};
+
+template <int R>
+__device__ __forceinline__ void csr_col_load(const DevCsr& D, int64_t j, int sub, CsrCol<R>& cc) {
+  cc.pb = __ldg(D.rowptr + j);
+  cc.pe = __ldg(D.rowptr + j + 1);
+#pragma unroll
+  for (int q = 0; q < kRounds; ++q) {
+    const int64_t idx = cc.pb + sub + kGroup * q;
+    const bool in = idx < cc.pe;
+    cc.c[q] = in ? __ldg(D.cols + idx) : 0;
+    cc.v[q] = in ? __ldg(D.vals + idx) : 0.0;
+  }
+}
+
+template <int R>
+__device__ __forceinline__ void csr_col_dot(const DevCsr& D, const CsrCol<R>& cc, int sub, const double* const* arow,
+                                            double (&p)[R]) {
+#pragma unroll
+  for (int r = 0; r < R; ++r) p[r] = 0.0;
+#pragma unroll
+  for (int q = 0; q < kRounds; ++q)
+#pragma unroll
+    for (int r = 0; r < R; ++r) p[r] = __fma_rn(cc.v[q], arow[r][cc.c[q]], p[r]);
+  for (int64_t idx = cc.pb + sub + kGroup * kRounds; idx < cc.pe; idx += kGroup) {  // long rows
+    const int32_t k = __ldg(D.cols + idx);
+    const double v = __ldg(D.vals + idx);
+#pragma unroll
+    for (int r = 0; r < R; ++r) p[r] = __fma_rn(v, arow[r][k], p[r]);
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+#pragma unroll
+    for (int o = kGroup / 2; o > 0; o >>= 1) p[r] += __shfl_xor_sync(0xffffffffu, p[r], o);
+  }
+}
+
 template <int R>
 __global__ void __launch_bounds__(kCsrThreads) csr_step_kernel(DevSolve s, DevCsr D, int use_smem) {
   if (s.state->done) return;
   const int jl = launch_index(s);
   extern __shared__ __align__(16) double sa[];  // [R][n] staged rows of A_{j-1}
-  __shared__ double red[kCsrThreads / 32][R][3];
+  __shared__ double red[kCsrThreads / 32][R][2];
   __shared__ double wred[kCsrThreads / 32][3];
   const int64_t n = s.n, ld = s.ld, rows = s.rows;
   const int64_t il0 = int64_t(blockIdx.x) * R;
@@ -62,67 +112,96 @@ __global__ void __launch_bounds__(kCsrThreads) csr_step_kernel(DevSolve s, DevCs
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const int rr = r < nr ? r : 0;
-    arow[r] = use_smem ? sa + size_t(r) * size_t(n) : a_in + size_t(il0 + rr) * size_t(ld);
+    arow[r] = use_smem ? sa + size_t(rr) * size_t(n) : a_in + size_t(il0 + rr) * size_t(ld);
   }
   if (use_smem) {
-    for (int r = 0; r < nr; ++r)
-      for (int64_t c = threadIdx.x; c < n; c += blockDim.x)
-        sa[size_t(r) * size_t(n) + size_t(c)] = a_in[size_t(il0 + r) * size_t(ld) + size_t(c)];
+    for (int r = 0; r < nr; ++r) {
+      const double2* src = reinterpret_cast<const double2*>(a_in + size_t(il0 + r) * size_t(ld));
+      double2* dst = reinterpret_cast<double2*>(sa + size_t(r) * size_t(n));
+      if ((n & 1) == 0) {
+        for (int64_t c = threadIdx.x; c < n / 2; c += blockDim.x) dst[c] = src[c];
+      } else {
+        for (int64_t c = threadIdx.x; c < n; c += blockDim.x)
+          sa[size_t(r) * size_t(n) + size_t(c)] = a_in[size_t(il0 + r) * size_t(ld) + size_t(c)];
+      }
+    }
     __syncthreads();
   }
   double ti[R], di[R], epsi[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    const int64_t gi = s.row0 + il0 + (r < nr ? r : 0);
-    ti[r] = s.theta[gi];
-    di[r] = d_in[il0 + (r < nr ? r : 0)];
+    const int rr = r < nr ? r : 0;
+    ti[r] = s.theta[s.row0 + il0 + rr];
+    di[r] = d_in[il0 + rr];
     epsi[r] = __dadd_rn(ti[r], __dmul_rn(lam, di[r]));
   }
-  double num[R], den[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) num[r] = den[r] = 0.0;
+  const int sub = threadIdx.x % kGroup;
+  double num = 0.0, den = 0.0;  // lane r < R of each group tracks row r
   double t_step = 0.0, t_max = 0.0, t_nonfin = 0.0;
 
-  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
-    double p[R];
+  auto epilogue = [&](int64_t j, const double (&p)[R]) {
+    if (sub >= nr) return;
+    const int r = sub;  // lane r finishes row r of column j
+    double pr = p[0];
 #pragma unroll
-    for (int r = 0; r < R; ++r) p[r] = 0.0;
-    const int64_t pb = D.rowptr[j], pe = D.rowptr[j + 1];
-    for (int64_t q = pb; q < pe; ++q) {
-      const int32_t k = __ldg(D.cols + q);
-      const double v = __ldg(D.vals + q);
+    for (int q = 1; q < R; ++q)
+      if (q == r) pr = p[q];
+    double tir = ti[0], dir = di[0], epr = epsi[0];
 #pragma unroll
-      for (int r = 0; r < R; ++r) p[r] = __fma_rn(v, arow[r][k], p[r]);
-    }
-    const double tj = s.theta[j];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      if (r >= nr) break;
-      const int64_t gi = s.row0 + il0 + r;
-      const double aij = arow[r][j];
-      double v;
-      if (gi == j) {
-        v = 1.0;
-      } else {
-        const double g = s.gapmat ? s.gapmat[size_t(il0 + r) * size_t(ld) + size_t(j)] : 1.0 / __dsub_rn(ti[r], tj);
-        v = __dmul_rn(__dmul_rn(lam_k, g), __dsub_rn(p[r], __dmul_rn(di[r], aij)));
+    for (int q = 1; q < R; ++q)
+      if (q == r) {
+        tir = ti[q];
+        dir = di[q];
+        epr = epsi[q];
       }
-      a_out[size_t(il0 + r) * size_t(ld) + size_t(j)] = v;
-      t_step = fmax(t_step, fabs(__dsub_rn(v, aij)));
-      t_max = fmax(t_max, fabs(v));
-      t_nonfin += isfinite(v) ? 0.0 : 1.0;
-      const double rr = __dadd_rn(__dmul_rn(__dsub_rn(tj, epsi[r]), aij), __dmul_rn(lam, p[r]));
-      num[r] = fmax(num[r], fabs(rr));
-      den[r] = fmax(den[r], fabs(aij));
+    const int64_t gi = s.row0 + il0 + r;
+    const double aij = use_smem ? sa[size_t(r) * size_t(n) + size_t(j)] : a_in[size_t(il0 + r) * size_t(ld) + size_t(j)];
+    const double tj = s.theta[j];
+    double v;
+    if (gi == j) {
+      v = 1.0;
+    } else {
+      const double g = s.gapmat ? s.gapmat[size_t(il0 + r) * size_t(ld) + size_t(j)] : 1.0 / __dsub_rn(tir, tj);
+      v = __dmul_rn(__dmul_rn(lam_k, g), __dsub_rn(pr, __dmul_rn(dir, aij)));
     }
+    a_out[size_t(il0 + r) * size_t(ld) + size_t(j)] = v;
+    t_step = fmax(t_step, fabs(__dsub_rn(v, aij)));
+    t_max = fmax(t_max, fabs(v));
+    t_nonfin += isfinite(v) ? 0.0 : 1.0;
+    const double rr = __dadd_rn(__dmul_rn(__dsub_rn(tj, epr), aij), __dmul_rn(lam, pr));
+    num = fmax(num, fabs(rr));
+    den = fmax(den, fabs(aij));
+  };
+
+  // Two columns in flight per 16-lane group (loads of both issued before the
+  // gathers).  The trip count is warp-uniform -- the group shuffles name the
+  // full warp -- and out-of-range columns are masked, not skipped.
+  const int half = (threadIdx.x & 31) / kGroup;
+  const int64_t nwarps = kCsrThreads / 32;
+  for (int64_t t = threadIdx.x >> 5; 4 * t < n; t += nwarps) {
+    const int64_t ja = 4 * t + half, jb = 4 * t + 2 + half;
+    const bool ha = ja < n, hb = jb < n;
+    CsrCol<R> ca, cb;
+    csr_col_load<R>(D, ha ? ja : n - 1, sub, ca);
+    csr_col_load<R>(D, hb ? jb : n - 1, sub, cb);
+    double pa[R], pb[R];
+    csr_col_dot<R>(D, ca, sub, arow, pa);
+    csr_col_dot<R>(D, cb, sub, arow, pb);
+    if (ha) epilogue(ja, pa);
+    if (hb) epilogue(jb, pb);
   }
+
+  // per-row maxima: lane r of every group holds row r's partial
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    const double a = warp_max(num[r]), b = warp_max(den[r]);
+    // lanes r and r + 16 of this warp carry row r
+    double a = (sub == r) ? num : 0.0, b = (sub == r) ? den : 0.0;
+    a = warp_max(a);
+    b = warp_max(b);
     if (l == 0) {
-      red[w][r][1] = a;
-      red[w][r][2] = b;
+      red[w][r][0] = a;
+      red[w][r][1] = b;
     }
   }
   t_step = warp_max(t_step);
@@ -134,22 +213,23 @@ __global__ void __launch_bounds__(kCsrThreads) csr_step_kernel(DevSolve s, DevCs
     wred[w][2] = t_nonfin;
   }
   __syncthreads();  // also orders this CTA's A' stores before the d' dots below
-  // exact d_j(i) = sum_m Delta(i,m) A_j(i,m) in CSR order (= next launch's P(i,i))
-  if (w < nr) {
+  // exact d_j(i) = P(A_j)(i,i): the same group routine on row i of Delta, A_j from global
+  if (w < nr) {  // warp-uniform; both half-warps run the same group routine
     const int64_t il = il0 + w, gi = s.row0 + il;
-    double part = 0.0;
-    // lane-serial in CSR order for bit-identity with the sequential dot above
+    CsrCol<1> cc;
+    csr_col_load<1>(D, gi, sub, cc);
+    const double* ar[1] = {a_out + size_t(il) * size_t(ld)};
+    double pd[1];
+    csr_col_dot<1>(D, cc, sub, ar, pd);
     if (l == 0) {
-      for (int64_t q = D.rowptr[gi]; q < D.rowptr[gi + 1]; ++q)
-        part = __fma_rn(D.vals[q], a_out[size_t(il) * size_t(ld) + size_t(D.cols[q])], part);
       double nu = 0.0, de = 0.0;
       for (int ww = 0; ww < kCsrThreads / 32; ++ww) {
-        nu = fmax(nu, red[ww][w][1]);
-        de = fmax(de, red[ww][w][2]);
+        nu = fmax(nu, red[ww][w][0]);
+        de = fmax(de, red[ww][w][1]);
       }
-      s.rowpart[(size_t(0)) * rows + il] = part;
-      s.rowpart[(size_t(1)) * rows + il] = nu;
-      s.rowpart[(size_t(2)) * rows + il] = de;
+      s.rowpart[rp_index(0, il, 0, rows, 1)] = pd[0];
+      s.rowpart[rp_index(1, il, 0, rows, 1)] = nu;
+      s.rowpart[rp_index(2, il, 0, rows, 1)] = de;
     }
   }
   if (threadIdx.x == 0) {
@@ -201,56 +281,78 @@ cudaError_t launch_csr_step(const DevSolve& s, const DevCsr& d, cudaStream_t st)
 }
 
 // ------------------------------------------------------------------ K3 ----
+// Row-dot "groups": G lanes cooperate on one row m of Delta.
+//   MODE 0  CSR with exactly 16 nonzeros per row (BASELINE c4): G = 4, each
+//           lane loads one int4 of columns + two double2 of values (a warp's
+//           column loads are one contiguous 512-byte span), 4 z gathers.
+//   MODE 1  general CSR: G = 1, the row in CSR order.
+//   MODE 2  dense Delta (GEMV): G = 32, lanes stride the row.
+// The lanes of a group combine with xor-shuffles, so every lane ends with the
+// bit-identical value; w[row] (needed by every block) is computed by warp 0 of
+// each block with the SAME routine, hence equals w[m = row] exactly.
 constexpr int kSingleThreads = 256;
-constexpr int kSingleRowsPerThread = 1;
+constexpr int kSingleMaxBlocks = 148 * 8;
 
-int single_ntiles(int64_t n) {
-  int64_t b = (n + kSingleThreads * kSingleRowsPerThread - 1) / (kSingleThreads * kSingleRowsPerThread);
-  return int(b < 1 ? 1 : b);
-}
-int single_ntn(int64_t n) { return single_ntiles(n); }
+template <int MODE>
+struct RowGroup {
+  static constexpr int G = MODE == 0 ? 4 : (MODE == 1 ? 1 : 32);
+};
 
-// w_row = Delta(row, :) . z, identical order in every block.
-__device__ __forceinline__ double row_dot(const DevCsr& D, const double* dense, int64_t n, int64_t ld,
-                                          int64_t row, const double* z) {
-  double s = 0.0;
-  if (dense) {
-    for (int64_t c = 0; c < n; ++c) s = __fma_rn(dense[size_t(row) * size_t(ld) + size_t(c)], z[c], s);
+template <int MODE>
+__device__ __forceinline__ double group_row_dot(const DevCsr& D, const double* __restrict__ dense, int64_t n,
+                                                int64_t ld, int64_t m, const double* __restrict__ z, int sub) {
+  double w = 0.0;
+  if constexpr (MODE == 0) {
+    const int4 c = __ldg(reinterpret_cast<const int4*>(D.cols + 16 * m) + sub);
+    const double2 v0 = __ldg(reinterpret_cast<const double2*>(D.vals + 16 * m) + 2 * sub);
+    const double2 v1 = __ldg(reinterpret_cast<const double2*>(D.vals + 16 * m) + 2 * sub + 1);
+    const double z0 = z[c.x], z1 = z[c.y], z2 = z[c.z], z3 = z[c.w];
+    w = __fma_rn(v0.x, z0, w);
+    w = __fma_rn(v0.y, z1, w);
+    w = __fma_rn(v1.x, z2, w);
+    w = __fma_rn(v1.y, z3, w);
+    w += __shfl_xor_sync(0xffffffffu, w, 1);
+    w += __shfl_xor_sync(0xffffffffu, w, 2);
+  } else if constexpr (MODE == 1) {
+    const int64_t pb = D.rowptr[m], pe = D.rowptr[m + 1];
+    for (int64_t q = pb; q < pe; ++q) w = __fma_rn(__ldg(D.vals + q), z[__ldg(D.cols + q)], w);
   } else {
-    for (int64_t q = D.rowptr[row]; q < D.rowptr[row + 1]; ++q) s = __fma_rn(D.vals[q], z[D.cols[q]], s);
+    const double* dr = dense + size_t(m) * size_t(ld);
+    for (int64_t c = sub; c < n; c += 32) w = __fma_rn(dr[c], z[c], w);
+    w = warp_sum(w);
   }
-  return s;
+  return w;
 }
 
+template <int MODE>
 __global__ void __launch_bounds__(kSingleThreads)
     single_step_kernel(DevSolve s, DevCsr D, const double* __restrict__ dense, int64_t row) {
   if (s.state->done) return;
+  constexpr int G = RowGroup<MODE>::G;
+  constexpr int ROWS_PER_ITER = kSingleThreads / G;
   const int jl = launch_index(s);
   __shared__ double wrow_s;
   __shared__ double red[kSingleThreads / 32][5];
   const int64_t n = s.n, ld = s.ld;
-  const double* z = s.slots + size_t((jl - 1) % s.nslots) * size_t(s.slot_elems);
-  double* zo = s.slots + size_t(jl % s.nslots) * size_t(s.slot_elems);
+  const double* __restrict__ z = s.slots + size_t((jl - 1) % s.nslots) * size_t(s.slot_elems);
+  double* __restrict__ zo = s.slots + size_t(jl % s.nslots) * size_t(s.slot_elems);
   const double lam_k = lam_of(s, jl), lam = s.lambda;
-  if (threadIdx.x == 0) {
-    wrow_s = row_dot(D, dense, n, ld, row, z);
-    if (blockIdx.x == 0) s.dvec[(jl - 1) & 1][0] = wrow_s;  // w[row] of z_{j-1} for the fold's eps
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int sub = threadIdx.x % G;
+  if (warp == 0) {  // one code path for the whole warp (the group shuffles name all lanes)
+    const double wr = (MODE == 1 && lane != 0) ? 0.0 : group_row_dot<MODE>(D, dense, n, ld, row, z, sub);
+    if (lane == 0) {
+      wrow_s = wr;
+      if (blockIdx.x == 0) s.dvec[(jl - 1) & 1][0] = wr;  // w[row] of z_{j-1} for the fold's eps
+    }
   }
   __syncthreads();
   const double wr = wrow_s;
   const double trow = s.theta[row];
   const double eps = __dadd_rn(trow, __dmul_rn(lam, wr));
   double num = 0.0, den = 0.0, t_step = 0.0, t_max = 0.0, t_nonfin = 0.0;
-  const int64_t m = int64_t(blockIdx.x) * kSingleThreads + threadIdx.x;
-  if (m < n) {
-    double w = 0.0;
-    if (dense) {
-      const double* dr = dense + size_t(m) * size_t(ld);
-      for (int64_t c = 0; c < n; ++c) w = __fma_rn(dr[c], z[c], w);
-    } else {
-      const int64_t pb = D.rowptr[m], pe = D.rowptr[m + 1];
-      for (int64_t q = pb; q < pe; ++q) w = __fma_rn(__ldg(D.vals + q), z[__ldg(D.cols + q)], w);
-    }
+  const int64_t stride = int64_t(gridDim.x) * ROWS_PER_ITER;
+  auto finish_row = [&](int64_t m, double w) {
     const double zm = z[m];
     const double tm = s.theta[m];
     double v;
@@ -261,25 +363,36 @@ __global__ void __launch_bounds__(kSingleThreads)
       v = __dmul_rn(__dmul_rn(lam_k, g), __dsub_rn(w, __dmul_rn(wr, zm)));
     }
     zo[m] = v;
-    t_step = fabs(__dsub_rn(v, zm));
-    t_max = fabs(v);
-    t_nonfin = isfinite(v) ? 0.0 : 1.0;
+    t_step = fmax(t_step, fabs(__dsub_rn(v, zm)));
+    t_max = fmax(t_max, fabs(v));
+    t_nonfin += isfinite(v) ? 0.0 : 1.0;
     const double r = __dadd_rn(__dmul_rn(__dsub_rn(tm, eps), zm), __dmul_rn(lam, w));
-    num = fabs(r);
-    den = fabs(zm);
+    num = fmax(num, fabs(r));
+    den = fmax(den, fabs(zm));
+  };
+  // two row groups per trip: twice the loads in flight per thread
+  for (int64_t m0 = int64_t(blockIdx.x) * ROWS_PER_ITER; m0 < n; m0 += 2 * stride) {
+    const int64_t ma = m0 + threadIdx.x / G, mb = ma + stride;
+    const bool oka = ma < n, okb = mb < n;
+    // MODE 0/2 shuffle inside the group: every lane of a warp runs the dots
+    const double wa = group_row_dot<MODE>(D, dense, n, ld, oka ? ma : n - 1, z, sub);
+    const double wb = group_row_dot<MODE>(D, dense, n, ld, okb ? mb : n - 1, z, sub);
+    if (sub == 0) {
+      if (oka) finish_row(ma, wa);
+      if (okb) finish_row(mb, wb);
+    }
   }
   num = warp_max(num);
   den = warp_max(den);
   t_step = warp_max(t_step);
   t_max = warp_max(t_max);
   t_nonfin = warp_sum(t_nonfin);
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  if (l == 0) {
-    red[w][0] = num;
-    red[w][1] = den;
-    red[w][2] = t_step;
-    red[w][3] = t_max;
-    red[w][4] = t_nonfin;
+  if (lane == 0) {
+    red[warp][0] = num;
+    red[warp][1] = den;
+    red[warp][2] = t_step;
+    red[warp][3] = t_max;
+    red[warp][4] = t_nonfin;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -292,9 +405,9 @@ __global__ void __launch_bounds__(kSingleThreads)
       a[4] += red[ww][4];
     }
     const int tn = blockIdx.x, ntn = s.ntn;
-    s.rowpart[(size_t(0) * ntn + tn)] = 0.0;
-    s.rowpart[(size_t(1) * ntn + tn)] = a[0];
-    s.rowpart[(size_t(2) * ntn + tn)] = a[1];
+    s.rowpart[rp_index(0, 0, tn, 1, ntn)] = 0.0;
+    s.rowpart[rp_index(1, 0, tn, 1, ntn)] = a[0];
+    s.rowpart[rp_index(2, 0, tn, 1, ntn)] = a[1];
     double* tp = s.tilepart + size_t(tn) * 4;
     tp[0] = a[2];
     tp[1] = a[3];
@@ -303,9 +416,25 @@ __global__ void __launch_bounds__(kSingleThreads)
   }
 }
 
-cudaError_t launch_single_step(const DevSolve& s, const DevCsr& d, const double* dense, int64_t row,
-                               const double*, cudaStream_t st) {
-  single_step_kernel<<<single_ntiles(s.n), kSingleThreads, 0, st>>>(s, d, dense, row);
+int single_mode(int dense, int uniform16) { return dense ? 2 : (uniform16 ? 0 : 1); }
+
+int single_ntiles(int64_t n, int mode) {
+  const int rows_per_iter = kSingleThreads / (mode == 0 ? 4 : (mode == 1 ? 1 : 32));
+  int64_t b = (n + rows_per_iter - 1) / rows_per_iter;
+  if (b > kSingleMaxBlocks) b = kSingleMaxBlocks;
+  return int(b < 1 ? 1 : b);
+}
+int single_ntn(int64_t n, int mode) { return single_ntiles(n, mode); }
+
+cudaError_t launch_single_step(const DevSolve& s, const DevCsr& d, const double* dense, int64_t row, int mode,
+                               cudaStream_t st) {
+  const unsigned grid = unsigned(single_ntiles(s.n, mode));
+  if (mode == 0)
+    single_step_kernel<0><<<grid, kSingleThreads, 0, st>>>(s, d, dense, row);
+  else if (mode == 1)
+    single_step_kernel<1><<<grid, kSingleThreads, 0, st>>>(s, d, dense, row);
+  else
+    single_step_kernel<2><<<grid, kSingleThreads, 0, st>>>(s, d, dense, row);
   return cudaGetLastError();
 }
 
