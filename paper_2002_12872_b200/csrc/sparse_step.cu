@@ -370,16 +370,66 @@ __global__ void __launch_bounds__(kSingleThreads)
     num = fmax(num, fabs(r));
     den = fmax(den, fabs(zm));
   };
-  // two row groups per trip: twice the loads in flight per thread
-  for (int64_t m0 = int64_t(blockIdx.x) * ROWS_PER_ITER; m0 < n; m0 += 2 * stride) {
-    const int64_t ma = m0 + threadIdx.x / G, mb = ma + stride;
-    const bool oka = ma < n, okb = mb < n;
-    // MODE 0/2 shuffle inside the group: every lane of a warp runs the dots
-    const double wa = group_row_dot<MODE>(D, dense, n, ld, oka ? ma : n - 1, z, sub);
-    const double wb = group_row_dot<MODE>(D, dense, n, ld, okb ? mb : n - 1, z, sub);
-    if (sub == 0) {
-      if (oka) finish_row(ma, wa);
-      if (okb) finish_row(mb, wb);
+  // UNROLL row groups per trip, in explicit phases (all row loads, then all z
+  // gathers, then the FMA chains) so every load of the trip is in flight
+  // together -- the step is bound by the L1/L2 sector traffic of the gathers.
+  if constexpr (MODE == 0) {
+    constexpr int U = 4;
+    for (int64_t m0 = int64_t(blockIdx.x) * ROWS_PER_ITER; m0 < n; m0 += U * stride) {
+      int4 c[U];
+      double2 v0[U], v1[U];
+      int64_t mm[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        mm[u] = m0 + u * stride + threadIdx.x / G;
+        const int64_t mc = mm[u] < n ? mm[u] : n - 1;
+        c[u] = __ldg(reinterpret_cast<const int4*>(D.cols + 16 * mc) + sub);
+        v0[u] = __ldg(reinterpret_cast<const double2*>(D.vals + 16 * mc) + 2 * sub);
+        v1[u] = __ldg(reinterpret_cast<const double2*>(D.vals + 16 * mc) + 2 * sub + 1);
+      }
+      double zg[U][4];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        zg[u][0] = z[c[u].x];
+        zg[u][1] = z[c[u].y];
+        zg[u][2] = z[c[u].z];
+        zg[u][3] = z[c[u].w];
+      }
+      double w[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {  // the same FMA order / shuffle tree as group_row_dot<0>
+        double a = 0.0;
+        a = __fma_rn(v0[u].x, zg[u][0], a);
+        a = __fma_rn(v0[u].y, zg[u][1], a);
+        a = __fma_rn(v1[u].x, zg[u][2], a);
+        a = __fma_rn(v1[u].y, zg[u][3], a);
+        w[u] = a;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) w[u] += __shfl_xor_sync(0xffffffffu, w[u], 1);
+#pragma unroll
+      for (int u = 0; u < U; ++u) w[u] += __shfl_xor_sync(0xffffffffu, w[u], 2);
+      if (sub == 0) {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (mm[u] < n) finish_row(mm[u], w[u]);
+      }
+    }
+  } else {
+    constexpr int U = 2;
+    for (int64_t m0 = int64_t(blockIdx.x) * ROWS_PER_ITER; m0 < n; m0 += U * stride) {
+      double w[U];
+      int64_t mm[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        mm[u] = m0 + u * stride + threadIdx.x / G;
+        w[u] = group_row_dot<MODE>(D, dense, n, ld, mm[u] < n ? mm[u] : n - 1, z, sub);
+      }
+      if (sub == 0) {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (mm[u] < n) finish_row(mm[u], w[u]);
+      }
     }
   }
   num = warp_max(num);
@@ -418,8 +468,12 @@ __global__ void __launch_bounds__(kSingleThreads)
 
 int single_mode(int dense, int uniform16) { return dense ? 2 : (uniform16 ? 0 : 1); }
 
+int u16_grid(int64_t n);
+cudaError_t launch_single_u16(const DevSolve& s, const DevCsr& d, int64_t row, cudaStream_t st);
+
 int single_ntiles(int64_t n, int mode) {
-  const int rows_per_iter = kSingleThreads / (mode == 0 ? 4 : (mode == 1 ? 1 : 32));
+  if (mode == 0) return u16_grid(n);
+  const int rows_per_iter = kSingleThreads / (mode == 1 ? 1 : 32);
   int64_t b = (n + rows_per_iter - 1) / rows_per_iter;
   if (b > kSingleMaxBlocks) b = kSingleMaxBlocks;
   return int(b < 1 ? 1 : b);
@@ -428,10 +482,9 @@ int single_ntn(int64_t n, int mode) { return single_ntiles(n, mode); }
 
 cudaError_t launch_single_step(const DevSolve& s, const DevCsr& d, const double* dense, int64_t row, int mode,
                                cudaStream_t st) {
+  if (mode == 0) return launch_single_u16(s, d, row, st);
   const unsigned grid = unsigned(single_ntiles(s.n, mode));
-  if (mode == 0)
-    single_step_kernel<0><<<grid, kSingleThreads, 0, st>>>(s, d, dense, row);
-  else if (mode == 1)
+  if (mode == 1)
     single_step_kernel<1><<<grid, kSingleThreads, 0, st>>>(s, d, dense, row);
   else
     single_step_kernel<2><<<grid, kSingleThreads, 0, st>>>(s, d, dense, row);
