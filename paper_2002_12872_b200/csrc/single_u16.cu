@@ -13,21 +13,51 @@
 // conflict-free.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "dpt_device.cuh"
 #include "dpt_kernels.h"
 
 namespace dpt {
 
-constexpr int kU16Rows = 256;  // rows (= threads) per trip
 constexpr int kU16Stages = 2;
-constexpr int kU16ColBytes = kU16Rows * 16 * 4;
-constexpr int kU16ValBytes = kU16Rows * 16 * 8;
-constexpr int kU16StageBytes = kU16ColBytes + kU16ValBytes;
-constexpr int kU16Smem = kU16Stages * kU16StageBytes + 64;
+template <int ROWS>
+struct U16 {
+  static constexpr int ColBytes = ROWS * 16 * 4;
+  static constexpr int ValBytes = ROWS * 16 * 8;
+  static constexpr int StageBytes = ColBytes + ValBytes;
+  static constexpr int Smem = kU16Stages * StageBytes + 64;
+};
 
-// w_m = sum_q vals[16m + q] * z[cols[16m + q]], q = 0..15 in order.
-__device__ __forceinline__ double u16_dot(const int32_t* c, const double* v, const double* __restrict__ z) {
+// Canonical order, select-based placement (no lane rotation of the dot).
+__device__ __forceinline__ double u16_dot_sel(const int4* crow, const double2* vrow, int lane,
+                                              const double* __restrict__ z) {
+  int32_t c[16];
+  double v[16];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int k = (q + lane) & 3;
+    const int4 t = crow[k];
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk)
+      if (kk == k) {
+        c[4 * kk + 0] = t.x;
+        c[4 * kk + 1] = t.y;
+        c[4 * kk + 2] = t.z;
+        c[4 * kk + 3] = t.w;
+      }
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int k = (q + lane) & 7;
+    const double2 t = vrow[k];
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk)
+      if (kk == k) {
+        v[2 * kk + 0] = t.x;
+        v[2 * kk + 1] = t.y;
+      }
+  }
   double zg[16];
 #pragma unroll
   for (int q = 0; q < 16; ++q) zg[q] = z[c[q]];
@@ -37,8 +67,51 @@ __device__ __forceinline__ double u16_dot(const int32_t* c, const double* v, con
   return w;
 }
 
-__global__ void __launch_bounds__(kU16Rows, 2)
+// Row dot in the lane-rotated chunk order used everywhere for this row:
+// chunks of 4 columns are visited in the order k = (q + rot) & 3 (rot = the
+// row's lane), which makes the shared-memory reads conflict-free.  Every
+// evaluation of a given row -- including the w[row] that each block needs --
+// uses the same rot, so the value is bit-identical.
+__device__ __forceinline__ double u16_dot_rot(const int4* crow, const double2* vrow, int rot,
+                                              const double* __restrict__ z) {
+  int4 c[4];
+  double2 va[4], vb[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int k = (q + rot) & 3;
+    c[q] = crow[k];
+    // values 4k..4k+3 are 16-byte chunks 2k, 2k+1; alternate which one is read
+    // first by (rot >> 2) & 1 so the 32 lanes spread over all 8 bank slots
+    const int f = (rot >> 2) & 1;
+    const double2 x0 = vrow[2 * k + f], x1 = vrow[2 * k + (f ^ 1)];
+    va[q] = f ? x1 : x0;
+    vb[q] = f ? x0 : x1;
+  }
+  double zg[16];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    zg[4 * q + 0] = z[c[q].x];
+    zg[4 * q + 1] = z[c[q].y];
+    zg[4 * q + 2] = z[c[q].z];
+    zg[4 * q + 3] = z[c[q].w];
+  }
+  double w = 0.0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    w = __fma_rn(va[q].x, zg[4 * q + 0], w);
+    w = __fma_rn(va[q].y, zg[4 * q + 1], w);
+    w = __fma_rn(vb[q].x, zg[4 * q + 2], w);
+    w = __fma_rn(vb[q].y, zg[4 * q + 3], w);
+  }
+  return w;
+}
+
+template <int ROWS, int MINB, bool ROT>
+__global__ void __launch_bounds__(ROWS, MINB)
     single_u16_kernel(DevSolve s, DevCsr D, int64_t row, int64_t ntrips) {
+  constexpr int kU16Rows = ROWS;
+  constexpr int kU16ColBytes = U16<ROWS>::ColBytes;
+  constexpr int kU16StageBytes = U16<ROWS>::StageBytes;
   if (s.state->done) return;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t bar[kU16Stages];
@@ -67,15 +140,10 @@ __global__ void __launch_bounds__(kU16Rows, 2)
   int64_t trip = blockIdx.x;
   if (tid == 0 && trip < ntrips) issue(trip, 0);
 
-  if (tid == 0) {  // w[row] of z_{j-1}: same order as the per-row dot
-    int32_t c[16];
-    double v[16];
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      c[q] = D.cols[16 * row + q];
-      v[q] = D.vals[16 * row + q];
-    }
-    const double wr = u16_dot(c, v, z);
+  if (tid == 0) {  // w[row] of z_{j-1}, in the rotation of the lane that owns row
+    const int4* cr = reinterpret_cast<const int4*>(D.cols + 16 * row);
+    const double2* vr = reinterpret_cast<const double2*>(D.vals + 16 * row);
+    const double wr = ROT ? u16_dot_rot(cr, vr, int(row & 31), z) : u16_dot_sel(cr, vr, int(row & 31), z);
     wrow_s = wr;
     if (blockIdx.x == 0) s.dvec[(jl - 1) & 1][0] = wr;  // for the fold's eps
   }
@@ -93,38 +161,11 @@ __global__ void __launch_bounds__(kU16Rows, 2)
     const int64_t m = trip * kU16Rows + tid;
     if (m < n) {
       const uint8_t* base = smem + st * kU16StageBytes;
-      const int4* crow = reinterpret_cast<const int4*>(base + size_t(tid) * 64);
-      const double2* vrow = reinterpret_cast<const double2*>(base + kU16ColBytes + size_t(tid) * 128);
-      int32_t c[16];
-      double v[16];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {  // rotated chunk order: conflict-free 64-byte row stride
-        const int k = (q + lane) & 3;
-        const int4 t = crow[k];
-        // place into c[4k..4k+3] without dynamic register indexing
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          if (kk == k) {
-            c[4 * kk + 0] = t.x;
-            c[4 * kk + 1] = t.y;
-            c[4 * kk + 2] = t.z;
-            c[4 * kk + 3] = t.w;
-          }
-      }
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int k = (q + lane) & 7;
-        const double2 t = vrow[k];
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          if (kk == k) {
-            v[2 * kk + 0] = t.x;
-            v[2 * kk + 1] = t.y;
-          }
-      }
-      const double w = u16_dot(c, v, z);
-      const double zm = z[m];
+      const double zm = z[m];  // issued before the gathers
       const double tm = s.theta[m];
+      const int4* cr = reinterpret_cast<const int4*>(base + size_t(tid) * 64);
+      const double2* vr = reinterpret_cast<const double2*>(base + kU16ColBytes + size_t(tid) * 128);
+      const double w = ROT ? u16_dot_rot(cr, vr, int(m & 31), z) : u16_dot_sel(cr, vr, int(m & 31), z);
       double val;
       if (m == row) {
         val = 1.0;
@@ -176,21 +217,48 @@ __global__ void __launch_bounds__(kU16Rows, 2)
   }
 }
 
+// Variant table (DPT_U16_VARIANT selects one for tuning runs; default 1: measured
+// 98 us / step on c4 vs 109 us (0), 147-160 us (128-row trips), 143 us (64-row)).
+struct U16Variant {
+  int rows, minb, rot;
+};
+static const U16Variant kU16Var[] = {{256, 2, 0}, {256, 2, 1}, {128, 4, 0}, {128, 4, 1}, {128, 6, 1}, {64, 8, 1}};
+
+static int u16_variant() {
+  const char* e = getenv("DPT_U16_VARIANT");
+  const int v = e ? atoi(e) : 1;  // 256-row trips, lane-rotated dot: fastest on B200 (tools/u16_sweep.sh)
+  return (v >= 0 && v < int(sizeof(kU16Var) / sizeof(kU16Var[0]))) ? v : 0;
+}
+
 int u16_grid(int64_t n) {
-  const int64_t trips = (n + kU16Rows - 1) / kU16Rows;
-  const int64_t g = 148 * 2;
+  const U16Variant& V = kU16Var[u16_variant()];
+  const int64_t trips = (n + V.rows - 1) / V.rows;
+  const int64_t g = 148 * V.minb;  // resident blocks
   return int(trips < g ? (trips < 1 ? 1 : trips) : g);
 }
 
-cudaError_t launch_single_u16(const DevSolve& s, const DevCsr& d, int64_t row, cudaStream_t st) {
+template <int ROWS, int MINB, bool ROT>
+static cudaError_t launch_u16(const DevSolve& s, const DevCsr& d, int64_t row, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(single_u16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kU16Smem);
+    cudaFuncSetAttribute(single_u16_kernel<ROWS, MINB, ROT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         U16<ROWS>::Smem);
     attr = true;
   }
-  const int64_t trips = (s.n + kU16Rows - 1) / kU16Rows;
-  single_u16_kernel<<<u16_grid(s.n), kU16Rows, kU16Smem, st>>>(s, d, row, trips);
+  const int64_t trips = (s.n + ROWS - 1) / ROWS;
+  single_u16_kernel<ROWS, MINB, ROT><<<u16_grid(s.n), ROWS, U16<ROWS>::Smem, st>>>(s, d, row, trips);
   return cudaGetLastError();
+}
+
+cudaError_t launch_single_u16(const DevSolve& s, const DevCsr& d, int64_t row, cudaStream_t st) {
+  switch (u16_variant()) {
+    case 1: return launch_u16<256, 2, true>(s, d, row, st);
+    case 2: return launch_u16<128, 4, false>(s, d, row, st);
+    case 3: return launch_u16<128, 4, true>(s, d, row, st);
+    case 4: return launch_u16<128, 6, true>(s, d, row, st);
+    case 5: return launch_u16<64, 8, true>(s, d, row, st);
+    default: return launch_u16<256, 2, false>(s, d, row, st);
+  }
 }
 
 }  // namespace dpt
