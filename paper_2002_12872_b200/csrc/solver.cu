@@ -19,6 +19,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <map>
 #include <cmath>
 #include <limits>
 #include <memory>
@@ -75,7 +76,68 @@ struct dpt_ctx {
   ncclComm_t comm = nullptr;
   int64_t launches = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // Caching allocator: device blocks released by a call are kept for the next
+  // call on this context (cudaMalloc / cudaFree synchronise and cost ~ms for
+  // the 100 MB-scale iterate buffers).  All work of a call is stream-ordered on
+  // `stream`, so a recycled block is never touched by stale kernels.
+  std::multimap<size_t, void*> free_blocks;
+  size_t cached = 0;
+  // pinned host snapshot buffers, kept across calls
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
 };
+
+namespace {
+thread_local dpt_ctx* t_ctx = nullptr;  // the context of the API call on this thread (set by Guard)
+
+size_t round_block(size_t bytes) {
+  const size_t g = bytes >= (size_t(1) << 20) ? (size_t(2) << 20) : 512;
+  return (bytes + g - 1) / g * g;
+}
+
+void* ctx_malloc(size_t bytes, cudaError_t* e) {
+  dpt_ctx* c = t_ctx;
+  bytes = round_block(bytes);
+  if (c) {
+    auto it = c->free_blocks.lower_bound(bytes);
+    if (it != c->free_blocks.end() && it->first <= bytes + bytes / 4) {
+      void* p = it->second;
+      c->cached -= it->first;
+      c->free_blocks.erase(it);
+      *e = cudaSuccess;
+      return p;
+    }
+  }
+  void* p = nullptr;
+  *e = cudaMalloc(&p, bytes);
+  if (*e != cudaSuccess && c && !c->free_blocks.empty()) {  // trim the cache and retry
+    cudaGetLastError();
+    for (auto& kv : c->free_blocks) cudaFree(kv.second);
+    c->free_blocks.clear();
+    c->cached = 0;
+    *e = cudaMalloc(&p, bytes);
+  }
+  return p;
+}
+
+void ctx_release(void* p, size_t bytes) {
+  dpt_ctx* c = t_ctx;
+  if (!c) {
+    cudaFree(p);
+    return;
+  }
+  bytes = round_block(bytes);
+  c->free_blocks.emplace(bytes, p);
+  c->cached += bytes;
+  const size_t limit = size_t(48) << 30;  // keep at most 48 GiB cached
+  while (c->cached > limit && !c->free_blocks.empty()) {
+    auto it = c->free_blocks.begin();
+    cudaFree(it->second);
+    c->cached -= it->first;
+    c->free_blocks.erase(it);
+  }
+}
+}  // namespace
 
 namespace {
 
@@ -115,11 +177,12 @@ bool debug_sync() {
 // RAII device buffer
 struct DBuf {
   void* p = nullptr;
+  size_t bytes = 0;
   DBuf() = default;
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
   ~DBuf() {
-    if (p) cudaFree(p);
+    if (p) ctx_release(p, bytes);
   }
   template <class T>
   T* as() const {
@@ -129,7 +192,9 @@ struct DBuf {
 
 void dalloc(DBuf& b, size_t bytes, dpt_error_info* err) {
   if (bytes == 0) bytes = 16;
-  cudaError_t e = cudaMalloc(&b.p, bytes);
+  cudaError_t e;
+  b.p = ctx_malloc(bytes, &e);
+  b.bytes = bytes;
   if (e != cudaSuccess) {
     set_err(err, DPT_ERR_CUDA, std::string("cudaMalloc(") + std::to_string(bytes) + "): " + cudaGetErrorString(e));
     throw Fail{DPT_ERR_CUDA};
@@ -309,12 +374,8 @@ struct Work {
       amaps, lam_table, settled_table;
   int ntiles_step = 0;
   int max_trace = 0;
-  dpt_sm_state* h_state = nullptr;  // pinned
+  dpt_sm_state* h_state = nullptr;  // pinned (the context's cached host buffer)
   double* h_trace = nullptr;        // pinned
-  ~Work() {
-    if (h_state) cudaFreeHost(h_state);
-    if (h_trace) cudaFreeHost(h_trace);
-  }
 };
 
 enum Mode { MODE_DENSE_FULL, MODE_CSR_FULL, MODE_SINGLE };
@@ -415,8 +476,18 @@ void make_work(Work& w, dpt_ctx* ctx, DevProblem& dp, Mode mode, int64_t row0, i
       CK(cudaMemcpyAsync(dp.dmap.p, &dm, sizeof(CUtensorMap), cudaMemcpyHostToDevice, st));
     }
   }
-  CK(cudaMallocHost(reinterpret_cast<void**>(&w.h_state), 2 * sizeof(dpt_sm_state)));
-  CK(cudaMallocHost(reinterpret_cast<void**>(&w.h_trace), size_t(w.max_trace) * 3 * 8));
+  {
+    const size_t need = 2 * sizeof(dpt_sm_state) + 64 + size_t(w.max_trace) * 3 * 8;
+    if (ctx->pinned_bytes < need) {
+      if (ctx->pinned) cudaFreeHost(ctx->pinned);
+      ctx->pinned = nullptr;
+      ctx->pinned_bytes = 0;
+      CK(cudaMallocHost(&ctx->pinned, need));
+      ctx->pinned_bytes = need;
+    }
+    w.h_state = static_cast<dpt_sm_state*>(ctx->pinned);
+    w.h_trace = reinterpret_cast<double*>(static_cast<char*>(ctx->pinned) + 2 * sizeof(dpt_sm_state) + 64);
+  }
 }
 
 void allreduce_stats(dpt_ctx* ctx, Work& w, dpt_error_info* err) {
@@ -564,12 +635,15 @@ void fill_nan(double* dst, size_t count, int out_mem, cudaStream_t st, dpt_error
 
 struct Guard {
   dpt_ctx* ctx;
+  dpt_ctx* prev_ctx;
   int old = -1;
-  explicit Guard(dpt_ctx* c) : ctx(c) {
+  explicit Guard(dpt_ctx* c) : ctx(c), prev_ctx(t_ctx) {
     cudaGetDevice(&old);
     cudaSetDevice(c->device);
+    t_ctx = c;
   }
   ~Guard() {
+    t_ctx = prev_ctx;
     if (old >= 0) cudaSetDevice(old);
   }
 };
@@ -994,6 +1068,10 @@ void dpt_ctx_destroy(dpt_ctx* ctx) {
   {
     Guard g(ctx);
     if (ctx->comm && nccl_api() && nccl_api()->comm_destroy) nccl_api()->comm_destroy(ctx->comm);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    for (auto& kv : ctx->free_blocks) cudaFree(kv.second);
+    ctx->free_blocks.clear();
+    if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);

@@ -302,7 +302,17 @@ class _Marshal:
             prob.delta = _ptr(delta)
         self.prob = prob
 
-    def out(self, *shape):
+    def out(self, *shape, given=None):
+        if given is not None:  # caller-provided output (e.g. pinned host memory)
+            if tuple(given.shape) != tuple(shape):
+                raise ShapeError("output buffer has the wrong shape")
+            if _is_torch(given):
+                if not given.is_contiguous() or str(given.dtype) != "torch.float64":
+                    raise ValueError("output tensor must be contiguous float64")
+            elif not (given.dtype == np.float64 and given.flags["C_CONTIGUOUS"]):
+                raise ValueError("output array must be C-contiguous float64")
+            self.keep.append(given)
+            return given, _ptr(given)
         if self.device:
             import torch
             t = torch.empty(shape, dtype=torch.float64, device=self.keep[0].device)
@@ -350,13 +360,14 @@ def _opts(o: Optional[IterationOptions]) -> N.dpt_options:
 
 
 # ------------------------------------------------------------------ API ----
-def _full(p, opts, trace, ramped, alpha, ctx):
+def _full(p, opts, trace, ramped, alpha, ctx, out=None):
     ctx = ctx or default_context()
     m = _Marshal(p)
     n = m.n
-    a, ap = m.out(n, n)
-    eig, ep = m.out(n)
-    res, rp = m.out(n)
+    oa, oe, orr = out if out is not None else (None, None, None)
+    a, ap = m.out(n, n, given=oa)
+    eig, ep = m.out(n, given=oe)
+    res, rp = m.out(n, given=orr)
     rep, err = N.dpt_report(), N.dpt_error_info()
     cb, box = _trace_cb(trace)
     o = _opts(opts)
@@ -374,9 +385,10 @@ def _full(p, opts, trace, ramped, alpha, ctx):
 
 
 def iterate_full(p: PartitionedProblem, opts: Optional[IterationOptions] = None,
-                 trace: Optional[Callable[[int, float, float], None]] = None, ctx: Context = None):
-    """Fixed-point iteration of the full map from A = I (dpt.hpp:74-83)."""
-    return _full(p, opts, trace, False, 0.0, ctx)
+                 trace: Optional[Callable[[int, float, float], None]] = None, ctx: Context = None, out=None):
+    """Fixed-point iteration of the full map from A = I (dpt.hpp:74-83).
+    out=(a, eigenvalues, residuals) writes into caller buffers (e.g. pinned)."""
+    return _full(p, opts, trace, False, 0.0, ctx, out)
 
 
 def iterate_ramped(p: PartitionedProblem, alpha: float, opts: Optional[IterationOptions] = None,
