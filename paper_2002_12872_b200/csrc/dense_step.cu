@@ -28,15 +28,16 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "dpt_device.cuh"
 #include "dpt_kernels.h"
 
 namespace dpt {
 
-template <int BM_, int BN_, int WARPS_M_, int WARPS_N_>
+template <int BM_, int BN_, int WARPS_M_, int WARPS_N_, int MINB_ = 1>
 struct DenseCfg {
-  static constexpr int BM = BM_, BN = BN_, WARPS_M = WARPS_M_, WARPS_N = WARPS_N_;
+  static constexpr int BM = BM_, BN = BN_, WARPS_M = WARPS_M_, WARPS_N = WARPS_N_, MINB = MINB_;
   static constexpr int BK = 16;  // 16 doubles = 128 B rows = one swizzle span
   static constexpr int STAGES = 4;
   static constexpr int NCW = WARPS_M * WARPS_N;  // consumer warps
@@ -49,8 +50,10 @@ struct DenseCfg {
   static constexpr int SMEM = STAGES * STAGE_BYTES + RED_BYTES + 2 * STAGES * 8 + 1024;
 };
 
-using CfgBig = DenseCfg<128, 128, 2, 4>;
-using CfgSmall = DenseCfg<64, 64, 2, 2>;
+using CfgBig = DenseCfg<128, 128, 2, 4>;      // cfg 1: one CTA per SM
+using CfgSmall = DenseCfg<64, 64, 2, 2, 3>;   // cfg 0: n < 2048 (enough CTAs for 148 SMs), 3 CTAs/SM
+using CfgMid = DenseCfg<128, 64, 4, 2, 2>;    // cfg 2: two CTAs per SM -> one CTA's epilogue
+                                              //        overlaps the other's DMMA mainloop
 
 // Byte offset of 16-byte chunk `chunk` of row `r` in a SWIZZLE_128B TMA box
 // with 128-byte rows.
@@ -59,7 +62,7 @@ __device__ __forceinline__ uint32_t swz(int r, int chunk) {
 }
 
 template <class C>
-__global__ void __launch_bounds__(C::THREADS, 1)
+__global__ void __launch_bounds__(C::THREADS, C::MINB)
     dense_step_kernel(DevSolve s, const CUtensorMap* __restrict__ amaps,
                       const CUtensorMap* __restrict__ dmap, const double* __restrict__ delta,
                       int ntm) {
@@ -134,17 +137,17 @@ __global__ void __launch_bounds__(C::THREADS, 1)
       // the same for every fragment of this lane: per-fragment addresses differ
       // by immediates (x * 1024 bytes).
       const uint32_t cofs = uint32_t(((4 * q + t) ^ gq) << 4) + uint32_t(gq) * 128u;
-      const uint8_t* pa = a_st + wm * C::WTM * 128 + cofs;
-      const uint8_t* pb = b_st + wn * C::WTN * 128 + cofs;
+      const uint32_t pa = smem_u32(a_st) + uint32_t(wm * C::WTM * 128) + cofs;
+      const uint32_t pb = smem_u32(b_st) + uint32_t(wn * C::WTN * 128) + cofs;
       // B fragments for both k4-steps of this 16-byte chunk stay live; A
       // fragments stream through (keeps the 64-double accumulator + operands
       // within the register budget).
       double2 bf[C::NB];
 #pragma unroll
-      for (int b = 0; b < C::NB; ++b) bf[b] = *reinterpret_cast<const double2*>(pb + b * 1024);
+      for (int b = 0; b < C::NB; ++b) bf[b] = lds128(pb + b * 1024);
 #pragma unroll
       for (int a = 0; a < C::MB; ++a) {
-        const double2 af = *reinterpret_cast<const double2*>(pa + a * 1024);
+        const double2 af = lds128(pa + a * 1024);
 #pragma unroll
         for (int b = 0; b < C::NB; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], af.x, bf[b].x);
 #pragma unroll
@@ -398,46 +401,57 @@ int make_tmap_rowmajor(CUtensorMap* out, const double* base, int64_t dim0, int64
   return r == CUDA_SUCCESS ? 0 : int(r);
 }
 
-int dense_tile_n(int big) { return big ? CfgBig::BN : CfgSmall::BN; }
-int dense_tile_m(int big) { return big ? CfgBig::BM : CfgSmall::BM; }
+template <class C>
+static int tile_n() { return C::BN; }
 
-cudaError_t launch_dense_step(const DevSolve& s, const CUtensorMap* amaps, const CUtensorMap* dmap,
-                              const double* delta, int big, cudaStream_t st) {
-  if (big) {
-    using C = CfgBig;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(dense_step_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-      attr = true;
-    }
-    const int ntm = int((s.rows + C::BM - 1) / C::BM);
-    dense_step_kernel<C><<<ntm * s.ntn, C::THREADS, C::SMEM, st>>>(s, amaps, dmap, delta, ntm);
-  } else {
-    using C = CfgSmall;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(dense_step_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-      attr = true;
-    }
-    const int ntm = int((s.rows + C::BM - 1) / C::BM);
-    dense_step_kernel<C><<<ntm * s.ntn, C::THREADS, C::SMEM, st>>>(s, amaps, dmap, delta, ntm);
+int dense_tile_n(int cfg) { return cfg == 0 ? CfgSmall::BN : (cfg == 1 ? CfgBig::BN : CfgMid::BN); }
+int dense_tile_m(int cfg) { return cfg == 0 ? CfgSmall::BM : (cfg == 1 ? CfgBig::BM : CfgMid::BM); }
+
+// Tile configuration for a problem size: 64x64 below n = 2048 (enough CTAs to
+// fill 148 SMs), otherwise 128x64 with two CTAs per SM (c2 n = 4096: 3.93 ms /
+// 94.3 % of the DMMA peak vs 4.21 ms / 87.8 % for 128x128 with one CTA per SM,
+// whose epilogue leaves the tensor pipe idle).  DPT_DENSE_CFG=1 forces 128x128.
+int dense_cfg_for(int64_t n) {
+  if (n < 2048) return 0;
+  const char* e = getenv("DPT_DENSE_CFG");
+  const int v = e ? atoi(e) : 2;
+  return (v == 1 || v == 2) ? v : 2;
+}
+
+template <class C>
+static cudaError_t launch_cfg(const DevSolve& s, const CUtensorMap* amaps, const CUtensorMap* dmap,
+                             const double* delta, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(dense_step_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    attr = true;
   }
+  const int ntm = int((s.rows + C::BM - 1) / C::BM);
+  dense_step_kernel<C><<<ntm * s.ntn, C::THREADS, C::SMEM, st>>>(s, amaps, dmap, delta, ntm);
   return cudaGetLastError();
 }
 
-int dense_step_ntiles(int64_t rows, int ntn, int big) {
-  const int bm = big ? CfgBig::BM : CfgSmall::BM;
+cudaError_t launch_dense_step(const DevSolve& s, const CUtensorMap* amaps, const CUtensorMap* dmap,
+                              const double* delta, int cfg, cudaStream_t st) {
+  if (cfg == 0) return launch_cfg<CfgSmall>(s, amaps, dmap, delta, st);
+  if (cfg == 2) return launch_cfg<CfgMid>(s, amaps, dmap, delta, st);
+  return launch_cfg<CfgBig>(s, amaps, dmap, delta, st);
+}
+
+int dense_step_ntiles(int64_t rows, int ntn, int cfg) {
+  const int bm = dense_tile_m(cfg);
   return int((rows + bm - 1) / bm) * ntn;
 }
 
 int dense_init_ntiles(int64_t rows, int ntn) { return int((rows + 31) / 32) * ntn; }
 
-cudaError_t launch_dense_init(const DevSolve& s, const double* delta, int big, cudaStream_t st) {
+cudaError_t launch_dense_init(const DevSolve& s, const double* delta, int cfg, cudaStream_t st) {
   dim3 grid(s.ntn, unsigned((s.rows + 31) / 32));
-  if (big)
-    dense_init_kernel<CfgBig::BN><<<grid, 256, 0, st>>>(s, delta);
+  const int bn = dense_tile_n(cfg);
+  if (bn == 128)
+    dense_init_kernel<128><<<grid, 256, 0, st>>>(s, delta);
   else
-    dense_init_kernel<CfgSmall::BN><<<grid, 256, 0, st>>>(s, delta);
+    dense_init_kernel<64><<<grid, 256, 0, st>>>(s, delta);
   return cudaGetLastError();
 }
 

@@ -113,6 +113,14 @@ __device__ __forceinline__ void prefetch_tmap(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];\n" ::"l"(tmap) : "memory");
 }
 
+// 16-byte shared-memory load from a 32-bit shared address (LDS.128, not a
+// generic LD that must resolve the address space at run time).
+__device__ __forceinline__ double2 lds128(uint32_t addr) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  return v;
+}
+
 // D(8x8) += A(8x4, row) * B(4x8, col), FP64 tensor core (SASS DMMA.8x8x4).
 // Fragments: a = A[lane>>2][lane&3], b = B[lane&3][lane>>2],
 // d = {D[lane>>2][2(lane&3)], D[lane>>2][2(lane&3)+1]}.

@@ -11,13 +11,14 @@ namespace dpt {
 // dense_step.cu (K1)
 int make_tmap_rowmajor(CUtensorMap* out, const double* base, int64_t dim0, int64_t dim1, int64_t ld,
                        int box1);
-int dense_tile_n(int big);
-int dense_tile_m(int big);
-int dense_step_ntiles(int64_t rows, int ntn, int big);
+int dense_cfg_for(int64_t n);
+int dense_tile_n(int cfg);
+int dense_tile_m(int cfg);
+int dense_step_ntiles(int64_t rows, int ntn, int cfg);
 int dense_init_ntiles(int64_t rows, int ntn);
 cudaError_t launch_dense_step(const DevSolve& s, const CUtensorMap* amaps, const CUtensorMap* dmap,
-                              const double* delta, int big, cudaStream_t st);
-cudaError_t launch_dense_init(const DevSolve& s, const double* delta, int big, cudaStream_t st);
+                              const double* delta, int cfg, cudaStream_t st);
+cudaError_t launch_dense_init(const DevSolve& s, const double* delta, int cfg, cudaStream_t st);
 
 // sparse_step.cu (K2: CSR full map; K3: CSR / dense row map)
 struct DevCsr {

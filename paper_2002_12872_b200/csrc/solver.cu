@@ -290,7 +290,7 @@ struct DevProblem {
   std::vector<double> d_host;  // theta on the host (gap policy)
   DBuf theta, delta, rowptr, cols, vals;
   DBuf dmap;  // CUtensorMap for dense Delta
-  bool big = true;
+  int big = 1;  // dense tile configuration (dense_cfg_for)
   int uniform16 = 0;  // CSR with exactly 16 nonzeros per row (K3 fast path)
   DevCsr csr() const { return DevCsr{rowptr.as<int64_t>(), cols.as<int32_t>(), vals.as<double>(), nnz}; }
 };
@@ -396,7 +396,7 @@ void make_work(Work& w, dpt_ctx* ctx, DevProblem& dp, Mode mode, int64_t row0, i
   s.fuse_decide = ctx->world <= 1 ? 1 : 0;
   int ntiles_aux = 1;
   if (mode == MODE_DENSE_FULL) {
-    dp.big = dp.n >= 2048;
+    dp.big = dense_cfg_for(dp.n);
     s.ntn = int((dp.n + dense_tile_n(dp.big) - 1) / dense_tile_n(dp.big));
     w.ntiles_step = dense_step_ntiles(rows, s.ntn, dp.big);
     ntiles_aux = dense_init_ntiles(rows, s.ntn);
