@@ -393,7 +393,7 @@ void make_work(Work& w, dpt_ctx* ctx, DevProblem& dp, Mode mode, int64_t row0, i
   s.lambda = lambda;
   s.opts = so;
   s.fixed_mode = fixed_mode;
-  s.fuse_decide = ctx->world <= 1 ? 1 : 0;
+  s.fuse_decide = ctx->comm ? 0 : 1;  // with a communicator the stats are max-allreduced first
   int ntiles_aux = 1;
   if (mode == MODE_DENSE_FULL) {
     dp.big = dense_cfg_for(dp.n);
@@ -491,7 +491,7 @@ void make_work(Work& w, dpt_ctx* ctx, DevProblem& dp, Mode mode, int64_t row0, i
 }
 
 void allreduce_stats(dpt_ctx* ctx, Work& w, dpt_error_info* err) {
-  if (ctx->world <= 1) return;
+  if (!ctx->comm) return;
   NcclApi* api = nccl_api();
   if (!api || api->all_reduce(w.s.stats, w.s.stats, DPT_NSTATS, kNcclFloat64, kNcclMax, ctx->comm, ctx->stream) != 0) {
     set_err(err, DPT_ERR_NCCL, "ncclAllReduce(max) of the iteration statistics failed");
@@ -683,7 +683,7 @@ void gather_rows(dpt_ctx* ctx, const Work& w, const DevProblem& dp, int slot, do
                  dpt_error_info* err) {
   if (!dst) return;
   cudaStream_t st = ctx->stream;
-  if (ctx->world <= 1) {
+  if (!ctx->comm) {
     copy_slot_out(dst, w, dp, slot, out_mem, st, err);
     return;
   }
@@ -837,7 +837,7 @@ int run_full(dpt_ctx* ctx, const dpt_problem* p, const dpt_options* opts_in, boo
   if (n > 0) {
     gather_rows(ctx, w, dp, final_iter % nslots, a_out, out_mem, err);
     if (readoffs) {
-      if (ctx->world > 1) {
+      if (ctx->comm) {
         gather_vec(ctx, w, w.s.eps, eig_out, out_mem, n, err);
         gather_vec(ctx, w, w.s.res, res_out, out_mem, n, err);
       } else {
@@ -862,7 +862,7 @@ int run_step_full(dpt_ctx* ctx, const dpt_problem* p, const double* a, const dou
                   double* out, int io_mem, double* eig_out, double* res_out, dpt_error_info* err) {
   Guard g(ctx);
   validate(p, err);
-  if (ctx->world > 1) {
+  if (ctx->comm) {
     set_err(err, DPT_ERR_UNSUPPORTED, "step_full is a single-device call");
     throw Fail{DPT_ERR_UNSUPPORTED};
   }
@@ -1098,13 +1098,17 @@ int dpt_nccl_unique_id(void* out, size_t bytes, dpt_error_info* err) {
 
 int dpt_ctx_set_comm(dpt_ctx* ctx, int rank, int world, const void* id, size_t bytes, dpt_error_info* err) {
   DPT_API_BEGIN
-  if (world <= 1) {
-    ctx->rank = 0;
-    ctx->world = 1;
-    return DPT_OK;
-  }
   NcclApi* api = nccl_api();
-  if (!api || bytes < sizeof(ncclUniqueId) || rank < 0 || rank >= world) {
+  if (ctx->comm && api && api->comm_destroy) {
+    api->comm_destroy(ctx->comm);
+    ctx->comm = nullptr;
+  }
+  ctx->rank = 0;
+  ctx->world = 1;
+  if (world <= 1 && !id) return DPT_OK;  // single device, no collectives
+  // world == 1 with an id builds a 1-rank communicator: the sharded code path
+  // (allreduce between fold and decision, allgather of the result) on one GPU.
+  if (!api || bytes < sizeof(ncclUniqueId) || rank < 0 || rank >= world || !id) {
     set_err(err, DPT_ERR_NCCL, "bad communicator arguments or libnccl.so.2 missing");
     return DPT_ERR_NCCL;
   }
@@ -1112,6 +1116,7 @@ int dpt_ctx_set_comm(dpt_ctx* ctx, int rank, int world, const void* id, size_t b
   ncclUniqueId uid;
   memcpy(&uid, id, sizeof(uid));
   if (api->comm_init_rank(&ctx->comm, world, uid, rank) != 0) {
+    ctx->comm = nullptr;
     set_err(err, DPT_ERR_NCCL, "ncclCommInitRank failed");
     return DPT_ERR_NCCL;
   }
@@ -1443,7 +1448,7 @@ int dpt_plan_steps(dpt_plan* pl, int k, double* kernel_ms, dpt_error_info* err) 
 int dpt_plan_read(dpt_plan* pl, double* out, int out_mem, dpt_error_info* err) {
   DPT_API_BEGIN
   Guard g(pl->ctx);
-  if (pl->mode == MODE_SINGLE || pl->ctx->world <= 1)
+  if (pl->mode == MODE_SINGLE || !pl->ctx->comm)
     copy_slot_out(out, pl->w, pl->dp, pl->issued % 2, out_mem, pl->ctx->stream, err);
   else
     gather_rows(pl->ctx, pl->w, pl->dp, pl->issued % 2, out, out_mem, err);
