@@ -27,9 +27,19 @@ struct DevCsr {
   const double* vals;     // [nnz]
   int64_t nnz;
 };
+// SELL-32 image of Delta for K2 (built by build_sell in solver.cu)
+struct DevSell {
+  const int32_t* cols;      // [padded]
+  const double* vals;       // [padded]
+  const int64_t* slice_off; // [nslices + 1], multiples of 32
+  const int32_t* lane_col;  // [nslices * 32] row of Delta (output column j) per lane, -1 = padding
+  const int32_t* lane_len;  // [nslices * 32]
+  const int64_t* pos_of;    // [n] lane index of row j
+  int64_t nslices;
+};
 int csr_step_ntiles(int64_t rows, int64_t n);
 int csr_ntn(int64_t n);
-cudaError_t launch_csr_step(const DevSolve& s, const DevCsr& d, cudaStream_t st);
+cudaError_t launch_csr_step(const DevSolve& s, const DevSell& d, cudaStream_t st);
 
 // row map (single vector): z slots are [nslots][n]
 int single_mode(int dense, int uniform16);

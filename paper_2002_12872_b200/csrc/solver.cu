@@ -292,8 +292,78 @@ struct DevProblem {
   DBuf dmap;  // CUtensorMap for dense Delta
   int big = 1;  // dense tile configuration (dense_cfg_for)
   int uniform16 = 0;  // CSR with exactly 16 nonzeros per row (K3 fast path)
+  DBuf s_cols, s_vals, s_off, s_lcol, s_llen, s_pos;  // SELL-32 image (K2)
+  int64_t nslices = 0;
   DevCsr csr() const { return DevCsr{rowptr.as<int64_t>(), cols.as<int32_t>(), vals.as<double>(), nnz}; }
+  DevSell sell() const {
+    return DevSell{s_cols.as<int32_t>(), s_vals.as<double>(), s_off.as<int64_t>(), s_lcol.as<int32_t>(),
+                   s_llen.as<int32_t>(), s_pos.as<int64_t>(), nslices};
+  }
 };
+
+// SELL-32 image of a CSR matrix for K2: rows sorted by length (descending,
+// stable) inside windows of 256, grouped 32 per slice, entry q of lane L at
+// slice_off + 32 q + L; padding entries hold column 0 / value 0 and are skipped
+// by the kernel (lane_len).  Within a lane the entries keep CSR order.
+void build_sell(DevProblem& dp, const std::vector<int64_t>& rp, const std::vector<int32_t>& cl,
+                const std::vector<double>& vl, cudaStream_t st, dpt_error_info* err) {
+  const int64_t n = dp.n;
+  const int64_t ns = (n + 31) / 32;
+  std::vector<int64_t> perm(size_t(ns * 32), -1);
+  for (int64_t w0 = 0; w0 < n; w0 += 256) {
+    const int64_t w1 = std::min(n, w0 + 256);
+    std::vector<int64_t> idx(size_t(w1 - w0));
+    std::iota(idx.begin(), idx.end(), w0);
+    std::stable_sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) {
+      return (rp[size_t(a) + 1] - rp[size_t(a)]) > (rp[size_t(b) + 1] - rp[size_t(b)]);
+    });
+    for (size_t q = 0; q < idx.size(); ++q) perm[size_t(w0) + q] = idx[q];
+  }
+  std::vector<int64_t> off(size_t(ns + 1), 0);
+  std::vector<int32_t> lcol(size_t(ns * 32), -1), llen(size_t(ns * 32), 0);
+  std::vector<int64_t> pos(size_t(n), 0);
+  for (int64_t sl = 0; sl < ns; ++sl) {
+    int64_t width = 0;
+    for (int L = 0; L < 32; ++L) {
+      const int64_t t = sl * 32 + L;
+      const int64_t j = perm[size_t(t)];
+      if (j < 0) continue;
+      const int64_t len = rp[size_t(j) + 1] - rp[size_t(j)];
+      lcol[size_t(t)] = int32_t(j);
+      llen[size_t(t)] = int32_t(len);
+      pos[size_t(j)] = t;
+      width = std::max(width, len);
+    }
+    off[size_t(sl) + 1] = off[size_t(sl)] + 32 * width;
+  }
+  const int64_t total = off[size_t(ns)];
+  std::vector<int32_t> sc(size_t(std::max<int64_t>(total, 1)), 0);
+  std::vector<double> sv(size_t(std::max<int64_t>(total, 1)), 0.0);
+  for (int64_t t = 0; t < ns * 32; ++t) {
+    const int32_t j = lcol[size_t(t)];
+    if (j < 0) continue;
+    const int64_t sl = t / 32, L = t % 32;
+    for (int64_t q = 0; q < llen[size_t(t)]; ++q) {
+      const int64_t src = rp[size_t(j)] + q, dst = off[size_t(sl)] + 32 * q + L;
+      sc[size_t(dst)] = cl[size_t(src)];
+      sv[size_t(dst)] = vl[size_t(src)];
+    }
+  }
+  dp.nslices = ns;
+  dalloc(dp.s_cols, sc.size() * 4, err);
+  dalloc(dp.s_vals, sv.size() * 8, err);
+  dalloc(dp.s_off, off.size() * 8, err);
+  dalloc(dp.s_lcol, lcol.size() * 4, err);
+  dalloc(dp.s_llen, llen.size() * 4, err);
+  dalloc(dp.s_pos, pos.size() * 8 + 8, err);
+  CK(cudaMemcpyAsync(dp.s_cols.p, sc.data(), sc.size() * 4, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dp.s_vals.p, sv.data(), sv.size() * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dp.s_off.p, off.data(), off.size() * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dp.s_lcol.p, lcol.data(), lcol.size() * 4, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dp.s_llen.p, llen.data(), llen.size() * 4, cudaMemcpyHostToDevice, st));
+  if (n) CK(cudaMemcpyAsync(dp.s_pos.p, pos.data(), pos.size() * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaStreamSynchronize(st));  // host vectors go out of scope
+}
 
 void validate(const dpt_problem* p, dpt_error_info* err) {
   if (!p || p->n < 0) {
@@ -320,7 +390,7 @@ void validate(const dpt_problem* p, dpt_error_info* err) {
   }
 }
 
-void upload(DevProblem& dp, dpt_ctx* ctx, const dpt_problem* p, dpt_error_info* err) {
+void upload(DevProblem& dp, dpt_ctx* ctx, const dpt_problem* p, dpt_error_info* err, bool sell = false) {
   validate(p, err);
   const int64_t n = p->n;
   dp.n = n;
@@ -349,12 +419,21 @@ void upload(DevProblem& dp, dpt_ctx* ctx, const dpt_problem* p, dpt_error_info* 
     }
     dp.nnz = nnz;
     {
+      const cudaMemcpyKind hk = p->mem == DPT_MEM_DEVICE ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost;
       std::vector<int64_t> rp(size_t(n + 1));
-      CK(cudaMemcpy(rp.data(), p->rowptr, size_t(n + 1) * 8,
-                    p->mem == DPT_MEM_DEVICE ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost));
+      CK(cudaMemcpy(rp.data(), p->rowptr, size_t(n + 1) * 8, hk));
       bool u = n > 0;
       for (int64_t i = 0; i <= n && u; ++i) u = rp[size_t(i)] == 16 * i;
       dp.uniform16 = u ? 1 : 0;
+      if (sell) {
+        std::vector<int32_t> cl(static_cast<size_t>(nnz));
+        std::vector<double> vl(static_cast<size_t>(nnz));
+        if (nnz) {
+          CK(cudaMemcpy(cl.data(), p->cols, size_t(nnz) * 4, hk));
+          CK(cudaMemcpy(vl.data(), p->vals, size_t(nnz) * 8, hk));
+        }
+        build_sell(dp, rp, cl, vl, st, err);
+      }
     }
     dalloc(dp.rowptr, size_t(n + 1) * 8, err);
     dalloc(dp.cols, size_t(nnz) * 4, err);
@@ -519,7 +598,7 @@ void step_launch(dpt_ctx* ctx, Work& w, DevProblem& dp, Mode mode, int64_t row, 
     CK(launch_dense_step(w.s, w.amaps.as<CUtensorMap>(), dp.dmap.as<CUtensorMap>(), dp.delta.as<double>(),
                          dp.big, ctx->stream));
   else if (mode == MODE_CSR_FULL)
-    CK(launch_csr_step(w.s, dp.csr(), ctx->stream));
+    CK(launch_csr_step(w.s, dp.sell(), ctx->stream));
   else
     CK(launch_single_step(w.s, dp.csr(), dp.kind == DPT_DELTA_DENSE ? dp.delta.as<double>() : nullptr, row,
                           single_mode(dp.kind == DPT_DELTA_DENSE, dp.uniform16), ctx->stream));
@@ -765,7 +844,7 @@ int run_full(dpt_ctx* ctx, const dpt_problem* p, const dpt_options* opts_in, boo
   // iterate_fixed builds theta with the default tolerance (dpt.cpp:383)
   if (find_degenerate(n, dh.data(), fixed ? 1e-12 : o.degeneracy_tol, &bi, &bj)) degenerate_error(err, bi, bj, dh.data());
   DevProblem dp;
-  upload(dp, ctx, p, err);
+  upload(dp, ctx, p, err, p->delta_kind == DPT_DELTA_CSR);
   const Mode mode = p->delta_kind == DPT_DELTA_DENSE ? MODE_DENSE_FULL : MODE_CSR_FULL;
   const int win = fixed ? 0 : effective_window(o.cycle_window, n);
   const int nslots = win > 0 ? win + 1 : 2;
@@ -869,7 +948,7 @@ int run_step_full(dpt_ctx* ctx, const dpt_problem* p, const double* a, const dou
   const int64_t n = p->n;
   if (n == 0) return DPT_OK;
   DevProblem dp;
-  upload(dp, ctx, p, err);
+  upload(dp, ctx, p, err, p->delta_kind == DPT_DELTA_CSR);
   const Mode mode = p->delta_kind == DPT_DELTA_DENSE ? MODE_DENSE_FULL : MODE_CSR_FULL;
   dpt_sm_options so{};
   so.max_iter = 1;
@@ -1355,7 +1434,7 @@ int dpt_plan_create(dpt_ctx* ctx, const dpt_problem* p, int single, int64_t row,
   validate(p, err);
   std::unique_ptr<dpt_plan> pl(new dpt_plan());
   pl->ctx = ctx;
-  upload(pl->dp, ctx, p, err);
+  upload(pl->dp, ctx, p, err, !single && p->delta_kind == DPT_DELTA_CSR);
   const int64_t n = p->n;
   if (n == 0) {
     set_err(err, DPT_ERR_SHAPE, "plan: empty problem");

@@ -42,58 +42,17 @@ int csr_step_ntiles(int64_t rows, int64_t n) {
   return int((rows + R - 1) / R);
 }
 
-// One CSR row of Delta dotted with R rows of A, by a 16-lane group: lanes take
-// nonzeros sub, sub+16, ... (up to 64 in registers, the rest in a tail loop),
-// then an xor-shuffle tree.  The fixed lane/round order makes the value
-// identical wherever it is recomputed (this launch's P(i,j) and the next
-// launch's P(i,i) = d(i)).
-constexpr int kGroup = 16;
-constexpr int kRounds = 4;
-
+// K2 works on a SELL-32 image of Delta built once per problem on the host
+// (build_sell in solver.cu): rows of Delta are grouped 32 to a slice (after a
+// by-length sort inside windows of 256 rows, so slices have little padding),
+// and entry q of slice lane L is stored at slice_off + 32 q + L.  A warp then
+// takes one slice, lane L owns one output column j of P (one row of Delta):
+// every column / value load is one coalesced 128 / 256-byte access, the dot
+// P(i, j) = sum_q val * A(i, col) accumulates sequentially in CSR order in one
+// lane (no shuffle trees), and the same sequence recomputes P(i,i) for the
+// next launch's diagonal, bit-identically.
 template <int R>
-struct CsrCol {
-  int32_t c[kRounds];
-  double v[kRounds];
-  int64_t pb, pe;
-};
-
-template <int R>
-__device__ __forceinline__ void csr_col_load(const DevCsr& D, int64_t j, int sub, CsrCol<R>& cc) {
-  cc.pb = __ldg(D.rowptr + j);
-  cc.pe = __ldg(D.rowptr + j + 1);
-#pragma unroll
-  for (int q = 0; q < kRounds; ++q) {
-    const int64_t idx = cc.pb + sub + kGroup * q;
-    const bool in = idx < cc.pe;
-    cc.c[q] = in ? __ldg(D.cols + idx) : 0;
-    cc.v[q] = in ? __ldg(D.vals + idx) : 0.0;
-  }
-}
-
-template <int R>
-__device__ __forceinline__ void csr_col_dot(const DevCsr& D, const CsrCol<R>& cc, int sub, const double* const* arow,
-                                            double (&p)[R]) {
-#pragma unroll
-  for (int r = 0; r < R; ++r) p[r] = 0.0;
-#pragma unroll
-  for (int q = 0; q < kRounds; ++q)
-#pragma unroll
-    for (int r = 0; r < R; ++r) p[r] = __fma_rn(cc.v[q], arow[r][cc.c[q]], p[r]);
-  for (int64_t idx = cc.pb + sub + kGroup * kRounds; idx < cc.pe; idx += kGroup) {  // long rows
-    const int32_t k = __ldg(D.cols + idx);
-    const double v = __ldg(D.vals + idx);
-#pragma unroll
-    for (int r = 0; r < R; ++r) p[r] = __fma_rn(v, arow[r][k], p[r]);
-  }
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-#pragma unroll
-    for (int o = kGroup / 2; o > 0; o >>= 1) p[r] += __shfl_xor_sync(0xffffffffu, p[r], o);
-  }
-}
-
-template <int R>
-__global__ void __launch_bounds__(kCsrThreads) csr_step_kernel(DevSolve s, DevCsr D, int use_smem) {
+__global__ void __launch_bounds__(kCsrThreads) csr_step_kernel(DevSolve s, DevSell S, int use_smem) {
   if (s.state->done) return;
   const int jl = launch_index(s);
   extern __shared__ __align__(16) double sa[];  // [R][n] staged rows of A_{j-1}
@@ -116,9 +75,9 @@ __global__ void __launch_bounds__(kCsrThreads) csr_step_kernel(DevSolve s, DevCs
   }
   if (use_smem) {
     for (int r = 0; r < nr; ++r) {
-      const double2* src = reinterpret_cast<const double2*>(a_in + size_t(il0 + r) * size_t(ld));
-      double2* dst = reinterpret_cast<double2*>(sa + size_t(r) * size_t(n));
       if ((n & 1) == 0) {
+        const double2* src = reinterpret_cast<const double2*>(a_in + size_t(il0 + r) * size_t(ld));
+        double2* dst = reinterpret_cast<double2*>(sa + size_t(r) * size_t(n));
         for (int64_t c = threadIdx.x; c < n / 2; c += blockDim.x) dst[c] = src[c];
       } else {
         for (int64_t c = threadIdx.x; c < n; c += blockDim.x)
@@ -135,106 +94,115 @@ __global__ void __launch_bounds__(kCsrThreads) csr_step_kernel(DevSolve s, DevCs
     di[r] = d_in[il0 + rr];
     epsi[r] = __dadd_rn(ti[r], __dmul_rn(lam, di[r]));
   }
-  const int sub = threadIdx.x % kGroup;
-  double num = 0.0, den = 0.0;  // lane r < R of each group tracks row r
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  constexpr int NW = kCsrThreads / 32;
+  double num[R], den[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) num[r] = den[r] = 0.0;
   double t_step = 0.0, t_max = 0.0, t_nonfin = 0.0;
 
-  auto epilogue = [&](int64_t j, const double (&p)[R]) {
-    if (sub >= nr) return;
-    const int r = sub;  // lane r finishes row r of column j
-    double pr = p[0];
+  for (int64_t sl = warp; sl < S.nslices; sl += NW) {
+    const int64_t t = sl * 32 + lane;
+    const int32_t j = S.lane_col[t];
+    const int32_t len = S.lane_len[t];
+    const int64_t off = S.slice_off[sl];
+    const int32_t width = int32_t((S.slice_off[sl + 1] - off) >> 5);
+    const int32_t* __restrict__ sc = S.cols + off + lane;
+    const double* __restrict__ sv = S.vals + off + lane;
+    double p[R];
 #pragma unroll
-    for (int q = 1; q < R; ++q)
-      if (q == r) pr = p[q];
-    double tir = ti[0], dir = di[0], epr = epsi[0];
+    for (int r = 0; r < R; ++r) p[r] = 0.0;
+    constexpr int U = 4;  // entries in flight per lane
+    for (int32_t q0 = 0; q0 < width; q0 += U) {
+      int32_t c[U];
+      double v[U];
 #pragma unroll
-    for (int q = 1; q < R; ++q)
-      if (q == r) {
-        tir = ti[q];
-        dir = di[q];
-        epr = epsi[q];
+      for (int u = 0; u < U; ++u) {
+        const bool in = q0 + u < width;
+        c[u] = in ? __ldg(sc + size_t(q0 + u) * 32) : 0;
+        v[u] = in ? __ldg(sv + size_t(q0 + u) * 32) : 0.0;
       }
-    const int64_t gi = s.row0 + il0 + r;
-    const double aij = use_smem ? sa[size_t(r) * size_t(n) + size_t(j)] : a_in[size_t(il0 + r) * size_t(ld) + size_t(j)];
-    const double tj = s.theta[j];
-    double v;
-    if (gi == j) {
-      v = 1.0;
-    } else {
-      const double g = s.gapmat ? s.gapmat[size_t(il0 + r) * size_t(ld) + size_t(j)] : 1.0 / __dsub_rn(tir, tj);
-      v = __dmul_rn(__dmul_rn(lam_k, g), __dsub_rn(pr, __dmul_rn(dir, aij)));
+      double g[U][R];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int r = 0; r < R; ++r) g[u][r] = arow[r][c[u]];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (q0 + u < len) {
+#pragma unroll
+          for (int r = 0; r < R; ++r) p[r] = __fma_rn(v[u], g[u][r], p[r]);
+        }
     }
-    a_out[size_t(il0 + r) * size_t(ld) + size_t(j)] = v;
-    t_step = fmax(t_step, fabs(__dsub_rn(v, aij)));
-    t_max = fmax(t_max, fabs(v));
-    t_nonfin += isfinite(v) ? 0.0 : 1.0;
-    const double rr = __dadd_rn(__dmul_rn(__dsub_rn(tj, epr), aij), __dmul_rn(lam, pr));
-    num = fmax(num, fabs(rr));
-    den = fmax(den, fabs(aij));
-  };
-
-  // Two columns in flight per 16-lane group (loads of both issued before the
-  // gathers).  The trip count is warp-uniform -- the group shuffles name the
-  // full warp -- and out-of-range columns are masked, not skipped.
-  const int half = (threadIdx.x & 31) / kGroup;
-  const int64_t nwarps = kCsrThreads / 32;
-  for (int64_t t = threadIdx.x >> 5; 4 * t < n; t += nwarps) {
-    const int64_t ja = 4 * t + half, jb = 4 * t + 2 + half;
-    const bool ha = ja < n, hb = jb < n;
-    CsrCol<R> ca, cb;
-    csr_col_load<R>(D, ha ? ja : n - 1, sub, ca);
-    csr_col_load<R>(D, hb ? jb : n - 1, sub, cb);
-    double pa[R], pb[R];
-    csr_col_dot<R>(D, ca, sub, arow, pa);
-    csr_col_dot<R>(D, cb, sub, arow, pb);
-    if (ha) epilogue(ja, pa);
-    if (hb) epilogue(jb, pb);
+    if (j >= 0) {
+      const double tj = s.theta[j];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (r >= nr) break;
+        const int64_t gi = s.row0 + il0 + r;
+        const double aij = arow[r][j];
+        double val;
+        if (gi == j) {
+          val = 1.0;
+        } else {
+          const double gg = s.gapmat ? s.gapmat[size_t(il0 + r) * size_t(ld) + size_t(j)] : 1.0 / __dsub_rn(ti[r], tj);
+          val = __dmul_rn(__dmul_rn(lam_k, gg), __dsub_rn(p[r], __dmul_rn(di[r], aij)));
+        }
+        a_out[size_t(il0 + r) * size_t(ld) + size_t(j)] = val;
+        t_step = fmax(t_step, fabs(__dsub_rn(val, aij)));
+        t_max = fmax(t_max, fabs(val));
+        t_nonfin += isfinite(val) ? 0.0 : 1.0;
+        const double rr = __dadd_rn(__dmul_rn(__dsub_rn(tj, epsi[r]), aij), __dmul_rn(lam, p[r]));
+        num[r] = fmax(num[r], fabs(rr));
+        den[r] = fmax(den[r], fabs(aij));
+      }
+    }
   }
 
-  // per-row maxima: lane r of every group holds row r's partial
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    // lanes r and r + 16 of this warp carry row r
-    double a = (sub == r) ? num : 0.0, b = (sub == r) ? den : 0.0;
-    a = warp_max(a);
-    b = warp_max(b);
-    if (l == 0) {
-      red[w][r][0] = a;
-      red[w][r][1] = b;
+    const double a = warp_max(num[r]), b = warp_max(den[r]);
+    if (lane == 0) {
+      red[warp][r][0] = a;
+      red[warp][r][1] = b;
     }
   }
   t_step = warp_max(t_step);
   t_max = warp_max(t_max);
   t_nonfin = warp_sum(t_nonfin);
-  if (l == 0) {
-    wred[w][0] = t_step;
-    wred[w][1] = t_max;
-    wred[w][2] = t_nonfin;
+  if (lane == 0) {
+    wred[warp][0] = t_step;
+    wred[warp][1] = t_max;
+    wred[warp][2] = t_nonfin;
   }
   __syncthreads();  // also orders this CTA's A' stores before the d' dots below
-  // exact d_j(i) = P(A_j)(i,i): the same group routine on row i of Delta, A_j from global
-  if (w < nr) {  // warp-uniform; both half-warps run the same group routine
-    const int64_t il = il0 + w, gi = s.row0 + il;
-    CsrCol<1> cc;
-    csr_col_load<1>(D, gi, sub, cc);
-    const double* ar[1] = {a_out + size_t(il) * size_t(ld)};
-    double pd[1];
-    csr_col_dot<1>(D, cc, sub, ar, pd);
-    if (l == 0) {
-      double nu = 0.0, de = 0.0;
-      for (int ww = 0; ww < kCsrThreads / 32; ++ww) {
-        nu = fmax(nu, red[ww][w][0]);
-        de = fmax(de, red[ww][w][1]);
-      }
-      s.rowpart[rp_index(0, il, 0, rows, 1)] = pd[0];
-      s.rowpart[rp_index(1, il, 0, rows, 1)] = nu;
-      s.rowpart[rp_index(2, il, 0, rows, 1)] = de;
+  // exact d_j(i) = P(A_j)(i,i): row i of Delta in its SELL lane, same sequence
+  if (threadIdx.x < nr) {
+    const int r = threadIdx.x;
+    const int64_t il = il0 + r, gi = s.row0 + il;
+    const int64_t t = S.pos_of[gi];
+    const int64_t sl = t >> 5;
+    const int L = int(t & 31);
+    const int32_t len = S.lane_len[t];
+    const int64_t off = S.slice_off[sl];
+    const double* arow_new = a_out + size_t(il) * size_t(ld);
+    double part = 0.0;
+    for (int32_t q = 0; q < len; ++q) {
+      const int64_t idx = off + int64_t(q) * 32 + L;
+      part = __fma_rn(S.vals[idx], arow_new[S.cols[idx]], part);
     }
+    double nu = 0.0, de = 0.0;
+    for (int ww = 0; ww < NW; ++ww) {
+      nu = fmax(nu, red[ww][r][0]);
+      de = fmax(de, red[ww][r][1]);
+    }
+    s.rowpart[rp_index(0, il, 0, rows, 1)] = part;
+    s.rowpart[rp_index(1, il, 0, rows, 1)] = nu;
+    s.rowpart[rp_index(2, il, 0, rows, 1)] = de;
   }
   if (threadIdx.x == 0) {
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-    for (int ww = 0; ww < kCsrThreads / 32; ++ww) {
+    for (int ww = 0; ww < NW; ++ww) {
       a0 = fmax(a0, wred[ww][0]);
       a1 = fmax(a1, wred[ww][1]);
       a2 += wred[ww][2];
@@ -247,7 +215,7 @@ __global__ void __launch_bounds__(kCsrThreads) csr_step_kernel(DevSolve s, DevCs
   }
 }
 
-cudaError_t launch_csr_step(const DevSolve& s, const DevCsr& d, cudaStream_t st) {
+cudaError_t launch_csr_step(const DevSolve& s, const DevSell& d, cudaStream_t st) {
   const int Rs = csr_rows_per_cta(s.n);
   const int use_smem = Rs > 0 ? 1 : 0;
   const int R = use_smem ? Rs : 1;
