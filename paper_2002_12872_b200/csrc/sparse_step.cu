@@ -49,13 +49,14 @@ int csr_step_ntiles(int64_t rows, int64_t n) {
 // takes one slice, lane L owns one output column j of P (one row of Delta):
 // every column / value load is one coalesced 128 / 256-byte access, the dot
 // P(i, j) = sum_q val * A(i, col) accumulates sequentially in CSR order in one
-// lane (no shuffle trees), and the same sequence recomputes P(i,i) for the
-// next launch's diagonal, bit-identically.
+// lane (no shuffle trees).  The next launch's diagonal d(i) = P(A')(i,i) is
+// formed at the end by one warp per owned row (lagged, like K1).
 template <int R>
 __global__ void __launch_bounds__(kCsrThreads) csr_step_kernel(DevSolve s, DevSell S, int use_smem) {
   if (s.state->done) return;
   const int jl = launch_index(s);
   extern __shared__ __align__(16) double sa[];  // [R][n] staged rows of A_{j-1}
+  __shared__ unsigned long long next_slice;
   __shared__ double red[kCsrThreads / 32][R][2];
   __shared__ double wred[kCsrThreads / 32][3];
   const int64_t n = s.n, ld = s.ld, rows = s.rows;
@@ -73,6 +74,8 @@ __global__ void __launch_bounds__(kCsrThreads) csr_step_kernel(DevSolve s, DevSe
     const int rr = r < nr ? r : 0;
     arow[r] = use_smem ? sa + size_t(rr) * size_t(n) : a_in + size_t(il0 + rr) * size_t(ld);
   }
+  if (threadIdx.x == 0) next_slice = 0ull;
+  if (!use_smem) __syncthreads();
   if (use_smem) {
     for (int r = 0; r < nr; ++r) {
       if ((n & 1) == 0) {
@@ -101,7 +104,15 @@ __global__ void __launch_bounds__(kCsrThreads) csr_step_kernel(DevSolve s, DevSe
   for (int r = 0; r < R; ++r) num[r] = den[r] = 0.0;
   double t_step = 0.0, t_max = 0.0, t_nonfin = 0.0;
 
-  for (int64_t sl = warp; sl < S.nslices; sl += NW) {
+  // Slices differ in width (sorted windows), so warps take them dynamically
+  // from a shared counter instead of a fixed stride (which pinned the widest
+  // slice of every window on the same warps).  The result does not depend on
+  // which warp computes a column.
+  while (true) {
+    int64_t sl = 0;
+    if (lane == 0) sl = atomicAdd(&next_slice, 1);
+    sl = __shfl_sync(0xffffffffu, sl, 0);
+    if (sl >= S.nslices) break;
     const int64_t t = sl * 32 + lane;
     const int32_t j = S.lane_col[t];
     const int32_t len = S.lane_len[t];
@@ -176,29 +187,32 @@ __global__ void __launch_bounds__(kCsrThreads) csr_step_kernel(DevSolve s, DevSe
     wred[warp][2] = t_nonfin;
   }
   __syncthreads();  // also orders this CTA's A' stores before the d' dots below
-  // exact d_j(i) = P(A_j)(i,i): row i of Delta in its SELL lane, same sequence
-  if (threadIdx.x < nr) {
-    const int r = threadIdx.x;
+  // d_j(i) = P(A_j)(i,i) for the next launch (lagged diagonal): one warp per
+  // row, lanes split the row's SELL entries, fixed shuffle tree (deterministic).
+  if (warp < nr) {
+    const int r = warp;
     const int64_t il = il0 + r, gi = s.row0 + il;
     const int64_t t = S.pos_of[gi];
-    const int64_t sl = t >> 5;
     const int L = int(t & 31);
     const int32_t len = S.lane_len[t];
-    const int64_t off = S.slice_off[sl];
+    const int64_t off = S.slice_off[t >> 5];
     const double* arow_new = a_out + size_t(il) * size_t(ld);
     double part = 0.0;
-    for (int32_t q = 0; q < len; ++q) {
+    for (int32_t q = lane; q < len; q += 32) {
       const int64_t idx = off + int64_t(q) * 32 + L;
-      part = __fma_rn(S.vals[idx], arow_new[S.cols[idx]], part);
+      part = __fma_rn(__ldg(S.vals + idx), arow_new[__ldg(S.cols + idx)], part);
     }
-    double nu = 0.0, de = 0.0;
-    for (int ww = 0; ww < NW; ++ww) {
-      nu = fmax(nu, red[ww][r][0]);
-      de = fmax(de, red[ww][r][1]);
+    part = warp_sum(part);
+    if (lane == 0) {
+      double nu = 0.0, de = 0.0;
+      for (int ww = 0; ww < NW; ++ww) {
+        nu = fmax(nu, red[ww][r][0]);
+        de = fmax(de, red[ww][r][1]);
+      }
+      s.rowpart[rp_index(0, il, 0, rows, 1)] = part;
+      s.rowpart[rp_index(1, il, 0, rows, 1)] = nu;
+      s.rowpart[rp_index(2, il, 0, rows, 1)] = de;
     }
-    s.rowpart[rp_index(0, il, 0, rows, 1)] = part;
-    s.rowpart[rp_index(1, il, 0, rows, 1)] = nu;
-    s.rowpart[rp_index(2, il, 0, rows, 1)] = de;
   }
   if (threadIdx.x == 0) {
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
