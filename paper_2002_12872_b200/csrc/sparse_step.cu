@@ -26,7 +26,7 @@
 
 namespace dpt {
 
-constexpr int kCsrThreads = 512;
+constexpr int kCsrThreads = 1024;
 constexpr int kCsrSmemBudget = 200 * 1024;
 
 static int csr_rows_per_cta(int64_t n) {
