@@ -54,7 +54,8 @@ cudaError_t launch_fold(const DevSolve& s, int ntiles_this, cudaStream_t st);
 cudaError_t launch_decide(const DevSolve& s, cudaStream_t st);
 cudaError_t launch_cycle(const DevSolve& s, int64_t elems, cudaStream_t st);
 cudaError_t launch_identity(const DevSolve& s, cudaStream_t st);
-cudaError_t launch_unit(const double* z, double* out, int64_t n, cudaStream_t st);
+cudaError_t launch_unit(const double* z, double* out, int64_t n, double* scratch /*[297]*/, unsigned* counter,
+                        cudaStream_t st);
 cudaError_t launch_rowdot(const DevSolve& s, const double* delta, const DevCsr* csr, cudaStream_t st);
 cudaError_t launch_set_diag_delta(const DevSolve& s, const double* delta, const DevCsr* csr,
                                   cudaStream_t st);

@@ -14,6 +14,7 @@
 #include <stdint.h>
 
 #include "dpt_device.cuh"
+#include "dpt_fold.cuh"
 #include "dpt_kernels.h"
 
 namespace dpt {
@@ -27,74 +28,6 @@ int fold_blocks(int64_t rows) {
   if (b > kFoldMaxBlocks) b = kFoldMaxBlocks;
   if (b < 1) b = 1;
   return int(b);
-}
-
-__device__ __forceinline__ double block_max(double v, double* sh) {
-  v = warp_max(v);
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  __syncthreads();
-  if (l == 0) sh[w] = v;
-  __syncthreads();
-  double r = 0.0;
-  if (threadIdx.x == 0)
-    for (int i = 0; i < int(blockDim.x >> 5); ++i) r = fmax(r, sh[i]);
-  return r;  // valid in thread 0
-}
-
-__device__ __forceinline__ double block_sum(double v, double* sh) {
-  v = warp_sum(v);
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  __syncthreads();
-  if (l == 0) sh[w] = v;
-  __syncthreads();
-  double r = 0.0;
-  if (threadIdx.x == 0)
-    for (int i = 0; i < int(blockDim.x >> 5); ++i) r += sh[i];
-  return r;
-}
-
-// Row fold of one row: column-block partials are summed (d) / maxed (num, den)
-// by `width` cooperating lanes in a fixed tree, so the result is deterministic.
-__device__ __forceinline__ void fold_row_store(const DevSolve& s, int64_t i, double d, double num, double den,
-                                               const double* dprev, double* dnext) {
-  const double r = num / fmax(den, 1e-300);  // kTinyDen, dpt.cpp:18, :40
-  s.eps[i] = __dadd_rn(s.theta[s.row0 + i], __dmul_rn(s.lambda, dprev[i]));
-  s.res[i] = r;
-  dnext[i] = d;
-}
-
-__device__ void decide_now(const DevSolve& s);
-
-// Sample-first part of the cycle test, run by one block right after the
-// decision: if the first entries already differ by >= tol from every window
-// entry, within_tol is false for all of them and the cycle kernel has nothing
-// to do (exact early-out, dpt.cpp:60-79).
-__device__ void cycle_sample_precheck(const DevSolve& s, double* sh) {
-  dpt_sm_state* st = s.state;
-  if (st->done || !st->cycle_pending) return;
-  const int j = st->j;
-  int npast = j - 1;
-  if (npast > s.opts.win - 1) npast = s.opts.win - 1;
-  const int64_t n = s.n, ld = s.ld;
-  const int64_t elems = s.rows * n;
-  const int64_t ns = elems < int64_t(blockDim.x) ? elems : int64_t(blockDim.x);
-  const double* cur = s.slots + size_t(j % s.nslots) * size_t(s.slot_elems);
-  int any = 0;
-  for (int p = 0; p < npast; ++p) {
-    const double* past = s.slots + size_t((j - 2 - p) % s.nslots) * size_t(s.slot_elems);
-    double m = 0.0;
-    const int64_t e = threadIdx.x;
-    if (e < ns) {
-      const int64_t r = e / n, c = e % n;
-      m = fabs(cur[r * ld + c] - past[r * ld + c]);
-    }
-    m = block_max(m, sh);
-    if (threadIdx.x == 0 && m < s.opts.tol) any = 1;
-  }
-  if (threadIdx.x == 0 && !any) {
-    st->cycle_pending = 0;  // refuted for every entry: the stats keep "not within"
-    for (int p = 0; p < DPT_MAX_WINDOW; ++p) s.stats[DPT_STATS_CYCLE0 + p] = 1.0;
-  }
 }
 
 __global__ void __launch_bounds__(kFoldThreads) fold_kernel(DevSolve s, int ntiles_this) {
@@ -127,7 +60,9 @@ __global__ void __launch_bounds__(kFoldThreads) fold_kernel(DevSolve s, int ntil
       }
     }
   } else {
-    // few rows (the row map has one): block per row, threads over the blocks
+    // few rows (the row map has one): block per row, threads over the blocks;
+    // the three row folds share one reduction pass (one barrier)
+    __shared__ double red3[kFoldThreads / 32][3];
     for (int64_t i = blockIdx.x; i < rows; i += gridDim.x) {
       double d = 0.0, num = 0.0, den = 0.0;
       for (int tn = threadIdx.x; tn < ntn; tn += blockDim.x) {
@@ -135,11 +70,23 @@ __global__ void __launch_bounds__(kFoldThreads) fold_kernel(DevSolve s, int ntil
         num = fmax(num, s.rowpart[rp_index(1, i, tn, rows, ntn)]);
         den = fmax(den, s.rowpart[rp_index(2, i, tn, rows, ntn)]);
       }
-      d = block_sum(d, sh);
-      num = block_max(num, sh);
-      den = block_max(den, sh);
+      d = warp_sum(d);
+      num = warp_max(num);
+      den = warp_max(den);
+      if (lane == 0) {
+        red3[threadIdx.x >> 5][0] = d;
+        red3[threadIdx.x >> 5][1] = num;
+        red3[threadIdx.x >> 5][2] = den;
+      }
+      __syncthreads();
       if (threadIdx.x == 0) {
-        fold_row_store(s, i, d, num, den, dprev, dnext);
+        double dd = 0.0, nn = 0.0, ee = 0.0;
+        for (int w = 0; w < int(blockDim.x >> 5); ++w) {
+          dd += red3[w][0];
+          nn = fmax(nn, red3[w][1]);
+          ee = fmax(ee, red3[w][2]);
+        }
+        fold_row_store(s, i, dd, nn, ee, dprev, dnext);
         rmax = fmax(rmax, s.res[i]);
       }
       __syncthreads();
@@ -151,10 +98,30 @@ __global__ void __launch_bounds__(kFoldThreads) fold_kernel(DevSolve s, int ntil
     a1 = fmax(a1, s.tilepart[size_t(t) * 4 + 1]);
     a2 += s.tilepart[size_t(t) * 4 + 2];
   }
-  a0 = block_max(a0, sh);
-  a1 = block_max(a1, sh);
-  a2 = block_sum(a2, sh);
-  rmax = block_max(rmax, sh);
+  {  // the four launch maxima in one reduction pass
+    __shared__ double red4[kFoldThreads / 32][4];
+    a0 = warp_max(a0);
+    a1 = warp_max(a1);
+    a2 = warp_sum(a2);
+    rmax = warp_max(rmax);
+    __syncthreads();
+    if (lane == 0) {
+      red4[threadIdx.x >> 5][0] = a0;
+      red4[threadIdx.x >> 5][1] = a1;
+      red4[threadIdx.x >> 5][2] = a2;
+      red4[threadIdx.x >> 5][3] = rmax;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      a0 = a1 = a2 = rmax = 0.0;
+      for (int w = 0; w < int(blockDim.x >> 5); ++w) {
+        a0 = fmax(a0, red4[w][0]);
+        a1 = fmax(a1, red4[w][1]);
+        a2 += red4[w][2];
+        rmax = fmax(rmax, red4[w][3]);
+      }
+    }
+  }
   if (threadIdx.x == 0) {
     double* bp = s.blockpart + size_t(blockIdx.x) * 8;
     bp[0] = a0;
@@ -188,19 +155,6 @@ __global__ void __launch_bounds__(kFoldThreads) fold_kernel(DevSolve s, int ntil
     __syncthreads();
     cycle_sample_precheck(s, sh);
   }
-}
-
-__device__ void decide_now(const DevSolve& s) {
-  dpt_sm_state* st = s.state;
-  if (st->done) return;
-  const int j = st->j + 1;
-  if (s.fixed_mode) {  // iterate_fixed: no gates (dpt.cpp:381-387)
-    st->j = j;
-    return;
-  }
-  const int sp = s.settled_table ? s.settled_table[j - 1] : 1;
-  const int sc = s.settled_table ? s.settled_table[j] : 1;
-  dpt_sm_decide(st, &s.opts, s.stats, j, sp, sc, s.trace);
 }
 
 __global__ void decide_kernel(DevSolve s) {
@@ -329,21 +283,44 @@ __global__ void rowdot_kernel(DevSolve s, const double* __restrict__ delta, cons
 
 // z_unit = z / ||z||_2 when the norm is finite and positive, else z
 // (dominant_eigenpair, dpt.cpp:432-436; vec_two_norm, matrix.cpp:372-376).
-__global__ void __launch_bounds__(1024) unit_kernel(const double* __restrict__ z, double* __restrict__ out, int64_t n) {
+// Fixed grid + fixed chunking + last-block combine: deterministic.
+constexpr int kUnitBlocks = 296;
+__global__ void __launch_bounds__(256) unit_norm_kernel(const double* __restrict__ z, int64_t n, double* part,
+                                                         unsigned* counter, double* nrm) {
   __shared__ double sh[32];
-  __shared__ double nrm;
+  __shared__ bool last;
+  const int64_t chunk = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t b0 = int64_t(blockIdx.x) * chunk, b1 = b0 + chunk < n ? b0 + chunk : n;
   double v = 0.0;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) v = __fma_rn(z[i], z[i], v);
+  for (int64_t i = b0 + threadIdx.x; i < b1; i += blockDim.x) v = __fma_rn(z[i], z[i], v);
   v = block_sum(v, sh);
-  if (threadIdx.x == 0) nrm = sqrt(v);
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = v;
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
   __syncthreads();
-  const double q = nrm;
-  const bool ok = q > 0.0 && isfinite(q);
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) out[i] = ok ? z[i] / q : z[i];
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    double t = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) t += ((volatile double*)part)[b];
+    *nrm = sqrt(t);
+    *counter = 0u;
+  }
 }
 
-cudaError_t launch_unit(const double* z, double* out, int64_t n, cudaStream_t st) {
-  unit_kernel<<<1, 1024, 0, st>>>(z, out, n);
+__global__ void unit_scale_kernel(const double* __restrict__ z, double* __restrict__ out, int64_t n,
+                                  const double* nrm) {
+  const double q = *nrm;
+  const bool ok = q > 0.0 && isfinite(q);
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    out[i] = ok ? z[i] / q : z[i];
+}
+
+cudaError_t launch_unit(const double* z, double* out, int64_t n, double* scratch, unsigned* counter,
+                        cudaStream_t st) {
+  unit_norm_kernel<<<kUnitBlocks, 256, 0, st>>>(z, n, scratch, counter, scratch + kUnitBlocks);
+  unit_scale_kernel<<<592, 256, 0, st>>>(z, out, n, scratch + kUnitBlocks);
   return cudaGetLastError();
 }
 

@@ -1055,7 +1055,10 @@ int run_single(dpt_ctx* ctx, const dpt_problem* p, int64_t row, const dpt_option
   if (n > 0 && z_unit) {  // dominant_eigenpair's z_unit = z / ||z||_2 (dpt.cpp:432-436)
     DBuf tmp;
     dalloc(tmp, size_t(n) * 8, err);
-    CK(launch_unit(w.s.slots + size_t(final_iter % nslots) * size_t(w.s.slot_elems), tmp.as<double>(), n, st));
+    DBuf scratch;
+    dalloc(scratch, 512 * 8, err);
+    CK(launch_unit(w.s.slots + size_t(final_iter % nslots) * size_t(w.s.slot_elems), tmp.as<double>(), n,
+                   scratch.as<double>(), w.s.counter + 2, st));
     copy_out(z_unit, tmp.as<double>(), size_t(n), out_mem, st, err);
     CK(cudaStreamSynchronize(st));
   }
