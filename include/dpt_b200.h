@@ -17,9 +17,10 @@
  *            dense row-major n*n, or CSR (int64 row offsets, int32 sorted
  *            columns, FP64 values; SparseMatrix, matrix.hpp:73-106)
  *   A        the iterate, row i = chart row i (ConvergenceReport::state.a)
- * Documented deviation: the reference computes in std::complex<double>; this
- * path is real FP64.  The C++ shim rejects inputs with a nonzero imaginary part
- * (DPT_ERR_NON_REAL) instead of silently dropping it.
+ * Arithmetic: the reference computes in std::complex<double>.  Real inputs run
+ * the real FP64 kernels (4x fewer flops, identical results: the reference's
+ * imaginary parts stay exactly 0); is_complex selects the complex FP64 path
+ * (same kernels over interleaved re/im data).
  *
  * Errors follow the reference's exception taxonomy (dpt.hpp, partition.hpp:13-26):
  * non-convergence is a STATUS in the report, never an error code.
@@ -35,7 +36,7 @@
 extern "C" {
 #endif
 
-#define DPT_B200_ABI_VERSION 1
+#define DPT_B200_ABI_VERSION 2
 
 /* ConvergenceStatus, dpt.hpp:13-18 (same order). */
 typedef enum dpt_status {
@@ -85,8 +86,12 @@ typedef struct dpt_problem {
   const int32_t* cols;   /* CSR: [nnz], sorted within rows */
   const double* vals;    /* CSR: [nnz] */
   int64_t nnz;
-  double lambda;         /* PartitionedProblem::lambda (real) */
+  double lambda;         /* Re PartitionedProblem::lambda */
   int mem;               /* dpt_mem of d / delta / rowptr / cols / vals */
+  int is_complex;        /* 1: d, delta, vals are std::complex<double> arrays
+                            (interleaved re, im), lambda_im used, and every
+                            complex output (a, eigenvalues, z) is interleaved */
+  double lambda_im;      /* Im PartitionedProblem::lambda */
 } dpt_problem;
 
 /* ConvergenceReport / SingleRowReport scalars (dpt.hpp:39-46, :98-105). */
@@ -100,14 +105,16 @@ typedef struct dpt_report {
   /* timings of the call on the device (not part of the reference report) */
   double device_ms;
   int launches;
+  double eigenvalue_im; /* single-row modes, complex problems */
 } dpt_report;
 
 /* DegenerateSpectrum payload + message for any error (partition.hpp:13-26). */
 typedef struct dpt_error_info {
   int code;
   int64_t i, j;
-  double ei, ej;
+  double ei, ej;       /* real parts of the offending levels */
   char message[256];
+  double ei_im, ej_im; /* imaginary parts (complex problems) */
 } dpt_error_info;
 
 /* TraceSink, dpt.hpp:48-49: (k, step_norm, max_residual).  Called on the
@@ -197,6 +204,20 @@ int dpt_step_single_gap(dpt_ctx* ctx, const dpt_problem* p, const double* z, int
 /* eigenvalue_of (dpt.hpp:68-72): d_row + lambda (Delta z)_row. */
 int dpt_eigenvalue_of(dpt_ctx* ctx, const dpt_problem* p, const double* z, int64_t row,
                       double lambda, double* out, int z_mem, dpt_error_info* err);
+
+/* ---- complex coupling variants (the reference's cdouble lambda arguments) ---
+ * Same as the real entry points with lambda = lambda + i lambda_im; for a
+ * complex problem every array is interleaved std::complex<double>
+ * (a, gap, z: n*n or n complex values; out2 of eigenvalue_of_c: 2 doubles). */
+int dpt_iterate_fixed_c(dpt_ctx* ctx, const dpt_problem* p, int k, double lambda, double lambda_im,
+                        double* a_out, int out_mem, dpt_report* rep, dpt_error_info* err);
+int dpt_step_full_gap_c(dpt_ctx* ctx, const dpt_problem* p, const double* a, const double* gap,
+                        double lambda, double lambda_im, double* out, int io_mem, dpt_error_info* err);
+int dpt_step_single_gap_c(dpt_ctx* ctx, const dpt_problem* p, const double* z, int64_t row,
+                          const double* gap_row, double lambda, double lambda_im, double* out, int io_mem,
+                          dpt_error_info* err);
+int dpt_eigenvalue_of_c(dpt_ctx* ctx, const dpt_problem* p, const double* z, int64_t row, double lambda,
+                        double lambda_im, double* out2, int z_mem, dpt_error_info* err);
 
 /* ---- plans: a problem kept resident in HBM ------------------------------------ */
 /* For repeated calls on one perturbation (the reference's scan_domain / bench

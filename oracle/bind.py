@@ -243,3 +243,123 @@ class Checker:
 
 def available(which: str) -> bool:
     return os.path.exists(REF_SO if which == "reference" else ORACLE_SO)
+
+
+# ---- complex inputs: the reference library's native std::complex<double> path ----
+class orc_cproblem(Structure):
+    _fields_ = [("n", c_int64), ("d", c_void_p), ("kind", c_int), ("delta", c_void_p), ("rowptr", c_void_p),
+                ("cols", c_void_p), ("vals", c_void_p), ("lam_re", c_double), ("lam_im", c_double)]
+
+
+class ComplexReference:
+    """The reference (oracle/_ref) on complex problems: results as complex128 numpy arrays."""
+
+    def __init__(self):
+        L = ctypes.CDLL(REF_SO)
+        P = POINTER
+        L.ref_c_iterate_full.argtypes = [P(orc_cproblem), P(orc_options), c_int, c_double, c_void_p, c_void_p,
+                                         c_void_p, P(orc_report), c_void_p, c_void_p]
+        L.ref_c_iterate_single.argtypes = [P(orc_cproblem), c_int64, P(orc_options), c_double, c_void_p, c_void_p,
+                                           P(orc_single_report)]
+        L.ref_c_dominant.argtypes = [P(orc_cproblem), P(orc_options), c_void_p, c_void_p, c_void_p,
+                                     P(orc_single_report), P(c_int64)]
+        L.ref_c_iterate_fixed.argtypes = [P(orc_cproblem), c_int, c_double, c_double, c_void_p]
+        L.ref_c_step_full.argtypes = [P(orc_cproblem), c_void_p, c_double, c_double, c_void_p]
+        L.ref_c_step_single.argtypes = [P(orc_cproblem), c_void_p, c_int64, c_double, c_double, c_void_p, c_void_p]
+        L.ref_c_check_degenerate.argtypes = [c_int64, c_void_p, c_double, P(c_int64), P(c_int64)]
+        self.L = L
+
+    @staticmethod
+    def _prob(p):
+        keep = []
+        d = np.ascontiguousarray(p.d, dtype=np.complex128)
+        keep.append(d)
+        pr = orc_cproblem()
+        pr.n = d.shape[0]
+        pr.d = d.ctypes.data
+        pr.lam_re, pr.lam_im = float(np.real(p.lam)), float(np.imag(p.lam))
+        if hasattr(p.delta, "rowptr"):
+            rp = np.ascontiguousarray(p.delta.rowptr, dtype=np.int64)
+            cl = np.ascontiguousarray(p.delta.cols, dtype=np.int32)
+            vl = np.ascontiguousarray(p.delta.vals, dtype=np.complex128)
+            keep += [rp, cl, vl]
+            pr.kind = ORC_CSR
+            pr.rowptr, pr.cols, pr.vals = rp.ctypes.data, cl.ctypes.data, vl.ctypes.data
+        else:
+            a = np.ascontiguousarray(p.delta, dtype=np.complex128)
+            keep.append(a)
+            pr.kind = ORC_DENSE
+            pr.delta = a.ctypes.data
+        return pr, keep
+
+    def iterate_full(self, p, opts=None, ramped=False, alpha=0.0, trace=False):
+        pr, keep = self._prob(p)
+        n = pr.n
+        o = Checker._opts(opts)
+        a = np.zeros((n, n), np.complex128)
+        eig = np.zeros(n, np.complex128)
+        res = np.zeros(n)
+        rep = orc_report()
+        cap = max(o.max_iter, 1) + 1
+        ts = np.full(cap, np.nan) if trace else None
+        tr = np.full(cap, np.nan) if trace else None
+        rc = self.L.ref_c_iterate_full(ctypes.byref(pr), ctypes.byref(o), int(ramped), float(alpha), a.ctypes.data,
+                                       eig.ctypes.data, res.ctypes.data, ctypes.byref(rep),
+                                       ts.ctypes.data if trace else None, tr.ctypes.data if trace else None)
+        k = rep.iterations if trace else 0
+        return FullResult(rc, rep.status, rep.iterations, rep.step_norm, a, eig, res,
+                          ts[:k] if trace else None, tr[:k] if trace else None,
+                          (rep.degenerate_i, rep.degenerate_j) if rc == ORC_ERR_DEGENERATE else None)
+
+    def iterate_single(self, p, row, opts=None, ramp_alpha=0.0):
+        pr, keep = self._prob(p)
+        o = Checker._opts(opts)
+        z = np.zeros(pr.n, np.complex128)
+        e = np.zeros(2)
+        rep = orc_single_report()
+        rc = self.L.ref_c_iterate_single(ctypes.byref(pr), int(row), ctypes.byref(o), float(ramp_alpha),
+                                         z.ctypes.data, e.ctypes.data, ctypes.byref(rep))
+        return SingleResult(rc, rep.status, rep.iterations, rep.step_norm, complex(e[0], e[1]), rep.residual, z)
+
+    def dominant_eigenpair(self, p, opts=None):
+        pr, keep = self._prob(p)
+        o = Checker._opts(opts)
+        zc = np.zeros(pr.n, np.complex128)
+        zu = np.zeros(pr.n, np.complex128)
+        e = np.zeros(2)
+        rep = orc_single_report()
+        row = ctypes.c_int64(-1)
+        rc = self.L.ref_c_dominant(ctypes.byref(pr), ctypes.byref(o), zc.ctypes.data, zu.ctypes.data,
+                                   e.ctypes.data, ctypes.byref(rep), ctypes.byref(row))
+        return SingleResult(rc, rep.status, rep.iterations, rep.step_norm, complex(e[0], e[1]), rep.residual, zc,
+                            zu, row.value)
+
+    def iterate_fixed(self, p, k, lam):
+        pr, keep = self._prob(p)
+        a = np.zeros((pr.n, pr.n), np.complex128)
+        self.L.ref_c_iterate_fixed(ctypes.byref(pr), int(k), float(np.real(lam)), float(np.imag(lam)), a.ctypes.data)
+        return a
+
+    def step_full(self, a, p, lam):
+        pr, keep = self._prob(p)
+        a = np.ascontiguousarray(a, dtype=np.complex128)
+        out = np.zeros_like(a)
+        self.L.ref_c_step_full(ctypes.byref(pr), a.ctypes.data, float(np.real(lam)), float(np.imag(lam)),
+                               out.ctypes.data)
+        return out
+
+    def step_single(self, z, row, p, lam):
+        """(step_single(z), eigenvalue_of(z)) for chart row."""
+        pr, keep = self._prob(p)
+        z = np.ascontiguousarray(z, dtype=np.complex128)
+        out = np.zeros_like(z)
+        e = np.zeros(2)
+        self.L.ref_c_step_single(ctypes.byref(pr), z.ctypes.data, int(row), float(np.real(lam)), float(np.imag(lam)),
+                                 out.ctypes.data, e.ctypes.data)
+        return out, complex(e[0], e[1])
+
+    def check_degenerate(self, d, tol=1e-12):
+        d = np.ascontiguousarray(d, dtype=np.complex128)
+        i, j = ctypes.c_int64(), ctypes.c_int64()
+        hit = self.L.ref_c_check_degenerate(d.shape[0], d.ctypes.data, float(tol), ctypes.byref(i), ctypes.byref(j))
+        return (i.value, j.value) if hit else None

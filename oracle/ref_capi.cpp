@@ -262,3 +262,171 @@ int ref_prepared_step_rows(void* h, int64_t row0, int64_t rows, const double* a,
 }
 
 }  // extern "C"
+
+// ---- complex inputs: the reference's native std::complex<double> path ------
+// Arrays are interleaved (re, im) = std::complex<double> layout.
+extern "C" {
+
+typedef struct {
+  int64_t n;
+  const double* d;  // [2n]
+  int kind;
+  const double* delta;  // dense [2 n n]
+  const int64_t* rowptr;
+  const int32_t* cols;
+  const double* vals;  // [2 nnz]
+  double lam_re, lam_im;
+} orc_cproblem;
+
+static PartitionedProblem to_cproblem(const orc_cproblem* p) {
+  const std::size_t n = std::size_t(p->n);
+  std::vector<cdouble> d(n);
+  for (std::size_t i = 0; i < n; ++i) d[i] = cdouble{p->d[2 * i], p->d[2 * i + 1]};
+  MatrixVariant delta;
+  if (p->kind == ORC_DENSE) {
+    DenseMatrix m(n, n);
+    for (std::size_t i = 0; i < n * n; ++i) m.data()[i] = cdouble{p->delta[2 * i], p->delta[2 * i + 1]};
+    delta = std::move(m);
+  } else {
+    std::vector<SparseMatrix::Triplet> t;
+    for (std::size_t i = 0; i < n; ++i)
+      for (int64_t q = p->rowptr[i]; q < p->rowptr[i + 1]; ++q)
+        t.push_back({i, std::size_t(p->cols[q]), cdouble{p->vals[2 * q], p->vals[2 * q + 1]}});
+    delta = SparseMatrix::from_triplets(n, n, std::move(t));
+  }
+  return make_problem(DiagonalMatrix(std::move(d)), std::move(delta), cdouble{p->lam_re, p->lam_im});
+}
+
+static void put_cdense(const DenseMatrix& a, double* out) {
+  for (std::size_t i = 0; i < a.rows() * a.cols(); ++i) {
+    out[2 * i] = a.data()[i].real();
+    out[2 * i + 1] = a.data()[i].imag();
+  }
+}
+
+int ref_c_iterate_full(const orc_cproblem* p, const orc_options* o, int ramped, double alpha, double* a_out,
+                       double* eig_out, double* res_out, orc_report* rep, double* trace_step, double* trace_res) {
+  std::memset(rep, 0, sizeof(*rep));
+  try {
+    const PartitionedProblem pp = to_cproblem(p);
+    int idx = 0;
+    TraceSink sink;
+    if (trace_step)
+      sink = [&](int, double s, double r) {
+        trace_step[idx] = s;
+        trace_res[idx] = r;
+        ++idx;
+      };
+    const ConvergenceReport r =
+        ramped ? iterate_ramped(pp, alpha, to_opts(o), sink) : iterate_full(pp, to_opts(o), sink);
+    rep->status = int(r.status);
+    rep->iterations = r.iterations;
+    rep->step_norm = r.step_norm;
+    put_cdense(r.state.a, a_out);
+    for (std::size_t i = 0; i < r.eigenvalues.size(); ++i) {
+      eig_out[2 * i] = r.eigenvalues[i].real();
+      eig_out[2 * i + 1] = r.eigenvalues[i].imag();
+      res_out[i] = r.residuals[i];
+    }
+    return ORC_OK;
+  } catch (const DegenerateSpectrum& e) {
+    rep->degenerate_i = int64_t(e.first());
+    rep->degenerate_j = int64_t(e.second());
+    return ORC_ERR_DEGENERATE;
+  } catch (const std::invalid_argument&) {
+    return ORC_ERR_INVALID;
+  }
+}
+
+int ref_c_iterate_single(const orc_cproblem* p, int64_t row, const orc_options* o, double ramp_alpha, double* z_out,
+                         double* eig2, orc_single_report* rep) {
+  std::memset(rep, 0, sizeof(*rep));
+  try {
+    const SingleRowReport r = iterate_single(to_cproblem(p), std::size_t(row), to_opts(o), ramp_alpha, {});
+    rep->status = int(r.status);
+    rep->iterations = r.iterations;
+    rep->step_norm = r.step_norm;
+    rep->residual = r.residual;
+    eig2[0] = r.eigenvalue.real();
+    eig2[1] = r.eigenvalue.imag();
+    for (std::size_t m = 0; m < r.z.size(); ++m) {
+      z_out[2 * m] = r.z[m].real();
+      z_out[2 * m + 1] = r.z[m].imag();
+    }
+    return ORC_OK;
+  } catch (const DegenerateSpectrum& e) {
+    rep->degenerate_i = int64_t(e.first());
+    rep->degenerate_j = int64_t(e.second());
+    return ORC_ERR_DEGENERATE;
+  }
+}
+
+int ref_c_dominant(const orc_cproblem* p, const orc_options* o, double* z_chart, double* z_unit, double* eig2,
+                   orc_single_report* rep, int64_t* row_out) {
+  std::memset(rep, 0, sizeof(*rep));
+  try {
+    const DominantEigenpair r = dominant_eigenpair(to_cproblem(p), to_opts(o));
+    rep->status = int(r.status);
+    rep->iterations = r.iterations;
+    rep->residual = r.residual;
+    *row_out = int64_t(r.row);
+    eig2[0] = r.eigenvalue.real();
+    eig2[1] = r.eigenvalue.imag();
+    for (std::size_t m = 0; m < r.z_chart.size(); ++m) {
+      z_chart[2 * m] = r.z_chart[m].real();
+      z_chart[2 * m + 1] = r.z_chart[m].imag();
+      z_unit[2 * m] = r.z_unit[m].real();
+      z_unit[2 * m + 1] = r.z_unit[m].imag();
+    }
+    return ORC_OK;
+  } catch (const DegenerateSpectrum& e) {
+    rep->degenerate_i = int64_t(e.first());
+    rep->degenerate_j = int64_t(e.second());
+    return ORC_ERR_DEGENERATE;
+  }
+}
+
+int ref_c_iterate_fixed(const orc_cproblem* p, int k, double lr, double li, double* a_out) {
+  put_cdense(iterate_fixed(to_cproblem(p), k, cdouble{lr, li}), a_out);
+  return ORC_OK;
+}
+
+int ref_c_step_full(const orc_cproblem* p, const double* a, double lr, double li, double* out) {
+  const PartitionedProblem pp = to_cproblem(p);
+  const std::size_t n = std::size_t(p->n);
+  DenseMatrix am(n, n);
+  for (std::size_t i = 0; i < n * n; ++i) am.data()[i] = cdouble{a[2 * i], a[2 * i + 1]};
+  put_cdense(step_full(am, build_theta(pp.d), pp.delta_t, cdouble{lr, li}), out);
+  return ORC_OK;
+}
+
+int ref_c_step_single(const orc_cproblem* p, const double* z, int64_t row, double lr, double li, double* out,
+                      double* eig2) {
+  const PartitionedProblem pp = to_cproblem(p);
+  std::vector<cdouble> zz(std::size_t(p->n));
+  for (int64_t m = 0; m < p->n; ++m) zz[std::size_t(m)] = cdouble{z[2 * m], z[2 * m + 1]};
+  const auto r = step_single(zz, build_gap_row(pp.d, std::size_t(row)), pp.delta, cdouble{lr, li});
+  for (std::size_t m = 0; m < r.size(); ++m) {
+    out[2 * m] = r[m].real();
+    out[2 * m + 1] = r[m].imag();
+  }
+  const cdouble e = eigenvalue_of(zz, std::size_t(row), pp.d, pp.delta, cdouble{lr, li});
+  eig2[0] = e.real();
+  eig2[1] = e.imag();
+  return ORC_OK;
+}
+
+int ref_c_check_degenerate(int64_t n, const double* d, double tol, int64_t* i, int64_t* j) {
+  std::vector<cdouble> dd(static_cast<std::size_t>(n));
+  for (int64_t q = 0; q < n; ++q) dd[std::size_t(q)] = cdouble{d[2 * q], d[2 * q + 1]};
+  try {
+    (void)build_theta(DiagonalMatrix(std::move(dd)), tol);
+    return 0;
+  } catch (const DegenerateSpectrum& e) {
+    *i = int64_t(e.first());
+    *j = int64_t(e.second());
+    return 1;
+  }
+}
+
+}  // extern "C"

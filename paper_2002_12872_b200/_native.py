@@ -31,18 +31,18 @@ class dpt_options(Structure):
 class dpt_problem(Structure):
     _fields_ = [("n", c_int64), ("d", c_void_p), ("delta_kind", c_int), ("delta", c_void_p),
                 ("rowptr", c_void_p), ("cols", c_void_p), ("vals", c_void_p), ("nnz", c_int64),
-                ("lambda_", c_double), ("mem", c_int)]
+                ("lambda_", c_double), ("mem", c_int), ("is_complex", c_int), ("lambda_im", c_double)]
 
 
 class dpt_report(Structure):
     _fields_ = [("status", c_int), ("iterations", c_int), ("step_norm", c_double),
                 ("eigenvalue", c_double), ("residual", c_double), ("row", c_int64),
-                ("device_ms", c_double), ("launches", c_int)]
+                ("device_ms", c_double), ("launches", c_int), ("eigenvalue_im", c_double)]
 
 
 class dpt_error_info(Structure):
     _fields_ = [("code", c_int), ("i", c_int64), ("j", c_int64), ("ei", c_double), ("ej", c_double),
-                ("message", c_char * 256)]
+                ("message", c_char * 256), ("ei_im", c_double), ("ej_im", c_double)]
 
 
 TRACE_FN = ctypes.CFUNCTYPE(c_int, c_int, c_double, c_double, c_void_p)
@@ -89,6 +89,20 @@ def lib() -> ctypes.CDLL:
                                       P(dpt_error_info)]
         L.dpt_eigenvalue_of.argtypes = [c_void_p, P(dpt_problem), c_void_p, I64, D, P(c_double),
                                         c_int, P(dpt_error_info)]
+        L.dpt_iterate_fixed_c.argtypes = [c_void_p, P(dpt_problem), I, D, D, c_void_p, c_int, P(dpt_report),
+                                          P(dpt_error_info)]
+        L.dpt_step_full_gap_c.argtypes = [c_void_p, P(dpt_problem), c_void_p, c_void_p, D, D, c_void_p, c_int,
+                                          P(dpt_error_info)]
+        L.dpt_step_single_gap_c.argtypes = [c_void_p, P(dpt_problem), c_void_p, I64, c_void_p, D, D, c_void_p,
+                                            c_int, P(dpt_error_info)]
+        L.dpt_eigenvalue_of_c.argtypes = [c_void_p, P(dpt_problem), c_void_p, I64, D, D, c_void_p, c_int,
+                                          P(dpt_error_info)]
+        L.dpt_step_full_gap.argtypes = [c_void_p, P(dpt_problem), c_void_p, c_void_p, D, c_void_p, c_int,
+                                        P(dpt_error_info)]
+        L.dpt_step_single_gap.argtypes = [c_void_p, P(dpt_problem), c_void_p, I64, c_void_p, D, c_void_p, c_int,
+                                          P(dpt_error_info)]
+        L.dpt_readoffs.argtypes = [c_void_p, P(dpt_problem), c_void_p, c_void_p, c_void_p, c_int,
+                                   P(dpt_error_info)]
         L.dpt_plan_create.argtypes = [c_void_p, P(dpt_problem), c_int, I64, D, P(c_void_p), P(dpt_error_info)]
         L.dpt_plan_destroy.argtypes = [c_void_p]
         L.dpt_plan_begin.argtypes = [c_void_p, P(dpt_error_info)]

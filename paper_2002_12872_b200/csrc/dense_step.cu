@@ -46,7 +46,7 @@ struct DenseCfg {
   static constexpr int MB = WTM / 8, NB = WTN / 8;
   static constexpr int A_BYTES = BM * BK * 8, B_BYTES = BN * BK * 8;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int RED_BYTES = WARPS_N * BM * 3 * 8 + NCW * 4 * 8;
+  static constexpr int RED_BYTES = WARPS_N * BM * 4 * 8 + NCW * 4 * 8;
   static constexpr int SMEM = STAGES * STAGE_BYTES + RED_BYTES + 2 * STAGES * 8 + 1024;
 };
 
@@ -61,7 +61,7 @@ __device__ __forceinline__ uint32_t swz(int r, int chunk) {
   return uint32_t(r) * 128u + uint32_t((chunk ^ (r & 7)) << 4);
 }
 
-template <class C>
+template <class C, bool CPLX>
 __global__ void __launch_bounds__(C::THREADS, C::MINB)
     dense_step_kernel(DevSolve s, const CUtensorMap* __restrict__ amaps,
                       const CUtensorMap* __restrict__ dmap, const double* __restrict__ delta,
@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;
   double* red = reinterpret_cast<double*>(smem + C::STAGES * C::STAGE_BYTES);
-  double* wred = red + C::WARPS_N * C::BM * 3;
+  double* wred = red + C::WARPS_N * C::BM * 4;
   uint64_t* full = reinterpret_cast<uint64_t*>(wred + C::NCW * 4);
   uint64_t* empty = full + C::STAGES;
 
@@ -92,7 +92,10 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
 
   const int slot_in = (j_launch - 1) % s.nslots;
   const int slot_out = j_launch % s.nslots;
-  const int64_t n = s.n, rows = s.rows;
+  // real: P = A Delta^T over n columns; complex: the same NT GEMM over the
+  // interleaved (re, im) columns against B = [[Re D, -Im D], [Im D, Re D]]
+  // (row 2j of B -> Re P(:, j), row 2j+1 -> Im P(:, j)), i.e. K = N = 2n.
+  const int64_t n = s.ncol, rows = s.rows;
   const int KT = int((n + C::BK - 1) / C::BK);
 
   if (threadIdx.x == 0) {
@@ -176,6 +179,69 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
 
   const int colbase = tn * C::BN + wn * C::WTN + 2 * t;
   double t_step = 0.0, t_max = 0.0, t_nonfin = 0.0;
+  if constexpr (CPLX) {
+    // complex element j = c / 2 of row i: the fragment pair (c, c+1) = (re, im)
+    const cd lamk = lamc_of(s, j_launch);
+    const cd lamc = cmake(s.lambda, s.lambda_im);
+#pragma unroll
+    for (int a = 0; a < C::MB; ++a) {
+      const int il = tm * C::BM + wm * C::WTM + a * 8 + gq;
+      const bool row_ok = il < rows;
+      const int64_t gi = s.row0 + il;
+      double num = 0.0, den = 0.0, dre = 0.0, dim = 0.0;
+      if (row_ok) {
+        const cd ti = cmake(theta[2 * gi], theta[2 * gi + 1]);
+        const cd di = cmake(d_in[2 * il], d_in[2 * il + 1]);
+        const cd eps_i = cadd(ti, cmul(lamc, di));
+        const double* arow = a_in + size_t(il) * size_t(s.ld);
+        double* orow = a_out + size_t(il) * size_t(s.ld);
+        const double* drow = delta + size_t(2 * gi) * size_t(s.ldd);  // (Re D(i,j), -Im D(i,j)) pairs
+#pragma unroll
+        for (int b = 0; b < C::NB; ++b) {
+          const int c = colbase + b * 8;
+          if (c >= n) continue;
+          const double2 av2 = *reinterpret_cast<const double2*>(arow + c);
+          const double2 dv2 = *reinterpret_cast<const double2*>(drow + c);
+          const double2 tc2 = *reinterpret_cast<const double2*>(theta + c);
+          const cd av = cmake(av2.x, av2.y), tc = cmake(tc2.x, tc2.y), dij = cmake(dv2.x, -dv2.y);
+          const cd p = cmake(acc[a][b][0], acc[a][b][1]);
+          cd v;
+          if (2 * gi == c) {
+            v = cmake(1.0, 0.0);
+          } else {
+            const cd g = s.gapmat ? cmake(s.gapmat[size_t(il) * size_t(s.ld) + size_t(c)],
+                                          s.gapmat[size_t(il) * size_t(s.ld) + size_t(c) + 1])
+                                  : crecip(csub(ti, tc));
+            v = cmul(cmul(lamk, g), csub(p, cmul(di, av)));
+          }
+          *reinterpret_cast<double2*>(orow + c) = make_double2(v.x, v.y);
+          t_step = fmax(t_step, cabs_(csub(v, av)));
+          t_max = fmax(t_max, cabs_(v));
+          t_nonfin += cfinite(v) ? 0.0 : 1.0;
+          const cd r = cadd(cmul(csub(tc, eps_i), av), cmul(lamc, p));
+          num = fmax(num, cabs_(r));
+          den = fmax(den, cabs_(av));
+          const cd vd = cmul(v, dij);
+          dre += vd.x;
+          dim += vd.y;
+        }
+      }
+#pragma unroll
+      for (int o = 1; o <= 2; o <<= 1) {
+        num = fmax(num, __shfl_xor_sync(0xffffffffu, num, o));
+        den = fmax(den, __shfl_xor_sync(0xffffffffu, den, o));
+        dre += __shfl_xor_sync(0xffffffffu, dre, o);
+        dim += __shfl_xor_sync(0xffffffffu, dim, o);
+      }
+      if (t == 0) {
+        const int rt = wm * C::WTM + a * 8 + gq;
+        red[(wn * C::BM + rt) * 4 + 0] = dre;
+        red[(wn * C::BM + rt) * 4 + 1] = num;
+        red[(wn * C::BM + rt) * 4 + 2] = den;
+        red[(wn * C::BM + rt) * 4 + 3] = dim;
+      }
+    }
+  } else {
 #pragma unroll
   for (int a = 0; a < C::MB; ++a) {
     const int il = tm * C::BM + wm * C::WTM + a * 8 + gq;  // local row
@@ -188,7 +254,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
       const double eps_i = __dadd_rn(ti, __dmul_rn(lam, di));
       const double* arow = a_in + size_t(il) * size_t(s.ld);
       double* orow = a_out + size_t(il) * size_t(s.ld);
-      const double* drow = delta + size_t(gi) * size_t(s.ld);
+      const double* drow = delta + size_t(gi) * size_t(s.ldd);
 #pragma unroll
       for (int b = 0; b < C::NB; ++b) {
         const int c = colbase + b * 8;
@@ -242,10 +308,12 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
     dsum += __shfl_xor_sync(0xffffffffu, dsum, 2);
     if (t == 0) {
       const int rt = wm * C::WTM + a * 8 + gq;  // row within tile
-      red[(wn * C::BM + rt) * 3 + 0] = dsum;
-      red[(wn * C::BM + rt) * 3 + 1] = num;
-      red[(wn * C::BM + rt) * 3 + 2] = den;
+      red[(wn * C::BM + rt) * 4 + 0] = dsum;
+      red[(wn * C::BM + rt) * 4 + 1] = num;
+      red[(wn * C::BM + rt) * 4 + 2] = den;
+      red[(wn * C::BM + rt) * 4 + 3] = 0.0;
     }
+  }
   }
   t_step = warp_max(t_step);
   t_max = warp_max(t_max);
@@ -261,16 +329,18 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
   for (int rt = ctid; rt < C::BM; rt += C::NCW * 32) {
     const int il = tm * C::BM + rt;
     if (il >= rows) continue;
-    double ds = 0.0, nu = 0.0, de = 0.0;
+    double ds = 0.0, nu = 0.0, de = 0.0, di = 0.0;
 #pragma unroll
     for (int w = 0; w < C::WARPS_N; ++w) {
-      ds += red[(w * C::BM + rt) * 3 + 0];
-      nu = fmax(nu, red[(w * C::BM + rt) * 3 + 1]);
-      de = fmax(de, red[(w * C::BM + rt) * 3 + 2]);
+      ds += red[(w * C::BM + rt) * 4 + 0];
+      nu = fmax(nu, red[(w * C::BM + rt) * 4 + 1]);
+      de = fmax(de, red[(w * C::BM + rt) * 4 + 2]);
+      di += red[(w * C::BM + rt) * 4 + 3];
     }
     s.rowpart[rp_index(0, il, tn, rows, ntn)] = ds;
     s.rowpart[rp_index(1, il, tn, rows, ntn)] = nu;
     s.rowpart[rp_index(2, il, tn, rows, ntn)] = de;
+    if (CPLX) s.rowpart[rp_index(3, il, tn, rows, ntn)] = di;
   }
   if (ctid == 0) {
     double a0 = 0.0, a1 = 0.0, a2 = 0.0;
@@ -313,7 +383,7 @@ __global__ void __launch_bounds__(256) dense_init_kernel(DevSolve s, const doubl
     for (int r = 0; r < 4; ++r) {  // sT[jj][ii] = Delta(j0 + jj, gi0 + ii)
       const int64_t jj = j0 + ty + 8 * r;
       const int64_t gi = s.row0 + il0 + tx;
-      sT[ty + 8 * r][tx] = (jj < n && il0 + tx < rows) ? delta[size_t(jj) * size_t(s.ld) + size_t(gi)] : 0.0;
+      sT[ty + 8 * r][tx] = (jj < n && il0 + tx < rows) ? delta[size_t(jj) * size_t(s.ldd) + size_t(gi)] : 0.0;
     }
     __syncthreads();
 #pragma unroll
@@ -334,7 +404,7 @@ __global__ void __launch_bounds__(256) dense_init_kernel(DevSolve s, const doubl
       t_step = fmax(t_step, fabs(__dsub_rn(v, prev)));
       t_max = fmax(t_max, fabs(v));
       t_nonfin += isfinite(v) ? 0.0 : 1.0;
-      dsum[r] = __fma_rn(v, delta[size_t(gi) * size_t(s.ld) + size_t(c)], dsum[r]);
+      dsum[r] = __fma_rn(v, delta[size_t(gi) * size_t(s.ldd) + size_t(c)], dsum[r]);
     }
   }
 #pragma unroll
@@ -364,6 +434,73 @@ __global__ void __launch_bounds__(256) dense_init_kernel(DevSolve s, const doubl
       a2 += wr[w][2];
     }
     double* tp = s.tilepart + size_t(tmb * gridDim.x + tn) * 4;
+    tp[0] = a0;
+    tp[1] = a1;
+    tp[2] = a2;
+    tp[3] = 0.0;
+  }
+}
+
+// Complex launch 1: A_1(i,j) = (lam_1 g(i,j)) * Delta(j,i) with Delta read from
+// the real image B (Re D(j,i) = B[2j][2i], Im D(j,i) = B[2j+1][2i]).  One block
+// per (row, BNI/2 complex columns), emitting the same partials as the step.
+template <int BNI>
+__global__ void __launch_bounds__(BNI / 2) dense_init_cplx_kernel(DevSolve s, const double* __restrict__ B) {
+  if (s.state->done) return;
+  __shared__ double wr[BNI / 64 > 0 ? BNI / 64 : 1][5];
+  const int64_t n = s.n;
+  const int tn = blockIdx.x;
+  const int64_t il = blockIdx.y, gi = s.row0 + il;
+  const int64_t j = int64_t(tn) * (BNI / 2) + threadIdx.x;
+  const cd lam1 = lamc_of(s, 1);
+  double* __restrict__ a_out = s.slots + size_t(1 % s.nslots) * size_t(s.slot_elems);
+  double t_step = 0.0, t_max = 0.0, t_nonfin = 0.0, dre = 0.0, dim = 0.0;
+  if (j < n) {
+    cd v;
+    if (gi == j) {
+      v = cmake(1.0, 0.0);
+    } else {
+      const cd g = crecip(csub(cmake(s.theta[2 * gi], s.theta[2 * gi + 1]), cmake(s.theta[2 * j], s.theta[2 * j + 1])));
+      const cd dji = cmake(B[size_t(2 * j) * size_t(s.ldd) + size_t(2 * gi)], B[size_t(2 * j + 1) * size_t(s.ldd) + size_t(2 * gi)]);
+      v = cmul(cmul(lam1, g), dji);
+    }
+    *reinterpret_cast<double2*>(a_out + size_t(il) * size_t(s.ld) + size_t(2 * j)) = make_double2(v.x, v.y);
+    t_step = cabs_(csub(v, cmake(gi == j ? 1.0 : 0.0, 0.0)));
+    t_max = cabs_(v);
+    t_nonfin = cfinite(v) ? 0.0 : 1.0;
+    const double2 dij2 = *reinterpret_cast<const double2*>(B + size_t(2 * gi) * size_t(s.ldd) + size_t(2 * j));
+    const cd vd = cmul(v, cmake(dij2.x, -dij2.y));
+    dre = vd.x;
+    dim = vd.y;
+  }
+  t_step = warp_max(t_step);
+  t_max = warp_max(t_max);
+  t_nonfin = warp_sum(t_nonfin);
+  dre = warp_sum(dre);
+  dim = warp_sum(dim);
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) {
+    wr[w][0] = t_step;
+    wr[w][1] = t_max;
+    wr[w][2] = t_nonfin;
+    wr[w][3] = dre;
+    wr[w][4] = dim;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0;
+    for (int q = 0; q < int(blockDim.x + 31) / 32; ++q) {
+      a0 = fmax(a0, wr[q][0]);
+      a1 = fmax(a1, wr[q][1]);
+      a2 += wr[q][2];
+      a3 += wr[q][3];
+      a4 += wr[q][4];
+    }
+    s.rowpart[rp_index(0, il, tn, s.rows, s.ntn)] = a3;
+    s.rowpart[rp_index(1, il, tn, s.rows, s.ntn)] = 0.0;
+    s.rowpart[rp_index(2, il, tn, s.rows, s.ntn)] = 0.0;
+    s.rowpart[rp_index(3, il, tn, s.rows, s.ntn)] = a4;
+    double* tp = s.tilepart + size_t(blockIdx.y * gridDim.x + tn) * 4;
     tp[0] = a0;
     tp[1] = a1;
     tp[2] = a2;
@@ -421,13 +558,22 @@ int dense_cfg_for(int64_t n) {
 template <class C>
 static cudaError_t launch_cfg(const DevSolve& s, const CUtensorMap* amaps, const CUtensorMap* dmap,
                              const double* delta, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(dense_step_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    attr = true;
-  }
   const int ntm = int((s.rows + C::BM - 1) / C::BM);
-  dense_step_kernel<C><<<ntm * s.ntn, C::THREADS, C::SMEM, st>>>(s, amaps, dmap, delta, ntm);
+  if (s.cplx) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(dense_step_kernel<C, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+      attr = true;
+    }
+    dense_step_kernel<C, true><<<ntm * s.ntn, C::THREADS, C::SMEM, st>>>(s, amaps, dmap, delta, ntm);
+  } else {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(dense_step_kernel<C, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+      attr = true;
+    }
+    dense_step_kernel<C, false><<<ntm * s.ntn, C::THREADS, C::SMEM, st>>>(s, amaps, dmap, delta, ntm);
+  }
   return cudaGetLastError();
 }
 
@@ -443,11 +589,21 @@ int dense_step_ntiles(int64_t rows, int ntn, int cfg) {
   return int((rows + bm - 1) / bm) * ntn;
 }
 
-int dense_init_ntiles(int64_t rows, int ntn) { return int((rows + 31) / 32) * ntn; }
+int dense_init_ntiles(int64_t rows, int ntn, int cplx) {
+  return cplx ? int(rows) * ntn : int((rows + 31) / 32) * ntn;
+}
 
 cudaError_t launch_dense_init(const DevSolve& s, const double* delta, int cfg, cudaStream_t st) {
-  dim3 grid(s.ntn, unsigned((s.rows + 31) / 32));
   const int bn = dense_tile_n(cfg);
+  if (s.cplx) {
+    dim3 grid(s.ntn, unsigned(s.rows));
+    if (bn == 128)
+      dense_init_cplx_kernel<128><<<grid, 64, 0, st>>>(s, delta);
+    else
+      dense_init_cplx_kernel<64><<<grid, 32, 0, st>>>(s, delta);
+    return cudaGetLastError();
+  }
+  dim3 grid(s.ntn, unsigned((s.rows + 31) / 32));
   if (bn == 128)
     dense_init_kernel<128><<<grid, 256, 0, st>>>(s, delta);
   else

@@ -15,7 +15,11 @@ namespace dpt {
 struct DevSolve {
   int64_t n;            // global problem size (columns of A, length of theta)
   int64_t row0, rows;   // this rank's row shard [row0, row0 + rows)
-  int64_t ld;           // leading dimension (doubles) of A slots and dense Delta rows: n rounded up to even
+  int64_t ld;           // leading dimension (doubles) of A slots: ncol rounded up to even
+  int64_t ncol;         // real columns per iterate row: n (real) or 2n (complex, interleaved re/im)
+  int64_t ldd;          // leading dimension (doubles) of the device Delta rows
+  int cplx;             // complex FP64 (std::complex<double> layout everywhere)
+  double lambda_im;     // Im p.lambda (complex problems)
   int nslots;           // ring of iterates A_m in slot m % nslots
   int64_t slot_elems;   // doubles per slot (>= rows * ld; equal on every rank for the gather)
   int ntn;              // column partial blocks per row (rowpart leading dim)
@@ -29,7 +33,7 @@ struct DevSolve {
   double* dvec[2];      // d_m(i) = P(A_m)(i,i) for local rows, m % 2
   double* eps;          // [rows] read-offs of the latest folded iterate
   double* res;          // [rows]
-  double* rowpart;      // [3][rows][ntn] (sum d, max num, max den), see rp_index
+  double* rowpart;      // [4][rows][ntn] (sum d, max num, max den, sum d im), see rp_index
   double* tilepart;     // [ntiles][4] (max step, max |A|, nonfinite count, spare)
   int ntiles;
   double* blockpart;    // fold partials [fold_blocks][8]
@@ -45,14 +49,43 @@ struct DevSolve {
 
 __device__ __forceinline__ int launch_index(const DevSolve& s) { return s.state->j + 1; }
 
-// rowpart layout [3][rows][ntn]: a row's column-block partials are contiguous
-// so the fold reads them coalesced.  k: 0 = sum d, 1 = max num, 2 = max den.
+// rowpart layout [4][rows][ntn]: a row's column-block partials are contiguous
+// so the fold reads them coalesced.  k: 0 = sum d (re), 1 = max num, 2 = max den,
+// 3 = sum d (im, complex problems).
 __device__ __forceinline__ size_t rp_index(int k, int64_t row, int tn, int64_t rows, int ntn) {
   return (size_t(k) * size_t(rows) + size_t(row)) * size_t(ntn) + size_t(tn);
 }
 
 __device__ __forceinline__ double lam_of(const DevSolve& s, int j) {
-  return s.lam_table ? s.lam_table[j] : s.lambda;
+  return s.lam_table ? s.lam_table[s.cplx ? 2 * j : j] : s.lambda;
+}
+
+// ------------------------------------------------------- complex FP64 ----
+// The reference computes in std::complex<double> compiled without FMA
+// contraction: products (ac - bd, ad + bc) with separately rounded terms,
+// |z| = hypot, and 1/z by Smith's algorithm (libgcc __divdc3, normal range).
+struct cd {
+  double x, y;
+};
+__device__ __forceinline__ cd cmake(double x, double y) { return cd{x, y}; }
+__device__ __forceinline__ cd cmul(cd a, cd b) {
+  return cd{__dsub_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y)), __dadd_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x))};
+}
+__device__ __forceinline__ cd cadd(cd a, cd b) { return cd{__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y)}; }
+__device__ __forceinline__ cd csub(cd a, cd b) { return cd{__dsub_rn(a.x, b.x), __dsub_rn(a.y, b.y)}; }
+__device__ __forceinline__ double cabs_(cd a) { return hypot(a.x, a.y); }
+__device__ __forceinline__ cd crecip(cd z) {  // (1 + 0i) / z
+  const double c = z.x, d = z.y;
+  if (fabs(c) < fabs(d)) {
+    const double ratio = c / d, denom = __dadd_rn(__dmul_rn(c, ratio), d);
+    return cd{ratio / denom, -1.0 / denom};
+  }
+  const double ratio = d / c, denom = __dadd_rn(__dmul_rn(d, ratio), c);
+  return cd{1.0 / denom, -ratio / denom};
+}
+__device__ __forceinline__ bool cfinite(cd a) { return isfinite(a.x) && isfinite(a.y); }
+__device__ __forceinline__ cd lamc_of(const DevSolve& s, int j) {
+  return s.lam_table ? cd{s.lam_table[2 * j], s.lam_table[2 * j + 1]} : cd{s.lambda, s.lambda_im};
 }
 
 // ---------------------------------------------------------------- PTX ----

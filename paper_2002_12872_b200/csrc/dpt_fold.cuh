@@ -32,11 +32,22 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
 
 // Row fold of one row: column-block partials are summed (d) / maxed (num, den)
 // by `width` cooperating lanes in a fixed tree, so the result is deterministic.
-__device__ __forceinline__ void fold_row_store(const DevSolve& s, int64_t i, double d, double num, double den,
-                                               const double* dprev, double* dnext) {
+// Complex problems keep d, eps interleaved (re, im) per row; dim = Im d.
+__device__ __forceinline__ void fold_row_store(const DevSolve& s, int64_t i, double d, double dim, double num,
+                                               double den, const double* dprev, double* dnext) {
   const double r = num / fmax(den, 1e-300);  // kTinyDen, dpt.cpp:18, :40
-  s.eps[i] = __dadd_rn(s.theta[s.row0 + i], __dmul_rn(s.lambda, dprev[i]));
   s.res[i] = r;
+  if (s.cplx) {  // eps_i = d_i + lambda P(i,i) in complex arithmetic
+    const int64_t gi = s.row0 + i;
+    const cd e = cadd(cmake(s.theta[2 * gi], s.theta[2 * gi + 1]),
+                      cmul(cmake(s.lambda, s.lambda_im), cmake(dprev[2 * i], dprev[2 * i + 1])));
+    s.eps[2 * i] = e.x;
+    s.eps[2 * i + 1] = e.y;
+    dnext[2 * i] = d;
+    dnext[2 * i + 1] = dim;
+    return;
+  }
+  s.eps[i] = __dadd_rn(s.theta[s.row0 + i], __dmul_rn(s.lambda, dprev[i]));
   dnext[i] = d;
 }
 
@@ -52,7 +63,7 @@ static __device__ void cycle_sample_precheck(const DevSolve& s, double* sh) {
   const int j = st->j;
   int npast = j - 1;
   if (npast > s.opts.win - 1) npast = s.opts.win - 1;
-  const int64_t n = s.n, ld = s.ld;
+  const int64_t n = s.ncol, ld = s.ld;
   const int64_t elems = s.rows * n;
   const int64_t ns = elems < int64_t(blockDim.x) ? elems : int64_t(blockDim.x);
   const double* cur = s.slots + size_t(j % s.nslots) * size_t(s.slot_elems);

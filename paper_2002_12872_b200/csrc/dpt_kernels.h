@@ -15,7 +15,7 @@ int dense_cfg_for(int64_t n);
 int dense_tile_n(int cfg);
 int dense_tile_m(int cfg);
 int dense_step_ntiles(int64_t rows, int ntn, int cfg);
-int dense_init_ntiles(int64_t rows, int ntn);
+int dense_init_ntiles(int64_t rows, int ntn, int cplx);
 cudaError_t launch_dense_step(const DevSolve& s, const CUtensorMap* amaps, const CUtensorMap* dmap,
                               const double* delta, int cfg, cudaStream_t st);
 cudaError_t launch_dense_init(const DevSolve& s, const double* delta, int cfg, cudaStream_t st);
@@ -47,6 +47,12 @@ int single_ntn(int64_t n, int mode);
 int single_ntiles(int64_t n, int mode);
 cudaError_t launch_single_step(const DevSolve& s, const DevCsr& d, const double* dense, int64_t row, int mode,
                                cudaStream_t st);
+
+// complex_steps.cu (complex K2 / K3)
+int csr_cplx_ntiles(int64_t rows, int64_t n);
+cudaError_t launch_csr_step_cplx(const DevSolve& s, const DevSell& d, cudaStream_t st);
+int single_cplx_ntiles(int64_t n, int dense);
+cudaError_t launch_single_cplx(const DevSolve& s, const DevCsr& d, const double* B, int64_t row, cudaStream_t st);
 
 // fold.cu (K4)
 int fold_blocks(int64_t rows);

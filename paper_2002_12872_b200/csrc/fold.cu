@@ -45,48 +45,54 @@ __global__ void __launch_bounds__(kFoldThreads) fold_kernel(DevSolve s, int ntil
     // warp per row, lanes stride over the column blocks (coalesced: [rows][ntn])
     const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
     for (int64_t i = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); i < rows; i += warps) {
-      double d = 0.0, num = 0.0, den = 0.0;
+      double d = 0.0, dim = 0.0, num = 0.0, den = 0.0;
       for (int tn = lane; tn < ntn; tn += 32) {
         d += s.rowpart[rp_index(0, i, tn, rows, ntn)];
         num = fmax(num, s.rowpart[rp_index(1, i, tn, rows, ntn)]);
         den = fmax(den, s.rowpart[rp_index(2, i, tn, rows, ntn)]);
+        if (s.cplx) dim += s.rowpart[rp_index(3, i, tn, rows, ntn)];
       }
       d = warp_sum(d);
+      dim = warp_sum(dim);
       num = warp_max(num);
       den = warp_max(den);
       if (lane == 0) {
-        fold_row_store(s, i, d, num, den, dprev, dnext);
+        fold_row_store(s, i, d, dim, num, den, dprev, dnext);
         rmax = fmax(rmax, s.res[i]);
       }
     }
   } else {
     // few rows (the row map has one): block per row, threads over the blocks;
     // the three row folds share one reduction pass (one barrier)
-    __shared__ double red3[kFoldThreads / 32][3];
+    __shared__ double red3[kFoldThreads / 32][4];
     for (int64_t i = blockIdx.x; i < rows; i += gridDim.x) {
-      double d = 0.0, num = 0.0, den = 0.0;
+      double d = 0.0, dim = 0.0, num = 0.0, den = 0.0;
       for (int tn = threadIdx.x; tn < ntn; tn += blockDim.x) {
         d += s.rowpart[rp_index(0, i, tn, rows, ntn)];
         num = fmax(num, s.rowpart[rp_index(1, i, tn, rows, ntn)]);
         den = fmax(den, s.rowpart[rp_index(2, i, tn, rows, ntn)]);
+        if (s.cplx) dim += s.rowpart[rp_index(3, i, tn, rows, ntn)];
       }
       d = warp_sum(d);
+      dim = warp_sum(dim);
       num = warp_max(num);
       den = warp_max(den);
       if (lane == 0) {
         red3[threadIdx.x >> 5][0] = d;
         red3[threadIdx.x >> 5][1] = num;
         red3[threadIdx.x >> 5][2] = den;
+        red3[threadIdx.x >> 5][3] = dim;
       }
       __syncthreads();
       if (threadIdx.x == 0) {
-        double dd = 0.0, nn = 0.0, ee = 0.0;
+        double dd = 0.0, nn = 0.0, ee = 0.0, di = 0.0;
         for (int w = 0; w < int(blockDim.x >> 5); ++w) {
           dd += red3[w][0];
           nn = fmax(nn, red3[w][1]);
           ee = fmax(ee, red3[w][2]);
+          di += red3[w][3];
         }
-        fold_row_store(s, i, dd, nn, ee, dprev, dnext);
+        fold_row_store(s, i, dd, di, nn, ee, dprev, dnext);
         rmax = fmax(rmax, s.res[i]);
       }
       __syncthreads();
@@ -176,7 +182,7 @@ __global__ void __launch_bounds__(kFoldThreads) cycle_kernel(DevSolve s, int64_t
   const int win = s.opts.win;
   int npast = j - 1;
   if (npast > win - 1) npast = win - 1;
-  const int64_t n = s.n, ld = s.ld;
+  const int64_t n = s.ncol, ld = s.ld;
   const double tol = s.opts.tol;
   const size_t slot_elems = size_t(s.slot_elems);
   const double* cur = s.slots + size_t(j % s.nslots) * slot_elems;
@@ -239,14 +245,27 @@ __global__ void set_diag_kernel(DevSolve s, const double* __restrict__ delta, co
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < s.rows;
        i += int64_t(gridDim.x) * blockDim.x) {
     const int64_t gi = s.row0 + i;
-    double v = 0.0;
+    double v = 0.0, vi = 0.0;
     if (delta) {
-      v = delta[size_t(gi) * size_t(s.ld) + size_t(gi)];
+      if (s.cplx) {  // B image: Re D(i,i) = B[2i][2i], Im D(i,i) = B[2i+1][2i]
+        v = delta[size_t(2 * gi) * size_t(s.ldd) + size_t(2 * gi)];
+        vi = delta[size_t(2 * gi + 1) * size_t(s.ldd) + size_t(2 * gi)];
+      } else {
+        v = delta[size_t(gi) * size_t(s.ldd) + size_t(gi)];
+      }
     } else {
       for (int64_t p = rp[gi]; p < rp[gi + 1]; ++p)
-        if (cl[p] == gi) v = vl[p];
+        if (cl[p] == gi) {
+          v = s.cplx ? vl[2 * p] : vl[p];
+          vi = s.cplx ? vl[2 * p + 1] : 0.0;
+        }
     }
-    s.dvec[0][i] = v;
+    if (s.cplx) {
+      s.dvec[0][2 * i] = v;
+      s.dvec[0][2 * i + 1] = vi;
+    } else {
+      s.dvec[0][i] = v;
+    }
   }
 }
 
@@ -256,7 +275,7 @@ __global__ void identity_kernel(DevSolve s) {
   for (size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
        e += size_t(gridDim.x) * blockDim.x) {
     const int64_t r = int64_t(e / size_t(s.ld)), c = int64_t(e % size_t(s.ld));
-    s.slots[e] = (c < s.n && s.row0 + r == c) ? 1.0 : 0.0;
+    s.slots[e] = (c < s.ncol && (s.cplx ? 2 * (s.row0 + r) == c : s.row0 + r == c)) ? 1.0 : 0.0;
   }
 }
 
@@ -270,14 +289,35 @@ __global__ void rowdot_kernel(DevSolve s, const double* __restrict__ delta, cons
   for (int64_t i = wid; i < s.rows; i += nw) {
     const int64_t gi = s.row0 + i;
     const double* a = s.slots + size_t(i) * size_t(s.ld);
-    double v = 0.0;
-    if (delta) {
-      for (int64_t k = lane; k < s.n; k += 32) v = __fma_rn(a[k], delta[size_t(gi) * size_t(s.ld) + size_t(k)], v);
+    double v = 0.0, vi = 0.0;
+    if (s.cplx) {
+      cd acc = cmake(0.0, 0.0);
+      if (delta) {
+        const double* brow = delta + size_t(2 * gi) * size_t(s.ldd);  // (Re D(i,k), -Im D(i,k))
+        for (int64_t k = lane; k < s.n; k += 32)
+          acc = cadd(acc, cmul(cmake(a[2 * k], a[2 * k + 1]), cmake(brow[2 * k], -brow[2 * k + 1])));
+        acc.x = warp_sum(acc.x);
+        acc.y = warp_sum(acc.y);
+      } else if (lane == 0) {
+        for (int64_t q = rp[gi]; q < rp[gi + 1]; ++q)
+          acc = cadd(acc, cmul(cmake(vl[2 * q], vl[2 * q + 1]), cmake(a[2 * cl[q]], a[2 * cl[q] + 1])));
+      }
+      v = acc.x;
+      vi = acc.y;
+    } else if (delta) {
+      for (int64_t k = lane; k < s.n; k += 32) v = __fma_rn(a[k], delta[size_t(gi) * size_t(s.ldd) + size_t(k)], v);
       v = warp_sum(v);
     } else if (lane == 0) {
       for (int64_t q = rp[gi]; q < rp[gi + 1]; ++q) v = __fma_rn(vl[q], a[cl[q]], v);
     }
-    if (lane == 0) s.dvec[0][i] = v;
+    if (lane == 0) {
+      if (s.cplx) {
+        s.dvec[0][2 * i] = v;
+        s.dvec[0][2 * i + 1] = vi;
+      } else {
+        s.dvec[0][i] = v;
+      }
+    }
   }
 }
 

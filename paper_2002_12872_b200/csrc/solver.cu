@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <map>
+#include <unordered_map>
 #include <cmath>
 #include <limits>
 #include <memory>
@@ -261,6 +262,80 @@ bool find_degenerate_row(int64_t n, const double* d, int64_t row, double tol, in
   return false;
 }
 
+// Complex levels (interleaved re, im): the same policies with |z| = hypot.
+double spread_of_c(int64_t n, const double* d) {  // bounding box, partition.cpp:42-53
+  if (n == 0) return 0.0;
+  double rl = d[0], rh = d[0], il = d[1], ih = d[1];
+  for (int64_t i = 0; i < n; ++i) {
+    rl = std::min(rl, d[2 * i]);
+    rh = std::max(rh, d[2 * i]);
+    il = std::min(il, d[2 * i + 1]);
+    ih = std::max(ih, d[2 * i + 1]);
+  }
+  return std::hypot(rh - rl, ih - il);
+}
+
+double threshold_of_c(int64_t n, const double* d, double tol) { return tol * std::max(1.0, spread_of_c(n, d)); }
+
+// First (i, j) in row-major order with |d_i - d_j| <= thresh, for complex
+// levels.  Points closer than thresh sit in neighbouring cells of a grid of
+// pitch thresh, so a hash of cells answers "does i have a partner" in O(1);
+// O(n^2) fallback when the grid would overflow or thresh is 0.
+bool find_degenerate_c(int64_t n, const double* d, double tol, int64_t* bi, int64_t* bj) {
+  if (n < 2) return false;
+  const double t = threshold_of_c(n, d, tol);
+  auto close = [&](int64_t a, int64_t b) { return std::hypot(d[2 * a] - d[2 * b], d[2 * a + 1] - d[2 * b + 1]) <= t; };
+  double amax = 0.0;
+  for (int64_t i = 0; i < 2 * n; ++i)
+    if (std::isfinite(d[i])) amax = std::max(amax, std::fabs(d[i]));
+  const bool grid = t > 0.0 && amax / t < 1e15;
+  if (!grid) {
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t j = 0; j < n; ++j)
+        if (i != j && close(i, j)) {
+          *bi = i;
+          *bj = j;
+          return true;
+        }
+    return false;
+  }
+  std::unordered_map<uint64_t, std::vector<int64_t>> cells;
+  auto key = [](int64_t x, int64_t y) { return (uint64_t(x) * 0x9E3779B97F4A7C15ull) ^ uint64_t(y); };
+  auto cx = [&](int64_t i) { return int64_t(std::floor(d[2 * i] / t)); };
+  auto cy = [&](int64_t i) { return int64_t(std::floor(d[2 * i + 1] / t)); };
+  for (int64_t i = 0; i < n; ++i)
+    if (std::isfinite(d[2 * i]) && std::isfinite(d[2 * i + 1])) cells[key(cx(i), cy(i))].push_back(i);
+  for (int64_t i = 0; i < n; ++i) {
+    if (!std::isfinite(d[2 * i]) || !std::isfinite(d[2 * i + 1])) continue;
+    int64_t best = std::numeric_limits<int64_t>::max();
+    for (int64_t ox = -2; ox <= 2; ++ox)
+      for (int64_t oy = -2; oy <= 2; ++oy) {
+        auto it = cells.find(key(cx(i) + ox, cy(i) + oy));
+        if (it == cells.end()) continue;
+        for (int64_t j : it->second)
+          if (j != i && close(i, j)) best = std::min(best, j);
+      }
+    if (best != std::numeric_limits<int64_t>::max()) {
+      *bi = i;
+      *bj = best;
+      return true;
+    }
+  }
+  return false;
+}
+
+bool find_degenerate_row_c(int64_t n, const double* d, int64_t row, double tol, int64_t* bj) {
+  const double t = threshold_of_c(n, d, tol);
+  for (int64_t m = 0; m < n; ++m) {
+    if (m == row) continue;
+    if (std::hypot(d[2 * row] - d[2 * m], d[2 * row + 1] - d[2 * m + 1]) <= t) {
+      *bj = m;
+      return true;
+    }
+  }
+  return false;
+}
+
 int effective_window(int requested, int64_t n) {  // dpt.cpp:83-90
   if (requested <= 0) return 0;
   const double entries = double(n) * double(n);
@@ -270,12 +345,14 @@ int effective_window(int requested, int64_t n) {  // dpt.cpp:83-90
   return win < 2 ? 0 : win;
 }
 
-void degenerate_error(dpt_error_info* err, int64_t i, int64_t j, const double* d) {
+void degenerate_error(dpt_error_info* err, int64_t i, int64_t j, const double* d, bool cplx = false) {
   if (err) {
     err->i = i;
     err->j = j;
-    err->ei = d[i];
-    err->ej = d[j];
+    err->ei = cplx ? d[2 * i] : d[i];
+    err->ej = cplx ? d[2 * j] : d[j];
+    err->ei_im = cplx ? d[2 * i + 1] : 0.0;
+    err->ej_im = cplx ? d[2 * j + 1] : 0.0;
   }
   set_err(err, DPT_ERR_DEGENERATE,
           "degenerate spectrum: levels " + std::to_string(i) + " and " + std::to_string(j) +
@@ -286,6 +363,10 @@ void degenerate_error(dpt_error_info* err, int64_t i, int64_t j, const double* d
 // ------------------------------------------------------ device problem ----
 struct DevProblem {
   int64_t n = 0, ld = 0, nnz = 0;
+  int64_t ncol = 0;  // real columns per iterate row (n, or 2n when complex)
+  int64_t ldd = 0;   // leading dimension of the device Delta image
+  int cplx = 0;
+  double lambda_im = 0.0;
   int kind = DPT_DELTA_DENSE;
   std::vector<double> d_host;  // theta on the host (gap policy)
   DBuf theta, delta, rowptr, cols, vals;
@@ -337,8 +418,9 @@ void build_sell(DevProblem& dp, const std::vector<int64_t>& rp, const std::vecto
     off[size_t(sl) + 1] = off[size_t(sl)] + 32 * width;
   }
   const int64_t total = off[size_t(ns)];
+  const int cx = dp.cplx ? 2 : 1;  // complex values are interleaved (re, im)
   std::vector<int32_t> sc(size_t(std::max<int64_t>(total, 1)), 0);
-  std::vector<double> sv(size_t(std::max<int64_t>(total, 1)), 0.0);
+  std::vector<double> sv(size_t(cx * std::max<int64_t>(total, 1)), 0.0);
   for (int64_t t = 0; t < ns * 32; ++t) {
     const int32_t j = lcol[size_t(t)];
     if (j < 0) continue;
@@ -346,7 +428,7 @@ void build_sell(DevProblem& dp, const std::vector<int64_t>& rp, const std::vecto
     for (int64_t q = 0; q < llen[size_t(t)]; ++q) {
       const int64_t src = rp[size_t(j)] + q, dst = off[size_t(sl)] + 32 * q + L;
       sc[size_t(dst)] = cl[size_t(src)];
-      sv[size_t(dst)] = vl[size_t(src)];
+      for (int c = 0; c < cx; ++c) sv[size_t(cx * dst + c)] = vl[size_t(cx * src + c)];
     }
   }
   dp.nslices = ns;
@@ -393,22 +475,52 @@ void validate(const dpt_problem* p, dpt_error_info* err) {
 void upload(DevProblem& dp, dpt_ctx* ctx, const dpt_problem* p, dpt_error_info* err, bool sell = false) {
   validate(p, err);
   const int64_t n = p->n;
+  const int cx = p->is_complex ? 2 : 1;  // doubles per scalar
   dp.n = n;
-  dp.ld = (n + 1) & ~int64_t(1);
+  dp.cplx = p->is_complex ? 1 : 0;
+  dp.lambda_im = p->is_complex ? p->lambda_im : 0.0;
+  dp.ncol = cx * n;
+  dp.ld = (dp.ncol + 1) & ~int64_t(1);
   dp.kind = p->delta_kind;
   const cudaMemcpyKind k = p->mem == DPT_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  const cudaMemcpyKind hk = p->mem == DPT_MEM_DEVICE ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost;
   cudaStream_t st = ctx->stream;
-  dp.d_host.resize(size_t(n));
-  if (n) CK(cudaMemcpy(dp.d_host.data(), p->d, size_t(n) * 8, p->mem == DPT_MEM_DEVICE ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost));
-  dalloc(dp.theta, size_t(n) * 8, err);
-  if (n) CK(cudaMemcpyAsync(dp.theta.p, dp.d_host.data(), size_t(n) * 8, cudaMemcpyHostToDevice, st));
+  dp.d_host.resize(size_t(cx * n));
+  if (n) CK(cudaMemcpy(dp.d_host.data(), p->d, size_t(cx * n) * 8, hk));
+  dalloc(dp.theta, size_t(cx * n) * 8, err);
+  if (n) CK(cudaMemcpyAsync(dp.theta.p, dp.d_host.data(), size_t(cx * n) * 8, cudaMemcpyHostToDevice, st));
   if (p->delta_kind == DPT_DELTA_DENSE) {
-    dalloc(dp.delta, size_t(n) * size_t(dp.ld) * 8 + 64, err);
-    if (n) {
-      if (dp.ld == n)
-        CK(cudaMemcpyAsync(dp.delta.p, p->delta, size_t(n) * size_t(n) * 8, k, st));
-      else
-        CK(cudaMemcpy2DAsync(dp.delta.p, size_t(dp.ld) * 8, p->delta, size_t(n) * 8, size_t(n) * 8, size_t(n), k, st));
+    if (dp.cplx) {
+      // real image B (2n x 2n): row 2j = (Re D(j,k), -Im D(j,k))_k, row 2j+1 = (Im D(j,k), Re D(j,k))_k,
+      // so the real NT GEMM of the interleaved iterate with B yields (Re P, Im P) pairs.
+      dp.ldd = 2 * n;
+      std::vector<double> D(size_t(2 * n) * size_t(n));
+      if (n) CK(cudaMemcpy(D.data(), p->delta, size_t(2 * n) * size_t(n) * 8, hk));
+      std::vector<double> B(size_t(2 * n) * size_t(2 * n));
+      for (int64_t j = 0; j < n; ++j) {
+        double* r0 = B.data() + size_t(2 * j) * size_t(2 * n);
+        double* r1 = r0 + 2 * n;
+        const double* src = D.data() + size_t(j) * size_t(2 * n);
+        for (int64_t q = 0; q < n; ++q) {
+          const double re = src[2 * q], im = src[2 * q + 1];
+          r0[2 * q] = re;
+          r0[2 * q + 1] = -im;
+          r1[2 * q] = im;
+          r1[2 * q + 1] = re;
+        }
+      }
+      dalloc(dp.delta, B.size() * 8 + 64, err);
+      if (n) CK(cudaMemcpyAsync(dp.delta.p, B.data(), B.size() * 8, cudaMemcpyHostToDevice, st));
+      CK(cudaStreamSynchronize(st));  // B goes out of scope
+    } else {
+      dp.ldd = dp.ld;
+      dalloc(dp.delta, size_t(n) * size_t(dp.ldd) * 8 + 64, err);
+      if (n) {
+        if (dp.ldd == n)
+          CK(cudaMemcpyAsync(dp.delta.p, p->delta, size_t(n) * size_t(n) * 8, k, st));
+        else
+          CK(cudaMemcpy2DAsync(dp.delta.p, size_t(dp.ldd) * 8, p->delta, size_t(n) * 8, size_t(n) * 8, size_t(n), k, st));
+      }
     }
   } else {
     int64_t nnz = p->nnz;
@@ -419,29 +531,28 @@ void upload(DevProblem& dp, dpt_ctx* ctx, const dpt_problem* p, dpt_error_info* 
     }
     dp.nnz = nnz;
     {
-      const cudaMemcpyKind hk = p->mem == DPT_MEM_DEVICE ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost;
       std::vector<int64_t> rp(size_t(n + 1));
       CK(cudaMemcpy(rp.data(), p->rowptr, size_t(n + 1) * 8, hk));
-      bool u = n > 0;
+      bool u = n > 0 && !dp.cplx;
       for (int64_t i = 0; i <= n && u; ++i) u = rp[size_t(i)] == 16 * i;
       dp.uniform16 = u ? 1 : 0;
       if (sell) {
         std::vector<int32_t> cl(static_cast<size_t>(nnz));
-        std::vector<double> vl(static_cast<size_t>(nnz));
+        std::vector<double> vl(static_cast<size_t>(cx * nnz));
         if (nnz) {
           CK(cudaMemcpy(cl.data(), p->cols, size_t(nnz) * 4, hk));
-          CK(cudaMemcpy(vl.data(), p->vals, size_t(nnz) * 8, hk));
+          CK(cudaMemcpy(vl.data(), p->vals, size_t(cx * nnz) * 8, hk));
         }
         build_sell(dp, rp, cl, vl, st, err);
       }
     }
     dalloc(dp.rowptr, size_t(n + 1) * 8, err);
     dalloc(dp.cols, size_t(nnz) * 4, err);
-    dalloc(dp.vals, size_t(nnz) * 8, err);
+    dalloc(dp.vals, size_t(cx * nnz) * 8, err);
     CK(cudaMemcpyAsync(dp.rowptr.p, p->rowptr, size_t(n + 1) * 8, k, st));
     if (nnz) {
       CK(cudaMemcpyAsync(dp.cols.p, p->cols, size_t(nnz) * 4, k, st));
-      CK(cudaMemcpyAsync(dp.vals.p, p->vals, size_t(nnz) * 8, k, st));
+      CK(cudaMemcpyAsync(dp.vals.p, p->vals, size_t(cx * nnz) * 8, k, st));
     }
   }
 }
@@ -466,6 +577,11 @@ void make_work(Work& w, dpt_ctx* ctx, DevProblem& dp, Mode mode, int64_t row0, i
   DevSolve& s = w.s;
   s.n = dp.n;
   s.ld = dp.ld;
+  s.ncol = dp.ncol;
+  s.ldd = dp.ldd;
+  s.cplx = dp.cplx;
+  s.lambda_im = dp.lambda_im;
+  const int cx = dp.cplx ? 2 : 1;
   s.row0 = row0;
   s.rows = rows;
   s.nslots = nslots;
@@ -476,12 +592,15 @@ void make_work(Work& w, dpt_ctx* ctx, DevProblem& dp, Mode mode, int64_t row0, i
   int ntiles_aux = 1;
   if (mode == MODE_DENSE_FULL) {
     dp.big = dense_cfg_for(dp.n);
-    s.ntn = int((dp.n + dense_tile_n(dp.big) - 1) / dense_tile_n(dp.big));
+    s.ntn = int((dp.ncol + dense_tile_n(dp.big) - 1) / dense_tile_n(dp.big));
     w.ntiles_step = dense_step_ntiles(rows, s.ntn, dp.big);
-    ntiles_aux = dense_init_ntiles(rows, s.ntn);
+    ntiles_aux = dense_init_ntiles(rows, s.ntn, dp.cplx);
   } else if (mode == MODE_CSR_FULL) {
     s.ntn = csr_ntn(dp.n);
-    w.ntiles_step = csr_step_ntiles(rows, dp.n);
+    w.ntiles_step = dp.cplx ? csr_cplx_ntiles(rows, dp.n) : csr_step_ntiles(rows, dp.n);
+  } else if (dp.cplx) {
+    s.ntn = single_cplx_ntiles(dp.n, dp.kind == DPT_DELTA_DENSE);
+    w.ntiles_step = s.ntn;
   } else {
     const int sm = single_mode(dp.kind == DPT_DELTA_DENSE, dp.uniform16);
     s.ntn = single_ntn(dp.n, sm);
@@ -491,10 +610,10 @@ void make_work(Work& w, dpt_ctx* ctx, DevProblem& dp, Mode mode, int64_t row0, i
   const size_t slot_elems = size_t(std::max<int64_t>(rows_alloc, 1)) * size_t(dp.ld);
   s.slot_elems = int64_t(slot_elems);
   dalloc(w.slots, size_t(nslots) * slot_elems * 8 + 64, err);
-  dalloc(w.dvec, size_t(2) * size_t(rows) * 8, err);
-  dalloc(w.eps, size_t(std::max<int64_t>(rows_alloc, 1)) * 8, err);
+  dalloc(w.dvec, size_t(2 * cx) * size_t(rows) * 8, err);
+  dalloc(w.eps, size_t(cx) * size_t(std::max<int64_t>(rows_alloc, 1)) * 8, err);
   dalloc(w.res, size_t(std::max<int64_t>(rows_alloc, 1)) * 8, err);
-  dalloc(w.rowpart, size_t(3) * size_t(s.ntn) * size_t(rows) * 8, err);
+  dalloc(w.rowpart, size_t(4) * size_t(s.ntn) * size_t(rows) * 8, err);
   dalloc(w.tilepart, size_t(s.ntiles) * 4 * 8, err);
   dalloc(w.blockpart, size_t(fold_blocks(rows) + 512) * 8 * 8, err);
   dalloc(w.stats, DPT_NSTATS * 8, err);
@@ -506,7 +625,7 @@ void make_work(Work& w, dpt_ctx* ctx, DevProblem& dp, Mode mode, int64_t row0, i
   s.theta = dp.theta.as<double>();
   s.slots = w.slots.as<double>();
   s.dvec[0] = w.dvec.as<double>();
-  s.dvec[1] = w.dvec.as<double>() + rows;
+  s.dvec[1] = w.dvec.as<double>() + cx * rows;
   s.eps = w.eps.as<double>();
   s.res = w.res.as<double>();
   s.rowpart = w.rowpart.as<double>();
@@ -520,7 +639,8 @@ void make_work(Work& w, dpt_ctx* ctx, DevProblem& dp, Mode mode, int64_t row0, i
   cudaStream_t st = ctx->stream;
   CK(cudaMemsetAsync(w.counter.p, 0, 16, st));
   CK(cudaMemsetAsync(w.state.p, 0, sizeof(dpt_sm_state), st));
-  CK(cudaMemsetAsync(w.dvec.p, 0, size_t(2) * size_t(rows) * 8, st));
+  CK(cudaMemsetAsync(w.dvec.p, 0, size_t(2 * cx) * size_t(rows) * 8, st));
+  CK(cudaMemsetAsync(w.rowpart.p, 0, size_t(4) * size_t(s.ntn) * size_t(rows) * 8, st));
   std::vector<double> ones(DPT_NSTATS, 1.0);
   CK(cudaMemcpyAsync(w.stats.p, ones.data(), DPT_NSTATS * 8, cudaMemcpyHostToDevice, st));
   if (lam_tab) {
@@ -538,7 +658,7 @@ void make_work(Work& w, dpt_ctx* ctx, DevProblem& dp, Mode mode, int64_t row0, i
     const int box = dense_tile_m(dp.big);
     std::vector<CUtensorMap> maps(static_cast<size_t>(nslots));
     for (int q = 0; q < nslots; ++q) {
-      if (make_tmap_rowmajor(&maps[size_t(q)], s.slots + size_t(q) * slot_elems, dp.n, rows, dp.ld, box) != 0) {
+      if (make_tmap_rowmajor(&maps[size_t(q)], s.slots + size_t(q) * slot_elems, dp.ncol, rows, dp.ld, box) != 0) {
         set_err(err, DPT_ERR_CUDA, "cuTensorMapEncodeTiled failed for an iterate slot");
         throw Fail{DPT_ERR_CUDA};
       }
@@ -547,7 +667,7 @@ void make_work(Work& w, dpt_ctx* ctx, DevProblem& dp, Mode mode, int64_t row0, i
     CK(cudaMemcpyAsync(w.amaps.p, maps.data(), sizeof(CUtensorMap) * size_t(nslots), cudaMemcpyHostToDevice, st));
     if (!dp.dmap.p) {
       CUtensorMap dm;
-      if (make_tmap_rowmajor(&dm, dp.delta.as<double>(), dp.n, dp.n, dp.ld, dense_tile_n(dp.big)) != 0) {
+      if (make_tmap_rowmajor(&dm, dp.delta.as<double>(), dp.ncol, dp.ncol, dp.ldd, dense_tile_n(dp.big)) != 0) {
         set_err(err, DPT_ERR_CUDA, "cuTensorMapEncodeTiled failed for Delta");
         throw Fail{DPT_ERR_CUDA};
       }
@@ -597,8 +717,13 @@ void step_launch(dpt_ctx* ctx, Work& w, DevProblem& dp, Mode mode, int64_t row, 
   if (mode == MODE_DENSE_FULL)
     CK(launch_dense_step(w.s, w.amaps.as<CUtensorMap>(), dp.dmap.as<CUtensorMap>(), dp.delta.as<double>(),
                          dp.big, ctx->stream));
+  else if (mode == MODE_CSR_FULL && dp.cplx)
+    CK(launch_csr_step_cplx(w.s, dp.sell(), ctx->stream));
   else if (mode == MODE_CSR_FULL)
     CK(launch_csr_step(w.s, dp.sell(), ctx->stream));
+  else if (dp.cplx)
+    CK(launch_single_cplx(w.s, dp.csr(), dp.kind == DPT_DELTA_DENSE ? dp.delta.as<double>() : nullptr, row,
+                          ctx->stream));
   else
     CK(launch_single_step(w.s, dp.csr(), dp.kind == DPT_DELTA_DENSE ? dp.delta.as<double>() : nullptr, row,
                           single_mode(dp.kind == DPT_DELTA_DENSE, dp.uniform16), ctx->stream));
@@ -613,12 +738,12 @@ void step_launch(dpt_ctx* ctx, Work& w, DevProblem& dp, Mode mode, int64_t row, 
 void drive(dpt_ctx* ctx, Work& w, DevProblem& dp, Mode mode, int64_t row, int total, bool first_is_init,
            dpt_trace_fn trace, void* user, dpt_error_info* err) {
   cudaStream_t st = ctx->stream;
-  const int64_t cycle_elems = (mode == MODE_SINGLE) ? dp.n : w.s.rows * dp.n;
+  const int64_t cycle_elems = (mode == MODE_SINGLE) ? dp.ncol : w.s.rows * dp.ncol;
   int issued = 0;
   if (first_is_init) {
     CK(launch_dense_init(w.s, dp.delta.as<double>(), dp.big, st));
     ctx->launches += 1;
-    post_step(ctx, w, dense_init_ntiles(w.s.rows, w.s.ntn), cycle_elems, err);
+    post_step(ctx, w, dense_init_ntiles(w.s.rows, w.s.ntn, w.s.cplx), cycle_elems, err);
     issued = 1;
   }
   dpt_sm_state* snap = w.h_state;  // [2] pinned snapshots, one per chunk in flight
@@ -694,10 +819,10 @@ void copy_slot_out(double* dst, const Work& w, const DevProblem& dp, int slot, i
   if (!dst || dp.n == 0) return;
   const double* src = w.s.slots + size_t(slot) * size_t(w.s.slot_elems);
   const cudaMemcpyKind k = out_mem == DPT_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-  if (dp.ld == dp.n)
-    CK(cudaMemcpyAsync(dst, src, size_t(w.s.rows) * size_t(dp.n) * 8, k, st));
+  if (dp.ld == dp.ncol)
+    CK(cudaMemcpyAsync(dst, src, size_t(w.s.rows) * size_t(dp.ncol) * 8, k, st));
   else
-    CK(cudaMemcpy2DAsync(dst, size_t(dp.n) * 8, src, size_t(dp.ld) * 8, size_t(dp.n) * 8, size_t(w.s.rows), k, st));
+    CK(cudaMemcpy2DAsync(dst, size_t(dp.ncol) * 8, src, size_t(dp.ld) * 8, size_t(dp.ncol) * 8, size_t(w.s.rows), k, st));
 }
 
 void fill_nan(double* dst, size_t count, int out_mem, cudaStream_t st, dpt_error_info* err) {
@@ -740,10 +865,10 @@ void put_slot(Work& w, const DevProblem& dp, int slot, const double* a, int mem,
   double* dst = w.s.slots + size_t(slot) * size_t(w.s.slot_elems);
   const cudaMemcpyKind k = mem == DPT_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   CK(cudaMemsetAsync(dst, 0, size_t(w.s.rows) * size_t(dp.ld) * 8, st));
-  if (dp.ld == dp.n)
-    CK(cudaMemcpyAsync(dst, a, size_t(w.s.rows) * size_t(dp.n) * 8, k, st));
+  if (dp.ld == dp.ncol)
+    CK(cudaMemcpyAsync(dst, a, size_t(w.s.rows) * size_t(dp.ncol) * 8, k, st));
   else
-    CK(cudaMemcpy2DAsync(dst, size_t(dp.ld) * 8, a, size_t(dp.n) * 8, size_t(dp.n) * 8, size_t(w.s.rows), k, st));
+    CK(cudaMemcpy2DAsync(dst, size_t(dp.ld) * 8, a, size_t(dp.ncol) * 8, size_t(dp.ncol) * 8, size_t(w.s.rows), k, st));
   CK(cudaStreamSynchronize(st));  // `a` may be pageable host memory owned by the caller
 }
 
@@ -776,15 +901,16 @@ void gather_rows(dpt_ctx* ctx, const Work& w, const DevProblem& dp, int slot, do
     throw Fail{DPT_ERR_NCCL};
   }
   const cudaMemcpyKind k = out_mem == DPT_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-  CK(cudaMemcpy2DAsync(dst, size_t(dp.n) * 8, all.p, size_t(dp.ld) * 8, size_t(dp.n) * 8, size_t(dp.n), k, st));
+  CK(cudaMemcpy2DAsync(dst, size_t(dp.ncol) * 8, all.p, size_t(dp.ld) * 8, size_t(dp.ncol) * 8, size_t(dp.n), k, st));
   CK(cudaStreamSynchronize(st));
 }
 
 void gather_vec(dpt_ctx* ctx, const Work& w, const double* src, double* dst, int out_mem, int64_t n,
-                dpt_error_info* err) {
+                dpt_error_info* err, int width = 1) {
   if (!dst) return;
   cudaStream_t st = ctx->stream;
-  const int64_t per = w.s.slot_elems / w.s.ld;
+  const int64_t per = width * (w.s.slot_elems / w.s.ld);
+  n *= width;
   DBuf all;
   dalloc(all, size_t(ctx->world) * size_t(per) * 8, err);
   NcclApi* api = nccl_api();
@@ -806,11 +932,19 @@ dpt_options opts_or_default(const dpt_options* o) {
 }
 
 std::vector<double> host_levels(const dpt_problem* p, dpt_error_info* err) {
-  std::vector<double> dh(size_t(p->n));
+  const size_t cnt = size_t(p->n) * (p->is_complex ? 2 : 1);  // interleaved when complex
+  std::vector<double> dh(cnt);
   if (p->n)
-    CK(cudaMemcpy(dh.data(), p->d, size_t(p->n) * 8,
-                  p->mem == DPT_MEM_DEVICE ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost));
+    CK(cudaMemcpy(dh.data(), p->d, cnt * 8, p->mem == DPT_MEM_DEVICE ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost));
   return dh;
+}
+
+// build_theta's degeneracy policy for real or complex levels.
+void check_levels(const dpt_problem* p, const std::vector<double>& dh, double tol, dpt_error_info* err) {
+  int64_t bi, bj;
+  const bool hit = p->is_complex ? find_degenerate_c(p->n, dh.data(), tol, &bi, &bj)
+                                 : find_degenerate(p->n, dh.data(), tol, &bi, &bj);
+  if (hit) degenerate_error(err, bi, bj, dh.data(), p->is_complex != 0);
 }
 
 void fill_report(dpt_ctx* ctx, dpt_report* rep, int status, int iters, double step) {
@@ -829,7 +963,8 @@ void fill_report(dpt_ctx* ctx, dpt_report* rep, int status, int iters, double st
 // run_full (dpt.cpp:92-192); fixed_k >= 0 selects iterate_fixed (:381-387).
 int run_full(dpt_ctx* ctx, const dpt_problem* p, const dpt_options* opts_in, bool ramped, double alpha,
              int fixed_k, double fixed_lambda, dpt_trace_fn trace, void* user, double* a_out,
-             double* eig_out, double* res_out, int out_mem, dpt_report* rep, dpt_error_info* err) {
+             double* eig_out, double* res_out, int out_mem, dpt_report* rep, dpt_error_info* err,
+             double fixed_lambda_im = 0.0) {
   const dpt_options o = opts_or_default(opts_in);
   Guard g(ctx);
   validate(p, err);
@@ -840,11 +975,12 @@ int run_full(dpt_ctx* ctx, const dpt_problem* p, const dpt_options* opts_in, boo
     throw Fail{DPT_ERR_SHAPE};
   }
   std::vector<double> dh = host_levels(p, err);
-  int64_t bi, bj;
   // iterate_fixed builds theta with the default tolerance (dpt.cpp:383)
-  if (find_degenerate(n, dh.data(), fixed ? 1e-12 : o.degeneracy_tol, &bi, &bj)) degenerate_error(err, bi, bj, dh.data());
+  check_levels(p, dh, fixed ? 1e-12 : o.degeneracy_tol, err);
   DevProblem dp;
   upload(dp, ctx, p, err, p->delta_kind == DPT_DELTA_CSR);
+  const int cx = dp.cplx ? 2 : 1;
+  if (fixed) dp.lambda_im = fixed_lambda_im;
   const Mode mode = p->delta_kind == DPT_DELTA_DENSE ? MODE_DENSE_FULL : MODE_CSR_FULL;
   const int win = fixed ? 0 : effective_window(o.cycle_window, n);
   const int nslots = win > 0 ? win + 1 : 2;
@@ -856,13 +992,21 @@ int run_full(dpt_ctx* ctx, const dpt_problem* p, const dpt_options* opts_in, boo
   const double lam = fixed ? fixed_lambda : p->lambda;
   std::vector<double> lam_tab;
   std::vector<int> set_tab;
-  if (ramped) {
-    lam_tab.resize(size_t(total) + 2);
-    set_tab.resize(size_t(total) + 2);
-    for (size_t k = 0; k < lam_tab.size(); ++k) {
-      const double lk = k == 0 ? 0.0 : lam * (1.0 - std::pow(alpha, double(int(k) - 1)));  // dpt.cpp:131-132
-      lam_tab[k] = lk;
-      set_tab[k] = std::fabs(lk - lam) <= o.tol * std::fabs(lam) ? 1 : 0;  // :133-134
+  if (ramped) {  // lambda_k = lambda (1 - alpha^(k-1)) in complex arithmetic (dpt.cpp:131-134)
+    const size_t nk = size_t(total) + 2;
+    lam_tab.resize(nk * size_t(cx));
+    set_tab.resize(nk);
+    const double lim = dp.lambda_im;
+    for (size_t k = 0; k < nk; ++k) {
+      const double f = k == 0 ? 0.0 : 1.0 - std::pow(alpha, double(int(k) - 1));
+      const double lr = lam * f, li = lim * f;
+      if (cx == 2) {
+        lam_tab[2 * k] = lr;
+        lam_tab[2 * k + 1] = li;
+      } else {
+        lam_tab[k] = lr;
+      }
+      set_tab[k] = std::hypot(lr - lam, li - lim) <= o.tol * std::hypot(lam, lim) ? 1 : 0;
     }
     set_tab[0] = 1;
   }
@@ -917,14 +1061,14 @@ int run_full(dpt_ctx* ctx, const dpt_problem* p, const dpt_options* opts_in, boo
     gather_rows(ctx, w, dp, final_iter % nslots, a_out, out_mem, err);
     if (readoffs) {
       if (ctx->comm) {
-        gather_vec(ctx, w, w.s.eps, eig_out, out_mem, n, err);
+        gather_vec(ctx, w, w.s.eps, eig_out, out_mem, n, err, cx);
         gather_vec(ctx, w, w.s.res, res_out, out_mem, n, err);
       } else {
-        copy_out(eig_out, w.s.eps, size_t(n), out_mem, st, err);
+        copy_out(eig_out, w.s.eps, size_t(cx * n), out_mem, st, err);
         copy_out(res_out, w.s.res, size_t(n), out_mem, st, err);
       }
     } else {
-      fill_nan(eig_out, size_t(n), out_mem, st, err);
+      fill_nan(eig_out, size_t(cx * n), out_mem, st, err);  // cdouble{nan, nan} (dpt.cpp:121-124)
       fill_nan(res_out, size_t(n), out_mem, st, err);
     }
   }
@@ -938,7 +1082,8 @@ int run_full(dpt_ctx* ctx, const dpt_problem* p, const dpt_options* opts_in, boo
 // eig_out / res_out the read-offs of `a` itself (residuals_of, dpt.cpp:23-44)
 // are returned as well (homotopy_solve's final report).
 int run_step_full(dpt_ctx* ctx, const dpt_problem* p, const double* a, const double* gap, double lambda,
-                  double* out, int io_mem, double* eig_out, double* res_out, dpt_error_info* err) {
+                  double* out, int io_mem, double* eig_out, double* res_out, dpt_error_info* err,
+                  double lambda_im = 0.0) {
   Guard g(ctx);
   validate(p, err);
   if (ctx->comm) {
@@ -953,12 +1098,14 @@ int run_step_full(dpt_ctx* ctx, const dpt_problem* p, const double* a, const dou
   dpt_sm_options so{};
   so.max_iter = 1;
   Work w;
+  dp.lambda_im = lambda_im;
   make_work(w, ctx, dp, mode, 0, n, n, 2, 1, nullptr, nullptr, so, lambda, 1, err);
   DBuf gbuf;
-  if (gap) {
+  if (gap) {  // caller GapMatrix, row-major n x n (interleaved complex when is_complex)
     dalloc(gbuf, size_t(n) * size_t(dp.ld) * 8, err);
     const cudaMemcpyKind k = io_mem == DPT_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    CK(cudaMemcpy2DAsync(gbuf.p, size_t(dp.ld) * 8, gap, size_t(n) * 8, size_t(n) * 8, size_t(n), k, ctx->stream));
+    CK(cudaMemcpy2DAsync(gbuf.p, size_t(dp.ld) * 8, gap, size_t(dp.ncol) * 8, size_t(dp.ncol) * 8, size_t(n), k,
+                         ctx->stream));
     w.s.gapmat = gbuf.as<double>();
   }
   put_slot(w, dp, 0, a, io_mem, ctx->stream, err);
@@ -967,7 +1114,7 @@ int run_step_full(dpt_ctx* ctx, const dpt_problem* p, const double* a, const dou
   step_launch(ctx, w, dp, mode, 0, err);
   post_step(ctx, w, w.ntiles_step, 0, err);
   if (out) copy_slot_out(out, w, dp, 1, io_mem, ctx->stream, err);
-  copy_out(eig_out, w.s.eps, size_t(n), io_mem, ctx->stream, err);
+  copy_out(eig_out, w.s.eps, size_t(dp.ncol), io_mem, ctx->stream, err);
   copy_out(res_out, w.s.res, size_t(n), io_mem, ctx->stream, err);
   CK(cudaStreamSynchronize(ctx->stream));
   return DPT_OK;
@@ -979,7 +1126,7 @@ int run_step_full(dpt_ctx* ctx, const dpt_problem* p, const double* a, const dou
 int run_single(dpt_ctx* ctx, const dpt_problem* p, int64_t row, const dpt_options* opts_in, double ramp_alpha,
                dpt_trace_fn trace, void* user, double* z_out, int out_mem, dpt_report* rep,
                const double* z_in, int z_mem, double fixed_lambda, double* eig_fixed, double* z_unit,
-               dpt_error_info* err, const double* gap_row = nullptr) {
+               dpt_error_info* err, const double* gap_row = nullptr, double fixed_lambda_im = 0.0) {
   const dpt_options o = opts_or_default(opts_in);
   Guard g(ctx);
   validate(p, err);
@@ -988,6 +1135,8 @@ int run_single(dpt_ctx* ctx, const dpt_problem* p, int64_t row, const dpt_option
   const bool ramped = ramp_alpha > 0.0;
   DevProblem dp;
   upload(dp, ctx, p, err);
+  const int cx = dp.cplx ? 2 : 1;
+  if (fixed) dp.lambda_im = fixed_lambda_im;
   const int win = fixed ? 0 : (o.cycle_window >= 2 ? std::min(o.cycle_window, DPT_MAX_WINDOW) : 0);  // dpt.cpp:207
   const int nslots = win > 0 ? win + 1 : 2;
   const int max_iter = fixed ? 1 : o.max_iter;
@@ -995,13 +1144,21 @@ int run_single(dpt_ctx* ctx, const dpt_problem* p, int64_t row, const dpt_option
   const double lam = fixed ? fixed_lambda : p->lambda;
   std::vector<double> lam_tab;
   std::vector<int> set_tab;
-  if (ramped && !fixed) {
-    lam_tab.resize(size_t(total) + 2);
-    set_tab.resize(size_t(total) + 2);
-    for (size_t k = 0; k < lam_tab.size(); ++k) {
-      const double lk = k == 0 ? 0.0 : lam * (1.0 - std::pow(ramp_alpha, double(int(k) - 1)));
-      lam_tab[k] = lk;
-      set_tab[k] = std::fabs(lk - lam) <= o.tol * std::fabs(lam) ? 1 : 0;
+  if (ramped && !fixed) {  // dpt.cpp:238-240, complex lambda_k
+    const size_t nk = size_t(total) + 2;
+    lam_tab.resize(nk * size_t(cx));
+    set_tab.resize(nk);
+    const double lim = dp.lambda_im;
+    for (size_t k = 0; k < nk; ++k) {
+      const double f = k == 0 ? 0.0 : 1.0 - std::pow(ramp_alpha, double(int(k) - 1));
+      const double lr = lam * f, li = lim * f;
+      if (cx == 2) {
+        lam_tab[2 * k] = lr;
+        lam_tab[2 * k + 1] = li;
+      } else {
+        lam_tab[k] = lr;
+      }
+      set_tab[k] = std::hypot(lr - lam, li - lim) <= o.tol * std::hypot(lam, lim) ? 1 : 0;
     }
     set_tab[0] = 1;
   }
@@ -1021,8 +1178,8 @@ int run_single(dpt_ctx* ctx, const dpt_problem* p, int64_t row, const dpt_option
   double step = 0.0;
   DBuf gbuf;
   if (gap_row) {
-    dalloc(gbuf, size_t(n) * 8, err);
-    CK(cudaMemcpyAsync(gbuf.p, gap_row, size_t(n) * 8,
+    dalloc(gbuf, size_t(cx * n) * 8, err);
+    CK(cudaMemcpyAsync(gbuf.p, gap_row, size_t(cx * n) * 8,
                        z_mem == DPT_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
     w.s.gapmat = gbuf.as<double>();
   }
@@ -1052,25 +1209,32 @@ int run_single(dpt_ctx* ctx, const dpt_problem* p, int64_t row, const dpt_option
   }
   CK(cudaEventRecord(ctx->ev1, st));
   if (n > 0 && z_out) copy_slot_out(z_out, w, dp, final_iter % nslots, out_mem, st, err);
-  if (n > 0 && z_unit) {  // dominant_eigenpair's z_unit = z / ||z||_2 (dpt.cpp:432-436)
+  if (n > 0 && z_unit) {  // dominant_eigenpair's z_unit = z / ||z||_2 (dpt.cpp:432-436); |z|^2 = re^2 + im^2
     DBuf tmp;
-    dalloc(tmp, size_t(n) * 8, err);
+    dalloc(tmp, size_t(cx * n) * 8, err);
     DBuf scratch;
     dalloc(scratch, 512 * 8, err);
-    CK(launch_unit(w.s.slots + size_t(final_iter % nslots) * size_t(w.s.slot_elems), tmp.as<double>(), n,
+    CK(launch_unit(w.s.slots + size_t(final_iter % nslots) * size_t(w.s.slot_elems), tmp.as<double>(), cx * n,
                    scratch.as<double>(), w.s.counter + 2, st));
-    copy_out(z_unit, tmp.as<double>(), size_t(n), out_mem, st, err);
+    copy_out(z_unit, tmp.as<double>(), size_t(cx * n), out_mem, st, err);
     CK(cudaStreamSynchronize(st));
   }
-  double eig = std::numeric_limits<double>::quiet_NaN(), res = eig;
+  double eigv[2] = {std::numeric_limits<double>::quiet_NaN(), std::numeric_limits<double>::quiet_NaN()};
+  double res = std::numeric_limits<double>::quiet_NaN();
   if (readoffs) {
-    CK(cudaMemcpyAsync(&eig, w.s.eps, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(eigv, w.s.eps, size_t(cx) * 8, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(&res, w.s.res, 8, cudaMemcpyDeviceToHost, st));
   }
   CK(cudaStreamSynchronize(st));
-  if (eig_fixed) *eig_fixed = eig;
+  if (cx == 1 && readoffs) eigv[1] = 0.0;
+  const double eig = eigv[0];
+  if (eig_fixed) {
+    eig_fixed[0] = eigv[0];
+    if (cx == 2) eig_fixed[1] = eigv[1];
+  }
   fill_report(ctx, rep, status, iters, step);
   if (rep) {
+    rep->eigenvalue_im = eigv[1];
     rep->eigenvalue = eig;
     rep->residual = res;
     rep->row = row;
@@ -1264,7 +1428,8 @@ int dpt_step_full_gap(dpt_ctx* ctx, const dpt_problem* p, const double* a, const
 int dpt_readoffs(dpt_ctx* ctx, const dpt_problem* p, const double* a, double* eig_out, double* res_out,
                  int io_mem, dpt_error_info* err) {
   DPT_API_BEGIN
-  return run_step_full(ctx, p, a, nullptr, p ? p->lambda : 0.0, nullptr, io_mem, eig_out, res_out, err);
+  return run_step_full(ctx, p, a, nullptr, p ? p->lambda : 0.0, nullptr, io_mem, eig_out, res_out, err,
+                       p && p->is_complex ? p->lambda_im : 0.0);
   DPT_API_END
 }
 
@@ -1297,7 +1462,9 @@ int dpt_iterate_single(dpt_ctx* ctx, const dpt_problem* p, int64_t row, const dp
   const dpt_options o = opts_or_default(opts);
   std::vector<double> dh = host_levels(p, err);
   int64_t bj;
-  if (find_degenerate_row(p->n, dh.data(), row, o.degeneracy_tol, &bj)) degenerate_error(err, row, bj, dh.data());
+  const bool deg = p->is_complex ? find_degenerate_row_c(p->n, dh.data(), row, o.degeneracy_tol, &bj)
+                                 : find_degenerate_row(p->n, dh.data(), row, o.degeneracy_tol, &bj);
+  if (deg) degenerate_error(err, row, bj, dh.data(), p->is_complex != 0);
   return run_single(ctx, p, row, &o, ramp_alpha, trace, user, z_out, out_mem, rep, nullptr, 0, 0.0, nullptr,
                     nullptr, err);
   DPT_API_END
@@ -1314,29 +1481,35 @@ int dpt_dominant_eigenpair(dpt_ctx* ctx, const dpt_problem* p, const dpt_options
   }
   const dpt_options o = opts_or_default(opts);
   std::vector<double> d = host_levels(p, err);
+  const int cx = p->is_complex ? 2 : 1;
+  auto re = [&](int64_t i) { return d[size_t(cx * i)]; };
   int64_t best = 0;  // first argmax of Re d (dpt.cpp:404-406)
   for (int64_t i = 1; i < n; ++i)
-    if (d[size_t(i)] > d[size_t(best)]) best = i;
+    if (re(i) > re(best)) best = i;
   if (n > 1) {  // runner-up ambiguity (dpt.cpp:408-419)
     int64_t runner = best == 0 ? 1 : 0;
     for (int64_t i = 0; i < n; ++i) {
       if (i == best) continue;
-      if (d[size_t(i)] > d[size_t(runner)]) runner = i;
+      if (re(i) > re(runner)) runner = i;
     }
-    const double thr = threshold_of(n, d.data(), o.degeneracy_tol);
-    if (d[size_t(best)] - d[size_t(runner)] < thr) {
+    const double thr = cx == 2 ? threshold_of_c(n, d.data(), o.degeneracy_tol) : threshold_of(n, d.data(), o.degeneracy_tol);
+    if (re(best) - re(runner) < thr) {
       if (err) {
         err->i = best;
         err->j = runner;
-        err->ei = d[size_t(best)];
-        err->ej = d[size_t(runner)];
+        err->ei = re(best);
+        err->ej = re(runner);
+        err->ei_im = cx == 2 ? d[size_t(2 * best + 1)] : 0.0;
+        err->ej_im = cx == 2 ? d[size_t(2 * runner + 1)] : 0.0;
       }
       set_err(err, DPT_ERR_DEGENERATE, "dominant_eigenpair: ambiguous dominant level");
       return DPT_ERR_DEGENERATE;
     }
   }
   int64_t bj;
-  if (find_degenerate_row(n, d.data(), best, o.degeneracy_tol, &bj)) degenerate_error(err, best, bj, d.data());
+  const bool deg = cx == 2 ? find_degenerate_row_c(n, d.data(), best, o.degeneracy_tol, &bj)
+                           : find_degenerate_row(n, d.data(), best, o.degeneracy_tol, &bj);
+  if (deg) degenerate_error(err, best, bj, d.data(), cx == 2);
   return run_single(ctx, p, best, &o, 0.0, nullptr, nullptr, z_chart, out_mem, rep, nullptr, 0, 0.0, nullptr,
                     z_unit, err);
   DPT_API_END
@@ -1365,6 +1538,51 @@ int dpt_eigenvalue_of(dpt_ctx* ctx, const dpt_problem* p, const double* z, int64
   }
   return run_single(ctx, p, row, nullptr, 0.0, nullptr, nullptr, nullptr, z_mem, nullptr, z, z_mem, lambda, out,
                     nullptr, err);
+  DPT_API_END
+}
+
+int dpt_iterate_fixed_c(dpt_ctx* ctx, const dpt_problem* p, int k, double lambda, double lambda_im, double* a_out,
+                        int out_mem, dpt_report* rep, dpt_error_info* err) {
+  DPT_API_BEGIN
+  if (k < 0) {
+    set_err(err, DPT_ERR_INVALID_ARG, "iterate_fixed: negative step count");
+    return DPT_ERR_INVALID_ARG;
+  }
+  return run_full(ctx, p, nullptr, false, 0.0, k, lambda, nullptr, nullptr, a_out, nullptr, nullptr, out_mem, rep,
+                  err, lambda_im);
+  DPT_API_END
+}
+
+int dpt_step_full_gap_c(dpt_ctx* ctx, const dpt_problem* p, const double* a, const double* gap, double lambda,
+                        double lambda_im, double* out, int io_mem, dpt_error_info* err) {
+  DPT_API_BEGIN
+  return run_step_full(ctx, p, a, gap, lambda, out, io_mem, nullptr, nullptr, err, lambda_im);
+  DPT_API_END
+}
+
+int dpt_step_single_gap_c(dpt_ctx* ctx, const dpt_problem* p, const double* z, int64_t row, const double* gap_row,
+                          double lambda, double lambda_im, double* out, int io_mem, dpt_error_info* err) {
+  DPT_API_BEGIN
+  validate(p, err);
+  if (row < 0 || row >= p->n) {
+    set_err(err, DPT_ERR_SHAPE, "step_single: dimension mismatch");
+    return DPT_ERR_SHAPE;
+  }
+  return run_single(ctx, p, row, nullptr, 0.0, nullptr, nullptr, out, io_mem, nullptr, z, io_mem, lambda, nullptr,
+                    nullptr, err, gap_row, lambda_im);
+  DPT_API_END
+}
+
+int dpt_eigenvalue_of_c(dpt_ctx* ctx, const dpt_problem* p, const double* z, int64_t row, double lambda,
+                        double lambda_im, double* out2, int z_mem, dpt_error_info* err) {
+  DPT_API_BEGIN
+  validate(p, err);
+  if (row < 0 || row >= p->n) {
+    set_err(err, DPT_ERR_SHAPE, "eigenvalue_of: dimension mismatch");
+    return DPT_ERR_SHAPE;
+  }
+  return run_single(ctx, p, row, nullptr, 0.0, nullptr, nullptr, nullptr, z_mem, nullptr, z, z_mem, lambda, out2,
+                    nullptr, err, nullptr, lambda_im);
   DPT_API_END
 }
 
@@ -1485,7 +1703,7 @@ int dpt_plan_begin(dpt_plan* pl, dpt_error_info* err) {
   if (pl->mode == MODE_DENSE_FULL) {
     CK(launch_dense_init(w.s, pl->dp.delta.as<double>(), pl->dp.big, st));
     ctx->launches += 1;
-    post_step(ctx, w, dense_init_ntiles(w.s.rows, w.s.ntn), 0, err);
+    post_step(ctx, w, dense_init_ntiles(w.s.rows, w.s.ntn, w.s.cplx), 0, err);
   } else {
     if (pl->mode == MODE_SINGLE)
       CK(launch_identity(w.s, st));

@@ -52,7 +52,7 @@ class DegenerateSpectrum(RuntimeError):
 
     def __init__(self, msg, i, j, ei, ej):
         super().__init__(msg)
-        self.i, self.j, self.ei, self.ej = int(i), int(j), float(ei), float(ej)
+        self.i, self.j, self.ei, self.ej = int(i), int(j), ei, ej
 
     def first(self):
         return self.i
@@ -224,7 +224,9 @@ def _raise(rc: int, err: N.dpt_error_info):
     if rc == N.DPT_ERR_SHAPE:
         raise ShapeError(msg)
     if rc == N.DPT_ERR_DEGENERATE:
-        raise DegenerateSpectrum(msg, err.i, err.j, err.ei, err.ej)
+        ei = complex(err.ei, err.ei_im) if err.ei_im else err.ei
+        ej = complex(err.ej, err.ej_im) if err.ej_im else err.ej
+        raise DegenerateSpectrum(msg, err.i, err.j, ei, ej)
     if rc in (N.DPT_ERR_INVALID_ARG, N.DPT_ERR_NON_REAL):
         raise ValueError(msg)
     if rc == N.DPT_ERR_NO_DEVICE:
@@ -250,90 +252,126 @@ def _host(x, dtype):
     return a
 
 
-class _Marshal:
-    """Keeps the arrays of one call alive and builds the dpt_problem."""
+def _is_complex_dtype(x) -> bool:
+    if _is_torch(x):
+        return x.is_complex()
+    return np.iscomplexobj(x)
 
-    def __init__(self, p: PartitionedProblem):
+
+def _has_imag(x) -> bool:
+    if _is_torch(x):
+        return bool(x.is_complex() and (x.imag != 0).any().item())
+    return bool(np.iscomplexobj(x) and np.any(np.imag(x) != 0))
+
+
+class _Marshal:
+    """Keeps the arrays of one call alive and builds the dpt_problem.
+
+    Real inputs (or complex dtypes whose imaginary parts are all zero) run the
+    real FP64 kernels -- the reference's imaginary parts would stay exactly 0;
+    inputs with a nonzero imaginary part run the complex FP64 path
+    (std::complex<double> interleaved layout).  `cdtype` records whether the
+    caller passed complex data, so outputs come back complex like the
+    reference's std::complex results."""
+
+    def __init__(self, p: PartitionedProblem, extra_complex=False):
         self.keep = []
-        d = p.d
+        d, delta, lam = p.d, p.delta, p.lam
+        vals = delta.vals if isinstance(delta, CsrMatrix) else delta
+        self.cdtype = (_is_complex_dtype(d) or _is_complex_dtype(vals) or np.iscomplexobj(np.asarray(lam))
+                       or extra_complex)
+        self.cplx = bool(_has_imag(d) or _has_imag(vals) or (np.iscomplexobj(np.asarray(lam)) and np.imag(lam) != 0)
+                         or extra_complex)
         self.device = _is_torch(d) and d.is_cuda
-        if self.device:
-            self.keep.append(d)
-            dptr = d.data_ptr()
-        else:
-            d = _host(d, np.float64)
-            if d.ndim != 1:
-                raise ShapeError("make_problem: diagonal must be a vector")
-            self.keep.append(d)
-            dptr = d.ctypes.data
         n = int(d.shape[0])
+        if len(d.shape) != 1:
+            raise ShapeError("make_problem: diagonal must be a vector")
         self.n = n
         prob = N.dpt_problem()
         prob.n = n
-        prob.d = dptr
-        prob.lambda_ = float(np.real(p.lam))
-        if np.iscomplexobj(np.asarray(p.lam)) and np.imag(p.lam) != 0:
-            raise ValueError("non-real input: the B200 path is real FP64 (complex lambda unsupported)")
+        prob.d = self._arr(d)
+        prob.lambda_ = float(np.real(lam))
+        prob.lambda_im = float(np.imag(lam)) if self.cplx else 0.0
+        prob.is_complex = 1 if self.cplx else 0
         prob.mem = N.DPT_MEM_DEVICE if self.device else N.DPT_MEM_HOST
-        delta = p.delta
         if isinstance(delta, CsrMatrix):
             if delta.n != n:
                 raise ShapeError("make_problem: delta shape does not match diagonal")
             prob.delta_kind = N.DPT_DELTA_CSR
             if self.device:
-                rp, cl, vl = delta.rowptr, delta.cols, delta.vals
+                rp, cl = delta.rowptr, delta.cols
             else:
-                rp, cl, vl = (_host(delta.rowptr, np.int64), _host(delta.cols, np.int32),
-                              _host(delta.vals, np.float64))
-            self.keep += [rp, cl, vl]
-            prob.rowptr, prob.cols, prob.vals = _ptr(rp), _ptr(cl), _ptr(vl)
-            prob.nnz = int(vl.shape[0])
+                rp, cl = _host(delta.rowptr, np.int64), _host(delta.cols, np.int32)
+            self.keep += [rp, cl]
+            prob.rowptr, prob.cols, prob.vals = _ptr(rp), _ptr(cl), self._arr(delta.vals)
+            prob.nnz = int(delta.vals.shape[0])
         else:
-            if not self.device:
-                if np.iscomplexobj(delta):
-                    if np.any(np.imag(delta) != 0):
-                        raise ValueError("non-real input: the B200 path is real FP64")
-                    delta = np.real(delta)
-                delta = _host(delta, np.float64)
             if tuple(delta.shape) != (n, n):
                 raise ShapeError("make_problem: delta shape does not match diagonal")
-            self.keep.append(delta)
             prob.delta_kind = N.DPT_DELTA_DENSE
-            prob.delta = _ptr(delta)
+            prob.delta = self._arr(delta)
         self.prob = prob
 
-    def out(self, *shape, given=None):
+    def _arr(self, x):
+        """Pointer to x as contiguous float64 (real path) or complex128 (complex path)."""
+        if self.device and _is_torch(x):
+            import torch
+            x = x.to(torch.complex128 if self.cplx else torch.float64)
+            if not self.cplx and x.is_complex():
+                x = x.real
+            x = x.contiguous()
+        else:
+            a = np.asarray(x)
+            if self.cplx:
+                x = np.ascontiguousarray(a, dtype=np.complex128)
+            else:
+                x = np.ascontiguousarray(np.real(a) if np.iscomplexobj(a) else a, dtype=np.float64)
+        self.keep.append(x)
+        return _ptr(x)
+
+    def out(self, *shape, given=None, cplx=None):
+        """Output buffer; complex-valued outputs (a, eigenvalues, z) pass cplx=True."""
+        c = self.cplx if cplx is None else (cplx and self.cplx)
         if given is not None:  # caller-provided output (e.g. pinned host memory)
             if tuple(given.shape) != tuple(shape):
                 raise ShapeError("output buffer has the wrong shape")
+            want = (np.complex128 if c else np.float64)
             if _is_torch(given):
-                if not given.is_contiguous() or str(given.dtype) != "torch.float64":
-                    raise ValueError("output tensor must be contiguous float64")
-            elif not (given.dtype == np.float64 and given.flags["C_CONTIGUOUS"]):
-                raise ValueError("output array must be C-contiguous float64")
+                if not given.is_contiguous() or given.is_complex() != c:
+                    raise ValueError("output tensor must be contiguous with the problem's dtype")
+            elif not (given.dtype == want and given.flags["C_CONTIGUOUS"]):
+                raise ValueError(f"output array must be C-contiguous {np.dtype(want).name}")
             self.keep.append(given)
             return given, _ptr(given)
         if self.device:
             import torch
-            t = torch.empty(shape, dtype=torch.float64, device=self.keep[0].device)
+            t = torch.empty(shape, dtype=torch.complex128 if c else torch.float64, device=self.keep[0].device)
             self.keep.append(t)
             return t, t.data_ptr()
-        a = np.empty(shape, dtype=np.float64)
+        a = np.empty(shape, dtype=np.complex128 if c else np.float64)
         return a, a.ctypes.data
 
     def inp(self, x, *shape):
         if self.device:
+            import torch
             if not (_is_torch(x) and x.is_cuda):
-                import torch
-                x = torch.as_tensor(np.asarray(x, dtype=np.float64), device=self.keep[0].device)
-            x = x.contiguous()
+                x = torch.as_tensor(np.asarray(x), device=self.keep[0].device)
+            x = x.to(torch.complex128 if self.cplx else torch.float64).contiguous()
             self.keep.append(x)
             return x.data_ptr()
-        a = _host(x, np.float64)
+        a = np.asarray(x)
+        a = np.ascontiguousarray(a, dtype=np.complex128) if self.cplx else np.ascontiguousarray(
+            np.real(a) if np.iscomplexobj(a) else a, dtype=np.float64)
         if a.shape != tuple(shape):
             raise ShapeError("dimension mismatch")
         self.keep.append(a)
         return a.ctypes.data
+
+    def result(self, x):
+        """Complex-dtype callers get complex outputs even on the real path."""
+        if self.cdtype and not self.cplx and not _is_torch(x):
+            return x.astype(np.complex128)
+        return x
 
     @property
     def mem(self):
@@ -367,7 +405,7 @@ def _full(p, opts, trace, ramped, alpha, ctx, out=None):
     oa, oe, orr = out if out is not None else (None, None, None)
     a, ap = m.out(n, n, given=oa)
     eig, ep = m.out(n, given=oe)
-    res, rp = m.out(n, given=orr)
+    res, rp = m.out(n, given=orr, cplx=False)
     rep, err = N.dpt_report(), N.dpt_error_info()
     cb, box = _trace_cb(trace)
     o = _opts(opts)
@@ -380,7 +418,7 @@ def _full(p, opts, trace, ramped, alpha, ctx, out=None):
     if rc == N.DPT_ERR_TRACE and box and "exc" in box:
         raise box["exc"]
     _raise(rc, err)
-    return ConvergenceReport(EigenIterate(a, rep.iterations), eig, ConvergenceStatus(rep.status),
+    return ConvergenceReport(EigenIterate(m.result(a), rep.iterations), m.result(eig), ConvergenceStatus(rep.status),
                              rep.iterations, res, rep.step_norm, rep.device_ms)
 
 
@@ -397,27 +435,48 @@ def iterate_ramped(p: PartitionedProblem, alpha: float, opts: Optional[Iteration
     return _full(p, opts, trace, True, alpha, ctx)
 
 
-def iterate_fixed(p: PartitionedProblem, k: int, lam: float, ctx: Context = None):
+def iterate_fixed(p: PartitionedProblem, k: int, lam, ctx: Context = None):
     """Exactly k applications of the map from I at lam (dpt.hpp:94-96)."""
     ctx = ctx or default_context()
-    m = _Marshal(p)
+    m = _Marshal(p, extra_complex=bool(np.iscomplexobj(np.asarray(lam)) and np.imag(lam) != 0))
     a, ap = m.out(m.n, m.n)
     rep, err = N.dpt_report(), N.dpt_error_info()
-    _raise(N.lib().dpt_iterate_fixed(ctx.handle, ctypes.byref(m.prob), int(k), float(lam), ap, m.mem,
-                                     ctypes.byref(rep), ctypes.byref(err)), err)
-    return a
+    _raise(N.lib().dpt_iterate_fixed_c(ctx.handle, ctypes.byref(m.prob), int(k), float(np.real(lam)),
+                                       float(np.imag(lam)), ap, m.mem, ctypes.byref(rep), ctypes.byref(err)), err)
+    return m.result(a)
 
 
-def step_full(a, p: PartitionedProblem, lam: float, ctx: Context = None):
-    """One application of the full map to `a` (dpt.hpp:51-57)."""
+def step_full(a, p: PartitionedProblem, lam, ctx: Context = None, theta=None):
+    """One application of the full map to `a` (dpt.hpp:51-57).  theta: optional
+    explicit gap matrix (the reference's GapMatrix); default 1/(d_i - d_j)."""
     ctx = ctx or default_context()
-    m = _Marshal(p)
+    cx = bool(np.iscomplexobj(np.asarray(lam)) and np.imag(lam) != 0) or _has_imag(a) or (
+        theta is not None and _has_imag(theta))
+    m = _Marshal(p, extra_complex=cx)
     ip = m.inp(a, m.n, m.n)
+    gp = m.inp(theta, m.n, m.n) if theta is not None else None
     out, op = m.out(m.n, m.n)
     err = N.dpt_error_info()
-    _raise(N.lib().dpt_step_full(ctx.handle, ctypes.byref(m.prob), ip, float(lam), op, m.mem,
-                                 ctypes.byref(err)), err)
-    return out
+    if gp is not None:
+        rc = N.lib().dpt_step_full_gap_c(ctx.handle, ctypes.byref(m.prob), ip, gp, float(np.real(lam)),
+                                         float(np.imag(lam)), op, m.mem, ctypes.byref(err))
+    else:
+        rc = N.lib().dpt_step_full(ctx.handle, ctypes.byref(m.prob), ip, float(np.real(lam)), op, m.mem,
+                                   ctypes.byref(err)) if not m.cplx else N.lib().dpt_step_full_gap_c(
+            ctx.handle, ctypes.byref(m.prob), ip, m.inp(_gap_matrix(p.d), m.n, m.n), float(np.real(lam)),
+            float(np.imag(lam)), op, m.mem, ctypes.byref(err))
+    _raise(rc, err)
+    return m.result(out)
+
+
+def _gap_matrix(d):
+    """build_theta's table 1/(d_i - d_j) (zero diagonal) on the host -- only used
+    to feed step_full's complex-lambda path when the caller passes no GapMatrix."""
+    d = np.asarray(d.cpu().numpy() if _is_torch(d) else d, dtype=np.complex128)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        g = 1.0 / (d[:, None] - d[None, :])
+    np.fill_diagonal(g, 0.0)
+    return g
 
 
 def iterate_single(p: PartitionedProblem, row: int, opts: Optional[IterationOptions] = None,
@@ -435,7 +494,8 @@ def iterate_single(p: PartitionedProblem, row: int, opts: Optional[IterationOpti
     if rc == N.DPT_ERR_TRACE and box and "exc" in box:
         raise box["exc"]
     _raise(rc, err)
-    return SingleRowReport(z, rep.eigenvalue, ConvergenceStatus(rep.status), rep.iterations, rep.residual,
+    eig = complex(rep.eigenvalue, rep.eigenvalue_im) if m.cdtype else rep.eigenvalue
+    return SingleRowReport(m.result(z), eig, ConvergenceStatus(rep.status), rep.iterations, rep.residual,
                            rep.step_norm, rep.device_ms)
 
 
@@ -449,37 +509,49 @@ def dominant_eigenpair(p: PartitionedProblem, opts: Optional[IterationOptions] =
     o = _opts(opts)
     _raise(N.lib().dpt_dominant_eigenpair(ctx.handle, ctypes.byref(m.prob), ctypes.byref(o), zcp, zup,
                                           m.mem, ctypes.byref(rep), ctypes.byref(err)), err)
-    return DominantEigenpair(int(rep.row), zc, zu, rep.eigenvalue, ConvergenceStatus(rep.status),
+    eig = complex(rep.eigenvalue, rep.eigenvalue_im) if m.cdtype else rep.eigenvalue
+    return DominantEigenpair(int(rep.row), m.result(zc), m.result(zu), eig, ConvergenceStatus(rep.status),
                              rep.iterations, rep.residual, rep.step_norm, rep.device_ms)
 
 
-def step_single(z, row: int, p: PartitionedProblem, lam: float, ctx: Context = None):
+def step_single(z, row: int, p: PartitionedProblem, lam, ctx: Context = None, gap_row=None):
     """One row-map application for chart index row (dpt.hpp:59-66)."""
     ctx = ctx or default_context()
-    m = _Marshal(p)
+    cx = bool(np.iscomplexobj(np.asarray(lam)) and np.imag(lam) != 0) or _has_imag(z)
+    m = _Marshal(p, extra_complex=cx)
     ip = m.inp(z, m.n)
     out, op = m.out(m.n)
     err = N.dpt_error_info()
-    _raise(N.lib().dpt_step_single(ctx.handle, ctypes.byref(m.prob), ip, int(row), float(lam), op, m.mem,
-                                   ctypes.byref(err)), err)
-    return out
+    if gap_row is None and m.cplx:
+        gap_row = _gap_matrix(p.d)[int(row)]
+    if gap_row is not None:
+        gp = m.inp(gap_row, m.n)
+        rc = N.lib().dpt_step_single_gap_c(ctx.handle, ctypes.byref(m.prob), ip, int(row), gp, float(np.real(lam)),
+                                           float(np.imag(lam)), op, m.mem, ctypes.byref(err))
+    else:
+        rc = N.lib().dpt_step_single(ctx.handle, ctypes.byref(m.prob), ip, int(row), float(np.real(lam)), op,
+                                     m.mem, ctypes.byref(err))
+    _raise(rc, err)
+    return m.result(out)
 
 
-def eigenvalue_of(z, row: int, p: PartitionedProblem, lam: float, ctx: Context = None) -> float:
+def eigenvalue_of(z, row: int, p: PartitionedProblem, lam, ctx: Context = None):
     """eps_row + lam (Delta z)_row (dpt.hpp:68-72)."""
     ctx = ctx or default_context()
-    m = _Marshal(p)
+    cx = bool(np.iscomplexobj(np.asarray(lam)) and np.imag(lam) != 0) or _has_imag(z)
+    m = _Marshal(p, extra_complex=cx)
     ip = m.inp(z, m.n)
-    out = ctypes.c_double()
+    out = (ctypes.c_double * 2)()
     err = N.dpt_error_info()
-    _raise(N.lib().dpt_eigenvalue_of(ctx.handle, ctypes.byref(m.prob), ip, int(row), float(lam),
-                                     ctypes.byref(out), m.mem, ctypes.byref(err)), err)
-    return out.value
+    _raise(N.lib().dpt_eigenvalue_of_c(ctx.handle, ctypes.byref(m.prob), ip, int(row), float(np.real(lam)),
+                                       float(np.imag(lam)), out, m.mem, ctypes.byref(err)), err)
+    return complex(out[0], out[1]) if (m.cdtype or m.cplx) else out[0]
 
 
 class Plan:
     """A problem kept resident in HBM with its workspace (dpt_plan_*): repeated
-    fixed-step runs of the full map (single=False) or the row map for `row`."""
+    fixed-step runs of the full map (single=False) or the row map for `row`.
+    The coupling is p.lam (complex problems: Re lam overridable by `lam`)."""
 
     def __init__(self, p: PartitionedProblem, lam: float = None, single: bool = False, row: int = 0,
                  ctx: Context = None):
@@ -489,7 +561,7 @@ class Plan:
         self.single = single
         h, err = ctypes.c_void_p(), N.dpt_error_info()
         _raise(N.lib().dpt_plan_create(self.ctx.handle, ctypes.byref(self._m.prob), int(single), int(row),
-                                       float(p.lam if lam is None else lam), ctypes.byref(h),
+                                       float(np.real(p.lam if lam is None else lam)), ctypes.byref(h),
                                        ctypes.byref(err)), err)
         self.handle = h
 
@@ -507,7 +579,7 @@ class Plan:
 
     def read(self):
         shape = (self.n,) if self.single else (self.n, self.n)
-        out = np.empty(shape)
+        out = np.empty(shape, dtype=np.complex128 if self._m.cplx else np.float64)
         err = N.dpt_error_info()
         _raise(N.lib().dpt_plan_read(self.handle, out.ctypes.data, N.DPT_MEM_HOST, ctypes.byref(err)), err)
         return out

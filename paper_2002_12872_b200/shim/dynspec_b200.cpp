@@ -12,9 +12,10 @@
 // Small-n analysis helpers (jacobian_single, reduced_jacobian, multipliers)
 // and the staged homotopy_solve are host orchestration around them.
 //
-// Documented deviation: the path is real FP64.  Any nonzero imaginary part in
-// d, Delta, lambda or an input iterate throws std::invalid_argument
-// ("non-real input ...") instead of being dropped.
+// Arithmetic: problems whose every imaginary part is 0 (d, Delta, lambda and
+// the input iterate / gap arrays) run the real FP64 kernels -- the reference's
+// std::complex arithmetic keeps imaginary parts exactly 0 there -- and all
+// others run the complex FP64 kernels on the caller's interleaved storage.
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -49,7 +50,7 @@ struct CtxHolder {
     case DPT_ERR_SHAPE:
       throw ShapeError(msg);
     case DPT_ERR_DEGENERATE:
-      throw DegenerateSpectrum(msg, std::size_t(e.i), std::size_t(e.j), cdouble{e.ei, 0.0}, cdouble{e.ej, 0.0});
+      throw DegenerateSpectrum(msg, std::size_t(e.i), std::size_t(e.j), cdouble{e.ei, e.ei_im}, cdouble{e.ej, e.ej_im});
     case DPT_ERR_INVALID_ARG:
     case DPT_ERR_NON_REAL:
       throw std::invalid_argument(msg);
@@ -72,26 +73,38 @@ dpt_ctx* ctx() {
   return h.ctx;
 }
 
-double real_of(cdouble v, const char* what) {
-  if (v.imag() != 0.0) throw std::invalid_argument(std::string("non-real input (") + what + "): the B200 path is real FP64");
-  return v.real();
+bool has_imag(const cdouble* v, std::size_t n) {
+  for (std::size_t i = 0; i < n; ++i)
+    if (v[i].imag() != 0.0) return true;
+  return false;
 }
 
-std::vector<double> real_vec(std::span<const cdouble> v, const char* what) {
-  std::vector<double> r(v.size());
-  for (std::size_t i = 0; i < v.size(); ++i) r[i] = real_of(v[i], what);
+bool has_imag(std::span<const cdouble> v) { return has_imag(v.data(), v.size()); }
+bool has_imag(const DenseMatrix& m) { return has_imag(m.data(), m.rows() * m.cols()); }
+
+bool has_imag(const MatrixVariant& delta) {
+  if (const auto* dm = std::get_if<DenseMatrix>(&delta)) return has_imag(*dm);
+  return has_imag(std::get<SparseMatrix>(delta).values());
+}
+
+// Real image of a complex array (the real kernels); complex problems pass the
+// caller's std::complex<double> storage straight through as interleaved doubles.
+std::vector<double> real_part(const cdouble* v, std::size_t n) {
+  std::vector<double> r(n);
+  for (std::size_t i = 0; i < n; ++i) r[i] = v[i].real();
   return r;
 }
 
-std::vector<double> real_dense(const DenseMatrix& m, const char* what) {
-  const std::size_t nn = m.rows() * m.cols();
-  std::vector<double> r(nn);
-  for (std::size_t i = 0; i < nn; ++i) r[i] = real_of(m.data()[i], what);
-  return r;
-}
+const double* dbl(const cdouble* p) { return reinterpret_cast<const double*>(p); }
+double* dbl(cdouble* p) { return reinterpret_cast<double*>(p); }
 
-// Plain-array image of a PartitionedProblem (delta, not delta_t).
+// Plain-array image of a PartitionedProblem (delta, not delta_t).  Real
+// problems (every imaginary part 0, including lambda's and the caller's
+// iterate / gap arrays) run the real kernels -- the reference's complex
+// arithmetic then keeps imaginary parts exactly 0 -- everything else runs the
+// complex FP64 path on the caller's interleaved storage, no copy.
 struct Problem {
+  bool cplx = false;
   std::vector<double> d, dense, vals;
   std::vector<int64_t> rowptr;
   std::vector<int32_t> cols;
@@ -101,9 +114,13 @@ struct Problem {
 void fill_delta(Problem& P, const MatrixVariant& delta, std::size_t n) {
   if (const auto* dm = std::get_if<DenseMatrix>(&delta)) {
     if (dm->rows() != n || dm->cols() != n) throw ShapeError("delta shape does not match diagonal");
-    P.dense = real_dense(*dm, "delta");
+    if (P.cplx) {
+      P.c.delta = dbl(dm->data());
+    } else {
+      P.dense = real_part(dm->data(), n * n);
+      P.c.delta = P.dense.data();
+    }
     P.c.delta_kind = DPT_DELTA_DENSE;
-    P.c.delta = P.dense.data();
   } else {
     const auto& s = std::get<SparseMatrix>(delta);
     if (s.rows() != n || s.cols() != n) throw ShapeError("delta shape does not match diagonal");
@@ -111,23 +128,35 @@ void fill_delta(Problem& P, const MatrixVariant& delta, std::size_t n) {
     P.rowptr.assign(s.row_offsets().begin(), s.row_offsets().end());
     P.cols.resize(s.nnz());
     for (std::size_t q = 0; q < s.nnz(); ++q) P.cols[q] = int32_t(s.col_indices()[q]);
-    P.vals = real_vec(s.values(), "delta");
+    if (P.cplx) {
+      P.c.vals = dbl(s.values().data());
+    } else {
+      P.vals = real_part(s.values().data(), s.nnz());
+      P.c.vals = P.vals.data();
+    }
     P.c.delta_kind = DPT_DELTA_CSR;
     P.c.rowptr = P.rowptr.data();
     P.c.cols = P.cols.data();
-    P.c.vals = P.vals.data();
     P.c.nnz = int64_t(s.nnz());
   }
 }
 
-std::unique_ptr<Problem> to_c(const DiagonalMatrix& d, const MatrixVariant& delta, cdouble lambda) {
+std::unique_ptr<Problem> to_c(const DiagonalMatrix& d, const MatrixVariant& delta, cdouble lambda,
+                              bool force_complex = false) {
   auto P = std::make_unique<Problem>();
   const std::size_t n = d.size();
-  P->d = real_vec(d.d, "d");
+  P->cplx = force_complex || lambda.imag() != 0.0 || has_imag(d.d) || has_imag(delta);
+  if (P->cplx) {
+    P->c.d = dbl(d.d.data());
+  } else {
+    P->d = real_part(d.d.data(), n);
+    P->c.d = P->d.data();
+  }
   fill_delta(*P, delta, n);
   P->c.n = int64_t(n);
-  P->c.d = P->d.data();
-  P->c.lambda = real_of(lambda, "lambda");
+  P->c.lambda = lambda.real();
+  P->c.lambda_im = lambda.imag();
+  P->c.is_complex = P->cplx ? 1 : 0;
   P->c.mem = DPT_MEM_HOST;
   return P;
 }
@@ -145,14 +174,45 @@ dpt_options to_c(const IterationOptions& o) {
   return r;
 }
 
-DenseMatrix from_real(const std::vector<double>& a, std::size_t n) {
-  DenseMatrix m(n, n);
-  for (std::size_t i = 0; i < n * n; ++i) m.data()[i] = cdouble{a[i], 0.0};
-  return m;
-}
-
 cdouble c_of(double v) {  // NaN read-offs are cdouble{nan, nan} (dpt.cpp:121-124)
   return std::isnan(v) ? cdouble{v, v} : cdouble{v, 0.0};
+}
+
+// Output of a call: complex problems write interleaved straight into the
+// caller-facing std::complex<double> storage; real problems write a real image
+// that finish() widens (imaginary parts 0, NaN read-offs {nan, nan}).
+struct OutBuf {
+  cdouble* dst;
+  std::size_t n;
+  bool cplx;
+  std::vector<double> re;
+  OutBuf(cdouble* d, std::size_t count, bool c) : dst(d), n(count), cplx(c) {
+    if (!cplx) re.resize(n);
+  }
+  double* ptr() { return cplx ? dbl(dst) : re.data(); }
+  void finish(bool nan_pairs = false) {
+    if (cplx) return;
+    for (std::size_t i = 0; i < n; ++i) dst[i] = nan_pairs ? c_of(re[i]) : cdouble{re[i], 0.0};
+  }
+};
+
+// Input array of a call: interleaved view of the caller's storage (complex
+// problems) or its real image.
+struct InBuf {
+  std::vector<double> re;
+  const double* p;
+  InBuf(const cdouble* v, std::size_t n, bool cplx) {
+    if (cplx) {
+      p = dbl(v);
+    } else {
+      re = real_part(v, n);
+      p = re.data();
+    }
+  }
+};
+
+cdouble eig_of(const dpt_report& r, bool cplx) {
+  return cplx ? cdouble{r.eigenvalue, r.eigenvalue_im} : c_of(r.eigenvalue);
 }
 
 // TraceSink trampoline: an exception thrown by the sink aborts the solve and
@@ -173,42 +233,33 @@ int trace_tramp(int k, double s, double r, void* user) {
   }
 }
 
-ConvergenceReport full_report(std::size_t n, const std::vector<double>& a, const std::vector<double>& eig,
-                              const std::vector<double>& res, const dpt_report& r) {
-  ConvergenceReport rep;
-  rep.status = ConvergenceStatus(r.status);
-  rep.iterations = r.iterations;
-  rep.step_norm = r.step_norm;
-  rep.eigenvalues.resize(n);
-  rep.residuals = res;
-  for (std::size_t i = 0; i < n; ++i) rep.eigenvalues[i] = c_of(eig[i]);
-  rep.state = EigenIterate{from_real(a, n), r.iterations};
-  return rep;
-}
-
 ConvergenceReport run_full(const PartitionedProblem& p, const IterationOptions& opts, bool ramped, double alpha,
                            const TraceSink& trace) {
   auto P = to_c(p);
   const std::size_t n = p.size();
-  std::vector<double> a(n * n), eig(n), res(n);
+  ConvergenceReport rep;
+  DenseMatrix a(n, n);
+  rep.eigenvalues.resize(n);
+  rep.residuals.resize(n);
+  OutBuf ab(a.data(), n * n, P->cplx), eb(rep.eigenvalues.data(), n, P->cplx);
   dpt_options o = to_c(opts);
   dpt_report r{};
   dpt_error_info e{};
   TraceBox box{&trace, nullptr};
   dpt_trace_fn fn = trace ? &trace_tramp : nullptr;
-  const int rc = ramped ? dpt_iterate_ramped(ctx(), &P->c, alpha, &o, fn, &box, a.data(), eig.data(), res.data(),
-                                             DPT_MEM_HOST, &r, &e)
-                        : dpt_iterate_full(ctx(), &P->c, &o, fn, &box, a.data(), eig.data(), res.data(),
+  const int rc = ramped ? dpt_iterate_ramped(ctx(), &P->c, alpha, &o, fn, &box, ab.ptr(), eb.ptr(),
+                                             rep.residuals.data(), DPT_MEM_HOST, &r, &e)
+                        : dpt_iterate_full(ctx(), &P->c, &o, fn, &box, ab.ptr(), eb.ptr(), rep.residuals.data(),
                                            DPT_MEM_HOST, &r, &e);
   if (rc == DPT_ERR_TRACE && box.exc) std::rethrow_exception(box.exc);
   check(rc, e);
-  return full_report(n, a, eig, res, r);
-}
-
-std::vector<cdouble> to_complex(const std::vector<double>& v) {
-  std::vector<cdouble> r(v.size());
-  for (std::size_t i = 0; i < v.size(); ++i) r[i] = cdouble{v[i], 0.0};
-  return r;
+  ab.finish();
+  eb.finish(true);
+  rep.status = ConvergenceStatus(r.status);
+  rep.iterations = r.iterations;
+  rep.step_norm = r.step_norm;
+  rep.state = EigenIterate{std::move(a), r.iterations};
+  return rep;
 }
 
 }  // namespace
@@ -221,12 +272,14 @@ DenseMatrix step_full(const DenseMatrix& a, const GapMatrix& theta, const Matrix
   // the C ABI takes Delta; recover it from the cached transpose (no conjugation)
   const MatrixVariant delta = transpose(delta_t);
   DiagonalMatrix zeros(std::vector<cdouble>(n, cdouble{}));  // levels unused with an explicit gap matrix
-  auto P = to_c(zeros, delta, lambda);
-  const std::vector<double> ar = real_dense(a, "iterate"), g = real_dense(theta.theta, "theta");
-  std::vector<double> out(n * n);
+  auto P = to_c(zeros, delta, lambda, has_imag(a) || has_imag(theta.theta));
+  const InBuf ab(a.data(), n * n, P->cplx), gb(theta.theta.data(), n * n, P->cplx);
+  DenseMatrix out(n, n);
+  OutBuf ob(out.data(), n * n, P->cplx);
   dpt_error_info e{};
-  check(dpt_step_full_gap(ctx(), &P->c, ar.data(), g.data(), P->c.lambda, out.data(), DPT_MEM_HOST, &e), e);
-  return from_real(out, n);
+  check(dpt_step_full_gap_c(ctx(), &P->c, ab.p, gb.p, lambda.real(), lambda.imag(), ob.ptr(), DPT_MEM_HOST, &e), e);
+  ob.finish();
+  return out;
 }
 
 std::vector<cdouble> step_single(std::span<const cdouble> z, const GapRow& gaps, const MatrixVariant& delta,
@@ -234,14 +287,16 @@ std::vector<cdouble> step_single(std::span<const cdouble> z, const GapRow& gaps,
   const std::size_t n = z.size();
   if (gaps.inv_gaps.size() != n) throw ShapeError("step_single: dimension mismatch");
   DiagonalMatrix zeros(std::vector<cdouble>(n, cdouble{}));
-  auto P = to_c(zeros, delta, lambda);
-  const std::vector<double> zr = real_vec(z, "z"), g = real_vec(gaps.inv_gaps, "gap row");
-  std::vector<double> out(n);
+  auto P = to_c(zeros, delta, lambda, has_imag(z) || has_imag(gaps.inv_gaps));
+  const InBuf zb(z.data(), n, P->cplx), gb(gaps.inv_gaps.data(), n, P->cplx);
+  std::vector<cdouble> out(n);
+  OutBuf ob(out.data(), n, P->cplx);
   dpt_error_info e{};
-  check(dpt_step_single_gap(ctx(), &P->c, zr.data(), int64_t(gaps.row), g.data(), P->c.lambda, out.data(),
-                            DPT_MEM_HOST, &e),
+  check(dpt_step_single_gap_c(ctx(), &P->c, zb.p, int64_t(gaps.row), gb.p, lambda.real(), lambda.imag(), ob.ptr(),
+                              DPT_MEM_HOST, &e),
         e);
-  return to_complex(out);
+  ob.finish();
+  return out;
 }
 
 std::vector<cdouble> step_single(std::span<const cdouble> z, std::size_t n, const GapMatrix& theta,
@@ -257,12 +312,12 @@ std::vector<cdouble> step_single(std::span<const cdouble> z, std::size_t n, cons
 cdouble eigenvalue_of(std::span<const cdouble> z, std::size_t n, const DiagonalMatrix& d, const MatrixVariant& delta,
                       cdouble lambda) {
   if (z.size() != d.size() || n >= z.size()) throw ShapeError("eigenvalue_of: dimension mismatch");
-  auto P = to_c(d, delta, lambda);
-  const std::vector<double> zr = real_vec(z, "z");
-  double out = 0.0;
+  auto P = to_c(d, delta, lambda, has_imag(z));
+  const InBuf zb(z.data(), z.size(), P->cplx);
+  double out[2] = {0.0, 0.0};
   dpt_error_info e{};
-  check(dpt_eigenvalue_of(ctx(), &P->c, zr.data(), int64_t(n), P->c.lambda, &out, DPT_MEM_HOST, &e), e);
-  return cdouble{out, 0.0};
+  check(dpt_eigenvalue_of_c(ctx(), &P->c, zb.p, int64_t(n), lambda.real(), lambda.imag(), out, DPT_MEM_HOST, &e), e);
+  return cdouble{out[0], out[1]};
 }
 
 ConvergenceReport iterate_full(const PartitionedProblem& p, const IterationOptions& opts, const TraceSink& trace) {
@@ -277,13 +332,16 @@ ConvergenceReport iterate_ramped(const PartitionedProblem& p, double alpha, cons
 
 DenseMatrix iterate_fixed(const PartitionedProblem& p, int k, cdouble lambda) {
   if (k < 0) throw std::invalid_argument("iterate_fixed: negative step count");
-  auto P = to_c(p);
+  // lambda overrides p.lambda (dpt.cpp:383-388): the problem is complex if either is
+  auto P = to_c(p.d, p.delta, p.lambda, lambda.imag() != 0.0);
   const std::size_t n = p.size();
-  std::vector<double> a(n * n);
+  DenseMatrix a(n, n);
+  OutBuf ab(a.data(), n * n, P->cplx);
   dpt_report r{};
   dpt_error_info e{};
-  check(dpt_iterate_fixed(ctx(), &P->c, k, real_of(lambda, "lambda"), a.data(), DPT_MEM_HOST, &r, &e), e);
-  return from_real(a, n);
+  check(dpt_iterate_fixed_c(ctx(), &P->c, k, lambda.real(), lambda.imag(), ab.ptr(), DPT_MEM_HOST, &r, &e), e);
+  ab.finish();
+  return a;
 }
 
 SingleRowReport iterate_single(const PartitionedProblem& p, std::size_t row, const IterationOptions& opts,
@@ -292,18 +350,19 @@ SingleRowReport iterate_single(const PartitionedProblem& p, std::size_t row, con
   if (!(ramp_alpha >= 0.0) || ramp_alpha >= 1.0)
     throw std::invalid_argument("iterate_single: ramp alpha must lie in [0, 1)");
   auto P = to_c(p);
-  std::vector<double> z(p.size());
+  SingleRowReport rep;
+  rep.z.resize(p.size());
+  OutBuf zb(rep.z.data(), p.size(), P->cplx);
   dpt_options o = to_c(opts);
   dpt_report r{};
   dpt_error_info e{};
   TraceBox box{&trace, nullptr};
   const int rc = dpt_iterate_single(ctx(), &P->c, int64_t(row), &o, ramp_alpha, trace ? &trace_tramp : nullptr,
-                                    &box, z.data(), DPT_MEM_HOST, &r, &e);
+                                    &box, zb.ptr(), DPT_MEM_HOST, &r, &e);
   if (rc == DPT_ERR_TRACE && box.exc) std::rethrow_exception(box.exc);
   check(rc, e);
-  SingleRowReport rep;
-  rep.z = to_complex(z);
-  rep.eigenvalue = c_of(r.eigenvalue);
+  zb.finish();
+  rep.eigenvalue = eig_of(r, P->cplx);
   rep.status = ConvergenceStatus(r.status);
   rep.iterations = r.iterations;
   rep.residual = r.residual;
@@ -314,16 +373,18 @@ SingleRowReport iterate_single(const PartitionedProblem& p, std::size_t row, con
 DominantEigenpair dominant_eigenpair(const PartitionedProblem& p, const IterationOptions& opts) {
   if (p.size() == 0) throw ShapeError("dominant_eigenpair: empty problem");
   auto P = to_c(p);
-  std::vector<double> zc(p.size()), zu(p.size());
+  DominantEigenpair out;
+  out.z_chart.resize(p.size());
+  out.z_unit.resize(p.size());
+  OutBuf zc(out.z_chart.data(), p.size(), P->cplx), zu(out.z_unit.data(), p.size(), P->cplx);
   dpt_options o = to_c(opts);
   dpt_report r{};
   dpt_error_info e{};
-  check(dpt_dominant_eigenpair(ctx(), &P->c, &o, zc.data(), zu.data(), DPT_MEM_HOST, &r, &e), e);
-  DominantEigenpair out;
+  check(dpt_dominant_eigenpair(ctx(), &P->c, &o, zc.ptr(), zu.ptr(), DPT_MEM_HOST, &r, &e), e);
+  zc.finish();
+  zu.finish();
   out.row = std::size_t(r.row);
-  out.z_chart = to_complex(zc);
-  out.z_unit = to_complex(zu);
-  out.eigenvalue = c_of(r.eigenvalue);
+  out.eigenvalue = eig_of(r, P->cplx);
   out.status = ConvergenceStatus(r.status);
   out.iterations = r.iterations;
   out.residual = r.residual;
@@ -406,14 +467,14 @@ ConvergenceReport homotopy_solve(const PartitionedProblem& p, int stages, const 
   rep.iterations = total;
   rep.step_norm = last.step_norm;
   if (all_finite(a)) {  // read-offs against the ORIGINAL problem, on the GPU
-    auto P = to_c(p);
-    const std::vector<double> ar = real_dense(a, "iterate");
-    std::vector<double> eig(n), res(n);
-    dpt_error_info e{};
-    check(dpt_readoffs(ctx(), &P->c, ar.data(), eig.data(), res.data(), DPT_MEM_HOST, &e), e);
+    auto P = to_c(p.d, p.delta, p.lambda, has_imag(a));
+    const InBuf ab(a.data(), n * n, P->cplx);
     rep.eigenvalues.resize(n);
-    for (std::size_t i = 0; i < n; ++i) rep.eigenvalues[i] = c_of(eig[i]);
-    rep.residuals = res;
+    rep.residuals.resize(n);
+    OutBuf eb(rep.eigenvalues.data(), n, P->cplx);
+    dpt_error_info e{};
+    check(dpt_readoffs(ctx(), &P->c, ab.p, eb.ptr(), rep.residuals.data(), DPT_MEM_HOST, &e), e);
+    eb.finish(true);
   } else {
     const double nan = std::numeric_limits<double>::quiet_NaN();
     rep.eigenvalues.assign(n, cdouble{nan, nan});

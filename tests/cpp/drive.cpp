@@ -33,6 +33,30 @@ static void put_mat(const std::string& key, const DenseMatrix& a) {
       put(key + "[" + std::to_string(i) + "," + std::to_string(j) + "]", a(i, j).real());
 }
 
+static void put_cvec(const std::string& key, const std::vector<cdouble>& v) {
+  for (std::size_t i = 0; i < v.size(); ++i) {
+    put(key + "[" + std::to_string(i) + "].re", v[i].real());
+    put(key + "[" + std::to_string(i) + "].im", v[i].imag());
+  }
+}
+
+static void put_cmat(const std::string& key, const DenseMatrix& a) {
+  for (std::size_t i = 0; i < a.rows(); ++i)
+    for (std::size_t j = 0; j < a.cols(); ++j) {
+      put(key + "[" + std::to_string(i) + "," + std::to_string(j) + "].re", a(i, j).real());
+      put(key + "[" + std::to_string(i) + "," + std::to_string(j) + "].im", a(i, j).imag());
+    }
+}
+
+static void put_creport(const std::string& key, const ConvergenceReport& r) {
+  std::printf("%s.status %s\n", key.c_str(), to_string(r.status).c_str());
+  put(key + ".iterations", r.iterations);
+  if (r.status != ConvergenceStatus::Diverged) {
+    put_cvec(key + ".eig", r.eigenvalues);
+    put_cmat(key + ".a", r.state.a);
+  }
+}
+
 static void put_report(const std::string& key, const ConvergenceReport& r) {
   std::printf("%s.status %s\n", key.c_str(), to_string(r.status).c_str());
   put(key + ".iterations", r.iterations);
@@ -121,6 +145,51 @@ int main() {
 
   // 5. staged continuation (homotopy_solve, dpt.hpp:145-152)
   put_report("homotopy", homotopy_solve(ru, 3));
+
+  // 6. complex coupling and complex levels (the scans' lambda plane)
+  auto rc = build_random_uniform(9, 17);
+  rc.lambda = cdouble{0.05, 0.02};
+  put_creport("c.random_uniform", iterate_full(rc));
+  put_creport("c.random_uniform_ramped", iterate_ramped(rc, 0.5));
+  put_cmat("c.fixed3", iterate_fixed(ru, 3, cdouble{0.03, 0.01}));
+  DenseMatrix ca = DenseMatrix::identity(9);
+  for (int k = 0; k < 4; ++k) ca = step_full(ca, theta, rc.delta_t, rc.lambda);
+  put_cmat("c.step_full4", ca);
+  std::vector<cdouble> cz(9, cdouble{});
+  cz[4] = 1.0;
+  for (int k = 0; k < 4; ++k) cz = step_single(cz, 4, theta, rc.delta, rc.lambda);
+  put_cvec("c.step_single4", cz);
+  const cdouble ce = eigenvalue_of(cz, 4, rc.d, rc.delta, rc.lambda);
+  put("c.eigenvalue_of.re", ce.real());
+  put("c.eigenvalue_of.im", ce.imag());
+  const auto csr_ = iterate_single(rc, 2);
+  std::printf("c.single.status %s\n", to_string(csr_.status).c_str());
+  put("c.single.iterations", csr_.iterations);
+  put("c.single.eig.re", csr_.eigenvalue.real());
+  put("c.single.eig.im", csr_.eigenvalue.imag());
+  put_cvec("c.single.z", csr_.z);
+  const auto cer = build_er_perturbed_oscillator(2000, 42, cdouble{0.01, 0.004});
+  const auto cdom = dominant_eigenpair(cer);
+  std::printf("c.dominant.status %s\n", to_string(cdom.status).c_str());
+  put("c.dominant.row", double(cdom.row));
+  put("c.dominant.iterations", cdom.iterations);
+  put("c.dominant.eig.re", cdom.eigenvalue.real());
+  put("c.dominant.eig.im", cdom.eigenvalue.imag());
+  put("c.dominant.z_unit[1999].im", cdom.z_unit[1999].imag());
+  ScanGrid cgrid = grid;
+  cgrid.im_min = -0.6;
+  cgrid.im_max = 0.6;
+  cgrid.res_re = 7;
+  cgrid.res_im = 5;
+  const DomainGrid cfull = scan_domain(build_two_by_two(cdouble{1.0, 0.0}), cgrid, {}, sopts, 4);
+  for (std::size_t c = 0; c < cfull.classes.size(); ++c) {
+    put("scan_cfull.class[" + std::to_string(c) + "]", double(int(cfull.classes[c])));
+    put("scan_cfull.iters[" + std::to_string(c) + "]", cfull.iterations[c]);
+  }
+  const DomainGrid csg = scan_domain(three, cgrid, single_mode, sopts, 3);
+  for (std::size_t c = 0; c < csg.classes.size(); ++c)
+    put("scan_csingle.class[" + std::to_string(c) + "]", double(int(csg.classes[c])));
+  put_creport("c.homotopy", homotopy_solve(rc, 3));
   std::printf("done 1\n");
   return 0;
 }

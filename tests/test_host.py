@@ -42,7 +42,7 @@ def test_library_exports_every_declared_symbol():
     assert len(names) >= 25
     missing = [n for n in names if not hasattr(L, n)]
     assert not missing, missing
-    assert L.dpt_abi_version() == 1
+    assert L.dpt_abi_version() == 2
 
 
 def test_options_defaults_and_status_strings():
@@ -60,11 +60,15 @@ def test_no_cpu_fallback():
         P.iterate_full(pr.two_by_two(0.3))
 
 
-def test_shape_errors_before_device():
+def test_shape_errors_and_complex_marshalling():
     with pytest.raises(P.ShapeError):
         P.dpt._Marshal(PartitionedProblem(np.zeros(3), np.zeros((2, 2)), 0.1))
-    with pytest.raises(ValueError):
-        P.dpt._Marshal(PartitionedProblem(np.zeros(2), np.zeros((2, 2)), 0.1 + 0.2j))
+    m = P.dpt._Marshal(PartitionedProblem(np.zeros(2), np.zeros((2, 2)), 0.1 + 0.2j))
+    assert m.prob.is_complex == 1 and m.prob.lambda_im == 0.2 and m.cplx
+    # complex dtype with zero imaginary parts takes the real kernels, returns complex
+    m = P.dpt._Marshal(PartitionedProblem(np.zeros(2, complex), np.zeros((2, 2), complex), 0.1 + 0j))
+    assert m.prob.is_complex == 0 and m.cdtype and not m.cplx
+    assert m.result(np.zeros(2)).dtype == np.complex128
 
 
 def test_degeneracy_scan_matches_brute_force():

@@ -16,11 +16,16 @@ HBM = 6547.2  # GB/s, MEASURED_PEAKS.json
 ap = argparse.ArgumentParser()
 ap.add_argument("--configs", default="c1,c2,c2b,c3,c4,c4b")
 ap.add_argument("--steps", type=int, default=20)
+ap.add_argument("--complex", action="store_true", help="complex coupling lambda(1 + 0.5i): the complex FP64 kernels")
 a = ap.parse_args()
 peak = P.fp64_peak_tflops(0)
 for name in a.configs.split(","):
     t0 = time.time()
     p, o, desc = pr.config(name)
+    cf = 4 if a.complex else 1  # complex: 4 real multiplies per product
+    if a.complex:
+        p = P.PartitionedProblem(p.d, p.delta, p.lam * (1 + 0.5j))
+        desc += " complex"
     gen = time.time() - t0
     n = len(p.d)
     single = name.startswith("c4")
@@ -48,15 +53,15 @@ for name in a.configs.split(","):
     rec = {"config": name, "n": n, "desc": desc, "kernel_ms": kms, "step_ms": sms, "gen_s": round(gen, 2)}
     if single:
         nnz = p.delta.nnz
-        byts = 12 * nnz + 8 * (n + 1) + 24 * n
+        byts = (12 + 8 * a.complex) * nnz + 8 * (n + 1) + 24 * n * (1 + a.complex)
         rec.update(bytes=byts, gbs=byts / (kms * 1e-3) / 1e9, hbm_frac=byts / (kms * 1e-3) / 1e9 / HBM)
     elif hasattr(p.delta, "rowptr"):
         nnz = p.delta.nnz
-        byts = 16 * n * n + 12 * nnz + 8 * (n + 1) + 8 * n
+        byts = 16 * n * n * (1 + a.complex) + (12 + 8 * a.complex) * nnz + 8 * (n + 1) + 8 * n
         rec.update(bytes=byts, gbs=byts / (kms * 1e-3) / 1e9, hbm_frac=byts / (kms * 1e-3) / 1e9 / HBM,
-                   tflops=2 * nnz * n / (kms * 1e-3) / 1e12)
+                   tflops=2 * cf * nnz * n / (kms * 1e-3) / 1e12)
     else:
-        rec.update(tflops=2 * n ** 3 / (kms * 1e-3) / 1e12, fp64_frac=2 * n ** 3 / (kms * 1e-3) / 1e12 / peak)
+        rec.update(tflops=2 * cf * n ** 3 / (kms * 1e-3) / 1e12, fp64_frac=2 * cf * n ** 3 / (kms * 1e-3) / 1e12 / peak)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     r = P.dominant_eigenpair(pd, P.IterationOptions(**o)) if single else P.iterate_full(pd, P.IterationOptions(**o))
