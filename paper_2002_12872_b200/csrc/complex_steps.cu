@@ -84,14 +84,15 @@ __global__ void __launch_bounds__(kCsrCThreads) csr_step_cplx_kernel(DevSolve s,
     if (sl >= S.nslices) break;
     const int64_t t = sl * 32 + lane;
     const int32_t j = S.lane_col[t];
-    const int32_t len = S.lane_len[t];
     const int64_t off = S.slice_off[sl];
+    const int32_t width = int32_t((S.slice_off[sl + 1] - off) >> 5);
     cd p[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) p[r] = cmake(0.0, 0.0);
-    for (int32_t q = 0; q < len; ++q) {  // sequential CSR order in this lane
+    for (int32_t q = 0; q < width; ++q) {  // sequential CSR order in this lane; col -1 = bubble
       const int64_t idx = off + int64_t(q) * 32 + lane;
       const int32_t c = __ldg(S.cols + idx);
+      if (c < 0) continue;
       const double2 v2 = __ldg(reinterpret_cast<const double2*>(S.vals) + idx);
       const cd v = cmake(v2.x, v2.y);
 #pragma unroll
@@ -149,13 +150,14 @@ __global__ void __launch_bounds__(kCsrCThreads) csr_step_cplx_kernel(DevSolve s,
     const int64_t il = il0 + r, gi = s.row0 + il;
     const int64_t t = S.pos_of[gi];
     const int L = int(t & 31);
-    const int32_t len = S.lane_len[t];
     const int64_t off = S.slice_off[t >> 5];
+    const int32_t width = int32_t((S.slice_off[(t >> 5) + 1] - off) >> 5);
     const double* arow_new = a_out + size_t(il) * size_t(ld);
     cd part = cmake(0.0, 0.0);
-    for (int32_t q = lane; q < len; q += 32) {
+    for (int32_t q = lane; q < width; q += 32) {
       const int64_t idx = off + int64_t(q) * 32 + L;
       const int32_t c = __ldg(S.cols + idx);
+      if (c < 0) continue;
       const double2 v2 = __ldg(reinterpret_cast<const double2*>(S.vals) + idx);
       part = cadd(part, cmul(cmake(v2.x, v2.y), cmake(arow_new[2 * c], arow_new[2 * c + 1])));
     }

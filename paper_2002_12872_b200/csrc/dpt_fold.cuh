@@ -73,14 +73,17 @@ static __device__ void cycle_sample_precheck(const DevSolve& s, double* sh) {
   const bool have = e < ns;
   const int64_t r = have ? e / n : 0, c = have ? e % n : 0;
   const double cv = have ? cur[r * ld + c] : 0.0;
+  // branch-free loads (clamped slot index) so all window entries are in flight
+  // at once: a guarded load per entry serialised ~1 us of latency per entry
+  double pv[DPT_MAX_WINDOW];
 #pragma unroll
   for (int p = 0; p < DPT_MAX_WINDOW; ++p) {
-    m[p] = 0.0;
-    if (p < npast && have) {
-      const double* past = s.slots + size_t((j - 2 - p) % s.nslots) * size_t(s.slot_elems);
-      m[p] = fabs(cv - past[r * ld + c]);
-    }
+    const int pp = p < npast ? p : 0;
+    const double* past = s.slots + size_t((j - 2 - pp) % s.nslots) * size_t(s.slot_elems);
+    pv[p] = (have && npast > 0) ? __ldcg(past + r * ld + c) : 0.0;
   }
+#pragma unroll
+  for (int p = 0; p < DPT_MAX_WINDOW; ++p) m[p] = (p < npast && have) ? fabs(cv - pv[p]) : 0.0;
   __shared__ double wm[32][DPT_MAX_WINDOW];
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
 #pragma unroll

@@ -384,8 +384,8 @@ struct DevProblem {
 
 // SELL-32 image of a CSR matrix for K2: rows sorted by length (descending,
 // stable) inside windows of 256, grouped 32 per slice, entry q of lane L at
-// slice_off + 32 q + L; padding entries hold column 0 / value 0 and are skipped
-// by the kernel (lane_len).  Within a lane the entries keep CSR order.
+// slice_off + 32 q + L; padding and bubble entries hold column -1 and are
+// skipped by the kernels.  Within a lane the entries keep CSR order.
 void build_sell(DevProblem& dp, const std::vector<int64_t>& rp, const std::vector<int32_t>& cl,
                 const std::vector<double>& vl, cudaStream_t st, dpt_error_info* err) {
   const int64_t n = dp.n;
@@ -400,35 +400,83 @@ void build_sell(DevProblem& dp, const std::vector<int64_t>& rp, const std::vecto
     });
     for (size_t q = 0; q < idx.size(); ++q) perm[size_t(w0) + q] = idx[q];
   }
+  // Bank-conflict-aware schedule.  K2 gathers A(i, col) from shared memory;
+  // the lanes the shared-memory unit serves in one wavefront (a half-warp for
+  // 8-byte elements, a quarter-warp for 16-byte complex ones) are conflict-free
+  // iff their columns differ mod G (rows are staged contiguously, so a row's
+  // base offset shifts every bank equally).  Each step issues, per lane group,
+  // the next entry of every lane whose bank is still free, longest remaining
+  // lane first; the others wait (bubble, col = -1).  Lanes keep CSR order, so
+  // each P(i, j) accumulates exactly as before.  DPT_SELL_SCHED=0 packs the
+  // entries densely instead (the unscheduled layout, for comparison).
+  const int cx = dp.cplx ? 2 : 1;  // complex values are interleaved (re, im)
+  const int NB = dp.cplx ? 8 : 16;  // banks (8-byte pairs / 16-byte quads) per 128-byte wavefront
+  const char* sched_env = std::getenv("DPT_SELL_SCHED");
+  const bool sched = !(sched_env && sched_env[0] == '0');
+  const char* g_env = std::getenv("DPT_SELL_GROUP");
+  const int G = g_env ? std::max(NB, std::min(32, std::atoi(g_env))) : NB;  // lanes scheduled together
+  const int cap = G / NB;                                                  // uses per bank per step
   std::vector<int64_t> off(size_t(ns + 1), 0);
   std::vector<int32_t> lcol(size_t(ns * 32), -1), llen(size_t(ns * 32), 0);
   std::vector<int64_t> pos(size_t(n), 0);
+  std::vector<std::vector<int64_t>> slot_src(static_cast<size_t>(ns));  // [step * 32 + lane] -> CSR index or -1
   for (int64_t sl = 0; sl < ns; ++sl) {
-    int64_t width = 0;
+    int64_t len[32], head[32], beg[32];
+    int64_t remaining = 0, width = 0;
     for (int L = 0; L < 32; ++L) {
       const int64_t t = sl * 32 + L;
       const int64_t j = perm[size_t(t)];
+      len[L] = head[L] = 0;
+      beg[L] = 0;
       if (j < 0) continue;
-      const int64_t len = rp[size_t(j) + 1] - rp[size_t(j)];
+      len[L] = rp[size_t(j) + 1] - rp[size_t(j)];
+      beg[L] = rp[size_t(j)];
       lcol[size_t(t)] = int32_t(j);
-      llen[size_t(t)] = int32_t(len);
+      llen[size_t(t)] = int32_t(len[L]);
       pos[size_t(j)] = t;
-      width = std::max(width, len);
+      remaining += len[L];
+      width = std::max(width, len[L]);
     }
-    off[size_t(sl) + 1] = off[size_t(sl)] + 32 * width;
+    std::vector<int64_t>& src = slot_src[size_t(sl)];
+    if (!sched) {
+      src.assign(size_t(width * 32), -1);
+      for (int L = 0; L < 32; ++L)
+        for (int64_t q = 0; q < len[L]; ++q) src[size_t(q * 32 + L)] = beg[L] + q;
+    } else {
+      int order[32];
+      while (remaining > 0) {
+        const size_t base = src.size();
+        src.resize(base + 32, -1);
+        for (int g0 = 0; g0 < 32; g0 += G) {
+          for (int q = 0; q < G; ++q) order[q] = g0 + q;
+          std::stable_sort(order, order + G, [&](int x, int y) { return len[x] - head[x] > len[y] - head[y]; });
+          int used[16] = {0};
+          for (int q = 0; q < G; ++q) {
+            const int L = order[q];
+            if (head[L] >= len[L]) continue;
+            const int b = int(uint32_t(cl[size_t(beg[L] + head[L])]) % uint32_t(NB));
+            if (used[b] >= cap) continue;
+            ++used[b];
+            src[base + size_t(L)] = beg[L] + head[L];
+            ++head[L];
+            --remaining;
+          }
+        }
+      }
+    }
+    src.resize((src.size() + 127) / 128 * 128, -1);  // K2 reads 4 entries per lane per trip (kCsrU)
+    off[size_t(sl) + 1] = off[size_t(sl)] + int64_t(src.size());
   }
   const int64_t total = off[size_t(ns)];
-  const int cx = dp.cplx ? 2 : 1;  // complex values are interleaved (re, im)
-  std::vector<int32_t> sc(size_t(std::max<int64_t>(total, 1)), 0);
+  std::vector<int32_t> sc(size_t(std::max<int64_t>(total, 1)), -1);
   std::vector<double> sv(size_t(cx * std::max<int64_t>(total, 1)), 0.0);
-  for (int64_t t = 0; t < ns * 32; ++t) {
-    const int32_t j = lcol[size_t(t)];
-    if (j < 0) continue;
-    const int64_t sl = t / 32, L = t % 32;
-    for (int64_t q = 0; q < llen[size_t(t)]; ++q) {
-      const int64_t src = rp[size_t(j)] + q, dst = off[size_t(sl)] + 32 * q + L;
-      sc[size_t(dst)] = cl[size_t(src)];
-      for (int c = 0; c < cx; ++c) sv[size_t(cx * dst + c)] = vl[size_t(cx * src + c)];
+  for (int64_t sl = 0; sl < ns; ++sl) {
+    const std::vector<int64_t>& src = slot_src[size_t(sl)];
+    for (size_t q = 0; q < src.size(); ++q) {
+      if (src[q] < 0) continue;
+      const size_t dst = size_t(off[size_t(sl)]) + q;
+      sc[dst] = cl[size_t(src[q])];
+      for (int c = 0; c < cx; ++c) sv[cx * dst + size_t(c)] = vl[size_t(cx * src[q] + c)];
     }
   }
   dp.nslices = ns;

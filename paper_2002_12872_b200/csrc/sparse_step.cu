@@ -32,6 +32,7 @@ constexpr int kCsrSmemBudget = 200 * 1024;
 static int csr_rows_per_cta(int64_t n) {
   int64_t r = kCsrSmemBudget / (n * 8);
   if (r > 8) r = 8;
+  if (r >= 2 && (r & 1) == 0 && (r + 1) * n * 8 > kCsrSmemBudget) --r;  // odd stride must fit (csr_stride)
   return int(r);  // 0 => rows gathered from global memory
 }
 
@@ -51,11 +52,24 @@ int csr_step_ntiles(int64_t rows, int64_t n) {
 // P(i, j) = sum_q val * A(i, col) accumulates sequentially in CSR order in one
 // lane (no shuffle trees).  The next launch's diagonal d(i) = P(A')(i,i) is
 // formed at the end by one warp per owned row (lagged, like K1).
-template <int R>
-__global__ void __launch_bounds__(kCsrThreads) csr_step_kernel(DevSolve s, DevSell S, int use_smem) {
+//
+// Shared-memory layout: the R staged rows are interleaved, element (k, r) at
+// sa[k * S + r] with an odd stride S = R | 1, so the R gathers of one entry
+// share one address computation (immediate offsets) and the bank of (k, r) is
+// a bijection of k mod 16 -- the bank-aware SELL schedule (build_sell) then
+// makes every half-warp's gathers conflict-free for every r.  Bubble entries
+// (col -1, value 0) load nothing and add fma(0, 0, p) = p exactly (p starts at
+// +0 and a sum never turns into -0), so the FMA chain needs no guard.
+// SMEM = false (rows too long for shared memory) gathers from global instead.
+constexpr int csr_stride(int R) { return (R & 1) ? R : R + 1; }
+constexpr int kCsrU = 4;  // entries in flight per lane; slice widths are padded to a multiple
+
+template <int R, bool SMEM>
+__global__ void __launch_bounds__(kCsrThreads) csr_step_kernel(DevSolve s, DevSell S) {
+  constexpr int ST = csr_stride(R);
   if (s.state->done) return;
   const int jl = launch_index(s);
-  extern __shared__ __align__(16) double sa[];  // [R][n] staged rows of A_{j-1}
+  extern __shared__ __align__(16) double sa[];  // [n][ST] staged rows of A_{j-1}
   __shared__ unsigned long long next_slice;
   __shared__ double red[kCsrThreads / 32][R][2];
   __shared__ double wred[kCsrThreads / 32][3];
@@ -67,28 +81,18 @@ __global__ void __launch_bounds__(kCsrThreads) csr_step_kernel(DevSolve s, DevSe
   double* a_out = s.slots + size_t(slot_out) * size_t(s.slot_elems);
   const double lam_k = lam_of(s, jl), lam = s.lambda;
   const double* d_in = s.dvec[(jl - 1) & 1];
+  const double* __restrict__ ain = a_in + size_t(il0) * size_t(ld);  // SMEM = false: row r at ain + r * ld
 
-  const double* arow[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int rr = r < nr ? r : 0;
-    arow[r] = use_smem ? sa + size_t(rr) * size_t(n) : a_in + size_t(il0 + rr) * size_t(ld);
-  }
   if (threadIdx.x == 0) next_slice = 0ull;
-  if (!use_smem) __syncthreads();
-  if (use_smem) {
-    for (int r = 0; r < nr; ++r) {
-      if ((n & 1) == 0) {
-        const double2* src = reinterpret_cast<const double2*>(a_in + size_t(il0 + r) * size_t(ld));
-        double2* dst = reinterpret_cast<double2*>(sa + size_t(r) * size_t(n));
-        for (int64_t c = threadIdx.x; c < n / 2; c += blockDim.x) dst[c] = src[c];
-      } else {
-        for (int64_t c = threadIdx.x; c < n; c += blockDim.x)
-          sa[size_t(r) * size_t(n) + size_t(c)] = a_in[size_t(il0 + r) * size_t(ld) + size_t(c)];
-      }
-    }
-    __syncthreads();
+  if constexpr (SMEM) {
+    for (int r = 0; r < nr; ++r)
+      for (int64_t c = threadIdx.x; c < n; c += blockDim.x) sa[size_t(c) * ST + r] = ain[size_t(r) * size_t(ld) + size_t(c)];
   }
+  __syncthreads();
+  auto A = [&](int r, int64_t c) -> double {
+    if constexpr (SMEM) return sa[size_t(c) * ST + r];
+    else return ain[size_t(r < nr ? r : 0) * size_t(ld) + size_t(c)];
+  };
   double ti[R], di[R], epsi[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
@@ -115,35 +119,30 @@ __global__ void __launch_bounds__(kCsrThreads) csr_step_kernel(DevSolve s, DevSe
     if (sl >= S.nslices) break;
     const int64_t t = sl * 32 + lane;
     const int32_t j = S.lane_col[t];
-    const int32_t len = S.lane_len[t];
     const int64_t off = S.slice_off[sl];
-    const int32_t width = int32_t((S.slice_off[sl + 1] - off) >> 5);
+    const int32_t width = int32_t((S.slice_off[sl + 1] - off) >> 5);  // multiple of kCsrU
     const int32_t* __restrict__ sc = S.cols + off + lane;
     const double* __restrict__ sv = S.vals + off + lane;
     double p[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) p[r] = 0.0;
-    constexpr int U = 4;  // entries in flight per lane
-    for (int32_t q0 = 0; q0 < width; q0 += U) {
-      int32_t c[U];
-      double v[U];
+    for (int32_t q0 = 0; q0 < width; q0 += kCsrU) {
+      int32_t c[kCsrU];
+      double v[kCsrU];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const bool in = q0 + u < width;
-        c[u] = in ? __ldg(sc + size_t(q0 + u) * 32) : 0;
-        v[u] = in ? __ldg(sv + size_t(q0 + u) * 32) : 0.0;
+      for (int u = 0; u < kCsrU; ++u) {
+        c[u] = __ldg(sc + (q0 + u) * 32);
+        v[u] = __ldg(sv + (q0 + u) * 32);
       }
-      double g[U][R];
+      double g[kCsrU][R];
 #pragma unroll
-      for (int u = 0; u < U; ++u)
+      for (int u = 0; u < kCsrU; ++u)
 #pragma unroll
-        for (int r = 0; r < R; ++r) g[u][r] = arow[r][c[u]];
+        for (int r = 0; r < R; ++r) g[u][r] = c[u] >= 0 ? A(r, c[u]) : 0.0;  // bubbles issue no load
 #pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (q0 + u < len) {
+      for (int u = 0; u < kCsrU; ++u)
 #pragma unroll
-          for (int r = 0; r < R; ++r) p[r] = __fma_rn(v[u], g[u][r], p[r]);
-        }
+        for (int r = 0; r < R; ++r) p[r] = __fma_rn(v[u], g[u][r], p[r]);
     }
     if (j >= 0) {
       const double tj = s.theta[j];
@@ -151,7 +150,7 @@ __global__ void __launch_bounds__(kCsrThreads) csr_step_kernel(DevSolve s, DevSe
       for (int r = 0; r < R; ++r) {
         if (r >= nr) break;
         const int64_t gi = s.row0 + il0 + r;
-        const double aij = arow[r][j];
+        const double aij = A(r, j);
         double val;
         if (gi == j) {
           val = 1.0;
@@ -194,13 +193,14 @@ __global__ void __launch_bounds__(kCsrThreads) csr_step_kernel(DevSolve s, DevSe
     const int64_t il = il0 + r, gi = s.row0 + il;
     const int64_t t = S.pos_of[gi];
     const int L = int(t & 31);
-    const int32_t len = S.lane_len[t];
     const int64_t off = S.slice_off[t >> 5];
+    const int32_t width = int32_t((S.slice_off[(t >> 5) + 1] - off) >> 5);
     const double* arow_new = a_out + size_t(il) * size_t(ld);
     double part = 0.0;
-    for (int32_t q = lane; q < len; q += 32) {
+    for (int32_t q = lane; q < width; q += 32) {
       const int64_t idx = off + int64_t(q) * 32 + L;
-      part = __fma_rn(__ldg(S.vals + idx), arow_new[__ldg(S.cols + idx)], part);
+      const int32_t c = __ldg(S.cols + idx);
+      if (c >= 0) part = __fma_rn(__ldg(S.vals + idx), arow_new[c], part);
     }
     part = warp_sum(part);
     if (lane == 0) {
@@ -234,16 +234,20 @@ cudaError_t launch_csr_step(const DevSolve& s, const DevSell& d, cudaStream_t st
   const int use_smem = Rs > 0 ? 1 : 0;
   const int R = use_smem ? Rs : 1;
   const unsigned grid = unsigned((s.rows + R - 1) / R);
-  const size_t smem = use_smem ? size_t(R) * size_t(s.n) * 8 : 0;
+  const size_t smem = use_smem ? size_t(csr_stride(R)) * size_t(s.n) * 8 : 0;
+  if (!use_smem) {
+    csr_step_kernel<1, false><<<grid, kCsrThreads, 0, st>>>(s, d);
+    return cudaGetLastError();
+  }
 #define DPT_CSR_CASE(RR)                                                                          \
   case RR: {                                                                                      \
     static bool attr = false;                                                                     \
     if (!attr) {                                                                                  \
-      cudaFuncSetAttribute(csr_step_kernel<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
+      cudaFuncSetAttribute(csr_step_kernel<RR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                            kCsrSmemBudget + 1024);                                                \
       attr = true;                                                                                \
     }                                                                                             \
-    csr_step_kernel<RR><<<grid, kCsrThreads, smem, st>>>(s, d, use_smem);                         \
+    csr_step_kernel<RR, true><<<grid, kCsrThreads, smem, st>>>(s, d);                             \
     break;                                                                                        \
   }
   switch (R) {
