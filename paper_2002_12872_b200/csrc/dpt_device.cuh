@@ -45,7 +45,19 @@ struct DevSolve {
   double* cyclepart;    // [fold_blocks][DPT_MAX_WINDOW]
   int fixed_mode;       // iterate_fixed: no decisions, step every launch
   int fuse_decide;      // single rank: the fold's last block also runs the decision
+  // device-side iteration loop (CUDA graph WHILE node, solver.cu drive_graph):
+  // the fold's decision sets the loop condition; 0 = launched from the host.
+  int has_loop;
+  int loop_total;                      // last launch index the loop may run
+  unsigned long long loop_cond;        // cudaGraphConditionalHandle
 };
+
+// Last-block election fences.  __threadfence() is fence.sc.gpu (MEMBAR.SC.GPU),
+// measured at 73k-165k cycles for the first one in a kernel on B200
+// (tools/probe/latency.cu); the release/acquire pattern only needs acq_rel
+// (~800 cycles): writers release their partials before the counter atomic,
+// the elected last block acquires them after it.
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
 __device__ __forceinline__ int launch_index(const DevSolve& s) { return s.state->j + 1; }
 

@@ -60,6 +60,13 @@ cudaError_t launch_fold(const DevSolve& s, int ntiles_this, cudaStream_t st);
 cudaError_t launch_decide(const DevSolve& s, cudaStream_t st);
 cudaError_t launch_cycle(const DevSolve& s, int64_t elems, cudaStream_t st);
 cudaError_t launch_identity(const DevSolve& s, cudaStream_t st);
+// levels.cu: device-side setup scans (dominant selection, gap-row degeneracy, uniform CSR)
+cudaError_t launch_levels_scan(const double* d, int64_t n, int cx, double* scratch, unsigned* counter, double* out,
+                               cudaStream_t st);
+cudaError_t launch_levels_partner(const double* d, int64_t n, int cx, int64_t row, double thresh,
+                                  unsigned long long* first, cudaStream_t st);
+cudaError_t launch_rowptr_uniform(const int64_t* rp, int64_t n, int64_t per, unsigned* bad, cudaStream_t st);
+int levels_scratch_doubles();
 cudaError_t launch_unit(const double* z, double* out, int64_t n, double* scratch /*[297]*/, unsigned* counter,
                         cudaStream_t st);
 cudaError_t launch_rowdot(const DevSolve& s, const double* delta, const DevCsr* csr, cudaStream_t st);

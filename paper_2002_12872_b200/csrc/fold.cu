@@ -30,10 +30,24 @@ int fold_blocks(int64_t rows) {
   return int(b);
 }
 
+// Loop condition of the device-side iteration loop.  It starts at 1 for every
+// graph launch and keeps its value between iterations, so only the stop is
+// written (cudaGraphSetConditional costs ~15 us of kernel tail; every
+// iteration paying it tripled the fold).  Every path that can end the loop --
+// the decision and the early return of a finished state -- reaches here.
+__device__ __forceinline__ void set_loop_condition(const DevSolve& s) {
+  if (s.has_loop) {
+    const dpt_sm_state* st = s.state;
+    if (st->done || st->j >= s.loop_total) cudaGraphSetConditional(s.loop_cond, 0u);
+  }
+}
+
 __global__ void __launch_bounds__(kFoldThreads) fold_kernel(DevSolve s, int ntiles_this) {
-  if (s.state->done) return;
+  if (s.state->done) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) set_loop_condition(s);
+    return;
+  }
   const int j = launch_index(s);
-  __shared__ double sh[32];
   __shared__ bool last;
   const int64_t rows = s.rows;
   const int ntn = s.ntn;
@@ -56,10 +70,7 @@ __global__ void __launch_bounds__(kFoldThreads) fold_kernel(DevSolve s, int ntil
       dim = warp_sum(dim);
       num = warp_max(num);
       den = warp_max(den);
-      if (lane == 0) {
-        fold_row_store(s, i, d, dim, num, den, dprev, dnext);
-        rmax = fmax(rmax, s.res[i]);
-      }
+      if (lane == 0) rmax = fmax(rmax, fold_row_store(s, i, d, dim, num, den, dprev, dnext));
     }
   } else {
     // few rows (the row map has one): block per row, threads over the blocks;
@@ -92,8 +103,7 @@ __global__ void __launch_bounds__(kFoldThreads) fold_kernel(DevSolve s, int ntil
           ee = fmax(ee, red3[w][2]);
           di += red3[w][3];
         }
-        fold_row_store(s, i, dd, di, nn, ee, dprev, dnext);
-        rmax = fmax(rmax, s.res[i]);
+        rmax = fmax(rmax, fold_row_store(s, i, dd, di, nn, ee, dprev, dnext));
       }
       __syncthreads();
     }
@@ -134,32 +144,44 @@ __global__ void __launch_bounds__(kFoldThreads) fold_kernel(DevSolve s, int ntil
     bp[1] = a1;
     bp[2] = a2;
     bp[3] = rmax;
-    __threadfence();
+    fence_acq_rel_gpu();
     const unsigned prev = atomicAdd(s.counter, 1u);
     last = (prev == gridDim.x - 1);
   }
   __syncthreads();
   if (!last) return;
+  __shared__ dpt_sm_state dec;  // the decided state, for the precheck
   if (threadIdx.x == 0) {
-    __threadfence();
-    double r0 = 0.0, r1 = 0.0, r2 = 0.0, r3 = 0.0;
-    for (unsigned b = 0; b < gridDim.x; ++b) {
-      const volatile double* bp = s.blockpart + size_t(b) * 8;
-      r0 = fmax(r0, bp[0]);
-      r1 = fmax(r1, bp[1]);
-      r2 += bp[2];
-      r3 = fmax(r3, bp[3]);
+    fence_acq_rel_gpu();
+    double r[4] = {0.0, 0.0, 0.0, 0.0};
+    if (gridDim.x == 1) {
+      r[0] = a0;  // this block's own maxima (already complete)
+      r[1] = a1;
+      r[2] = a2;
+      r[3] = rmax;
+    } else {
+      for (unsigned b = 0; b < gridDim.x; ++b) {  // __ldcg: L2, where the other blocks' stores landed
+        const double2 p01 = __ldcg(reinterpret_cast<const double2*>(s.blockpart + size_t(b) * 8));
+        const double2 p23 = __ldcg(reinterpret_cast<const double2*>(s.blockpart + size_t(b) * 8 + 2));
+        r[0] = fmax(r[0], p01.x);
+        r[1] = fmax(r[1], p01.y);
+        r[2] += p23.x;
+        r[3] = fmax(r[3], p23.y);
+      }
     }
-    s.stats[0] = r0;
-    s.stats[1] = r1;
-    s.stats[2] = r2;
-    s.stats[3] = r3;
+    s.stats[0] = r[0];
+    s.stats[1] = r[1];
+    s.stats[2] = r[2];
+    s.stats[3] = r[3];
     *s.counter = 0u;
-    if (s.fuse_decide) decide_now(s);  // single rank: no cross-rank max in between
+    if (s.fuse_decide) {  // single rank: no cross-rank max in between
+      dec = decide_local(s, r);
+      if (s.has_loop && (dec.done || dec.j >= s.loop_total)) cudaGraphSetConditional(s.loop_cond, 0u);
+    }
   }
   if (s.fuse_decide) {
     __syncthreads();
-    cycle_sample_precheck(s, sh);
+    cycle_sample_precheck(s, dec);
   }
 }
 
@@ -219,12 +241,12 @@ __global__ void __launch_bounds__(kFoldThreads) cycle_kernel(DevSolve s, int64_t
     if (threadIdx.x == 0) s.cyclepart[size_t(blockIdx.x) * DPT_MAX_WINDOW + p] = m;
   }
   if (threadIdx.x == 0) {
-    __threadfence();
+    fence_acq_rel_gpu();
     last = (atomicAdd(s.counter, 1u) == gridDim.x - 1);
   }
   __syncthreads();
   if (last && threadIdx.x == 0) {
-    __threadfence();
+    fence_acq_rel_gpu();
     for (int p = 0; p < DPT_MAX_WINDOW; ++p) {
       double m = 0.0;
       if (p < npast && cand[p]) {
@@ -336,12 +358,12 @@ __global__ void __launch_bounds__(256) unit_norm_kernel(const double* __restrict
   v = block_sum(v, sh);
   if (threadIdx.x == 0) {
     part[blockIdx.x] = v;
-    __threadfence();
+    fence_acq_rel_gpu();
     last = atomicAdd(counter, 1u) == gridDim.x - 1;
   }
   __syncthreads();
   if (last && threadIdx.x == 0) {
-    __threadfence();
+    fence_acq_rel_gpu();
     double t = 0.0;
     for (unsigned b = 0; b < gridDim.x; ++b) t += ((volatile double*)part)[b];
     *nrm = sqrt(t);

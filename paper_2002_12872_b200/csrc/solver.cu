@@ -19,6 +19,10 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <set>
+#include <cstdio>
 #include <map>
 #include <unordered_map>
 #include <cmath>
@@ -81,11 +85,26 @@ struct dpt_ctx {
   // call on this context (cudaMalloc / cudaFree synchronise and cost ~ms for
   // the 100 MB-scale iterate buffers).  All work of a call is stream-ordered on
   // `stream`, so a recycled block is never touched by stale kernels.
-  std::multimap<size_t, void*> free_blocks;
+  // Ordered by (size, address): a request takes the smallest fitting size and,
+  // among equal sizes, the lowest address -- independent of release order, so
+  // an identical call sequence gets identical buffers (cached loop graphs hit).
+  std::set<std::pair<size_t, void*>> free_blocks;
   size_t cached = 0;
   // pinned host snapshot buffers, kept across calls
   void* pinned = nullptr;
   size_t pinned_bytes = 0;
+  // Instantiated device-loop graphs (drive_graph), keyed by every parameter
+  // the captured launches depend on.  Repeated solves of one problem get the
+  // same workspace blocks from the caching allocator, hence the same key, and
+  // skip the ~0.45 ms instantiation.
+  struct LoopGraph {
+    std::vector<unsigned char> key;
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ge = nullptr;
+    unsigned long long cond = 0;
+    int64_t per_body = 0;
+  };
+  std::vector<LoopGraph> loop_graphs;  // most recent last, at most kMaxLoopGraphs
 };
 
 namespace {
@@ -100,7 +119,7 @@ void* ctx_malloc(size_t bytes, cudaError_t* e) {
   dpt_ctx* c = t_ctx;
   bytes = round_block(bytes);
   if (c) {
-    auto it = c->free_blocks.lower_bound(bytes);
+    auto it = c->free_blocks.lower_bound(std::make_pair(bytes, static_cast<void*>(nullptr)));
     if (it != c->free_blocks.end() && it->first <= bytes + bytes / 4) {
       void* p = it->second;
       c->cached -= it->first;
@@ -128,7 +147,7 @@ void ctx_release(void* p, size_t bytes) {
     return;
   }
   bytes = round_block(bytes);
-  c->free_blocks.emplace(bytes, p);
+  c->free_blocks.emplace(std::make_pair(bytes, p));
   c->cached += bytes;
   const size_t limit = size_t(48) << 30;  // keep at most 48 GiB cached
   while (c->cached > limit && !c->free_blocks.empty()) {
@@ -179,11 +198,16 @@ bool debug_sync() {
 struct DBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  bool owned = true;  // false: a view of caller-owned device memory (never released)
   DBuf() = default;
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
   ~DBuf() {
-    if (p) ctx_release(p, bytes);
+    if (p && owned) ctx_release(p, bytes);
+  }
+  void view(const void* q) {
+    p = const_cast<void*>(q);
+    owned = false;
   }
   template <class T>
   T* as() const {
@@ -368,7 +392,6 @@ struct DevProblem {
   int cplx = 0;
   double lambda_im = 0.0;
   int kind = DPT_DELTA_DENSE;
-  std::vector<double> d_host;  // theta on the host (gap policy)
   DBuf theta, delta, rowptr, cols, vals;
   DBuf dmap;  // CUtensorMap for dense Delta
   int big = 1;  // dense tile configuration (dense_cfg_for)
@@ -533,10 +556,16 @@ void upload(DevProblem& dp, dpt_ctx* ctx, const dpt_problem* p, dpt_error_info* 
   const cudaMemcpyKind k = p->mem == DPT_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   const cudaMemcpyKind hk = p->mem == DPT_MEM_DEVICE ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost;
   cudaStream_t st = ctx->stream;
-  dp.d_host.resize(size_t(cx * n));
-  if (n) CK(cudaMemcpy(dp.d_host.data(), p->d, size_t(cx * n) * 8, hk));
-  dalloc(dp.theta, size_t(cx * n) * 8, err);
-  if (n) CK(cudaMemcpyAsync(dp.theta.p, dp.d_host.data(), size_t(cx * n) * 8, cudaMemcpyHostToDevice, st));
+  // Device-resident inputs whose layout the kernels take as is are used in
+  // place (views); host inputs and re-laid-out arrays are copied.
+  const bool dev = p->mem == DPT_MEM_DEVICE;
+  auto aligned16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15u) == 0; };
+  if (dev && n) {
+    dp.theta.view(p->d);
+  } else {
+    dalloc(dp.theta, size_t(cx * n) * 8, err);
+    if (n) CK(cudaMemcpyAsync(dp.theta.p, p->d, size_t(cx * n) * 8, k, st));
+  }
   if (p->delta_kind == DPT_DELTA_DENSE) {
     if (dp.cplx) {
       // real image B (2n x 2n): row 2j = (Re D(j,k), -Im D(j,k))_k, row 2j+1 = (Im D(j,k), Re D(j,k))_k,
@@ -560,6 +589,9 @@ void upload(DevProblem& dp, dpt_ctx* ctx, const dpt_problem* p, dpt_error_info* 
       dalloc(dp.delta, B.size() * 8 + 64, err);
       if (n) CK(cudaMemcpyAsync(dp.delta.p, B.data(), B.size() * 8, cudaMemcpyHostToDevice, st));
       CK(cudaStreamSynchronize(st));  // B goes out of scope
+    } else if (dev && n && dp.ld == n && aligned16(p->delta)) {
+      dp.ldd = dp.ld;
+      dp.delta.view(p->delta);  // TMA-ready as is: 16-byte aligned, even leading dimension
     } else {
       dp.ldd = dp.ld;
       dalloc(dp.delta, size_t(n) * size_t(dp.ldd) * 8 + 64, err);
@@ -578,13 +610,30 @@ void upload(DevProblem& dp, dpt_ctx* ctx, const dpt_problem* p, dpt_error_info* 
       CK(cudaMemcpy(&nnz, p->rowptr + n, 8, cudaMemcpyDeviceToHost));
     }
     dp.nnz = nnz;
-    {
+    if (!sell) {  // K3 only needs the uniform-16 test: on the device for device inputs
+      if (n > 0 && !dp.cplx && nnz == 16 * n) {
+        if (dev) {
+          DBuf bad;
+          dalloc(bad, 16, err);
+          CK(cudaMemsetAsync(bad.p, 0, 4, st));
+          CK(launch_rowptr_uniform(p->rowptr, n, 16, bad.as<unsigned>(), st));
+          unsigned hb = 1;
+          CK(cudaMemcpyAsync(&hb, bad.p, 4, cudaMemcpyDeviceToHost, st));
+          CK(cudaStreamSynchronize(st));
+          dp.uniform16 = hb == 0 ? 1 : 0;
+        } else {
+          bool u = true;
+          for (int64_t i = 0; i <= n && u; ++i) u = p->rowptr[i] == 16 * i;
+          dp.uniform16 = u ? 1 : 0;
+        }
+      }
+    } else {
       std::vector<int64_t> rp(size_t(n + 1));
       CK(cudaMemcpy(rp.data(), p->rowptr, size_t(n + 1) * 8, hk));
       bool u = n > 0 && !dp.cplx;
       for (int64_t i = 0; i <= n && u; ++i) u = rp[size_t(i)] == 16 * i;
       dp.uniform16 = u ? 1 : 0;
-      if (sell) {
+      {
         std::vector<int32_t> cl(static_cast<size_t>(nnz));
         std::vector<double> vl(static_cast<size_t>(cx * nnz));
         if (nnz) {
@@ -594,13 +643,19 @@ void upload(DevProblem& dp, dpt_ctx* ctx, const dpt_problem* p, dpt_error_info* 
         build_sell(dp, rp, cl, vl, st, err);
       }
     }
-    dalloc(dp.rowptr, size_t(n + 1) * 8, err);
-    dalloc(dp.cols, size_t(nnz) * 4, err);
-    dalloc(dp.vals, size_t(cx * nnz) * 8, err);
-    CK(cudaMemcpyAsync(dp.rowptr.p, p->rowptr, size_t(n + 1) * 8, k, st));
-    if (nnz) {
-      CK(cudaMemcpyAsync(dp.cols.p, p->cols, size_t(nnz) * 4, k, st));
-      CK(cudaMemcpyAsync(dp.vals.p, p->vals, size_t(cx * nnz) * 8, k, st));
+    if (dev && nnz && aligned16(p->cols) && aligned16(p->vals) && aligned16(p->rowptr)) {
+      dp.rowptr.view(p->rowptr);  // K3 reads int4 / double2 vectors: 16-byte alignment
+      dp.cols.view(p->cols);
+      dp.vals.view(p->vals);
+    } else {
+      dalloc(dp.rowptr, size_t(n + 1) * 8, err);
+      dalloc(dp.cols, size_t(nnz) * 4, err);
+      dalloc(dp.vals, size_t(cx * nnz) * 8, err);
+      CK(cudaMemcpyAsync(dp.rowptr.p, p->rowptr, size_t(n + 1) * 8, k, st));
+      if (nnz) {
+        CK(cudaMemcpyAsync(dp.cols.p, p->cols, size_t(nnz) * 4, k, st));
+        CK(cudaMemcpyAsync(dp.vals.p, p->vals, size_t(cx * nnz) * 8, k, st));
+      }
     }
   }
 }
@@ -623,6 +678,7 @@ void make_work(Work& w, dpt_ctx* ctx, DevProblem& dp, Mode mode, int64_t row0, i
                int max_iter, const std::vector<double>* lam_tab, const std::vector<int>* set_tab,
                const dpt_sm_options& so, double lambda, int fixed_mode, dpt_error_info* err) {
   DevSolve& s = w.s;
+  std::memset(&s, 0, sizeof(s));  // padding too: the bytes key the cached loop graphs
   s.n = dp.n;
   s.ld = dp.ld;
   s.ncol = dp.ncol;
@@ -778,6 +834,128 @@ void step_launch(dpt_ctx* ctx, Work& w, DevProblem& dp, Mode mode, int64_t row, 
   ctx->launches += 1;
 }
 
+bool graph_loop_enabled() {
+  const char* e = std::getenv("DPT_GRAPH_LOOP");
+  return !(e && e[0] == '0');
+}
+
+void replay_trace(Work& w, int nt, int from, dpt_trace_fn trace, void* user, dpt_error_info* err) {
+  if (!trace || nt <= from) return;
+  CK(cudaMemcpy(w.h_trace, w.s.trace, size_t(nt) * 3 * 8, cudaMemcpyDeviceToHost));
+  for (int q = from; q < nt; ++q)
+    if (trace(int(w.h_trace[3 * q]), w.h_trace[3 * q + 1], w.h_trace[3 * q + 2], user) != 0) {
+      set_err(err, DPT_ERR_TRACE, "trace sink aborted the iteration");
+      throw Fail{DPT_ERR_TRACE};
+    }
+}
+
+// Device-side iteration loop (single rank): one CUDA graph whose WHILE
+// conditional node repeats {step, fold (+decision), cycle}; the decision in
+// the fold's last block sets the loop condition, so the loop stops exactly at
+// the terminal launch -- no host round trips, no speculative no-op launches.
+// The trace log is replayed to the sink afterwards, in k order.
+constexpr size_t kMaxLoopGraphs = 8;
+
+template <class T>
+void key_add(std::vector<unsigned char>& k, const T& v) {
+  const unsigned char* p = reinterpret_cast<const unsigned char*>(&v);
+  k.insert(k.end(), p, p + sizeof(T));
+}
+
+void drive_graph(dpt_ctx* ctx, Work& w, DevProblem& dp, Mode mode, int64_t row, int total, int issued,
+                 int64_t cycle_elems, dpt_trace_fn trace, void* user, dpt_error_info* err) {
+  cudaStream_t st = ctx->stream;
+  struct LoopReset {
+    DevSolve* s;
+    ~LoopReset() { s->has_loop = 0; }
+  } lr{&w.s};
+  // every input of the captured launches (step_launch + post_step)
+  std::vector<unsigned char> key;
+  key_add(key, w.s);
+  key_add(key, int(mode));
+  key_add(key, row);
+  key_add(key, total);
+  key_add(key, cycle_elems);
+  key_add(key, w.ntiles_step);
+  key_add(key, w.amaps.p);
+  key_add(key, dp.delta.p);
+  key_add(key, dp.dmap.p);
+  key_add(key, dp.big);
+  key_add(key, dp.cplx);
+  key_add(key, dp.kind);
+  key_add(key, dp.uniform16);
+  key_add(key, dp.csr());
+  key_add(key, dp.sell());
+  dpt_ctx::LoopGraph* hit = nullptr;
+  for (auto& lg : ctx->loop_graphs)
+    if (lg.key == key) hit = &lg;
+  static const bool dbg = std::getenv("DPT_GRAPH_DEBUG") != nullptr;
+  if (dbg) std::fprintf(stderr, "[dpt] loop graph %s (%zu cached)\n", hit ? "hit" : "miss", ctx->loop_graphs.size());
+  if (!hit) {
+    dpt_ctx::LoopGraph lg;
+    lg.key = key;
+    CK(cudaGraphCreate(&lg.g, 0));
+    struct Drop {  // destroy the half-built graph on failure
+      dpt_ctx::LoopGraph* p;
+      ~Drop() {
+        if (p && p->ge) cudaGraphExecDestroy(p->ge);
+        if (p && p->g) cudaGraphDestroy(p->g);
+      }
+    } drop{&lg};
+    cudaGraphConditionalHandle h;
+    CK(cudaGraphConditionalHandleCreate(&h, lg.g, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    CK(cudaGraphAddNode(&node, lg.g, nullptr, 0, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    w.s.has_loop = 1;
+    w.s.loop_total = total;
+    w.s.loop_cond = static_cast<unsigned long long>(h);
+    const int64_t before = ctx->launches;
+    CK(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    try {
+      step_launch(ctx, w, dp, mode, row, err);
+      post_step(ctx, w, w.ntiles_step, cycle_elems, err);
+    } catch (...) {
+      cudaGraph_t junk;
+      cudaStreamEndCapture(st, &junk);
+      throw;
+    }
+    cudaGraph_t captured;
+    CK(cudaStreamEndCapture(st, &captured));
+    lg.per_body = ctx->launches - before;
+    ctx->launches = before;
+    lg.cond = static_cast<unsigned long long>(h);
+    CK(cudaGraphInstantiate(&lg.ge, lg.g, 0));
+    if (ctx->loop_graphs.size() >= kMaxLoopGraphs) {
+      auto& old = ctx->loop_graphs.front();
+      cudaGraphExecDestroy(old.ge);
+      cudaGraphDestroy(old.g);
+      ctx->loop_graphs.erase(ctx->loop_graphs.begin());
+    }
+    ctx->loop_graphs.push_back(lg);
+    drop.p = nullptr;
+    hit = &ctx->loop_graphs.back();
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  CK(cudaGraphLaunch(hit->ge, st));
+  const auto t1 = std::chrono::steady_clock::now();
+  CK(cudaMemcpyAsync(w.h_state, w.s.state, sizeof(dpt_sm_state), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const auto t2 = std::chrono::steady_clock::now();
+  if (dbg)
+    std::fprintf(stderr, "[dpt] loop graph launch %.1f us, run+sync %.1f us\n",
+                 std::chrono::duration<double, std::micro>(t1 - t0).count(),
+                 std::chrono::duration<double, std::micro>(t2 - t1).count());
+  const int bodies = std::max(1, w.h_state->j - issued);
+  ctx->launches += hit->per_body * bodies;
+  replay_trace(w, w.h_state->trace_len, 0, trace, user, err);
+}
+
 // Runs launches 1 .. until the state machine terminates (or `total` launches).
 // Launch 1 is the special init (dense) or the generic step from slot 0.
 // Chunks are double-buffered: chunk c+1 is enqueued before the host waits for
@@ -793,6 +971,10 @@ void drive(dpt_ctx* ctx, Work& w, DevProblem& dp, Mode mode, int64_t row, int to
     ctx->launches += 1;
     post_step(ctx, w, dense_init_ntiles(w.s.rows, w.s.ntn, w.s.cplx), cycle_elems, err);
     issued = 1;
+  }
+  if (w.s.fuse_decide && issued < total && graph_loop_enabled()) {
+    drive_graph(ctx, w, dp, mode, row, total, issued, cycle_elems, trace, user, err);
+    return;
   }
   dpt_sm_state* snap = w.h_state;  // [2] pinned snapshots, one per chunk in flight
   cudaEvent_t ev[2];
@@ -978,6 +1160,82 @@ dpt_options opts_or_default(const dpt_options* o) {
     dpt_options_default(&r);
   return r;
 }
+
+// Device-side level scans for device-resident levels (levels.cu): the
+// single-row entry points' selection and gap-row degeneracy policy without
+// copying d to the host.  Return false (caller falls back to the sequential
+// host scans) for host levels or when d holds a NaN.
+bool dev_levels_scan(dpt_ctx* ctx, const dpt_problem* p, double out[7], dpt_error_info* err) {
+  if (p->mem != DPT_MEM_DEVICE || p->n == 0) return false;
+  Guard g(ctx);
+  cudaStream_t st = ctx->stream;
+  const int ns = levels_scratch_doubles();
+  DBuf scratch;
+  dalloc(scratch, size_t(ns + 16) * 8, err);
+  double* base = scratch.as<double>();
+  unsigned* counter = reinterpret_cast<unsigned*>(base + ns);
+  CK(cudaMemsetAsync(counter, 0, 8, st));
+  CK(launch_levels_scan(p->d, p->n, p->is_complex ? 2 : 1, base, counter, base + ns + 2, st));
+  CK(cudaMemcpyAsync(out, base + ns + 2, 7 * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return out[6] == 0.0;
+}
+
+// (Re, Im) of level i of device-resident levels
+void dev_level(dpt_ctx* ctx, const dpt_problem* p, int64_t i, double* re, double* im) {
+  const int cx = p->is_complex ? 2 : 1;
+  double v[2] = {0.0, 0.0};
+  Guard g(ctx);
+  if (cudaMemcpy(v, p->d + cx * i, size_t(cx) * 8, cudaMemcpyDeviceToHost) != cudaSuccess) throw Fail{DPT_ERR_CUDA};
+  *re = v[0];
+  *im = cx == 2 ? v[1] : 0.0;
+}
+
+// first m != row with |d_row - d_m| <= thresh, or -1
+int64_t dev_partner(dpt_ctx* ctx, const dpt_problem* p, int64_t row, double thresh, dpt_error_info* err) {
+  Guard g(ctx);
+  cudaStream_t st = ctx->stream;
+  DBuf f;
+  dalloc(f, 16, err);
+  CK(cudaMemsetAsync(f.p, 0xff, 8, st));
+  CK(launch_levels_partner(p->d, p->n, p->is_complex ? 2 : 1, row, thresh, f.as<unsigned long long>(), st));
+  unsigned long long h = ~0ull;
+  CK(cudaMemcpyAsync(&h, f.p, 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return h == ~0ull ? -1 : int64_t(h);
+}
+
+[[noreturn]] void degenerate_error_dev(dpt_ctx* ctx, const dpt_problem* p, int64_t i, int64_t j, dpt_error_info* err) {
+  double v[4];
+  dev_level(ctx, p, i, &v[0], &v[1]);
+  dev_level(ctx, p, j, &v[2], &v[3]);
+  const double d2[4] = {v[0], v[1], v[2], v[3]};
+  // degenerate_error indexes interleaved (re, im) pairs when cplx
+  const double* dd = d2;
+  if (p->is_complex) {
+    if (err) {
+      err->i = i; err->j = j; err->ei = dd[0]; err->ei_im = dd[1]; err->ej = dd[2]; err->ej_im = dd[3];
+    }
+  } else if (err) {
+    err->i = i; err->j = j; err->ei = dd[0]; err->ej = dd[2]; err->ei_im = 0.0; err->ej_im = 0.0;
+  }
+  set_err(err, DPT_ERR_DEGENERATE,
+          "degenerate spectrum: levels " + std::to_string(i) + " and " + std::to_string(j) +
+              " coincide within tolerance");
+  throw Fail{DPT_ERR_DEGENERATE};
+}
+
+// Host phase timer (DPT_TIMING=1 prints each phase of an API call to stderr).
+struct PhaseTimer {
+  bool on = std::getenv("DPT_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[dpt] %-24s %9.1f us\n", what, std::chrono::duration<double, std::micro>(now - t).count());
+    t = now;
+  }
+};
 
 std::vector<double> host_levels(const dpt_problem* p, dpt_error_info* err) {
   const size_t cnt = size_t(p->n) * (p->is_complex ? 2 : 1);  // interleaved when complex
@@ -1181,8 +1439,10 @@ int run_single(dpt_ctx* ctx, const dpt_problem* p, int64_t row, const dpt_option
   const int64_t n = p->n;
   const bool fixed = z_in != nullptr;
   const bool ramped = ramp_alpha > 0.0;
+  PhaseTimer pt;
   DevProblem dp;
   upload(dp, ctx, p, err);
+  pt.mark("single: upload");
   const int cx = dp.cplx ? 2 : 1;
   if (fixed) dp.lambda_im = fixed_lambda_im;
   const int win = fixed ? 0 : (o.cycle_window >= 2 ? std::min(o.cycle_window, DPT_MAX_WINDOW) : 0);  // dpt.cpp:207
@@ -1220,6 +1480,7 @@ int run_single(dpt_ctx* ctx, const dpt_problem* p, int64_t row, const dpt_option
   Work w;
   make_work(w, ctx, dp, MODE_SINGLE, row, 1, 1, nslots, max_iter, ramped && !fixed ? &lam_tab : nullptr,
             ramped && !fixed ? &set_tab : nullptr, so, lam, fixed ? 1 : 0, err);
+  pt.mark("single: make_work");
   cudaStream_t st = ctx->stream;
   CK(cudaEventRecord(ctx->ev0, st));
   int final_iter = 0, status = DPT_MAX_ITERATIONS, iters = max_iter, readoffs = 1;
@@ -1245,6 +1506,7 @@ int run_single(dpt_ctx* ctx, const dpt_problem* p, int64_t row, const dpt_option
   } else {
     CK(launch_identity(w.s, st));  // z = e_row (rows == 1, row0 == row)
     drive(ctx, w, dp, MODE_SINGLE, row, total, false, trace, user, err);
+    pt.mark("single: drive");
     if (!w.h_state->done) {
       set_err(err, DPT_ERR_CUDA, "internal: iteration budget consumed without a terminal status");
       throw Fail{DPT_ERR_CUDA};
@@ -1287,6 +1549,7 @@ int run_single(dpt_ctx* ctx, const dpt_problem* p, int64_t row, const dpt_option
     rep->residual = res;
     rep->row = row;
   }
+  pt.mark("single: outputs");
   return DPT_OK;
 }
 
@@ -1363,6 +1626,11 @@ void dpt_ctx_destroy(dpt_ctx* ctx) {
     Guard g(ctx);
     if (ctx->comm && nccl_api() && nccl_api()->comm_destroy) nccl_api()->comm_destroy(ctx->comm);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    for (auto& lg : ctx->loop_graphs) {
+      if (lg.ge) cudaGraphExecDestroy(lg.ge);
+      if (lg.g) cudaGraphDestroy(lg.g);
+    }
+    ctx->loop_graphs.clear();
     for (auto& kv : ctx->free_blocks) cudaFree(kv.second);
     ctx->free_blocks.clear();
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
@@ -1508,11 +1776,18 @@ int dpt_iterate_single(dpt_ctx* ctx, const dpt_problem* p, int64_t row, const dp
     return DPT_ERR_INVALID_ARG;
   }
   const dpt_options o = opts_or_default(opts);
-  std::vector<double> dh = host_levels(p, err);
-  int64_t bj;
-  const bool deg = p->is_complex ? find_degenerate_row_c(p->n, dh.data(), row, o.degeneracy_tol, &bj)
-                                 : find_degenerate_row(p->n, dh.data(), row, o.degeneracy_tol, &bj);
-  if (deg) degenerate_error(err, row, bj, dh.data(), p->is_complex != 0);
+  double sc[7];
+  if (dev_levels_scan(ctx, p, sc, err)) {  // device-resident levels, no NaN
+    const double thr = o.degeneracy_tol * std::max(1.0, std::hypot(sc[3] - sc[2], sc[5] - sc[4]));
+    const int64_t bj = dev_partner(ctx, p, row, thr, err);
+    if (bj >= 0) degenerate_error_dev(ctx, p, row, bj, err);
+  } else {
+    std::vector<double> dh = host_levels(p, err);
+    int64_t bj;
+    const bool deg = p->is_complex ? find_degenerate_row_c(p->n, dh.data(), row, o.degeneracy_tol, &bj)
+                                   : find_degenerate_row(p->n, dh.data(), row, o.degeneracy_tol, &bj);
+    if (deg) degenerate_error(err, row, bj, dh.data(), p->is_complex != 0);
+  }
   return run_single(ctx, p, row, &o, ramp_alpha, trace, user, z_out, out_mem, rep, nullptr, 0, 0.0, nullptr,
                     nullptr, err);
   DPT_API_END
@@ -1528,7 +1803,38 @@ int dpt_dominant_eigenpair(dpt_ctx* ctx, const dpt_problem* p, const dpt_options
     return DPT_ERR_SHAPE;
   }
   const dpt_options o = opts_or_default(opts);
+  PhaseTimer pt;
+  double sc[7];
+  if (dev_levels_scan(ctx, p, sc, err)) {  // device-resident levels, no NaN: scans on the GPU
+    const int64_t best = int64_t(sc[0]);
+    if (n > 1) {
+      const int64_t runner = int64_t(sc[1]);
+      const double spread = std::hypot(sc[3] - sc[2], sc[5] - sc[4]);  // spread_of / spread_of_c
+      const double thr = o.degeneracy_tol * std::max(1.0, spread);
+      double br, bi, rr, ri;
+      dev_level(ctx, p, best, &br, &bi);
+      dev_level(ctx, p, runner, &rr, &ri);
+      if (br - rr < thr) {
+        if (err) {
+          err->i = best;
+          err->j = runner;
+          err->ei = br;
+          err->ej = rr;
+          err->ei_im = bi;
+          err->ej_im = ri;
+        }
+        set_err(err, DPT_ERR_DEGENERATE, "dominant_eigenpair: ambiguous dominant level");
+        return DPT_ERR_DEGENERATE;
+      }
+      const int64_t bj = dev_partner(ctx, p, best, thr, err);
+      if (bj >= 0) degenerate_error_dev(ctx, p, best, bj, err);
+    }
+    pt.mark("dominant: device selection");
+    return run_single(ctx, p, best, &o, 0.0, nullptr, nullptr, z_chart, out_mem, rep, nullptr, 0, 0.0, nullptr,
+                      z_unit, err);
+  }
   std::vector<double> d = host_levels(p, err);
+  pt.mark("dominant: host_levels");
   const int cx = p->is_complex ? 2 : 1;
   auto re = [&](int64_t i) { return d[size_t(cx * i)]; };
   int64_t best = 0;  // first argmax of Re d (dpt.cpp:404-406)
@@ -1558,6 +1864,7 @@ int dpt_dominant_eigenpair(dpt_ctx* ctx, const dpt_problem* p, const dpt_options
   const bool deg = cx == 2 ? find_degenerate_row_c(n, d.data(), best, o.degeneracy_tol, &bj)
                            : find_degenerate_row(n, d.data(), best, o.degeneracy_tol, &bj);
   if (deg) degenerate_error(err, best, bj, d.data(), cx == 2);
+  pt.mark("dominant: selection");
   return run_single(ctx, p, best, &o, 0.0, nullptr, nullptr, z_chart, out_mem, rep, nullptr, 0, 0.0, nullptr,
                     z_unit, err);
   DPT_API_END
