@@ -60,6 +60,15 @@ cudaError_t launch_fold(const DevSolve& s, int ntiles_this, cudaStream_t st);
 cudaError_t launch_decide(const DevSolve& s, cudaStream_t st);
 cudaError_t launch_cycle(const DevSolve& s, int64_t elems, cudaStream_t st);
 cudaError_t launch_identity(const DevSolve& s, cudaStream_t st);
+// sell_build.cu: K2's SELL-32 image built on the device from the CSR in HBM
+cudaError_t launch_sell_perm(const int64_t* rp, int64_t n, int32_t* lane_col, int32_t* lane_len, int64_t* pos_of,
+                             cudaStream_t st);
+cudaError_t launch_sell_widths(const int64_t* rp, const int32_t* cl, int64_t nslices, const int32_t* lane_col, int G,
+                               int sched, int64_t* widths, cudaStream_t st);
+cudaError_t launch_sell_scan(int64_t* widths, int64_t nslices, int64_t* total, cudaStream_t st);
+cudaError_t launch_sell_fill(const int64_t* rp, const int32_t* cl, const double* vl, int cx, int64_t nslices,
+                             const int32_t* lane_col, int G, int sched, const int64_t* off, int32_t* s_cols,
+                             double* s_vals, cudaStream_t st);
 // levels.cu: device-side setup scans (dominant selection, gap-row degeneracy, uniform CSR)
 cudaError_t launch_levels_scan(const double* d, int64_t n, int cx, double* scratch, unsigned* counter, double* out,
                                cudaStream_t st);

@@ -405,117 +405,40 @@ struct DevProblem {
   }
 };
 
-// SELL-32 image of a CSR matrix for K2: rows sorted by length (descending,
-// stable) inside windows of 256, grouped 32 per slice, entry q of lane L at
-// slice_off + 32 q + L; padding and bubble entries hold column -1 and are
-// skipped by the kernels.  Within a lane the entries keep CSR order.
-void build_sell(DevProblem& dp, const std::vector<int64_t>& rp, const std::vector<int32_t>& cl,
-                const std::vector<double>& vl, cudaStream_t st, dpt_error_info* err) {
+// SELL-32 image of a CSR matrix for K2 (layout and bank-aware schedule:
+// csrc/sell_build.cu), built on the device from the CSR already in HBM.
+void build_sell_device(DevProblem& dp, cudaStream_t st, dpt_error_info* err) {
   const int64_t n = dp.n;
   const int64_t ns = (n + 31) / 32;
-  std::vector<int64_t> perm(size_t(ns * 32), -1);
-  for (int64_t w0 = 0; w0 < n; w0 += 256) {
-    const int64_t w1 = std::min(n, w0 + 256);
-    std::vector<int64_t> idx(size_t(w1 - w0));
-    std::iota(idx.begin(), idx.end(), w0);
-    std::stable_sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) {
-      return (rp[size_t(a) + 1] - rp[size_t(a)]) > (rp[size_t(b) + 1] - rp[size_t(b)]);
-    });
-    for (size_t q = 0; q < idx.size(); ++q) perm[size_t(w0) + q] = idx[q];
-  }
-  // Bank-conflict-aware schedule.  K2 gathers A(i, col) from shared memory;
-  // the lanes the shared-memory unit serves in one wavefront (a half-warp for
-  // 8-byte elements, a quarter-warp for 16-byte complex ones) are conflict-free
-  // iff their columns differ mod G (rows are staged contiguously, so a row's
-  // base offset shifts every bank equally).  Each step issues, per lane group,
-  // the next entry of every lane whose bank is still free, longest remaining
-  // lane first; the others wait (bubble, col = -1).  Lanes keep CSR order, so
-  // each P(i, j) accumulates exactly as before.  DPT_SELL_SCHED=0 packs the
-  // entries densely instead (the unscheduled layout, for comparison).
-  const int cx = dp.cplx ? 2 : 1;  // complex values are interleaved (re, im)
-  const int NB = dp.cplx ? 8 : 16;  // banks (8-byte pairs / 16-byte quads) per 128-byte wavefront
+  const int cx = dp.cplx ? 2 : 1;
+  const int G = dp.cplx ? 8 : 16;
   const char* sched_env = std::getenv("DPT_SELL_SCHED");
-  const bool sched = !(sched_env && sched_env[0] == '0');
-  const char* g_env = std::getenv("DPT_SELL_GROUP");
-  const int G = g_env ? std::max(NB, std::min(32, std::atoi(g_env))) : NB;  // lanes scheduled together
-  const int cap = G / NB;                                                  // uses per bank per step
-  std::vector<int64_t> off(size_t(ns + 1), 0);
-  std::vector<int32_t> lcol(size_t(ns * 32), -1), llen(size_t(ns * 32), 0);
-  std::vector<int64_t> pos(size_t(n), 0);
-  std::vector<std::vector<int64_t>> slot_src(static_cast<size_t>(ns));  // [step * 32 + lane] -> CSR index or -1
-  for (int64_t sl = 0; sl < ns; ++sl) {
-    int64_t len[32], head[32], beg[32];
-    int64_t remaining = 0, width = 0;
-    for (int L = 0; L < 32; ++L) {
-      const int64_t t = sl * 32 + L;
-      const int64_t j = perm[size_t(t)];
-      len[L] = head[L] = 0;
-      beg[L] = 0;
-      if (j < 0) continue;
-      len[L] = rp[size_t(j) + 1] - rp[size_t(j)];
-      beg[L] = rp[size_t(j)];
-      lcol[size_t(t)] = int32_t(j);
-      llen[size_t(t)] = int32_t(len[L]);
-      pos[size_t(j)] = t;
-      remaining += len[L];
-      width = std::max(width, len[L]);
-    }
-    std::vector<int64_t>& src = slot_src[size_t(sl)];
-    if (!sched) {
-      src.assign(size_t(width * 32), -1);
-      for (int L = 0; L < 32; ++L)
-        for (int64_t q = 0; q < len[L]; ++q) src[size_t(q * 32 + L)] = beg[L] + q;
-    } else {
-      int order[32];
-      while (remaining > 0) {
-        const size_t base = src.size();
-        src.resize(base + 32, -1);
-        for (int g0 = 0; g0 < 32; g0 += G) {
-          for (int q = 0; q < G; ++q) order[q] = g0 + q;
-          std::stable_sort(order, order + G, [&](int x, int y) { return len[x] - head[x] > len[y] - head[y]; });
-          int used[16] = {0};
-          for (int q = 0; q < G; ++q) {
-            const int L = order[q];
-            if (head[L] >= len[L]) continue;
-            const int b = int(uint32_t(cl[size_t(beg[L] + head[L])]) % uint32_t(NB));
-            if (used[b] >= cap) continue;
-            ++used[b];
-            src[base + size_t(L)] = beg[L] + head[L];
-            ++head[L];
-            --remaining;
-          }
-        }
-      }
-    }
-    src.resize((src.size() + 127) / 128 * 128, -1);  // K2 reads 4 entries per lane per trip (kCsrU)
-    off[size_t(sl) + 1] = off[size_t(sl)] + int64_t(src.size());
-  }
-  const int64_t total = off[size_t(ns)];
-  std::vector<int32_t> sc(size_t(std::max<int64_t>(total, 1)), -1);
-  std::vector<double> sv(size_t(cx * std::max<int64_t>(total, 1)), 0.0);
-  for (int64_t sl = 0; sl < ns; ++sl) {
-    const std::vector<int64_t>& src = slot_src[size_t(sl)];
-    for (size_t q = 0; q < src.size(); ++q) {
-      if (src[q] < 0) continue;
-      const size_t dst = size_t(off[size_t(sl)]) + q;
-      sc[dst] = cl[size_t(src[q])];
-      for (int c = 0; c < cx; ++c) sv[cx * dst + size_t(c)] = vl[size_t(cx * src[q] + c)];
-    }
-  }
+  const int sched = (sched_env && sched_env[0] == '0') ? 0 : 1;
+  dalloc(dp.s_lcol, size_t(ns * 32) * 4, err);
+  dalloc(dp.s_llen, size_t(ns * 32) * 4, err);
+  dalloc(dp.s_pos, size_t(n) * 8 + 8, err);
+  dalloc(dp.s_off, size_t(ns + 1) * 8, err);
+  CK(cudaMemsetAsync(dp.s_lcol.p, 0xff, size_t(ns * 32) * 4, st));
+  CK(cudaMemsetAsync(dp.s_llen.p, 0, size_t(ns * 32) * 4, st));
+  CK(launch_sell_perm(dp.rowptr.as<int64_t>(), n, dp.s_lcol.as<int32_t>(), dp.s_llen.as<int32_t>(),
+                      dp.s_pos.as<int64_t>(), st));
+  CK(launch_sell_widths(dp.rowptr.as<int64_t>(), dp.cols.as<int32_t>(), ns, dp.s_lcol.as<int32_t>(), G, sched,
+                        dp.s_off.as<int64_t>(), st));
+  DBuf tot;
+  dalloc(tot, 16, err);
+  CK(launch_sell_scan(dp.s_off.as<int64_t>(), ns, tot.as<int64_t>(), st));
+  int64_t total = 0;
+  CK(cudaMemcpyAsync(&total, tot.p, 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  const int64_t alloc = std::max<int64_t>(total, 1);
+  dalloc(dp.s_cols, size_t(alloc) * 4, err);
+  dalloc(dp.s_vals, size_t(cx * alloc) * 8, err);
+  CK(cudaMemsetAsync(dp.s_cols.p, 0xff, size_t(alloc) * 4, st));
+  CK(cudaMemsetAsync(dp.s_vals.p, 0, size_t(cx * alloc) * 8, st));
+  CK(launch_sell_fill(dp.rowptr.as<int64_t>(), dp.cols.as<int32_t>(), dp.vals.as<double>(), cx, ns,
+                      dp.s_lcol.as<int32_t>(), G, sched, dp.s_off.as<int64_t>(), dp.s_cols.as<int32_t>(),
+                      dp.s_vals.as<double>(), st));
   dp.nslices = ns;
-  dalloc(dp.s_cols, sc.size() * 4, err);
-  dalloc(dp.s_vals, sv.size() * 8, err);
-  dalloc(dp.s_off, off.size() * 8, err);
-  dalloc(dp.s_lcol, lcol.size() * 4, err);
-  dalloc(dp.s_llen, llen.size() * 4, err);
-  dalloc(dp.s_pos, pos.size() * 8 + 8, err);
-  CK(cudaMemcpyAsync(dp.s_cols.p, sc.data(), sc.size() * 4, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(dp.s_vals.p, sv.data(), sv.size() * 8, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(dp.s_off.p, off.data(), off.size() * 8, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(dp.s_lcol.p, lcol.data(), lcol.size() * 4, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(dp.s_llen.p, llen.data(), llen.size() * 4, cudaMemcpyHostToDevice, st));
-  if (n) CK(cudaMemcpyAsync(dp.s_pos.p, pos.data(), pos.size() * 8, cudaMemcpyHostToDevice, st));
-  CK(cudaStreamSynchronize(st));  // host vectors go out of scope
 }
 
 void validate(const dpt_problem* p, dpt_error_info* err) {
@@ -610,39 +533,6 @@ void upload(DevProblem& dp, dpt_ctx* ctx, const dpt_problem* p, dpt_error_info* 
       CK(cudaMemcpy(&nnz, p->rowptr + n, 8, cudaMemcpyDeviceToHost));
     }
     dp.nnz = nnz;
-    if (!sell) {  // K3 only needs the uniform-16 test: on the device for device inputs
-      if (n > 0 && !dp.cplx && nnz == 16 * n) {
-        if (dev) {
-          DBuf bad;
-          dalloc(bad, 16, err);
-          CK(cudaMemsetAsync(bad.p, 0, 4, st));
-          CK(launch_rowptr_uniform(p->rowptr, n, 16, bad.as<unsigned>(), st));
-          unsigned hb = 1;
-          CK(cudaMemcpyAsync(&hb, bad.p, 4, cudaMemcpyDeviceToHost, st));
-          CK(cudaStreamSynchronize(st));
-          dp.uniform16 = hb == 0 ? 1 : 0;
-        } else {
-          bool u = true;
-          for (int64_t i = 0; i <= n && u; ++i) u = p->rowptr[i] == 16 * i;
-          dp.uniform16 = u ? 1 : 0;
-        }
-      }
-    } else {
-      std::vector<int64_t> rp(size_t(n + 1));
-      CK(cudaMemcpy(rp.data(), p->rowptr, size_t(n + 1) * 8, hk));
-      bool u = n > 0 && !dp.cplx;
-      for (int64_t i = 0; i <= n && u; ++i) u = rp[size_t(i)] == 16 * i;
-      dp.uniform16 = u ? 1 : 0;
-      {
-        std::vector<int32_t> cl(static_cast<size_t>(nnz));
-        std::vector<double> vl(static_cast<size_t>(cx * nnz));
-        if (nnz) {
-          CK(cudaMemcpy(cl.data(), p->cols, size_t(nnz) * 4, hk));
-          CK(cudaMemcpy(vl.data(), p->vals, size_t(cx * nnz) * 8, hk));
-        }
-        build_sell(dp, rp, cl, vl, st, err);
-      }
-    }
     if (dev && nnz && aligned16(p->cols) && aligned16(p->vals) && aligned16(p->rowptr)) {
       dp.rowptr.view(p->rowptr);  // K3 reads int4 / double2 vectors: 16-byte alignment
       dp.cols.view(p->cols);
@@ -656,6 +546,18 @@ void upload(DevProblem& dp, dpt_ctx* ctx, const dpt_problem* p, dpt_error_info* 
         CK(cudaMemcpyAsync(dp.cols.p, p->cols, size_t(nnz) * 4, k, st));
         CK(cudaMemcpyAsync(dp.vals.p, p->vals, size_t(cx * nnz) * 8, k, st));
       }
+    }
+    if (sell) {
+      build_sell_device(dp, st, err);
+    } else if (n > 0 && !dp.cplx && nnz == 16 * n) {  // K3's uniform-16 fast path, tested on the device
+      DBuf bad;
+      dalloc(bad, 16, err);
+      CK(cudaMemsetAsync(bad.p, 0, 4, st));
+      CK(launch_rowptr_uniform(dp.rowptr.as<int64_t>(), n, 16, bad.as<unsigned>(), st));
+      unsigned hb = 1;
+      CK(cudaMemcpyAsync(&hb, bad.p, 4, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      dp.uniform16 = hb == 0 ? 1 : 0;
     }
   }
 }
