@@ -250,6 +250,24 @@ int dpt_check_degenerate(int64_t n, const double* d, double degeneracy_tol, int6
 double dpt_spectral_spread(int64_t n, const double* d);
 int dpt_effective_window(int requested, int64_t n); /* dpt.cpp:83-90 */
 
+/* ---- batched lambda-plane scan -------------------
+ * scan_domain, proj/src/analysis.cpp:68-138 (declared in
+ * proj/include/dynspec/analysis.hpp:63-69): classify every cell of the grid by
+ * solving the base problem at lambda = (re_at(j), im_at(i)).  The base
+ * problem's lambda is ignored.  classes[i * res_re + j] receives CellClass
+ * (0 Converged, 1 BoundedNonConverged -- including MaxIterations -- 2 Diverged),
+ * iterations[] the report's iteration count.  n <= 32 (full) / 2048 (row)
+ * run batched on the device, one warp per cell, in the reference's operation
+ * order; larger problems are solved cell by cell. */
+typedef struct dpt_scan_grid {
+  double re_min, re_max, im_min, im_max;
+  int64_t res_re, res_im;
+} dpt_scan_grid;
+enum { DPT_SCAN_FULL = 0, DPT_SCAN_SINGLE_ROW = 1 };
+int dpt_scan_domain(dpt_ctx* ctx, const dpt_problem* base, const dpt_scan_grid* grid, int mode, int64_t row,
+                    double ramp_alpha, const dpt_options* opts, uint8_t* classes, int32_t* iterations,
+                    dpt_error_info* err);
+
 /* The per-iteration decision function the device runs (dpt_state.h), exposed
  * for host-side tests: feeds one launch's statistics into the state machine.
  * state / opts are opaque byte blobs of dpt_sm_state_bytes() / dpt_sm_options_bytes(). */

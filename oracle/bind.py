@@ -267,6 +267,9 @@ class ComplexReference:
         L.ref_c_step_full.argtypes = [P(orc_cproblem), c_void_p, c_double, c_double, c_void_p]
         L.ref_c_step_single.argtypes = [P(orc_cproblem), c_void_p, c_int64, c_double, c_double, c_void_p, c_void_p]
         L.ref_c_check_degenerate.argtypes = [c_int64, c_void_p, c_double, P(c_int64), P(c_int64)]
+        L.ref_scan_domain.argtypes = [P(orc_cproblem), c_double, c_double, c_double, c_double, c_int64, c_int64, c_int,
+                                      c_int64, c_double, P(orc_options), c_int, c_void_p, c_void_p, P(c_int64),
+                                      P(c_int64)]
         self.L = L
 
     @staticmethod
@@ -363,3 +366,18 @@ class ComplexReference:
         i, j = ctypes.c_int64(), ctypes.c_int64()
         hit = self.L.ref_c_check_degenerate(d.shape[0], d.ctypes.data, float(tol), ctypes.byref(i), ctypes.byref(j))
         return (i.value, j.value) if hit else None
+
+    def scan_domain(self, p, grid, mode="Full", row=0, ramp_alpha=0.0, opts=None, threads=0):
+        """The reference's scan_domain: (rc, classes[res_im, res_re] uint8, iterations int32, degenerate)."""
+        pr, keep = self._prob(p)
+        o = Checker._opts(opts)
+        cells = int(grid.res_re) * int(grid.res_im)
+        cls = np.zeros(max(cells, 1), np.uint8)
+        its = np.zeros(max(cells, 1), np.int32)
+        di, dj = ctypes.c_int64(-1), ctypes.c_int64(-1)
+        rc = self.L.ref_scan_domain(ctypes.byref(pr), grid.re_min, grid.re_max, grid.im_min, grid.im_max,
+                                    int(grid.res_re), int(grid.res_im), 1 if mode == "SingleRow" else 0, int(row),
+                                    float(ramp_alpha), ctypes.byref(o), int(threads), cls.ctypes.data,
+                                    its.ctypes.data, ctypes.byref(di), ctypes.byref(dj))
+        shape = (int(grid.res_im), int(grid.res_re))
+        return rc, cls[:cells].reshape(shape), its[:cells].reshape(shape), (di.value, dj.value)

@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "dpt_oracle.h"
+#include "dynspec/analysis.hpp"
 #include "dynspec/dpt.hpp"
 #include "dynspec/matrix.hpp"
 #include "dynspec/partition.hpp"
@@ -430,3 +431,39 @@ int ref_c_check_degenerate(int64_t n, const double* d, double tol, int64_t* i, i
 }
 
 }  // extern "C"
+
+// scan_domain (proj/src/analysis.cpp:68-138) of the reference: classes[cells]
+// (CellClass), iterations[cells].  mode 0 Full, 1 SingleRow.
+extern "C" int ref_scan_domain(const orc_cproblem* p, double re_min, double re_max, double im_min, double im_max,
+                               int64_t res_re, int64_t res_im, int mode, int64_t row, double ramp_alpha,
+                               const orc_options* o, int threads, uint8_t* classes, int32_t* iterations,
+                               int64_t* deg_i, int64_t* deg_j) {
+  try {
+    const PartitionedProblem pp = to_cproblem(p);
+    ScanGrid g;
+    g.re_min = re_min;
+    g.re_max = re_max;
+    g.im_min = im_min;
+    g.im_max = im_max;
+    g.res_re = std::size_t(res_re);
+    g.res_im = std::size_t(res_im);
+    ScanMode m;
+    m.kind = mode == 1 ? ScanMode::Kind::SingleRow : ScanMode::Kind::Full;
+    m.row = std::size_t(row);
+    m.ramp_alpha = ramp_alpha;
+    const DomainGrid r = scan_domain(pp, g, m, to_opts(o), unsigned(threads));
+    for (std::size_t c = 0; c < r.classes.size(); ++c) {
+      classes[c] = uint8_t(r.classes[c]);
+      iterations[c] = r.iterations[c];
+    }
+    return ORC_OK;
+  } catch (const DegenerateSpectrum& e) {
+    if (deg_i) *deg_i = int64_t(e.first());
+    if (deg_j) *deg_j = int64_t(e.second());
+    return ORC_ERR_DEGENERATE;
+  } catch (const std::invalid_argument&) {
+    return ORC_ERR_SHAPE;
+  } catch (...) {
+    return ORC_ERR_INVALID;
+  }
+}

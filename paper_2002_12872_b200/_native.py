@@ -51,6 +51,14 @@ _lib = None
 _plib = None
 
 
+class dpt_scan_grid(Structure):
+    _fields_ = [("re_min", c_double), ("re_max", c_double), ("im_min", c_double), ("im_max", c_double),
+                ("res_re", c_int64), ("res_im", c_int64)]
+
+
+DPT_SCAN_FULL, DPT_SCAN_SINGLE_ROW = 0, 1
+
+
 def lib() -> ctypes.CDLL:
     """Load libdpt_b200.so (raises if it was not built -- no fallback)."""
     global _lib
@@ -114,6 +122,8 @@ def lib() -> ctypes.CDLL:
         L.dpt_spectral_spread.argtypes = [I64, c_void_p]
         L.dpt_spectral_spread.restype = D
         L.dpt_effective_window.argtypes = [c_int, I64]
+        L.dpt_scan_domain.argtypes = [c_void_p, P(dpt_problem), P(dpt_scan_grid), c_int, I64, D, P(dpt_options),
+                                      c_void_p, c_void_p, P(dpt_error_info)]
         L.dpt_sm_state_bytes.restype = c_size_t
         L.dpt_sm_init.argtypes = [c_void_p, c_void_p, P(dpt_options), c_int, c_int]
         L.dpt_sm_decide_host.argtypes = [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_void_p]

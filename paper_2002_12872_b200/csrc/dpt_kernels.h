@@ -60,6 +60,30 @@ cudaError_t launch_fold(const DevSolve& s, int ntiles_this, cudaStream_t st);
 cudaError_t launch_decide(const DevSolve& s, cudaStream_t st);
 cudaError_t launch_cycle(const DevSolve& s, int64_t elems, cudaStream_t st);
 cudaError_t launch_identity(const DevSolve& s, cudaStream_t st);
+// scan.cu: batched scan_domain, one warp per lambda cell (complex arithmetic in
+// the reference's operation order).  All arrays complex interleaved unless noted.
+struct ScanArgs {
+  int64_t cells, res_re;
+  int n, single, row, max_iter, win;
+  int ring_smem;   // set by launch_scan: window ring in shared memory
+  int warp_elems;  // set by launch_scan: complex elements of shared memory per warp
+  double tol, res_tol, div_thr;
+  const double* d;        // [n] levels
+  const double* delta;    // [n*n] Delta (row map: w = Delta z)
+  const double* delta_t;  // [n*n] Delta^T (full map: P = A Delta^T)
+  const double* theta;    // [n*n] 1 / (d_i - d_j) (host std::complex division)
+  const double* gap_row;  // [n] 1 / (d_row - d_m)
+  const double* re_at;    // [res_re] real grid coordinates
+  const double* im_at;    // [res_im] imaginary grid coordinates
+  const double* ramp;     // [max_iter + 1] 1 - alpha^(k-1) (host std::pow), or null
+  double* ring;           // per-warp cycle window ring
+  uint8_t* classes;       // [cells] CellClass
+  int32_t* iterations;    // [cells]
+};
+int scan_max_n(int single);
+int64_t scan_tiny_threads(const ScanArgs& a);  // > 0: n <= 3 runs one thread per cell (ring per thread)
+cudaError_t launch_scan(const ScanArgs& a, int warps_total, cudaStream_t st);
+
 // sell_build.cu: K2's SELL-32 image built on the device from the CSR in HBM
 cudaError_t launch_sell_perm(const int64_t* rp, int64_t n, int32_t* lane_col, int32_t* lane_len, int64_t* pos_of,
                              cudaStream_t st);

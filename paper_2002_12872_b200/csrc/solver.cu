@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <complex>
 #include <cstring>
 #include <set>
 #include <cstdio>
@@ -1850,6 +1851,197 @@ int dpt_check_degenerate(int64_t n, const double* d, double tol, int64_t* i, int
 double dpt_spectral_spread(int64_t n, const double* d) { return spread_of(n, d); }
 
 int dpt_effective_window(int requested, int64_t n) { return effective_window(requested, n); }
+// ------------------------------------------------------------ scan_domain ----
+// analysis.cpp:68-138.  Cells of the lambda grid are independent solves; small
+// problems run batched (scan.cu, one warp per cell, the reference's operation
+// order), larger ones cell by cell through the solver.
+static double grid_coordinate(double lo, double hi, int64_t res, int64_t i) {  // analysis.cpp:42-46
+  if (res == 1) return 0.5 * (lo + hi);
+  return lo + (hi - lo) * (double(i) / double(res - 1));
+}
+
+int dpt_scan_domain(dpt_ctx* ctx, const dpt_problem* p, const dpt_scan_grid* grid, int mode, int64_t row,
+                    double ramp_alpha, const dpt_options* opts, uint8_t* classes, int32_t* iterations,
+                    dpt_error_info* err) {
+  DPT_API_BEGIN
+  Guard g(ctx);
+  validate(p, err);
+  if (!grid || grid->res_re <= 0 || grid->res_im <= 0) {
+    set_err(err, DPT_ERR_SHAPE, "scan_domain: empty grid");
+    return DPT_ERR_SHAPE;
+  }
+  const bool single = mode == DPT_SCAN_SINGLE_ROW;
+  const int64_t n = p->n;
+  if (single && (row < 0 || row >= n)) {
+    set_err(err, DPT_ERR_SHAPE, "scan_domain: row out of range");
+    return DPT_ERR_SHAPE;
+  }
+  if (!(ramp_alpha >= 0.0) || ramp_alpha >= 1.0) {
+    set_err(err, DPT_ERR_INVALID_ARG, "scan_domain: ramp alpha must lie in [0, 1)");
+    return DPT_ERR_INVALID_ARG;
+  }
+  const dpt_options o = opts_or_default(opts);
+  // the spectrum is validated once up front (analysis.cpp:76-80)
+  std::vector<double> dh = host_levels(p, err);
+  if (single) {
+    int64_t bj;
+    const bool deg = p->is_complex ? find_degenerate_row_c(n, dh.data(), row, o.degeneracy_tol, &bj)
+                                   : find_degenerate_row(n, dh.data(), row, o.degeneracy_tol, &bj);
+    if (deg) degenerate_error(err, row, bj, dh.data(), p->is_complex != 0);
+  } else {
+    check_levels(p, dh, o.degeneracy_tol, err);
+  }
+  const int64_t cells = grid->res_re * grid->res_im;
+  if (cells == 0 || !classes || !iterations) return DPT_OK;
+  // complex host images of the problem (the reference's cdouble data)
+  typedef std::complex<double> cd_t;
+  std::vector<cd_t> d(static_cast<size_t>(n)), D(static_cast<size_t>(n * n), cd_t(0.0, 0.0));
+  for (int64_t i = 0; i < n; ++i) d[size_t(i)] = p->is_complex ? cd_t(dh[size_t(2 * i)], dh[size_t(2 * i + 1)]) : cd_t(dh[size_t(i)], 0.0);
+  {
+    const cudaMemcpyKind hk = p->mem == DPT_MEM_DEVICE ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost;
+    const int cx = p->is_complex ? 2 : 1;
+    if (p->delta_kind == DPT_DELTA_DENSE) {
+      std::vector<double> raw(size_t(cx * n * n));
+      if (n) CK(cudaMemcpy(raw.data(), p->delta, raw.size() * 8, hk));
+      for (int64_t q = 0; q < n * n; ++q) D[size_t(q)] = cx == 2 ? cd_t(raw[size_t(2 * q)], raw[size_t(2 * q + 1)]) : cd_t(raw[size_t(q)], 0.0);
+    } else {
+      std::vector<int64_t> rp(size_t(n + 1));
+      CK(cudaMemcpy(rp.data(), p->rowptr, size_t(n + 1) * 8, hk));
+      const int64_t nnz = rp[size_t(n)];
+      std::vector<int32_t> cl(static_cast<size_t>(nnz));
+      std::vector<double> vl(static_cast<size_t>(cx * nnz));
+      if (nnz) {
+        CK(cudaMemcpy(cl.data(), p->cols, size_t(nnz) * 4, hk));
+        CK(cudaMemcpy(vl.data(), p->vals, size_t(cx * nnz) * 8, hk));
+      }
+      for (int64_t i = 0; i < n; ++i)
+        for (int64_t q = rp[size_t(i)]; q < rp[size_t(i + 1)]; ++q)
+          D[size_t(i * n + cl[size_t(q)])] = cx == 2 ? cd_t(vl[size_t(2 * q)], vl[size_t(2 * q + 1)]) : cd_t(vl[size_t(q)], 0.0);
+    }
+  }
+  std::vector<double> re_at(static_cast<size_t>(grid->res_re)), im_at(static_cast<size_t>(grid->res_im));
+  for (int64_t j = 0; j < grid->res_re; ++j) re_at[size_t(j)] = grid_coordinate(grid->re_min, grid->re_max, grid->res_re, j);
+  for (int64_t i = 0; i < grid->res_im; ++i) im_at[size_t(i)] = grid_coordinate(grid->im_min, grid->im_max, grid->res_im, i);
+  const bool ramped = ramp_alpha > 0.0;
+  std::vector<double> ramp;
+  if (ramped) {
+    ramp.assign(size_t(std::max(o.max_iter, 0)) + 2, 0.0);
+    for (int k = 1; k <= o.max_iter; ++k) ramp[size_t(k)] = 1.0 - std::pow(ramp_alpha, double(k - 1));
+  }
+  cudaStream_t st = ctx->stream;
+
+  if (n <= scan_max_n(single ? 1 : 0)) {
+    std::vector<cd_t> tab(static_cast<size_t>(single ? n : n * n), cd_t(0.0, 0.0));
+    if (single) {
+      for (int64_t m = 0; m < n; ++m)
+        if (m != row) tab[size_t(m)] = 1.0 / (d[size_t(row)] - d[size_t(m)]);  // build_gap_row, partition.cpp:83-96
+    } else {
+      for (int64_t i = 0; i < n; ++i)
+        for (int64_t j = 0; j < n; ++j)
+          if (i != j) tab[size_t(i * n + j)] = 1.0 / (d[size_t(i)] - d[size_t(j)]);  // build_theta, :69-81
+    }
+    std::vector<cd_t> Dt;
+    if (!single) {
+      Dt.resize(size_t(n * n));
+      for (int64_t i = 0; i < n; ++i)
+        for (int64_t j = 0; j < n; ++j) Dt[size_t(j * n + i)] = D[size_t(i * n + j)];
+    }
+    const int win = single ? (o.cycle_window >= 2 ? o.cycle_window : 0) : effective_window(o.cycle_window, n);
+    int64_t warps = std::min<int64_t>(cells, 148 * 64);
+    const size_t per_warp = size_t(win > 1 ? win - 1 : 0) * size_t(single ? n : n * n) * 16;
+    if (per_warp > 0) warps = std::max<int64_t>(1, std::min<int64_t>(warps, int64_t((size_t(1) << 30) / per_warp)));
+    {  // n <= 3: one thread per cell, a ring per thread
+      ScanArgs probe{};
+      probe.n = int(n);
+      probe.cells = cells;
+      const int64_t tt = scan_tiny_threads(probe);
+      if (tt > 0) warps = tt;  // ring sized per thread below (per_warp is per ring owner)
+    }
+    DBuf bd, bD, bt, bre, bim, bramp, bring, bcls, bit;
+    dalloc(bd, size_t(n) * 16, err);
+    dalloc(bD, size_t(n * n) * 16, err);
+    dalloc(bt, tab.size() * 16, err);
+    dalloc(bre, re_at.size() * 8, err);
+    dalloc(bim, im_at.size() * 8, err);
+    if (ramped) dalloc(bramp, ramp.size() * 8, err);
+    dalloc(bring, std::max<size_t>(per_warp * size_t(warps), 16), err);
+    dalloc(bcls, size_t(cells), err);
+    dalloc(bit, size_t(cells) * 4, err);
+    CK(cudaMemcpyAsync(bd.p, d.data(), size_t(n) * 16, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(bD.p, single ? D.data() : Dt.data(), size_t(n * n) * 16, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(bt.p, tab.data(), tab.size() * 16, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(bre.p, re_at.data(), re_at.size() * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(bim.p, im_at.data(), im_at.size() * 8, cudaMemcpyHostToDevice, st));
+    if (ramped) CK(cudaMemcpyAsync(bramp.p, ramp.data(), ramp.size() * 8, cudaMemcpyHostToDevice, st));
+    ScanArgs a{};
+    a.cells = cells;
+    a.res_re = grid->res_re;
+    a.n = int(n);
+    a.single = single ? 1 : 0;
+    a.row = int(row);
+    a.max_iter = o.max_iter;
+    a.win = win;
+    a.tol = o.tol;
+    a.res_tol = o.residual_tol;
+    a.div_thr = o.divergence_threshold;
+    a.d = bd.as<double>();
+    a.delta = single ? bD.as<double>() : nullptr;
+    a.delta_t = single ? nullptr : bD.as<double>();
+    a.theta = single ? nullptr : bt.as<double>();
+    a.gap_row = single ? bt.as<double>() : nullptr;
+    a.re_at = bre.as<double>();
+    a.im_at = bim.as<double>();
+    a.ramp = ramped ? bramp.as<double>() : nullptr;
+    a.ring = bring.as<double>();
+    a.classes = bcls.as<uint8_t>();
+    a.iterations = bit.as<int32_t>();
+    CK(cudaEventRecord(ctx->ev0, st));
+    CK(launch_scan(a, int(warps), st));
+    ctx->launches += 1;
+    CK(cudaEventRecord(ctx->ev1, st));
+    CK(cudaMemcpyAsync(classes, bcls.p, size_t(cells), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(iterations, bit.p, size_t(cells) * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return DPT_OK;
+  }
+
+  // larger problems: one GPU solve per cell on the complex path
+  std::vector<double> dc(size_t(2 * n)), Dc;
+  for (int64_t i = 0; i < n; ++i) {
+    dc[size_t(2 * i)] = d[size_t(i)].real();
+    dc[size_t(2 * i + 1)] = d[size_t(i)].imag();
+  }
+  Dc.resize(size_t(2 * n * n));
+  for (int64_t q = 0; q < n * n; ++q) {
+    Dc[size_t(2 * q)] = D[size_t(q)].real();
+    Dc[size_t(2 * q + 1)] = D[size_t(q)].imag();
+  }
+  dpt_problem c{};
+  c.n = n;
+  c.d = dc.data();
+  c.delta_kind = DPT_DELTA_DENSE;
+  c.delta = Dc.data();
+  c.mem = DPT_MEM_HOST;
+  c.is_complex = 1;
+  for (int64_t cell = 0; cell < cells; ++cell) {
+    c.lambda = re_at[size_t(cell % grid->res_re)];
+    c.lambda_im = im_at[size_t(cell / grid->res_re)];
+    dpt_report r{};
+    int rc;
+    if (single)
+      rc = run_single(ctx, &c, row, &o, ramp_alpha, nullptr, nullptr, nullptr, DPT_MEM_HOST, &r, nullptr, 0, 0.0,
+                      nullptr, nullptr, err);
+    else
+      rc = run_full(ctx, &c, &o, ramped, ramp_alpha, -1, 0.0, nullptr, nullptr, nullptr, nullptr, nullptr,
+                    DPT_MEM_HOST, &r, err);
+    if (rc != DPT_OK) return rc;
+    classes[cell] = uint8_t(r.status == DPT_CONVERGED ? 0 : (r.status == DPT_DIVERGED ? 2 : 1));
+    iterations[cell] = r.iterations;
+  }
+  return DPT_OK;
+  DPT_API_END
+}
+
 
 size_t dpt_sm_state_bytes(void) { return sizeof(dpt_sm_state) + sizeof(dpt_sm_options); }
 

@@ -626,3 +626,77 @@ def spectral_spread(d) -> float:
 
 def effective_window(requested: int, n: int) -> int:
     return int(N.lib().dpt_effective_window(int(requested), int(n)))
+
+
+# ------------------------------------------------------------- scan_domain ----
+class CellClass(enum.IntEnum):
+    """proj/include/dynspec/analysis.hpp:33-37"""
+    Converged = 0
+    BoundedNonConverged = 1
+    Diverged = 2
+
+
+@dataclass
+class ScanGrid:
+    """proj/include/dynspec/analysis.hpp:20-27"""
+    re_min: float = -1.0
+    re_max: float = 1.0
+    im_min: float = -1.0
+    im_max: float = 1.0
+    res_re: int = 100
+    res_im: int = 100
+
+
+@dataclass
+class ScanMode:
+    """proj/include/dynspec/analysis.hpp:56-61: Full or SingleRow (kind), chart row, ramp alpha."""
+    kind: str = "Full"
+    row: int = 0
+    ramp_alpha: float = 0.0
+
+
+def grid_coordinate(lo: float, hi: float, res: int, i: int) -> float:
+    """analysis.cpp:42-46"""
+    if res == 0:
+        raise ShapeError("grid_coordinate: empty axis")
+    if res == 1:
+        return 0.5 * (lo + hi)
+    return lo + (hi - lo) * (float(i) / float(res - 1))
+
+
+@dataclass
+class DomainGrid:
+    """analysis.hpp:39-54: classes / iterations are row-major with the
+    imaginary index major, shape (res_im, res_re)."""
+    grid: ScanGrid
+    classes: np.ndarray
+    iterations: np.ndarray
+
+    def re_at(self, j: int) -> float:
+        return grid_coordinate(self.grid.re_min, self.grid.re_max, self.grid.res_re, j)
+
+    def im_at(self, i: int) -> float:
+        return grid_coordinate(self.grid.im_min, self.grid.im_max, self.grid.res_im, i)
+
+
+def scan_domain(base: PartitionedProblem, grid: ScanGrid, mode: ScanMode = None, opts: IterationOptions = None,
+                threads: int = 0, ctx: Context = None) -> DomainGrid:
+    """scan_domain (proj/src/analysis.cpp:68-138): classify every lambda cell.
+    Batched on the device (one warp per cell) for small problems; `threads` is
+    accepted for signature parity and ignored (the output is thread-independent
+    in the reference too)."""
+    mode = mode or ScanMode()
+    ctx = ctx or default_context()
+    m = _Marshal(base)  # the base lambda is ignored (each cell sets its own)
+    g = N.dpt_scan_grid(float(grid.re_min), float(grid.re_max), float(grid.im_min), float(grid.im_max),
+                        int(grid.res_re), int(grid.res_im))
+    cells = int(grid.res_re) * int(grid.res_im)
+    cls = np.zeros(max(cells, 0), dtype=np.uint8)
+    its = np.zeros(max(cells, 0), dtype=np.int32)
+    err = N.dpt_error_info()
+    kind = N.DPT_SCAN_SINGLE_ROW if mode.kind == "SingleRow" else N.DPT_SCAN_FULL
+    _raise(N.lib().dpt_scan_domain(ctx.handle, ctypes.byref(m.prob), ctypes.byref(g), kind, int(mode.row),
+                                   float(mode.ramp_alpha), ctypes.byref(_opts(opts)), cls.ctypes.data,
+                                   its.ctypes.data, ctypes.byref(err)), err)
+    shape = (int(grid.res_im), int(grid.res_re))
+    return DomainGrid(grid, cls.reshape(shape), its.reshape(shape))

@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "dpt_b200.h"
+#include "dynspec/analysis.hpp"
 #include "dynspec/dpt.hpp"
 #include "dynspec/roots.hpp"
 
@@ -482,6 +483,34 @@ ConvergenceReport homotopy_solve(const PartitionedProblem& p, int stages, const 
   }
   rep.state = EigenIterate{std::move(a), total};
   return rep;
+}
+
+// ---- batched scan_domain (analysis.hpp:63-69, analysis.cpp:68-138) ---------
+// Every lambda cell solved on the device in one launch (one warp -- or, for
+// n <= 3, one thread -- per cell) in the reference's operation order, so the
+// classes and iteration counts equal the reference's.  To use it, compile the
+// reference's analysis.cpp with -Dscan_domain=dynspec_reference_scan_domain
+// (INTEGRATION.md); its other callers bind this definition unchanged.
+DomainGrid scan_domain(const PartitionedProblem& base, const ScanGrid& grid, const ScanMode& mode,
+                       const IterationOptions& opts, unsigned /*threads: the device decides*/) {
+  if (grid.res_re == 0 || grid.res_im == 0) throw ShapeError("scan_domain: empty grid");
+  if (mode.kind == ScanMode::Kind::SingleRow && mode.row >= base.size())
+    throw ShapeError("scan_domain: row out of range");
+  auto P = to_c(base.d, base.delta, cdouble{0.0, 0.0});  // each cell sets its own lambda
+  dpt_scan_grid g{grid.re_min, grid.re_max, grid.im_min, grid.im_max, int64_t(grid.res_re), int64_t(grid.res_im)};
+  DomainGrid out;
+  out.grid = grid;
+  const std::size_t cells = grid.res_re * grid.res_im;
+  std::vector<uint8_t> cls(cells);
+  out.iterations.assign(cells, 0);
+  const dpt_options o = to_c(opts);
+  dpt_error_info e{};
+  check(dpt_scan_domain(ctx(), &P->c, &g, mode.kind == ScanMode::Kind::SingleRow ? DPT_SCAN_SINGLE_ROW : DPT_SCAN_FULL,
+                        int64_t(mode.row), mode.ramp_alpha, &o, cls.data(), out.iterations.data(), &e),
+        e);
+  out.classes.resize(cells);
+  for (std::size_t c = 0; c < cells; ++c) out.classes[c] = CellClass(cls[c]);
+  return out;
 }
 
 }  // namespace dynspec
