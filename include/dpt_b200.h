@@ -57,7 +57,8 @@ typedef enum dpt_error {
   DPT_ERR_NON_REAL = 6,     /* documented deviation: complex input */
   DPT_ERR_NO_DEVICE = 7,
   DPT_ERR_TRACE = 8,        /* the trace callback asked to abort */
-  DPT_ERR_UNSUPPORTED = 9
+  DPT_ERR_UNSUPPORTED = 9,
+  DPT_ERR_IO = 10           /* IoError (matrix_market.hpp:10-13) */
 } dpt_error;
 
 /* Where the pointers of a call live. */
@@ -249,6 +250,32 @@ int dpt_check_degenerate(int64_t n, const double* d, double degeneracy_tol, int6
                          int64_t* j);
 double dpt_spectral_spread(int64_t n, const double* d);
 int dpt_effective_window(int requested, int64_t n); /* dpt.cpp:83-90 */
+
+/* ---- Matrix Market I/O ------------------------------
+ * read_matrix_market / write_matrix_market, proj/include/dynspec/matrix_market.hpp
+ * (proj/src/matrix_market.cpp:70-191): coordinate and array formats, real and
+ * complex fields, general and symmetric symmetry (expanded).  Coordinate data
+ * becomes CSR through from_triplets' steps (sorted by (row, col), duplicates
+ * summed); array data a row-major dense matrix.  Values interleave (re, im) when
+ * is_complex.  Results are bit-identical to the reference's; parsing and
+ * formatting use `threads` host threads (0 = all).  Errors: DPT_ERR_IO with the
+ * reference's IoError message. */
+typedef struct dpt_mm_matrix {
+  int64_t rows, cols;
+  int is_sparse;    /* 1: CSR (coordinate file), 0: dense row-major (array file) */
+  int is_complex;   /* field complex */
+  int64_t nnz;      /* stored entries (dense: rows * cols) */
+  int64_t* rowptr;  /* [rows + 1] (sparse) */
+  int64_t* colidx;  /* [nnz] (sparse) */
+  double* vals;     /* sparse: [nnz] scalars; dense: [rows * cols] scalars */
+  void* store;      /* owner of the arrays (dpt_mm_free) */
+} dpt_mm_matrix;
+int dpt_mm_read(const char* path, int threads, dpt_mm_matrix* out, dpt_error_info* err);
+void dpt_mm_free(dpt_mm_matrix* m);
+int dpt_mm_write_dense(const char* path, int64_t rows, int64_t cols, const double* vals, int is_complex, int threads,
+                       dpt_error_info* err);
+int dpt_mm_write_csr(const char* path, int64_t rows, int64_t cols, const int64_t* rowptr, const int64_t* colidx,
+                     const double* vals, int is_complex, int threads, dpt_error_info* err);
 
 /* ---- batched lambda-plane scan -------------------
  * scan_domain, proj/src/analysis.cpp:68-138 (declared in

@@ -381,3 +381,50 @@ class ComplexReference:
                                     its.ctypes.data, ctypes.byref(di), ctypes.byref(dj))
         shape = (int(grid.res_im), int(grid.res_re))
         return rc, cls[:cells].reshape(shape), its[:cells].reshape(shape), (di.value, dj.value)
+
+
+class ReferenceMatrixMarket:
+    """The reference's read_matrix_market / write_matrix_market (oracle/_ref)."""
+
+    def __init__(self):
+        L = ctypes.CDLL(REF_SO)
+        P = POINTER
+        L.ref_mm_read.argtypes = [ctypes.c_char_p, P(c_int64), P(c_int64), P(c_int), P(c_int64), P(c_void_p),
+                                  ctypes.c_char_p, c_int]
+        L.ref_mm_get.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p]
+        L.ref_mm_release.argtypes = [c_void_p]
+        L.ref_mm_write_dense.argtypes = [ctypes.c_char_p, c_int64, c_int64, c_void_p]
+        L.ref_mm_write_csr.argtypes = [ctypes.c_char_p, c_int64, c_int64, c_void_p, c_void_p, c_void_p]
+        self.L = L
+
+    def read(self, path):
+        """(rc, message, result): result = ('dense', complex array) or ('csr', rowptr, colidx, complex vals)."""
+        rows, cols, nnz = c_int64(), c_int64(), c_int64()
+        sp = c_int()
+        h = c_void_p()
+        msg = ctypes.create_string_buffer(1024)
+        rc = self.L.ref_mm_read(str(path).encode(), ctypes.byref(rows), ctypes.byref(cols), ctypes.byref(sp),
+                                ctypes.byref(nnz), ctypes.byref(h), msg, 1024)
+        if rc != 0:
+            return rc, msg.value.decode(errors="replace"), None
+        try:
+            vals = np.zeros(2 * max(nnz.value, 1))
+            if sp.value:
+                rp = np.zeros(rows.value + 1, np.int64)
+                ci = np.zeros(max(nnz.value, 1), np.int64)
+                self.L.ref_mm_get(h, rp.ctypes.data, ci.ctypes.data, vals.ctypes.data)
+                return 0, "", ("csr", rp, ci[:nnz.value], vals[:2 * nnz.value].view(np.complex128), cols.value)
+            self.L.ref_mm_get(h, None, None, vals.ctypes.data)
+            return 0, "", ("dense", vals[:2 * nnz.value].view(np.complex128).reshape(rows.value, cols.value))
+        finally:
+            self.L.ref_mm_release(h)
+
+    def write_dense(self, a, path):
+        a = np.ascontiguousarray(a, dtype=np.complex128)
+        self.L.ref_mm_write_dense(str(path).encode(), a.shape[0], a.shape[1], a.ctypes.data)
+
+    def write_csr(self, rows, cols, rp, ci, vals, path):
+        rp = np.ascontiguousarray(rp, dtype=np.int64)
+        ci = np.ascontiguousarray(ci, dtype=np.int64)
+        vals = np.ascontiguousarray(vals, dtype=np.complex128)
+        self.L.ref_mm_write_csr(str(path).encode(), rows, cols, rp.ctypes.data, ci.ctypes.data, vals.ctypes.data)

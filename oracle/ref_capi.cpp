@@ -11,6 +11,7 @@
 #include "dpt_oracle.h"
 #include "dynspec/analysis.hpp"
 #include "dynspec/dpt.hpp"
+#include "dynspec/matrix_market.hpp"
 #include "dynspec/matrix.hpp"
 #include "dynspec/partition.hpp"
 
@@ -466,4 +467,74 @@ extern "C" int ref_scan_domain(const orc_cproblem* p, double re_min, double re_m
   } catch (...) {
     return ORC_ERR_INVALID;
   }
+}
+
+// read_matrix_market / write_matrix_market (proj/src/matrix_market.cpp) of the
+// reference, for the row-f3 parity tests.  Values are complex interleaved.
+struct RefMM {
+  MatrixVariant m;
+};
+
+extern "C" int ref_mm_read(const char* path, int64_t* rows, int64_t* cols, int* is_sparse, int64_t* nnz, void** handle,
+                           char* msg, int msglen) {
+  try {
+    auto* h = new RefMM{read_matrix_market(path)};
+    *handle = h;
+    if (const auto* d = std::get_if<DenseMatrix>(&h->m)) {
+      *rows = int64_t(d->rows());
+      *cols = int64_t(d->cols());
+      *is_sparse = 0;
+      *nnz = int64_t(d->rows() * d->cols());
+    } else {
+      const auto& sp = std::get<SparseMatrix>(h->m);
+      *rows = int64_t(sp.rows());
+      *cols = int64_t(sp.cols());
+      *is_sparse = 1;
+      *nnz = int64_t(sp.nnz());
+    }
+    return 0;
+  } catch (const IoError& e) {
+    std::snprintf(msg, size_t(msglen), "%s", e.what());
+    return 10;
+  } catch (const std::exception& e) {
+    std::snprintf(msg, size_t(msglen), "%s", e.what());
+    return 1;
+  }
+}
+
+extern "C" void ref_mm_get(void* handle, int64_t* rowptr, int64_t* colidx, double* vals) {
+  const auto* h = static_cast<RefMM*>(handle);
+  if (const auto* d = std::get_if<DenseMatrix>(&h->m)) {
+    for (std::size_t q = 0; q < d->rows() * d->cols(); ++q) {
+      vals[2 * q] = d->data()[q].real();
+      vals[2 * q + 1] = d->data()[q].imag();
+    }
+    return;
+  }
+  const auto& sp = std::get<SparseMatrix>(h->m);
+  for (std::size_t i = 0; i <= sp.rows(); ++i) rowptr[i] = int64_t(sp.row_offsets()[i]);
+  for (std::size_t q = 0; q < sp.nnz(); ++q) {
+    colidx[q] = int64_t(sp.col_indices()[q]);
+    vals[2 * q] = sp.values()[q].real();
+    vals[2 * q + 1] = sp.values()[q].imag();
+  }
+}
+
+extern "C" void ref_mm_release(void* handle) { delete static_cast<RefMM*>(handle); }
+
+extern "C" int ref_mm_write_dense(const char* path, int64_t rows, int64_t cols, const double* vals) {
+  DenseMatrix m(static_cast<std::size_t>(rows), static_cast<std::size_t>(cols));
+  for (std::size_t q = 0; q < std::size_t(rows * cols); ++q) m.data()[q] = cdouble{vals[2 * q], vals[2 * q + 1]};
+  write_matrix_market(m, path);
+  return 0;
+}
+
+extern "C" int ref_mm_write_csr(const char* path, int64_t rows, int64_t cols, const int64_t* rowptr,
+                                const int64_t* colidx, const double* vals) {
+  std::vector<SparseMatrix::Triplet> t;
+  for (int64_t i = 0; i < rows; ++i)
+    for (int64_t q = rowptr[i]; q < rowptr[i + 1]; ++q)
+      t.push_back({std::size_t(i), std::size_t(colidx[q]), cdouble{vals[2 * q], vals[2 * q + 1]}});
+  write_matrix_market(SparseMatrix::from_triplets(std::size_t(rows), std::size_t(cols), std::move(t)), path);
+  return 0;
 }

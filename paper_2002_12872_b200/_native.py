@@ -19,7 +19,7 @@ DPT_MEM_HOST, DPT_MEM_DEVICE = 0, 1
 DPT_DELTA_DENSE, DPT_DELTA_CSR = 0, 1
 
 (DPT_OK, DPT_ERR_SHAPE, DPT_ERR_DEGENERATE, DPT_ERR_INVALID_ARG, DPT_ERR_CUDA, DPT_ERR_NCCL,
- DPT_ERR_NON_REAL, DPT_ERR_NO_DEVICE, DPT_ERR_TRACE, DPT_ERR_UNSUPPORTED) = range(10)
+ DPT_ERR_NON_REAL, DPT_ERR_NO_DEVICE, DPT_ERR_TRACE, DPT_ERR_UNSUPPORTED, DPT_ERR_IO) = range(11)
 
 
 class dpt_options(Structure):
@@ -49,6 +49,12 @@ TRACE_FN = ctypes.CFUNCTYPE(c_int, c_int, c_double, c_double, c_void_p)
 
 _lib = None
 _plib = None
+
+
+class dpt_mm_matrix(Structure):
+    _fields_ = [("rows", c_int64), ("cols", c_int64), ("is_sparse", c_int), ("is_complex", c_int),
+                ("nnz", c_int64), ("rowptr", c_void_p), ("colidx", c_void_p), ("vals", c_void_p),
+                ("store", c_void_p)]
 
 
 class dpt_scan_grid(Structure):
@@ -122,6 +128,11 @@ def lib() -> ctypes.CDLL:
         L.dpt_spectral_spread.argtypes = [I64, c_void_p]
         L.dpt_spectral_spread.restype = D
         L.dpt_effective_window.argtypes = [c_int, I64]
+        L.dpt_mm_read.argtypes = [ctypes.c_char_p, c_int, P(dpt_mm_matrix), P(dpt_error_info)]
+        L.dpt_mm_free.argtypes = [P(dpt_mm_matrix)]
+        L.dpt_mm_write_dense.argtypes = [ctypes.c_char_p, I64, I64, c_void_p, c_int, c_int, P(dpt_error_info)]
+        L.dpt_mm_write_csr.argtypes = [ctypes.c_char_p, I64, I64, c_void_p, c_void_p, c_void_p, c_int, c_int,
+                                       P(dpt_error_info)]
         L.dpt_scan_domain.argtypes = [c_void_p, P(dpt_problem), P(dpt_scan_grid), c_int, I64, D, P(dpt_options),
                                       c_void_p, c_void_p, P(dpt_error_info)]
         L.dpt_sm_state_bytes.restype = c_size_t

@@ -61,6 +61,10 @@ class DegenerateSpectrum(RuntimeError):
         return self.j
 
 
+class IoError(RuntimeError):
+    """IoError (matrix_market.hpp:10-13)."""
+
+
 class NoDeviceError(RuntimeError):
     """No CUDA device: the DPT path has no CPU fallback."""
 
@@ -89,18 +93,20 @@ class IterationOptions:  # dpt.hpp:22-31
 
 @dataclass
 class CsrMatrix:
-    """CSR with int64 row offsets, int32 sorted columns, FP64 values (matrix.hpp:73-106)."""
+    """CSR with int64 row offsets, int32 sorted columns, FP64 values (matrix.hpp:73-106).
+    `n` rows; `ncols` columns when not square (Matrix Market files)."""
     n: int
     rowptr: np.ndarray
     cols: np.ndarray
     vals: np.ndarray
+    ncols: Optional[int] = None
 
     @property
     def nnz(self) -> int:
         return int(self.vals.shape[0])
 
     def todense(self) -> np.ndarray:
-        out = np.zeros((self.n, self.n))
+        out = np.zeros((self.n, self.ncols or self.n), dtype=np.asarray(self.vals).dtype)
         for i in range(self.n):
             s, e = int(self.rowptr[i]), int(self.rowptr[i + 1])
             out[i, self.cols[s:e]] = self.vals[s:e]
@@ -233,6 +239,8 @@ def _raise(rc: int, err: N.dpt_error_info):
         raise NoDeviceError(msg)
     if rc == N.DPT_ERR_TRACE:
         raise TraceAborted(msg)
+    if rc == N.DPT_ERR_IO:
+        raise IoError(msg)
     raise DeviceError(f"dpt error {rc}: {msg}")
 
 
@@ -700,3 +708,59 @@ def scan_domain(base: PartitionedProblem, grid: ScanGrid, mode: ScanMode = None,
                                    its.ctypes.data, ctypes.byref(err)), err)
     shape = (int(grid.res_im), int(grid.res_re))
     return DomainGrid(grid, cls.reshape(shape), its.reshape(shape))
+
+
+# ----------------------------------------------------------- Matrix Market ----
+def read_matrix_market(path: str, threads: int = 0):
+    """read_matrix_market (proj/src/matrix_market.cpp:70-143): a CsrMatrix for
+    coordinate files, a dense row-major ndarray for array files; complex dtype
+    for the complex field.  Bit-identical to the reference; parsed with
+    `threads` host threads (0 = all).  Raises IoError like the reference."""
+    m = N.dpt_mm_matrix()
+    err = N.dpt_error_info()
+    _raise(N.lib().dpt_mm_read(str(path).encode(), int(threads), ctypes.byref(m), ctypes.byref(err)), err)
+    try:
+        cx = 2 if m.is_complex else 1
+        nval = int(m.nnz) * cx
+
+        def arr(ptr, count, ctype, dtype):
+            if count == 0:
+                return np.zeros(0, dtype=dtype)
+            return np.ctypeslib.as_array(ctypes.cast(ptr, ctypes.POINTER(ctype)), shape=(count,)).astype(dtype, copy=True)
+
+        vals = arr(m.vals, nval, ctypes.c_double, np.float64)
+        if m.is_complex:
+            vals = vals.view(np.complex128)
+        if not m.is_sparse:
+            return vals.reshape(int(m.rows), int(m.cols))
+        rp = arr(m.rowptr, int(m.rows) + 1, ctypes.c_int64, np.int64)
+        ci = arr(m.colidx, int(m.nnz), ctypes.c_int64, np.int64)
+        cols = ci.astype(np.int32) if int(m.cols) < 2 ** 31 else ci
+        if int(m.rows) != int(m.cols):
+            return CsrMatrix(int(m.rows), rp, cols, vals, ncols=int(m.cols))
+        return CsrMatrix(int(m.rows), rp, cols, vals)
+    finally:
+        N.lib().dpt_mm_free(ctypes.byref(m))
+
+
+def write_matrix_market(m, path: str, threads: int = 0) -> None:
+    """write_matrix_market (matrix_market.cpp:170-195): array format for dense,
+    coordinate for CSR, real field when every imaginary part is 0, "%.17g"."""
+    err = N.dpt_error_info()
+    if isinstance(m, CsrMatrix):
+        vals = np.asarray(m.vals)
+        cplx = np.iscomplexobj(vals)
+        vals = np.ascontiguousarray(vals, dtype=np.complex128 if cplx else np.float64)
+        rp = np.ascontiguousarray(m.rowptr, dtype=np.int64)
+        ci = np.ascontiguousarray(m.cols, dtype=np.int64)
+        ncols = getattr(m, "ncols", None) or m.n
+        _raise(N.lib().dpt_mm_write_csr(str(path).encode(), int(m.n), int(ncols), rp.ctypes.data, ci.ctypes.data,
+                                        vals.ctypes.data, int(cplx), int(threads), ctypes.byref(err)), err)
+        return
+    a = np.asarray(m)
+    if a.ndim != 2:
+        raise ShapeError("write_matrix_market: dense matrix must be 2-D")
+    cplx = np.iscomplexobj(a)
+    a = np.ascontiguousarray(a, dtype=np.complex128 if cplx else np.float64)
+    _raise(N.lib().dpt_mm_write_dense(str(path).encode(), int(a.shape[0]), int(a.shape[1]), a.ctypes.data, int(cplx),
+                                      int(threads), ctypes.byref(err)), err)

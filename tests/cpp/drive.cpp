@@ -12,10 +12,12 @@
 #include <complex>
 #include <cstdio>
 #include <string>
+#include <unistd.h>
 #include <vector>
 
 #include "dynspec/analysis.hpp"
 #include "dynspec/dpt.hpp"
+#include "dynspec/matrix_market.hpp"
 #include "dynspec/partition.hpp"
 #include "dynspec/rspt.hpp"
 
@@ -190,6 +192,36 @@ int main() {
   for (std::size_t c = 0; c < csg.classes.size(); ++c)
     put("scan_csingle.class[" + std::to_string(c) + "]", double(int(csg.classes[c])));
   put_creport("c.homotopy", homotopy_solve(rc, 3));
+
+  // 7. Matrix Market (row f3): the CLI's --file-d / --file-delta flow -- write
+  // a problem, read it back, solve; plus a complex dense round trip
+  const std::string dir = std::string(std::getenv("TMPDIR") ? std::getenv("TMPDIR") : "/tmp") + "/dpt_drive_" +
+                          std::to_string(getpid()) + "_";
+  {
+    auto er = build_er_perturbed_oscillator(300, 7, cdouble{0.02, 0.0});
+    std::vector<SparseMatrix::Triplet> dt;
+    for (std::size_t i = 0; i < er.size(); ++i) dt.push_back({i, i, er.d.d[i]});
+    write_matrix_market(SparseMatrix::from_triplets(er.size(), er.size(), std::move(dt)), dir + "d.mtx");
+    write_matrix_market(er.delta, dir + "delta.mtx");
+    const MatrixVariant dm = read_matrix_market(dir + "d.mtx");
+    const MatrixVariant delta = read_matrix_market(dir + "delta.mtx");
+    const auto& ds = std::get<SparseMatrix>(dm);
+    std::vector<cdouble> diag(ds.rows());
+    for (std::size_t i = 0; i < ds.rows(); ++i) diag[i] = ds.at(i, i);
+    const PartitionedProblem fp = make_problem(DiagonalMatrix{diag}, delta, cdouble{0.02, 0.0});
+    put("mm.delta_nnz", double(std::get<SparseMatrix>(delta).nnz()));
+    put_report("mm.solve", iterate_full(fp, sopts));
+    DenseMatrix cm(4, 3);
+    for (std::size_t q = 0; q < 12; ++q) cm.data()[q] = cdouble{0.1 * double(q) - 0.37, 1.0 / (3.0 + double(q))};
+    write_matrix_market(cm, dir + "c.mtx");
+    put_cmat("mm.complex_round_trip", std::get<DenseMatrix>(read_matrix_market(dir + "c.mtx")));
+    try {
+      (void)read_matrix_market(dir + "missing.mtx");
+    } catch (const IoError& e) {
+      std::printf("mm.missing.status IoError\n");
+    }
+    for (const char* f : {"d.mtx", "delta.mtx", "c.mtx"}) std::remove((dir + f).c_str());
+  }
   std::printf("done 1\n");
   return 0;
 }
