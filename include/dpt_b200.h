@@ -251,6 +251,19 @@ int dpt_check_degenerate(int64_t n, const double* d, double degeneracy_tol, int6
 double dpt_spectral_spread(int64_t n, const double* d);
 int dpt_effective_window(int requested, int64_t n); /* dpt.cpp:83-90 */
 
+/* ---- staged continuation ---------------------------
+ * homotopy_solve, dpt.hpp:145-152 / dpt.cpp:505-556: `stages` solves along
+ * lambda_s = lambda s / stages, each on the problem rebased by the product W of
+ * the converged bases (R = W^-1 (lambda_s Delta + diag d) W, re-split with
+ * lambda 1), all on the device (cuBLAS GEMM / cuSOLVER LU for the basis
+ * algebra, the solver's kernels for the stage solves).  Outputs as
+ * dpt_iterate_full: a = the normalised eigenvector matrix, read-offs against
+ * the original problem, rep.iterations = the sum over stages, rep.status = the
+ * last stage's.  Errors: stages < 1 -> DPT_ERR_INVALID_ARG; a singular basis
+ * -> DPT_ERR_UNSUPPORTED (the reference's std::runtime_error). */
+int dpt_homotopy_solve(dpt_ctx* ctx, const dpt_problem* p, int stages, const dpt_options* opts, double* a_out,
+                       double* eig_out, double* res_out, int out_mem, dpt_report* rep, dpt_error_info* err);
+
 /* ---- Matrix Market I/O ------------------------------
  * read_matrix_market / write_matrix_market, proj/include/dynspec/matrix_market.hpp
  * (proj/src/matrix_market.cpp:70-191): coordinate and array formats, real and

@@ -267,6 +267,8 @@ class ComplexReference:
         L.ref_c_step_full.argtypes = [P(orc_cproblem), c_void_p, c_double, c_double, c_void_p]
         L.ref_c_step_single.argtypes = [P(orc_cproblem), c_void_p, c_int64, c_double, c_double, c_void_p, c_void_p]
         L.ref_c_check_degenerate.argtypes = [c_int64, c_void_p, c_double, P(c_int64), P(c_int64)]
+        L.ref_c_homotopy.argtypes = [P(orc_cproblem), c_int, P(orc_options), c_void_p, c_void_p, c_void_p,
+                                     P(orc_report)]
         L.ref_scan_domain.argtypes = [P(orc_cproblem), c_double, c_double, c_double, c_double, c_int64, c_int64, c_int,
                                       c_int64, c_double, P(orc_options), c_int, c_void_p, c_void_p, P(c_int64),
                                       P(c_int64)]
@@ -366,6 +368,17 @@ class ComplexReference:
         i, j = ctypes.c_int64(), ctypes.c_int64()
         hit = self.L.ref_c_check_degenerate(d.shape[0], d.ctypes.data, float(tol), ctypes.byref(i), ctypes.byref(j))
         return (i.value, j.value) if hit else None
+
+    def homotopy(self, p, stages, opts=None):
+        pr, keep = self._prob(p)
+        n = pr.n
+        a = np.zeros((n, n), np.complex128)
+        eig = np.zeros(n, np.complex128)
+        res = np.zeros(n)
+        rep = orc_report()
+        rc = self.L.ref_c_homotopy(ctypes.byref(pr), int(stages), ctypes.byref(Checker._opts(opts)), a.ctypes.data,
+                                   eig.ctypes.data, res.ctypes.data, ctypes.byref(rep))
+        return FullResult(rc, rep.status, rep.iterations, rep.step_norm, a, eig, res)
 
     def scan_domain(self, p, grid, mode="Full", row=0, ramp_alpha=0.0, opts=None, threads=0):
         """The reference's scan_domain: (rc, classes[res_im, res_re] uint8, iterations int32, degenerate)."""

@@ -538,3 +538,30 @@ extern "C" int ref_mm_write_csr(const char* path, int64_t rows, int64_t cols, co
   write_matrix_market(SparseMatrix::from_triplets(std::size_t(rows), std::size_t(cols), std::move(t)), path);
   return 0;
 }
+
+// homotopy_solve (proj/src/dpt.cpp:505-556) of the reference, complex outputs.
+extern "C" int ref_c_homotopy(const orc_cproblem* p, int stages, const orc_options* o, double* a_out, double* eig_out,
+                              double* res_out, orc_report* rep) {
+  std::memset(rep, 0, sizeof(*rep));
+  try {
+    const ConvergenceReport r = homotopy_solve(to_cproblem(p), stages, to_opts(o));
+    rep->status = int(r.status);
+    rep->iterations = r.iterations;
+    rep->step_norm = r.step_norm;
+    put_cdense(r.state.a, a_out);
+    for (std::size_t i = 0; i < r.eigenvalues.size(); ++i) {
+      eig_out[2 * i] = r.eigenvalues[i].real();
+      eig_out[2 * i + 1] = r.eigenvalues[i].imag();
+      res_out[i] = r.residuals[i];
+    }
+    return ORC_OK;
+  } catch (const DegenerateSpectrum& e) {
+    rep->degenerate_i = int64_t(e.first());
+    rep->degenerate_j = int64_t(e.second());
+    return ORC_ERR_DEGENERATE;
+  } catch (const std::invalid_argument&) {
+    return ORC_ERR_INVALID;
+  } catch (...) {
+    return 9;
+  }
+}

@@ -128,6 +128,8 @@ def lib() -> ctypes.CDLL:
         L.dpt_spectral_spread.argtypes = [I64, c_void_p]
         L.dpt_spectral_spread.restype = D
         L.dpt_effective_window.argtypes = [c_int, I64]
+        L.dpt_homotopy_solve.argtypes = [c_void_p, P(dpt_problem), c_int, P(dpt_options), c_void_p, c_void_p,
+                                         c_void_p, c_int, P(dpt_report), P(dpt_error_info)]
         L.dpt_mm_read.argtypes = [ctypes.c_char_p, c_int, P(dpt_mm_matrix), P(dpt_error_info)]
         L.dpt_mm_free.argtypes = [P(dpt_mm_matrix)]
         L.dpt_mm_write_dense.argtypes = [ctypes.c_char_p, I64, I64, c_void_p, c_int, c_int, P(dpt_error_info)]

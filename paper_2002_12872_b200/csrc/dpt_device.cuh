@@ -95,6 +95,15 @@ __device__ __forceinline__ cd crecip(cd z) {  // (1 + 0i) / z
   const double ratio = d / c, denom = __dadd_rn(__dmul_rn(d, ratio), c);
   return cd{1.0 / denom, -ratio / denom};
 }
+__device__ __forceinline__ cd cdiv(cd x, cd z) {  // x / z, Smith's method (the finite-value path of __divdc3)
+  const double a = x.x, b = x.y, c = z.x, d = z.y;
+  if (fabs(c) < fabs(d)) {
+    const double ratio = c / d, denom = __dadd_rn(__dmul_rn(c, ratio), d);
+    return cd{__dadd_rn(__dmul_rn(a, ratio), b) / denom, __dsub_rn(__dmul_rn(b, ratio), a) / denom};
+  }
+  const double ratio = d / c, denom = __dadd_rn(__dmul_rn(d, ratio), c);
+  return cd{__dadd_rn(__dmul_rn(b, ratio), a) / denom, __dsub_rn(b, __dmul_rn(a, ratio)) / denom};
+}
 __device__ __forceinline__ bool cfinite(cd a) { return isfinite(a.x) && isfinite(a.y); }
 __device__ __forceinline__ cd lamc_of(const DevSolve& s, int j) {
   return s.lam_table ? cd{s.lam_table[2 * j], s.lam_table[2 * j + 1]} : cd{s.lambda, s.lambda_im};

@@ -60,6 +60,17 @@ cudaError_t launch_fold(const DevSolve& s, int ntiles_this, cudaStream_t st);
 cudaError_t launch_decide(const DevSolve& s, cudaStream_t st);
 cudaError_t launch_cycle(const DevSolve& s, int64_t elems, cudaStream_t st);
 cudaError_t launch_identity(const DevSolve& s, cudaStream_t st);
+// homotopy.cu: element-wise steps of the device homotopy_solve (row-major, cx = 1 | 2)
+cudaError_t launch_hom_stage_matrix(const double* D, const double* d, double lr, double li, int cx, int64_t n,
+                                    double* M, cudaStream_t st);
+cudaError_t launch_hom_transpose(const double* src, double* dst, int cx, int64_t n, cudaStream_t st);
+cudaError_t launch_hom_partition(const double* R, double* dlev, double* Dp, int cx, int64_t n, cudaStream_t st);
+cudaError_t launch_hom_normalise(const double* W, double* a, int cx, int64_t n, unsigned* singular, cudaStream_t st);
+cudaError_t launch_hom_densify(const int64_t* rp, const int32_t* cl, const double* vl, int cx, int64_t n, double* D,
+                               cudaStream_t st);
+cudaError_t launch_hom_identity(double* W, int cx, int64_t n, cudaStream_t st);
+cudaError_t launch_hom_nonfinite(const double* a, int64_t count, unsigned* bad, cudaStream_t st);
+
 // scan.cu: batched scan_domain, one warp per lambda cell (complex arithmetic in
 // the reference's operation order).  All arrays complex interleaved unless noted.
 struct ScanArgs {

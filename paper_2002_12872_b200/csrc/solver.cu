@@ -12,6 +12,8 @@
 // trace log to the TraceSink in k order, and stops.
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <cublas_v2.h>
+#include <cusolverDn.h>
 #include <dlfcn.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -106,6 +108,9 @@ struct dpt_ctx {
     int64_t per_body = 0;
   };
   std::vector<LoopGraph> loop_graphs;  // most recent last, at most kMaxLoopGraphs
+  // library handles for the homotopy's plain GEMM / LU (created on first use)
+  cublasHandle_t cublas = nullptr;
+  cusolverDnHandle_t cusolver = nullptr;
 };
 
 namespace {
@@ -215,6 +220,21 @@ struct DBuf {
     return static_cast<T*>(p);
   }
 };
+
+// Copy a problem array to the host in stream order: device inputs may have
+// been produced by this context's own kernels (e.g. a homotopy stage) on its
+// non-blocking stream, which the legacy-stream cudaMemcpy does not wait for.
+cudaError_t to_host_ordered(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind) {
+  if (bytes == 0) return cudaSuccess;
+  if (kind == cudaMemcpyHostToHost) {
+    std::memcpy(dst, src, bytes);
+    return cudaSuccess;
+  }
+  cudaStream_t st = t_ctx ? t_ctx->stream : nullptr;
+  cudaError_t e = cudaMemcpyAsync(dst, src, bytes, kind, st);
+  if (e != cudaSuccess) return e;
+  return cudaStreamSynchronize(st);
+}
 
 void dalloc(DBuf& b, size_t bytes, dpt_error_info* err) {
   if (bytes == 0) bytes = 16;
@@ -496,7 +516,7 @@ void upload(DevProblem& dp, dpt_ctx* ctx, const dpt_problem* p, dpt_error_info* 
       // so the real NT GEMM of the interleaved iterate with B yields (Re P, Im P) pairs.
       dp.ldd = 2 * n;
       std::vector<double> D(size_t(2 * n) * size_t(n));
-      if (n) CK(cudaMemcpy(D.data(), p->delta, size_t(2 * n) * size_t(n) * 8, hk));
+      if (n) CK(to_host_ordered(D.data(), p->delta, size_t(2 * n) * size_t(n) * 8, hk));
       std::vector<double> B(size_t(2 * n) * size_t(2 * n));
       for (int64_t j = 0; j < n; ++j) {
         double* r0 = B.data() + size_t(2 * j) * size_t(2 * n);
@@ -531,7 +551,7 @@ void upload(DevProblem& dp, dpt_ctx* ctx, const dpt_problem* p, dpt_error_info* 
     if (p->mem == DPT_MEM_HOST) {
       nnz = p->rowptr[n];
     } else {
-      CK(cudaMemcpy(&nnz, p->rowptr + n, 8, cudaMemcpyDeviceToHost));
+      CK(to_host_ordered(&nnz, p->rowptr + n, 8, cudaMemcpyDeviceToHost));
     }
     dp.nnz = nnz;
     if (dev && nnz && aligned16(p->cols) && aligned16(p->vals) && aligned16(p->rowptr)) {
@@ -1089,7 +1109,7 @@ void dev_level(dpt_ctx* ctx, const dpt_problem* p, int64_t i, double* re, double
   const int cx = p->is_complex ? 2 : 1;
   double v[2] = {0.0, 0.0};
   Guard g(ctx);
-  if (cudaMemcpy(v, p->d + cx * i, size_t(cx) * 8, cudaMemcpyDeviceToHost) != cudaSuccess) throw Fail{DPT_ERR_CUDA};
+  if (to_host_ordered(v, p->d + cx * i, size_t(cx) * 8, cudaMemcpyDeviceToHost) != cudaSuccess) throw Fail{DPT_ERR_CUDA};
   *re = v[0];
   *im = cx == 2 ? v[1] : 0.0;
 }
@@ -1144,7 +1164,7 @@ std::vector<double> host_levels(const dpt_problem* p, dpt_error_info* err) {
   const size_t cnt = size_t(p->n) * (p->is_complex ? 2 : 1);  // interleaved when complex
   std::vector<double> dh(cnt);
   if (p->n)
-    CK(cudaMemcpy(dh.data(), p->d, cnt * 8, p->mem == DPT_MEM_DEVICE ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost));
+    CK(to_host_ordered(dh.data(), p->d, cnt * 8, p->mem == DPT_MEM_DEVICE ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost));
   return dh;
 }
 
@@ -1457,6 +1477,185 @@ int run_single(dpt_ctx* ctx, const dpt_problem* p, int64_t row, const dpt_option
 }
 
 
+// ------------------------------------------------------ homotopy_solve ----
+// dpt.cpp:505-556 on the device.  Per stage s: M_s = lam_s Delta + diag(d),
+// R = W^-1 (M_s W) (cuBLAS GEMM + cuSOLVER LU -- plain library linear algebra),
+// partition(R) -> d', Delta' (lambda 1), the DPT solve of that problem in the
+// solver's kernels (A_s stays in HBM), W <- W A_s^T.  Then a(i, m) =
+// W(m, i) / W(i, i) and the read-offs of a against the original problem.
+#define CB(x)                                                                                   \
+  do {                                                                                          \
+    const cublasStatus_t s_ = (x);                                                              \
+    if (s_ != CUBLAS_STATUS_SUCCESS) {                                                          \
+      set_err(err, DPT_ERR_CUDA, std::string("cuBLAS status ") + std::to_string(int(s_)) + ": " #x); \
+      throw Fail{DPT_ERR_CUDA};                                                                 \
+    }                                                                                           \
+  } while (0)
+#define CSV(x)                                                                                    \
+  do {                                                                                            \
+    const cusolverStatus_t s_ = (x);                                                              \
+    if (s_ != CUSOLVER_STATUS_SUCCESS) {                                                          \
+      set_err(err, DPT_ERR_CUDA, std::string("cuSOLVER status ") + std::to_string(int(s_)) + ": " #x); \
+      throw Fail{DPT_ERR_CUDA};                                                                   \
+    }                                                                                             \
+  } while (0)
+
+// row-major C = A B (n x n): the column-major product B^T-view x A^T-view
+void gemm_rm(dpt_ctx* ctx, int cx, int64_t n, const double* A, const double* B, double* C, bool b_transposed,
+             dpt_error_info* err) {
+  const int nn = int(n);
+  // row-major buffers are column-major transposes: C^T = B^T A^T (or A B^T -> C^T = B A^T)
+  const cublasOperation_t opA = b_transposed ? CUBLAS_OP_T : CUBLAS_OP_N;
+  if (cx == 2) {
+    const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0);
+    CB(cublasZgemm(ctx->cublas, opA, CUBLAS_OP_N, nn, nn, nn, &one, reinterpret_cast<const cuDoubleComplex*>(B), nn,
+                   reinterpret_cast<const cuDoubleComplex*>(A), nn, &zero, reinterpret_cast<cuDoubleComplex*>(C), nn));
+  } else {
+    const double one = 1.0, zero = 0.0;
+    CB(cublasDgemm(ctx->cublas, opA, CUBLAS_OP_N, nn, nn, nn, &one, B, nn, A, nn, &zero, C, nn));
+  }
+}
+
+int run_homotopy(dpt_ctx* ctx, const dpt_problem* p, int stages, const dpt_options* opts_in, double* a_out,
+                 double* eig_out, double* res_out, int out_mem, dpt_report* rep, dpt_error_info* err) {
+  Guard g(ctx);
+  validate(p, err);
+  if (stages < 1) {
+    set_err(err, DPT_ERR_INVALID_ARG, "homotopy_solve: stages must be >= 1");
+    return DPT_ERR_INVALID_ARG;
+  }
+  const dpt_options o = opts_or_default(opts_in);
+  const int64_t n = p->n;
+  const int cx = p->is_complex ? 2 : 1;
+  cudaStream_t st = ctx->stream;
+  if (!ctx->cublas) CB(cublasCreate(&ctx->cublas));
+  if (!ctx->cusolver) CSV(cusolverDnCreate(&ctx->cusolver));
+  CB(cublasSetStream(ctx->cublas, st));
+  CSV(cusolverDnSetStream(ctx->cusolver, st));
+  const size_t mat = size_t(cx) * size_t(n) * size_t(n) * 8;
+  const cudaMemcpyKind k = p->mem == DPT_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  DBuf bd, bD, bW, bM, bT1, bT2, bA, bdl, bDp, bpiv, binfo, bflag;
+  dalloc(bd, size_t(cx * n) * 8, err);
+  dalloc(bD, mat, err);
+  dalloc(bW, mat, err);
+  dalloc(bM, mat, err);
+  dalloc(bT1, mat, err);
+  dalloc(bT2, mat, err);
+  dalloc(bA, mat, err);
+  dalloc(bdl, size_t(cx * n) * 8, err);
+  dalloc(bDp, mat, err);
+  dalloc(bpiv, size_t(n) * 4 + 16, err);
+  dalloc(binfo, 16, err);
+  dalloc(bflag, 16, err);
+  if (n) CK(cudaMemcpyAsync(bd.p, p->d, size_t(cx * n) * 8, k, st));
+  if (p->delta_kind == DPT_DELTA_DENSE) {  // densify(p.delta) (dpt.cpp:510)
+    if (n) CK(cudaMemcpyAsync(bD.p, p->delta, mat, k, st));
+  } else {
+    DevProblem dp;
+    upload(dp, ctx, p, err);
+    CK(cudaMemsetAsync(bD.p, 0, mat, st));
+    CK(launch_hom_densify(dp.rowptr.as<int64_t>(), dp.cols.as<int32_t>(), dp.vals.as<double>(), cx, n,
+                          bD.as<double>(), st));
+    CK(cudaStreamSynchronize(st));  // dp's buffers go out of scope
+  }
+  CK(launch_hom_identity(bW.as<double>(), cx, n, st));
+  int lwork = 0;
+  if (cx == 2)
+    CSV(cusolverDnZgetrf_bufferSize(ctx->cusolver, int(n), int(n), reinterpret_cast<cuDoubleComplex*>(bT1.p),
+                                    int(n), &lwork));
+  else
+    CSV(cusolverDnDgetrf_bufferSize(ctx->cusolver, int(n), int(n), bT1.as<double>(), int(n), &lwork));
+  DBuf bwork;
+  dalloc(bwork, size_t(std::max(lwork, 1)) * size_t(cx) * 8, err);
+  dpt_report last{};
+  int total = 0;
+  double* W = bW.as<double>();
+  double* Wn = bT2.as<double>();
+  for (int s = 1; s <= stages; ++s) {
+    const double f = double(s) / double(stages);  // lam_s = lambda * (s / stages), complex * double
+    const double lr = p->lambda * f, li = (p->is_complex ? p->lambda_im : 0.0) * f;
+    CK(launch_hom_stage_matrix(bD.as<double>(), bd.as<double>(), lr, li, cx, n, bM.as<double>(), st));
+    gemm_rm(ctx, cx, n, bM.as<double>(), W, bT1.as<double>(), false, err);  // M W
+    // R = W^-1 (M W): column-major LU of W, solve against (M W), back to row-major
+    CK(launch_hom_transpose(W, bA.as<double>(), cx, n, st));                  // W (column-major)
+    CK(launch_hom_transpose(bT1.as<double>(), bDp.as<double>(), cx, n, st));  // M W (column-major)
+    int* piv = bpiv.as<int>();
+    int* info = binfo.as<int>();
+    if (cx == 2) {
+      CSV(cusolverDnZgetrf(ctx->cusolver, int(n), int(n), reinterpret_cast<cuDoubleComplex*>(bA.p), int(n),
+                           reinterpret_cast<cuDoubleComplex*>(bwork.p), piv, info));
+    } else {
+      CSV(cusolverDnDgetrf(ctx->cusolver, int(n), int(n), bA.as<double>(), int(n), bwork.as<double>(), piv, info));
+    }
+    int hinfo = 0;
+    CK(cudaMemcpyAsync(&hinfo, info, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (hinfo > 0) {  // lu_factor's exact-zero pivot (matrix.cpp:485)
+      set_err(err, DPT_ERR_UNSUPPORTED, "solve_linear: singular matrix");
+      throw Fail{DPT_ERR_UNSUPPORTED};
+    }
+    if (cx == 2)
+      CSV(cusolverDnZgetrs(ctx->cusolver, CUBLAS_OP_N, int(n), int(n), reinterpret_cast<cuDoubleComplex*>(bA.p),
+                           int(n), piv, reinterpret_cast<cuDoubleComplex*>(bDp.p), int(n), info));
+    else
+      CSV(cusolverDnDgetrs(ctx->cusolver, CUBLAS_OP_N, int(n), int(n), bA.as<double>(), int(n), piv, bDp.as<double>(),
+                           int(n), info));
+    CK(launch_hom_transpose(bDp.as<double>(), bM.as<double>(), cx, n, st));  // R (row-major)
+    CK(launch_hom_partition(bM.as<double>(), bdl.as<double>(), bDp.as<double>(), cx, n, st));
+    dpt_problem sp{};
+    sp.n = n;
+    sp.d = bdl.as<double>();
+    sp.delta_kind = DPT_DELTA_DENSE;
+    sp.delta = bDp.as<double>();
+    sp.lambda = 1.0;  // partition() sets lambda = 1 (partition.cpp:31)
+    sp.mem = DPT_MEM_DEVICE;
+    sp.is_complex = p->is_complex;
+    sp.lambda_im = 0.0;
+    last = dpt_report{};
+    const int rc = run_full(ctx, &sp, &o, false, 0.0, -1, 0.0, nullptr, nullptr, bA.as<double>(), nullptr, nullptr,
+                            DPT_MEM_DEVICE, &last, err);
+    if (rc != DPT_OK) return rc;
+    total += last.iterations;
+    if (last.status != DPT_CONVERGED) break;
+    gemm_rm(ctx, cx, n, W, bA.as<double>(), Wn, true, err);  // W V, V = A^T (no conjugation)
+    std::swap(W, Wn);
+  }
+  // a(i, m) = W(m, i) / W(i, i)
+  CK(cudaMemsetAsync(bflag.p, 0, 8, st));
+  CK(launch_hom_normalise(W, bA.as<double>(), cx, n, bflag.as<unsigned>(), st));
+  CK(launch_hom_nonfinite(bA.as<double>(), int64_t(cx) * n * n, bflag.as<unsigned>() + 1, st));
+  unsigned hf[2] = {0, 0};
+  CK(cudaMemcpyAsync(hf, bflag.p, 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (hf[0]) {
+    set_err(err, DPT_ERR_UNSUPPORTED, "homotopy_solve: singular stage basis");
+    throw Fail{DPT_ERR_UNSUPPORTED};
+  }
+  if (hf[1] == 0) {  // read-offs against the ORIGINAL problem (dpt.cpp:547-550)
+    DBuf be, br;
+    dalloc(be, size_t(cx * n) * 8, err);
+    dalloc(br, size_t(n) * 8, err);
+    const int rc = run_step_full(ctx, p, bA.as<double>(), nullptr, p->lambda, nullptr, DPT_MEM_DEVICE,
+                                 be.as<double>(), br.as<double>(), err, p->is_complex ? p->lambda_im : 0.0);
+    if (rc != DPT_OK) return rc;
+    copy_out(eig_out, be.as<double>(), size_t(cx * n), out_mem, st, err);
+    copy_out(res_out, br.as<double>(), size_t(n), out_mem, st, err);
+  } else {
+    fill_nan(eig_out, size_t(cx * n), out_mem, st, err);
+    fill_nan(res_out, size_t(n), out_mem, st, err);
+  }
+  copy_out(a_out, bA.as<double>(), size_t(cx) * size_t(n) * size_t(n), out_mem, st, err);
+  CK(cudaStreamSynchronize(st));
+  if (rep) {
+    std::memset(rep, 0, sizeof(*rep));
+    rep->status = last.status;
+    rep->iterations = total;
+    rep->step_norm = last.step_norm;
+    rep->launches = int(ctx->launches);
+  }
+  return DPT_OK;
+}
+
 }  // namespace
 
 // ================================================================ C ABI ====
@@ -1529,6 +1728,8 @@ void dpt_ctx_destroy(dpt_ctx* ctx) {
     Guard g(ctx);
     if (ctx->comm && nccl_api() && nccl_api()->comm_destroy) nccl_api()->comm_destroy(ctx->comm);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    if (ctx->cublas) cublasDestroy(ctx->cublas);
+    if (ctx->cusolver) cusolverDnDestroy(ctx->cusolver);
     for (auto& lg : ctx->loop_graphs) {
       if (lg.ge) cudaGraphExecDestroy(lg.ge);
       if (lg.g) cudaGraphDestroy(lg.g);
@@ -1851,6 +2052,13 @@ int dpt_check_degenerate(int64_t n, const double* d, double tol, int64_t* i, int
 double dpt_spectral_spread(int64_t n, const double* d) { return spread_of(n, d); }
 
 int dpt_effective_window(int requested, int64_t n) { return effective_window(requested, n); }
+int dpt_homotopy_solve(dpt_ctx* ctx, const dpt_problem* p, int stages, const dpt_options* opts, double* a_out,
+                       double* eig_out, double* res_out, int out_mem, dpt_report* rep, dpt_error_info* err) {
+  DPT_API_BEGIN
+  return run_homotopy(ctx, p, stages, opts, a_out, eig_out, res_out, out_mem, rep, err);
+  DPT_API_END
+}
+
 // ------------------------------------------------------------ scan_domain ----
 // analysis.cpp:68-138.  Cells of the lambda grid are independent solves; small
 // problems run batched (scan.cu, one warp per cell, the reference's operation
@@ -1902,17 +2110,17 @@ int dpt_scan_domain(dpt_ctx* ctx, const dpt_problem* p, const dpt_scan_grid* gri
     const int cx = p->is_complex ? 2 : 1;
     if (p->delta_kind == DPT_DELTA_DENSE) {
       std::vector<double> raw(size_t(cx * n * n));
-      if (n) CK(cudaMemcpy(raw.data(), p->delta, raw.size() * 8, hk));
+      if (n) CK(to_host_ordered(raw.data(), p->delta, raw.size() * 8, hk));
       for (int64_t q = 0; q < n * n; ++q) D[size_t(q)] = cx == 2 ? cd_t(raw[size_t(2 * q)], raw[size_t(2 * q + 1)]) : cd_t(raw[size_t(q)], 0.0);
     } else {
       std::vector<int64_t> rp(size_t(n + 1));
-      CK(cudaMemcpy(rp.data(), p->rowptr, size_t(n + 1) * 8, hk));
+      CK(to_host_ordered(rp.data(), p->rowptr, size_t(n + 1) * 8, hk));
       const int64_t nnz = rp[size_t(n)];
       std::vector<int32_t> cl(static_cast<size_t>(nnz));
       std::vector<double> vl(static_cast<size_t>(cx * nnz));
       if (nnz) {
-        CK(cudaMemcpy(cl.data(), p->cols, size_t(nnz) * 4, hk));
-        CK(cudaMemcpy(vl.data(), p->vals, size_t(cx * nnz) * 8, hk));
+        CK(to_host_ordered(cl.data(), p->cols, size_t(nnz) * 4, hk));
+        CK(to_host_ordered(vl.data(), p->vals, size_t(cx * nnz) * 8, hk));
       }
       for (int64_t i = 0; i < n; ++i)
         for (int64_t q = rp[size_t(i)]; q < rp[size_t(i + 1)]; ++q)

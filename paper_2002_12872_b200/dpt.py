@@ -437,6 +437,24 @@ def iterate_full(p: PartitionedProblem, opts: Optional[IterationOptions] = None,
     return _full(p, opts, trace, False, 0.0, ctx, out)
 
 
+def homotopy_solve(p: PartitionedProblem, stages: int, opts: Optional[IterationOptions] = None,
+                   ctx: Context = None):
+    """Staged continuation (dpt.hpp:145-152, dpt.cpp:505-556) on the device:
+    `stages` solves along lambda s / stages, each on the problem rebased by the
+    converged bases.  Report as iterate_full (iterations summed over stages)."""
+    ctx = ctx or default_context()
+    m = _Marshal(p)
+    n = m.n
+    a, ap = m.out(n, n)
+    eig, ep = m.out(n)
+    res, rp = m.out(n, cplx=False)
+    rep, err = N.dpt_report(), N.dpt_error_info()
+    _raise(N.lib().dpt_homotopy_solve(ctx.handle, ctypes.byref(m.prob), int(stages), ctypes.byref(_opts(opts)), ap,
+                                      ep, rp, m.mem, ctypes.byref(rep), ctypes.byref(err)), err)
+    return ConvergenceReport(EigenIterate(m.result(a), rep.iterations), m.result(eig), ConvergenceStatus(rep.status),
+                             rep.iterations, res, rep.step_norm, rep.device_ms)
+
+
 def iterate_ramped(p: PartitionedProblem, alpha: float, opts: Optional[IterationOptions] = None,
                    trace=None, ctx: Context = None):
     """lambda_k = lambda (1 - alpha^(k-1)) (dpt.hpp:85-92); alpha in [0, 1)."""

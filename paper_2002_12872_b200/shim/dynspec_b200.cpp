@@ -436,52 +436,28 @@ std::vector<cdouble> multipliers(const DenseMatrix& reduced) {
   return eigenvalues_dense_small(reduced);
 }
 
-// Staged continuation (dpt.hpp:145-152): stage s solves the problem rebased by
-// the composition W of the converged eigenvector bases, M -> W^-1 M W, re-split
-// with a zero-diagonal perturbation; each stage's solve runs on the GPU.
+// Staged continuation (dpt.hpp:145-152): every stage's basis algebra and solve
+// run on the device (dpt_homotopy_solve).
 ConvergenceReport homotopy_solve(const PartitionedProblem& p, int stages, const IterationOptions& opts) {
   if (stages < 1) throw std::invalid_argument("homotopy_solve: stages must be >= 1");
+  auto P = to_c(p);
   const std::size_t n = p.size();
-  const DenseMatrix delta = densify(p.delta);
-  DenseMatrix w = DenseMatrix::identity(n);
-  ConvergenceReport last;
-  int total = 0;
-  for (int s = 1; s <= stages; ++s) {
-    const cdouble lam_s = p.lambda * (double(s) / double(stages));
-    DenseMatrix m = delta;
-    for (std::size_t q = 0; q < n * n; ++q) m.data()[q] *= lam_s;
-    for (std::size_t i = 0; i < n; ++i) m(i, i) += p.d.d[i];
-    const PartitionedProblem sub = partition(MatrixVariant{solve_linear_multi(w, matmul(m, w))});
-    last = iterate_full(sub, opts);
-    total += last.iterations;
-    if (last.status != ConvergenceStatus::Converged) break;
-    w = matmul(w, transpose(last.state.a));
-  }
-  DenseMatrix a(n, n);
-  for (std::size_t i = 0; i < n; ++i) {
-    const cdouble wii = w(i, i);
-    if (std::abs(wii) == 0.0) throw std::runtime_error("homotopy_solve: singular stage basis");
-    for (std::size_t m = 0; m < n; ++m) a(i, m) = w(m, i) / wii;
-  }
   ConvergenceReport rep;
-  rep.status = last.status;
-  rep.iterations = total;
-  rep.step_norm = last.step_norm;
-  if (all_finite(a)) {  // read-offs against the ORIGINAL problem, on the GPU
-    auto P = to_c(p.d, p.delta, p.lambda, has_imag(a));
-    const InBuf ab(a.data(), n * n, P->cplx);
-    rep.eigenvalues.resize(n);
-    rep.residuals.resize(n);
-    OutBuf eb(rep.eigenvalues.data(), n, P->cplx);
-    dpt_error_info e{};
-    check(dpt_readoffs(ctx(), &P->c, ab.p, eb.ptr(), rep.residuals.data(), DPT_MEM_HOST, &e), e);
-    eb.finish(true);
-  } else {
-    const double nan = std::numeric_limits<double>::quiet_NaN();
-    rep.eigenvalues.assign(n, cdouble{nan, nan});
-    rep.residuals.assign(n, nan);
-  }
-  rep.state = EigenIterate{std::move(a), total};
+  DenseMatrix a(n, n);
+  rep.eigenvalues.resize(n);
+  rep.residuals.resize(n);
+  OutBuf ab(a.data(), n * n, P->cplx), eb(rep.eigenvalues.data(), n, P->cplx);
+  const dpt_options o = to_c(opts);
+  dpt_report r{};
+  dpt_error_info e{};
+  check(dpt_homotopy_solve(ctx(), &P->c, stages, &o, ab.ptr(), eb.ptr(), rep.residuals.data(), DPT_MEM_HOST, &r, &e),
+        e);
+  ab.finish();
+  eb.finish(true);
+  rep.status = ConvergenceStatus(r.status);
+  rep.iterations = r.iterations;
+  rep.step_norm = r.step_norm;
+  rep.state = EigenIterate{std::move(a), r.iterations};
   return rep;
 }
 
