@@ -12,7 +12,7 @@ from ctypes import (POINTER, Structure, c_char, c_double, c_int, c_int32, c_int6
                     c_void_p)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdpt_b200.so")
+LIB_PATH = os.environ.get("DPT_LIB_PATH") or os.path.join(_HERE, "libdpt_b200.so")  # override: A/B builds
 PROBLEMS_PATH = os.path.join(_HERE, "libdpt_problems.so")
 
 DPT_MEM_HOST, DPT_MEM_DEVICE = 0, 1
