@@ -27,6 +27,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
+#include <type_traits>
 #include <stdint.h>
 #include <stdlib.h>
 
@@ -61,115 +62,18 @@ __device__ __forceinline__ uint32_t swz(int r, int chunk) {
   return uint32_t(r) * 128u + uint32_t((chunk ^ (r & 7)) << 4);
 }
 
+// The fused DPT epilogue of one output tile (tm, tn): map, step / max /
+// nonfinite, residual partials and the lagged diagonal (shared by the
+// one-tile-per-CTA kernel and the stream-K kernel).  Called by every consumer
+// thread; ends with the tile's partials written.
 template <class C, bool CPLX>
-__global__ void __launch_bounds__(C::THREADS, C::MINB)
-    dense_step_kernel(DevSolve s, const CUtensorMap* __restrict__ amaps,
-                      const CUtensorMap* __restrict__ dmap, const double* __restrict__ delta,
-                      int ntm) {
-  const int j_launch = launch_index(s);
-  if (s.state->done) return;  // a terminal status was reached: no-op launch
-
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sA = smem;
-  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
-  double* red = reinterpret_cast<double*>(smem + C::STAGES * C::STAGE_BYTES);
-  double* wred = red + C::WARPS_N * C::BM * 4;
-  uint64_t* full = reinterpret_cast<uint64_t*>(wred + C::NCW * 4);
-  uint64_t* empty = full + C::STAGES;
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // grouped rasterisation: 8 row blocks share each column block sweep (L2 reuse)
-  const int ntn = s.ntn;
-  const int bid = blockIdx.x;
-  const int group = 8;
-  const int per_group = group * ntn;
-  const int g = bid / per_group;
-  const int first_tm = g * group;
-  const int gsize = min(group, ntm - first_tm);
-  const int tm = first_tm + (bid % per_group) % gsize;
-  const int tn = (bid % per_group) / gsize;
-
-  const int slot_in = (j_launch - 1) % s.nslots;
-  const int slot_out = j_launch % s.nslots;
-  // real: P = A Delta^T over n columns; complex: the same NT GEMM over the
-  // interleaved (re, im) columns against B = [[Re D, -Im D], [Im D, Re D]]
-  // (row 2j of B -> Re P(:, j), row 2j+1 -> Im P(:, j)), i.e. K = N = 2n.
-  const int64_t n = s.ncol, rows = s.rows;
-  const int KT = int((n + C::BK - 1) / C::BK);
-
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < C::STAGES; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], C::NCW);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-
-  const CUtensorMap* am = amaps + slot_in;
-  const bool producer = (threadIdx.x == 0);
-  if (producer) {  // prologue: fill the pipeline
-    prefetch_tmap(am);
-    prefetch_tmap(dmap);
-    const int pre = KT < C::STAGES ? KT : C::STAGES;
-    for (int kt = 0; kt < pre; ++kt) {
-      mbar_arrive_expect_tx(&full[kt], C::STAGE_BYTES);
-      tma_load_2d(sA + kt * C::A_BYTES, am, &full[kt], kt * C::BK, tm * C::BM);
-      tma_load_2d(sB + kt * C::B_BYTES, dmap, &full[kt], kt * C::BK, tn * C::BN);
-    }
-  }
-
-  // ------------------------------------------------------ MMA consumers ----
+__device__ __forceinline__ void dense_epilogue(const DevSolve& s, double (&acc)[C::MB][C::NB][2], int tm, int tn,
+                                               int j_launch, int slot_in, int slot_out, const double* __restrict__ delta,
+                                               double* red, double* wred, int warp, int lane) {
   const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N;
   const int t = lane & 3, gq = lane >> 2;
-  double acc[C::MB][C::NB][2];
-#pragma unroll
-  for (int a = 0; a < C::MB; ++a)
-#pragma unroll
-    for (int b = 0; b < C::NB; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-
-  for (int kt = 0; kt < KT; ++kt) {
-    const int st = kt % C::STAGES;
-    mbar_wait(&full[st], (kt / C::STAGES) & 1);
-    const uint8_t* a_st = sA + st * C::A_BYTES;
-    const uint8_t* b_st = sB + st * C::B_BYTES;
-#pragma unroll
-    for (int q = 0; q < 2; ++q) {
-      // Row r = base + 8x + gq has (r & 7) == gq, so the swizzled chunk offset is
-      // the same for every fragment of this lane: per-fragment addresses differ
-      // by immediates (x * 1024 bytes).
-      const uint32_t cofs = uint32_t(((4 * q + t) ^ gq) << 4) + uint32_t(gq) * 128u;
-      const uint32_t pa = smem_u32(a_st) + uint32_t(wm * C::WTM * 128) + cofs;
-      const uint32_t pb = smem_u32(b_st) + uint32_t(wn * C::WTN * 128) + cofs;
-      // B fragments for both k4-steps of this 16-byte chunk stay live; A
-      // fragments stream through (keeps the 64-double accumulator + operands
-      // within the register budget).
-      double2 bf[C::NB];
-#pragma unroll
-      for (int b = 0; b < C::NB; ++b) bf[b] = lds128(pb + b * 1024);
-#pragma unroll
-      for (int a = 0; a < C::MB; ++a) {
-        const double2 af = lds128(pa + a * 1024);
-#pragma unroll
-        for (int b = 0; b < C::NB; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], af.x, bf[b].x);
-#pragma unroll
-        for (int b = 0; b < C::NB; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], af.y, bf[b].y);
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);
-    if (producer && kt + C::STAGES < KT) {  // refill this stage once every warp released it
-      const int kn = kt + C::STAGES;
-      mbar_wait(&empty[st], (kt / C::STAGES) & 1);
-      mbar_arrive_expect_tx(&full[st], C::STAGE_BYTES);
-      tma_load_2d(sA + st * C::A_BYTES, am, &full[st], kn * C::BK, tm * C::BM);
-      tma_load_2d(sB + st * C::B_BYTES, dmap, &full[st], kn * C::BK, tn * C::BN);
-    }
-    __syncwarp();
-  }
-
-  // --------------------------------------------------- fused DPT epilogue ----
+  const int64_t n = s.ncol, rows = s.rows;
+  const int ntn = s.ntn;
   const double lam_k = lam_of(s, j_launch);
   const double lam = s.lambda;
   const double* __restrict__ a_in = s.slots + size_t(slot_in) * size_t(s.slot_elems);
@@ -354,6 +258,284 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
     tp[1] = a1;
     tp[2] = a2;
     tp[3] = 0.0;
+  }
+}
+
+template <class C, bool CPLX>
+__global__ void __launch_bounds__(C::THREADS, C::MINB)
+    dense_step_kernel(DevSolve s, const CUtensorMap* __restrict__ amaps,
+                      const CUtensorMap* __restrict__ dmap, const double* __restrict__ delta,
+                      int ntm) {
+  const int j_launch = launch_index(s);
+  if (s.state->done) return;  // a terminal status was reached: no-op launch
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
+  double* red = reinterpret_cast<double*>(smem + C::STAGES * C::STAGE_BYTES);
+  double* wred = red + C::WARPS_N * C::BM * 4;
+  uint64_t* full = reinterpret_cast<uint64_t*>(wred + C::NCW * 4);
+  uint64_t* empty = full + C::STAGES;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // grouped rasterisation: 8 row blocks share each column block sweep (L2 reuse)
+  const int ntn = s.ntn;
+  const int bid = blockIdx.x;
+  const int group = 8;
+  const int per_group = group * ntn;
+  const int g = bid / per_group;
+  const int first_tm = g * group;
+  const int gsize = min(group, ntm - first_tm);
+  const int tm = first_tm + (bid % per_group) % gsize;
+  const int tn = (bid % per_group) / gsize;
+
+  const int slot_in = (j_launch - 1) % s.nslots;
+  const int slot_out = j_launch % s.nslots;
+  // real: P = A Delta^T over n columns; complex: the same NT GEMM over the
+  // interleaved (re, im) columns against B = [[Re D, -Im D], [Im D, Re D]]
+  // (row 2j of B -> Re P(:, j), row 2j+1 -> Im P(:, j)), i.e. K = N = 2n.
+  const int64_t n = s.ncol;
+  const int KT = int((n + C::BK - 1) / C::BK);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < C::STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], C::NCW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  const CUtensorMap* am = amaps + slot_in;
+  const bool producer = (threadIdx.x == 0);
+  if (producer) {  // prologue: fill the pipeline
+    prefetch_tmap(am);
+    prefetch_tmap(dmap);
+    const int pre = KT < C::STAGES ? KT : C::STAGES;
+    for (int kt = 0; kt < pre; ++kt) {
+      mbar_arrive_expect_tx(&full[kt], C::STAGE_BYTES);
+      tma_load_2d(sA + kt * C::A_BYTES, am, &full[kt], kt * C::BK, tm * C::BM);
+      tma_load_2d(sB + kt * C::B_BYTES, dmap, &full[kt], kt * C::BK, tn * C::BN);
+    }
+  }
+
+  // ------------------------------------------------------ MMA consumers ----
+  const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N;
+  const int t = lane & 3, gq = lane >> 2;
+  double acc[C::MB][C::NB][2];
+#pragma unroll
+  for (int a = 0; a < C::MB; ++a)
+#pragma unroll
+    for (int b = 0; b < C::NB; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+  for (int kt = 0; kt < KT; ++kt) {
+    const int st = kt % C::STAGES;
+    mbar_wait(&full[st], (kt / C::STAGES) & 1);
+    const uint8_t* a_st = sA + st * C::A_BYTES;
+    const uint8_t* b_st = sB + st * C::B_BYTES;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      // Row r = base + 8x + gq has (r & 7) == gq, so the swizzled chunk offset is
+      // the same for every fragment of this lane: per-fragment addresses differ
+      // by immediates (x * 1024 bytes).
+      const uint32_t cofs = uint32_t(((4 * q + t) ^ gq) << 4) + uint32_t(gq) * 128u;
+      const uint32_t pa = smem_u32(a_st) + uint32_t(wm * C::WTM * 128) + cofs;
+      const uint32_t pb = smem_u32(b_st) + uint32_t(wn * C::WTN * 128) + cofs;
+      // B fragments for both k4-steps of this 16-byte chunk stay live; A
+      // fragments stream through (keeps the 64-double accumulator + operands
+      // within the register budget).
+      double2 bf[C::NB];
+#pragma unroll
+      for (int b = 0; b < C::NB; ++b) bf[b] = lds128(pb + b * 1024);
+#pragma unroll
+      for (int a = 0; a < C::MB; ++a) {
+        const double2 af = lds128(pa + a * 1024);
+#pragma unroll
+        for (int b = 0; b < C::NB; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], af.x, bf[b].x);
+#pragma unroll
+        for (int b = 0; b < C::NB; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], af.y, bf[b].y);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+    if (producer && kt + C::STAGES < KT) {  // refill this stage once every warp released it
+      const int kn = kt + C::STAGES;
+      mbar_wait(&empty[st], (kt / C::STAGES) & 1);
+      mbar_arrive_expect_tx(&full[st], C::STAGE_BYTES);
+      tma_load_2d(sA + st * C::A_BYTES, am, &full[st], kn * C::BK, tm * C::BM);
+      tma_load_2d(sB + st * C::B_BYTES, dmap, &full[st], kn * C::BK, tn * C::BN);
+    }
+    __syncwarp();
+  }
+
+  dense_epilogue<C, CPLX>(s, acc, tm, tn, j_launch, slot_in, slot_out, delta, red, wred, warp, lane);
+}
+
+// Stream-K variant for small n (cfg 0): with few output tiles per SM (c1:
+// 256 tiles on 148 SMs) the SMs holding two tiles set the step time while the
+// rest idle.  Here a persistent grid of exactly the resident CTAs splits the
+// flat (tile, k-tile) work evenly: CTA c owns units [c T / G, (c+1) T / G).
+// A tile whose k-range spans several CTAs is finished by whichever of them
+// completes last: every part stores its accumulators to a per-CTA workspace
+// slot and bumps the tile's counter; the last one sums the parts in k order
+// (deterministic) and runs the epilogue.  Nobody waits, so no co-residency
+// assumption is needed.  The TMA pipeline runs across tile boundaries, so the
+// next segment's loads overlap the current segment's epilogue.
+__device__ __forceinline__ int64_t sk_cta_of(int64_t u, int64_t total, int64_t G) {
+  int64_t c = (u * G) / total;  // floor(c T / G) <= u < floor((c + 1) T / G)
+  while (c + 1 < G && ((c + 1) * total) / G <= u) ++c;
+  while (c > 0 && (c * total) / G > u) --c;
+  return c;
+}
+
+template <class C, bool CPLX>
+__global__ void __launch_bounds__(C::THREADS, C::MINB)
+    dense_step_sk_kernel(DevSolve s, const CUtensorMap* __restrict__ amaps,
+                         const CUtensorMap* __restrict__ dmap, const double* __restrict__ delta, int ntm) {
+  const int j_launch = launch_index(s);
+  if (s.state->done) return;
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
+  double* red = reinterpret_cast<double*>(smem + C::STAGES * C::STAGE_BYTES);
+  double* wred = red + C::WARPS_N * C::BM * 4;
+  uint64_t* full = reinterpret_cast<uint64_t*>(wred + C::NCW * 4);
+  uint64_t* empty = full + C::STAGES;
+  __shared__ int sk_last;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ntn = s.ntn;
+  const int group = 8, per_group = group * ntn;
+  auto raster = [&](int64_t q, int& tm, int& tn) {  // the grouped rasterisation of the one-tile kernel
+    const int b = int(q);
+    const int g = b / per_group, first_tm = g * group, gsize = min(group, ntm - first_tm);
+    tm = first_tm + (b % per_group) % gsize;
+    tn = (b % per_group) / gsize;
+  };
+  const int slot_in = (j_launch - 1) % s.nslots;
+  const int slot_out = j_launch % s.nslots;
+  const int64_t n = s.ncol;
+  const int KT = int((n + C::BK - 1) / C::BK);
+  const int64_t total = int64_t(ntm) * ntn * KT, G = gridDim.x, cta = blockIdx.x;
+  const int64_t u0 = cta * total / G, u1 = (cta + 1) * total / G;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < C::STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], C::NCW);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const CUtensorMap* am = amaps + slot_in;
+  const bool producer = (threadIdx.x == 0);
+  auto issue = [&](int64_t v, int st) {
+    int tm, tn;
+    raster(v / KT, tm, tn);
+    const int kt = int(v % KT);
+    mbar_arrive_expect_tx(&full[st], C::STAGE_BYTES);
+    tma_load_2d(sA + st * C::A_BYTES, am, &full[st], kt * C::BK, tm * C::BM);
+    tma_load_2d(sB + st * C::B_BYTES, dmap, &full[st], kt * C::BK, tn * C::BN);
+  };
+  if (producer) {
+    prefetch_tmap(am);
+    prefetch_tmap(dmap);
+    for (int64_t i = 0; i < C::STAGES && u0 + i < u1; ++i) issue(u0 + i, int(i));
+  }
+
+  const int wm = warp / C::WARPS_N, wn = warp % C::WARPS_N;
+  const int t = lane & 3, gq = lane >> 2;
+  constexpr int PART = C::NCW * C::MB * C::NB * 64;  // doubles per partial tile
+  double acc[C::MB][C::NB][2];
+  int64_t it = 0;  // units consumed by this CTA (pipeline stage / phase)
+  for (int64_t v = u0; v < u1;) {
+    const int64_t tile = v / KT;
+    const int ka = int(v % KT);
+    const int kb = int(min(int64_t(KT), int64_t(ka) + (u1 - v)));
+#pragma unroll
+    for (int a = 0; a < C::MB; ++a)
+#pragma unroll
+      for (int b = 0; b < C::NB; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int kt = ka; kt < kb; ++kt, ++it) {
+      const int st = int(it % C::STAGES);
+      mbar_wait(&full[st], uint32_t((it / C::STAGES) & 1));
+      const uint8_t* a_st = sA + st * C::A_BYTES;
+      const uint8_t* b_st = sB + st * C::B_BYTES;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const uint32_t cofs = uint32_t(((4 * q + t) ^ gq) << 4) + uint32_t(gq) * 128u;
+        const uint32_t pa = smem_u32(a_st) + uint32_t(wm * C::WTM * 128) + cofs;
+        const uint32_t pb = smem_u32(b_st) + uint32_t(wn * C::WTN * 128) + cofs;
+        double2 bf[C::NB];
+#pragma unroll
+        for (int b = 0; b < C::NB; ++b) bf[b] = lds128(pb + b * 1024);
+#pragma unroll
+        for (int a = 0; a < C::MB; ++a) {
+          const double2 af = lds128(pa + a * 1024);
+#pragma unroll
+          for (int b = 0; b < C::NB; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], af.x, bf[b].x);
+#pragma unroll
+          for (int b = 0; b < C::NB; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], af.y, bf[b].y);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      if (producer && u0 + it + C::STAGES < u1) {  // refill this stage with the unit STAGES ahead
+        mbar_wait(&empty[st], uint32_t((it / C::STAGES) & 1));
+        issue(u0 + it + C::STAGES, st);
+      }
+      __syncwarp();
+    }
+    int tm, tn;
+    raster(tile, tm, tn);
+    asm volatile("bar.sync 1, %0;\n" ::"r"(C::NCW * 32) : "memory");  // red / wred / flag reuse
+    if (ka == 0 && kb == KT) {
+      dense_epilogue<C, CPLX>(s, acc, tm, tn, j_launch, slot_in, slot_out, delta, red, wred, warp, lane);
+    } else {
+      const int which = v == u0 ? 0 : 1;  // a CTA's partial segments are its first and / or last
+      double* part = s.sk_ws + (size_t(cta) * 2 + size_t(which)) * size_t(PART);
+#pragma unroll
+      for (int a = 0; a < C::MB; ++a)
+#pragma unroll
+        for (int b = 0; b < C::NB; ++b)
+          *reinterpret_cast<double2*>(part + ((size_t(warp) * C::MB + a) * C::NB + b) * 64 + 2 * lane) =
+              make_double2(acc[a][b][0], acc[a][b][1]);
+      const int64_t c_first = sk_cta_of(tile * KT, total, G), c_last = sk_cta_of(tile * KT + KT - 1, total, G);
+      asm volatile("bar.sync 1, %0;\n" ::"r"(C::NCW * 32) : "memory");
+      if (threadIdx.x == 0) {
+        fence_acq_rel_gpu();  // release this part
+        const unsigned prev = atomicAdd(s.sk_cnt + tile, 1u);
+        sk_last = prev == unsigned(c_last - c_first);
+        if (sk_last) fence_acq_rel_gpu();  // acquire the other parts
+      }
+      asm volatile("bar.sync 1, %0;\n" ::"r"(C::NCW * 32) : "memory");
+      if (sk_last) {
+        // P = part(c_first) + part(c_first + 1) + ... in k order
+#pragma unroll
+        for (int a = 0; a < C::MB; ++a)
+#pragma unroll
+          for (int b = 0; b < C::NB; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+        for (int64_t cc = c_first; cc <= c_last; ++cc) {
+          const int w2 = (cc * total) / G < tile * KT ? 1 : 0;
+          const double* pp = s.sk_ws + (size_t(cc) * 2 + size_t(w2)) * size_t(PART);
+#pragma unroll
+          for (int a = 0; a < C::MB; ++a)
+#pragma unroll
+            for (int b = 0; b < C::NB; ++b) {
+              const double2 o = __ldcg(reinterpret_cast<const double2*>(
+                  pp + ((size_t(warp) * C::MB + a) * C::NB + b) * 64 + 2 * lane));
+              acc[a][b][0] += o.x;
+              acc[a][b][1] += o.y;
+            }
+        }
+        if (threadIdx.x == 0) s.sk_cnt[tile] = 0u;  // ready for the next launch
+        dense_epilogue<C, CPLX>(s, acc, tm, tn, j_launch, slot_in, slot_out, delta, red, wred, warp, lane);
+      }
+    }
+    v += kb - ka;
   }
 }
 
@@ -555,10 +737,39 @@ int dense_cfg_for(int64_t n) {
   return (v == 1 || v == 2) ? v : 2;
 }
 
+// Resident CTAs of the stream-K kernel (its persistent grid).
+template <class C, bool CPLX>
+static int sk_grid() {
+  static int g = 0;
+  if (!g) {
+    cudaFuncSetAttribute(dense_step_sk_kernel<C, CPLX>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    int per_sm = 0, dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dense_step_sk_kernel<C, CPLX>, C::THREADS, C::SMEM);
+    g = (per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 148);
+  }
+  return g;
+}
+
+int dense_sk_grid(int) { return sk_grid<CfgSmall, true>(); }
+size_t dense_sk_part_doubles() { return size_t(CfgSmall::NCW) * CfgSmall::MB * CfgSmall::NB * 64; }
+
 template <class C>
 static cudaError_t launch_cfg(const DevSolve& s, const CUtensorMap* amaps, const CUtensorMap* dmap,
                              const double* delta, cudaStream_t st) {
   const int ntm = int((s.rows + C::BM - 1) / C::BM);
+  if constexpr (std::is_same<C, CfgSmall>::value) {
+    // stream-K (workspace allocated by make_work) where it measured faster:
+    // complex small problems (c1 complex: 0.344 vs 0.366 ms); real c1 is faster
+    // one tile per CTA (0.088 vs 0.101 ms).  Every CTA must own >= 1 unit, and
+    // a few units per CTA keep the part count per tile small.
+    const int64_t units = int64_t(ntm) * s.ntn * ((s.ncol + C::BK - 1) / C::BK);
+    if (s.sk_ws && s.cplx && units >= 4 * int64_t(sk_grid<C, true>())) {
+      dense_step_sk_kernel<C, true><<<sk_grid<C, true>(), C::THREADS, C::SMEM, st>>>(s, amaps, dmap, delta, ntm);
+      return cudaGetLastError();
+    }
+  }
   if (s.cplx) {
     static bool attr = false;
     if (!attr) {

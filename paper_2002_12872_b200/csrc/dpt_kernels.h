@@ -61,6 +61,8 @@ cudaError_t launch_decide(const DevSolve& s, cudaStream_t st);
 cudaError_t launch_cycle(const DevSolve& s, int64_t elems, cudaStream_t st);
 cudaError_t launch_identity(const DevSolve& s, cudaStream_t st);
 // homotopy.cu: element-wise steps of the device homotopy_solve (row-major, cx = 1 | 2)
+int dense_sk_grid(int cplx);          // stream-K K1: resident CTAs (persistent grid)
+size_t dense_sk_part_doubles();       // stream-K K1: doubles per partial tile
 cudaError_t launch_hom_stage_matrix(const double* D, const double* d, double lr, double li, int cx, int64_t n,
                                     double* M, cudaStream_t st);
 cudaError_t launch_hom_transpose(const double* src, double* dst, int cx, int64_t n, cudaStream_t st);

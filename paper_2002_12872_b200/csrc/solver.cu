@@ -587,7 +587,7 @@ void upload(DevProblem& dp, dpt_ctx* ctx, const dpt_problem* p, dpt_error_info* 
 struct Work {
   DevSolve s{};
   DBuf slots, dvec, eps, res, rowpart, tilepart, blockpart, stats, state, trace, counter, cyclepart,
-      amaps, lam_table, settled_table;
+      amaps, lam_table, settled_table, sk_ws, sk_cnt;
   int ntiles_step = 0;
   int max_trace = 0;
   dpt_sm_state* h_state = nullptr;  // pinned (the context's cached host buffer)
@@ -692,6 +692,17 @@ void make_work(Work& w, dpt_ctx* ctx, DevProblem& dp, Mode mode, int64_t row0, i
     }
     dalloc(w.amaps, sizeof(CUtensorMap) * size_t(nslots), err);
     CK(cudaMemcpyAsync(w.amaps.p, maps.data(), sizeof(CUtensorMap) * size_t(nslots), cudaMemcpyHostToDevice, st));
+    // stream-K K1 for the small-tile configuration (dense_step.cu): partial-tile
+    // slots per resident CTA and per-tile counters (zero; the kernel re-zeroes)
+    const char* sk_env = std::getenv("DPT_DENSE_SK");
+    if (dp.big == 0 && dp.cplx && !(sk_env && sk_env[0] == '0')) {  // (used for complex problems)
+      const int g = dense_sk_grid(dp.cplx);
+      dalloc(w.sk_ws, size_t(g) * 2 * dense_sk_part_doubles() * 8, err);
+      dalloc(w.sk_cnt, size_t(std::max(w.ntiles_step, 1)) * 4, err);
+      CK(cudaMemsetAsync(w.sk_cnt.p, 0, size_t(std::max(w.ntiles_step, 1)) * 4, st));
+      s.sk_ws = w.sk_ws.as<double>();
+      s.sk_cnt = w.sk_cnt.as<unsigned>();
+    }
     if (!dp.dmap.p) {
       CUtensorMap dm;
       if (make_tmap_rowmajor(&dm, dp.delta.as<double>(), dp.ncol, dp.ncol, dp.ldd, dense_tile_n(dp.big)) != 0) {
