@@ -1,1 +1,1 @@
-timeout 300 python tools/config_times.py --configs c1 --steps 30 2>&1 | tail -12 | cut -c1-300
+timeout 1200 python -m pytest tests/test_gpu_fuzz.py -q --timeout 300 2>&1 | tail -25
