@@ -116,16 +116,36 @@ __global__ void __launch_bounds__(32 * kWarpsMax) scan_full_kernel(ScanArgs a) {
         break;
       }
       __syncwarp();
-      // Pn = An * delta_t, k order, zero a(i,k) skipped (matrix.cpp:130-143)
-      for (int e = lane; e < nn; e += 32) {
-        const int i = e / n, j = e % n;
-        C s = mk(0.0, 0.0);
-        for (int q = 0; q < n; ++q) {
-          const C aik = An[i * n + q];
-          if (aik.x == 0.0 && aik.y == 0.0) continue;
-          s = add(s, mul(aik, DT[q * n + j]));
+      // Pn = An * delta_t, k order, zero a(i,k) skipped (matrix.cpp:130-143).
+      // A lane's entries advance together, TB at a time, one k per step: TB
+      // independent dependency chains in flight instead of one (each entry
+      // still sums its terms in k order, so the result is unchanged).
+      {
+        constexpr int T = (NMAX * NMAX + 31) / 32, TB = T < 8 ? T : 8;
+        for (int t0 = 0; t0 < T; t0 += TB) {
+          C acc[TB];
+          int ei[TB], ej[TB];
+#pragma unroll
+          for (int u = 0; u < TB; ++u) {
+            const int e = lane + 32 * (t0 + u);
+            const int ee = e < nn ? e : 0;
+            ei[u] = ee / n;
+            ej[u] = ee % n;
+            acc[u] = mk(0.0, 0.0);
+          }
+          for (int q = 0; q < n; ++q) {
+#pragma unroll
+            for (int u = 0; u < TB; ++u) {
+              const C aik = An[ei[u] * n + q];
+              if (!(aik.x == 0.0 && aik.y == 0.0)) acc[u] = add(acc[u], mul(aik, DT[q * n + ej[u]]));
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < TB; ++u) {
+            const int e = lane + 32 * (t0 + u);
+            if (e < nn) Pn[e] = acc[u];
+          }
         }
-        Pn[e] = s;
       }
       __syncwarp();
       bool stop = false;
@@ -152,18 +172,32 @@ __global__ void __launch_bounds__(32 * kWarpsMax) scan_full_kernel(ScanArgs a) {
         // within_tol against every window entry at once: bit s of `differs`
         // = "ring slot s has a component >= tol away"; Bounded if any filled
         // slot has none (which one is irrelevant to the outcome)
+        // Sample first: entry `lane` of every slot (one load per slot per
+        // lane) refutes almost every slot; only the survivors are compared
+        // in full.  Exact: a refuted slot has a component >= tol away.
         bool within_any = false;
+        const C cv0 = lane < nn ? An[lane] : mk(0.0, 0.0);
         for (int s0 = 0; s0 < filled && !within_any; s0 += 32) {  // 32 slots per mask
           const int cnt = filled - s0 < 32 ? filled - s0 : 32;
           unsigned differs = 0u;
-          for (int q = lane; q < cnt * nn; q += 32) {
-            const int sl = q / nn, e = q - sl * nn;
-            const C pv = ring[size_t(s0 + sl) * size_t(rstride) + e], cv = An[e];
-            if (fabs(__dsub_rn(cv.x, pv.x)) >= tol || fabs(__dsub_rn(cv.y, pv.y)) >= tol) differs |= 1u << sl;
-          }
+          if (lane < nn)
+            for (int sl = 0; sl < cnt; ++sl) {
+              const C pv = ring[size_t(s0 + sl) * size_t(rstride) + lane];
+              if (fabs(__dsub_rn(cv0.x, pv.x)) >= tol || fabs(__dsub_rn(cv0.y, pv.y)) >= tol) differs |= 1u << sl;
+            }
           differs = __reduce_or_sync(0xffffffffu, differs);
           const unsigned full_mask = cnt == 32 ? 0xffffffffu : ((1u << cnt) - 1u);
-          within_any = (differs & full_mask) != full_mask;
+          unsigned open = full_mask & ~differs;  // slots the sample did not refute
+          while (open && !within_any) {
+            const int sl = __ffs(open) - 1;
+            open &= open - 1;
+            bool d = false;
+            for (int e = lane + 32; e < nn; e += 32) {
+              const C pv = ring[size_t(s0 + sl) * size_t(rstride) + e], cv = An[e];
+              if (fabs(__dsub_rn(cv.x, pv.x)) >= tol || fabs(__dsub_rn(cv.y, pv.y)) >= tol) d = true;
+            }
+            within_any = !__any_sync(0xffffffffu, d);
+          }
         }
         if (within_any) {
           status = 1;
@@ -279,18 +313,29 @@ __global__ void __launch_bounds__(32 * kWarpsMax) scan_single_kernel(ScanArgs a)
       } else if (win > 0 && settled && step > margin && filled > 0) {
         // all window entries at once (see the full kernel); the ring holds at
         // most 31 entries per pass of the mask, more are checked in rounds
-        bool within_any = false;
+        bool within_any = false;  // sample first (see the full kernel), then the survivors in full
+        const C cv0 = lane < n ? zn[lane] : mk(0.0, 0.0);
         for (int s0 = 0; s0 < filled && !within_any; s0 += 32) {
           const int cnt = filled - s0 < 32 ? filled - s0 : 32;
           unsigned differs = 0u;
-          for (int q = lane; q < cnt * n; q += 32) {
-            const int sl = q / n, m = q - sl * n;
-            const C pv = ring[size_t(s0 + sl) * size_t(rstride) + m], cv = zn[m];
-            if (fabs(__dsub_rn(cv.x, pv.x)) >= tol || fabs(__dsub_rn(cv.y, pv.y)) >= tol) differs |= 1u << sl;
-          }
+          if (lane < n)
+            for (int sl = 0; sl < cnt; ++sl) {
+              const C pv = ring[size_t(s0 + sl) * size_t(rstride) + lane];
+              if (fabs(__dsub_rn(cv0.x, pv.x)) >= tol || fabs(__dsub_rn(cv0.y, pv.y)) >= tol) differs |= 1u << sl;
+            }
           differs = __reduce_or_sync(0xffffffffu, differs);
           const unsigned full_mask = cnt == 32 ? 0xffffffffu : ((1u << cnt) - 1u);
-          within_any = (differs & full_mask) != full_mask;
+          unsigned open = full_mask & ~differs;
+          while (open && !within_any) {
+            const int sl = __ffs(open) - 1;
+            open &= open - 1;
+            bool d = false;
+            for (int m = lane + 32; m < n; m += 32) {
+              const C pv = ring[size_t(s0 + sl) * size_t(rstride) + m], cv = zn[m];
+              if (fabs(__dsub_rn(cv.x, pv.x)) >= tol || fabs(__dsub_rn(cv.y, pv.y)) >= tol) d = true;
+            }
+            within_any = !__any_sync(0xffffffffu, d);
+          }
         }
         if (within_any) {
           status = 1;

@@ -1,1 +1,1 @@
-timeout 1200 python -m pytest tests/test_gpu_fuzz.py -q --timeout 300 2>&1 | tail -25
+timeout 900 python -m pytest tests/test_gpu_scan.py tests/test_gpu_shim.py -q --timeout 300 -x 2>&1 | tail -2
