@@ -385,6 +385,8 @@ int ref_c_dominant(const orc_cproblem* p, const orc_options* o, double* z_chart,
     rep->degenerate_i = int64_t(e.first());
     rep->degenerate_j = int64_t(e.second());
     return ORC_ERR_DEGENERATE;
+  } catch (const std::invalid_argument&) {  // ShapeError: empty problem (dpt.cpp:402)
+    return ORC_ERR_SHAPE;
   }
 }
 

@@ -1217,6 +1217,19 @@ int run_full(dpt_ctx* ctx, const dpt_problem* p, const dpt_options* opts_in, boo
   std::vector<double> dh = host_levels(p, err);
   // iterate_fixed builds theta with the default tolerance (dpt.cpp:383)
   check_levels(p, dh, fixed ? 1e-12 : o.degeneracy_tol, err);
+  if (n == 0) {  // run_full on an empty problem (dpt.cpp:92-192): every norm is 0
+    int status = DPT_MAX_ITERATIONS, iters = fixed ? fixed_k : std::max(o.max_iter, 0);
+    if (!fixed && o.max_iter >= 1 && 0.0 < o.tol && 0.0 < o.residual_tol) {
+      status = DPT_CONVERGED;  // k = 1: step 0 < tol, max residual 0 < residual_tol
+      iters = 1;
+    }
+    if (rep) {
+      std::memset(rep, 0, sizeof(*rep));
+      rep->status = status;
+      rep->iterations = iters;
+    }
+    return DPT_OK;
+  }
   DevProblem dp;
   upload(dp, ctx, p, err, p->delta_kind == DPT_DELTA_CSR);
   const int cx = dp.cplx ? 2 : 1;
