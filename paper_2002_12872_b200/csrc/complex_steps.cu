@@ -12,6 +12,7 @@
 // a real NT GEMM against B = [[Re D, -Im D], [Im D, Re D]], dense_step.cu.)
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "dpt_device.cuh"
 #include "dpt_kernels.h"
@@ -24,6 +25,10 @@ constexpr int kCsrCSmemBudget = 200 * 1024;
 static int csr_c_rows_per_cta(int64_t n) {
   int64_t r = kCsrCSmemBudget / (n * 16);
   if (r > 4) r = 4;
+  if (const char* e = getenv("DPT_CSR_ROWS")) {  // tests: force fewer staged rows (0 = global gathers)
+    const int64_t f = atoi(e);
+    if (f >= 0 && f < r) r = f;
+  }
   return int(r);
 }
 

@@ -20,6 +20,7 @@
 // values + columns stream once, z is gathered from L2.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "dpt_device.cuh"
 #include "dpt_kernels.h"
@@ -32,6 +33,10 @@ constexpr int kCsrSmemBudget = 200 * 1024;
 static int csr_rows_per_cta(int64_t n) {
   int64_t r = kCsrSmemBudget / (n * 8);
   if (r > 8) r = 8;
+  if (const char* e = getenv("DPT_CSR_ROWS")) {  // tests: force fewer staged rows (0 = global gathers)
+    const int64_t f = atoi(e);
+    if (f >= 0 && f < r) r = f;
+  }
   if (r >= 2 && (r & 1) == 0 && (r + 1) * n * 8 > kCsrSmemBudget) --r;  // odd stride must fit (csr_stride)
   return int(r);  // 0 => rows gathered from global memory
 }
