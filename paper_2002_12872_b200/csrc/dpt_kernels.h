@@ -36,6 +36,9 @@ struct DevSell {
   const int32_t* lane_len;  // [nslices * 32]
   const int64_t* pos_of;    // [n] lane index of row j
   int64_t nslices;
+  const int32_t* perm;      // [n] shared-memory position of column k (bank balance), null = identity
+  const int32_t* inv;       // [npad] column at position p (-1 = unused), null = identity
+  int64_t npad;             // staged row length in positions (>= n)
 };
 int csr_step_ntiles(int64_t rows, int64_t n);
 int csr_ntn(int64_t n);
@@ -101,11 +104,17 @@ cudaError_t launch_scan(const ScanArgs& a, int warps_total, cudaStream_t st);
 cudaError_t launch_sell_perm(const int64_t* rp, int64_t n, int32_t* lane_col, int32_t* lane_len, int64_t* pos_of,
                              cudaStream_t st);
 cudaError_t launch_sell_widths(const int64_t* rp, const int32_t* cl, int64_t nslices, const int32_t* lane_col, int G,
-                               int sched, int64_t* widths, cudaStream_t st);
+                               int sched, const int32_t* perm, int64_t* widths, cudaStream_t st);
 cudaError_t launch_sell_scan(int64_t* widths, int64_t nslices, int64_t* total, cudaStream_t st);
 cudaError_t launch_sell_fill(const int64_t* rp, const int32_t* cl, const double* vl, int cx, int64_t nslices,
-                             const int32_t* lane_col, int G, int sched, const int64_t* off, int32_t* s_cols,
-                             double* s_vals, cudaStream_t st);
+                             const int32_t* lane_col, int G, int sched, const int32_t* perm, const int64_t* off,
+                             int32_t* s_cols, double* s_vals, cudaStream_t st);
+// column relabelling for bank balance (real K2): pos / inv permutation, padded staged-row length
+size_t relabel_smem_bytes(int64_t nslices);
+cudaError_t launch_relabel(const int64_t* rp, const int32_t* cl, int64_t n, int64_t nnz, int64_t nslices,
+                           const int64_t* slot_of, int cap, int passes, int32_t* scratch, int32_t* bank, int32_t* pos,
+                           int32_t* inv, int64_t npad_alloc, int32_t* npad_out, cudaStream_t st);
+int csr_staged_cols_max(int64_t n);  // longest staged row (positions) keeping K2's natural R; 0 = global gathers
 // levels.cu: device-side setup scans (dominant selection, gap-row degeneracy, uniform CSR)
 cudaError_t launch_levels_scan(const double* d, int64_t n, int cx, double* scratch, unsigned* counter, double* out,
                                cudaStream_t st);

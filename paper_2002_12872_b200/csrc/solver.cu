@@ -418,11 +418,13 @@ struct DevProblem {
   int big = 1;  // dense tile configuration (dense_cfg_for)
   int uniform16 = 0;  // CSR with exactly 16 nonzeros per row (K3 fast path)
   DBuf s_cols, s_vals, s_off, s_lcol, s_llen, s_pos;  // SELL-32 image (K2)
-  int64_t nslices = 0;
+  DBuf s_perm, s_inv;                                 // column relabelling (bank balance), empty = identity
+  int64_t nslices = 0, s_npad = 0;
   DevCsr csr() const { return DevCsr{rowptr.as<int64_t>(), cols.as<int32_t>(), vals.as<double>(), nnz}; }
   DevSell sell() const {
     return DevSell{s_cols.as<int32_t>(), s_vals.as<double>(), s_off.as<int64_t>(), s_lcol.as<int32_t>(),
-                   s_llen.as<int32_t>(), s_pos.as<int64_t>(), nslices};
+                   s_llen.as<int32_t>(), s_pos.as<int64_t>(), nslices, s_perm.as<int32_t>(), s_inv.as<int32_t>(),
+                   s_npad};
   }
 };
 
@@ -434,7 +436,8 @@ void build_sell_device(DevProblem& dp, cudaStream_t st, dpt_error_info* err) {
   const int cx = dp.cplx ? 2 : 1;
   const int G = dp.cplx ? 8 : 16;
   const char* sched_env = std::getenv("DPT_SELL_SCHED");
-  const int sched = (sched_env && sched_env[0] == '0') ? 0 : 1;
+  // 2: free-order bank schedule (default); 1: CSR-order bank schedule; 0: dense packing
+  const int sched = (sched_env && sched_env[0] >= '0' && sched_env[0] <= '2') ? sched_env[0] - '0' : 2;
   dalloc(dp.s_lcol, size_t(ns * 32) * 4, err);
   dalloc(dp.s_llen, size_t(ns * 32) * 4, err);
   dalloc(dp.s_pos, size_t(n) * 8 + 8, err);
@@ -443,21 +446,47 @@ void build_sell_device(DevProblem& dp, cudaStream_t st, dpt_error_info* err) {
   CK(cudaMemsetAsync(dp.s_llen.p, 0, size_t(ns * 32) * 4, st));
   CK(launch_sell_perm(dp.rowptr.as<int64_t>(), n, dp.s_lcol.as<int32_t>(), dp.s_llen.as<int32_t>(),
                       dp.s_pos.as<int64_t>(), st));
-  CK(launch_sell_widths(dp.rowptr.as<int64_t>(), dp.cols.as<int32_t>(), ns, dp.s_lcol.as<int32_t>(), G, sched,
-                        dp.s_off.as<int64_t>(), st));
+  // Real problems whose rows are staged in shared memory get their columns
+  // relabelled for bank balance (sell_build.cu, relabel_kernel); the staged
+  // row then has npad >= n positions, at most what keeps K2's natural R.
   DBuf tot;
   dalloc(tot, 16, err);
+  const int64_t per_bank = (n + 15) / 16;
+  const int64_t cap = std::min<int64_t>(per_bank + 16, csr_staged_cols_max(n) / 16);
+  const char* rl_env = std::getenv("DPT_SELL_RELABEL");
+  const bool relabel = !dp.cplx && sched == 2 && n >= 64 && cap >= per_bank && !(rl_env && rl_env[0] == '0') &&
+                       relabel_smem_bytes(ns) <= size_t(200 * 1024);
+  dp.s_npad = n;
+  DBuf scratch, bankb;  // released after the synchronize below
+  if (relabel) {
+    dalloc(scratch, size_t(3 * n + 1 + dp.nnz) * 4, err);
+    dalloc(bankb, size_t(n) * 4, err);
+    dalloc(dp.s_perm, size_t(n) * 4, err);
+    dalloc(dp.s_inv, size_t(16 * cap) * 4, err);
+    CK(launch_relabel(dp.rowptr.as<int64_t>(), dp.cols.as<int32_t>(), n, dp.nnz, ns, dp.s_pos.as<int64_t>(), int(cap),
+                      3, scratch.as<int32_t>(), bankb.as<int32_t>(), dp.s_perm.as<int32_t>(), dp.s_inv.as<int32_t>(),
+                      16 * cap, tot.as<int32_t>() + 2, st));
+  }
+  CK(launch_sell_widths(dp.rowptr.as<int64_t>(), dp.cols.as<int32_t>(), ns, dp.s_lcol.as<int32_t>(), G, sched,
+                        dp.s_perm.as<int32_t>(), dp.s_off.as<int64_t>(), st));
   CK(launch_sell_scan(dp.s_off.as<int64_t>(), ns, tot.as<int64_t>(), st));
   int64_t total = 0;
+  int32_t npad = 0;
   CK(cudaMemcpyAsync(&total, tot.p, 8, cudaMemcpyDeviceToHost, st));
+  if (relabel) CK(cudaMemcpyAsync(&npad, tot.as<int32_t>() + 2, 4, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  if (relabel) dp.s_npad = std::max<int64_t>(npad, n);
+  if (std::getenv("DPT_SELL_DEBUG"))
+    std::fprintf(stderr, "[dpt] SELL image: n=%lld slices=%lld steps=%lld sched=%d relabel=%d npad=%lld\n",
+                 (long long)n, (long long)ns, (long long)(total / 32), sched, int(relabel), (long long)dp.s_npad);
   const int64_t alloc = std::max<int64_t>(total, 1);
   dalloc(dp.s_cols, size_t(alloc) * 4, err);
   dalloc(dp.s_vals, size_t(cx * alloc) * 8, err);
   CK(cudaMemsetAsync(dp.s_cols.p, 0xff, size_t(alloc) * 4, st));
   CK(cudaMemsetAsync(dp.s_vals.p, 0, size_t(cx * alloc) * 8, st));
   CK(launch_sell_fill(dp.rowptr.as<int64_t>(), dp.cols.as<int32_t>(), dp.vals.as<double>(), cx, ns,
-                      dp.s_lcol.as<int32_t>(), G, sched, dp.s_off.as<int64_t>(), dp.s_cols.as<int32_t>(),
+                      dp.s_lcol.as<int32_t>(), G, sched, dp.s_perm.as<int32_t>(), dp.s_off.as<int64_t>(),
+                      dp.s_cols.as<int32_t>(),
                       dp.s_vals.as<double>(), st));
   dp.nslices = ns;
 }

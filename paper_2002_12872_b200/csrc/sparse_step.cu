@@ -30,15 +30,31 @@ namespace dpt {
 constexpr int kCsrThreads = 1024;
 constexpr int kCsrSmemBudget = 200 * 1024;
 
-static int csr_rows_per_cta(int64_t n) {
+constexpr int csr_stride(int R) { return (R & 1) ? R : R + 1; }
+
+// Rows of A staged per CTA from the shared-memory budget (0 = rows too long:
+// gathers from global memory).  Independent of DPT_CSR_ROWS, so the SELL image
+// (and with it every accumulation order) is the same for every staging variant.
+static int csr_rows_natural(int64_t n) {
   int64_t r = kCsrSmemBudget / (n * 8);
   if (r > 8) r = 8;
+  if (r >= 2 && (r & 1) == 0 && (r + 1) * n * 8 > kCsrSmemBudget) --r;  // odd stride must fit (csr_stride)
+  return int(r);
+}
+
+static int csr_rows_per_cta(int64_t n) {
+  int r = csr_rows_natural(n);
   if (const char* e = getenv("DPT_CSR_ROWS")) {  // tests: force fewer staged rows (0 = global gathers)
-    const int64_t f = atoi(e);
+    const int f = atoi(e);
     if (f >= 0 && f < r) r = f;
   }
-  if (r >= 2 && (r & 1) == 0 && (r + 1) * n * 8 > kCsrSmemBudget) --r;  // odd stride must fit (csr_stride)
-  return int(r);  // 0 => rows gathered from global memory
+  if (r >= 2 && (r & 1) == 0 && (r + 1) * n * 8 > kCsrSmemBudget) --r;
+  return r;
+}
+
+int csr_staged_cols_max(int64_t n) {
+  const int r = csr_rows_natural(n);
+  return r > 0 ? int(kCsrSmemBudget / (8 * csr_stride(r))) : 0;
 }
 
 int csr_ntn(int64_t) { return 1; }
@@ -66,18 +82,17 @@ int csr_step_ntiles(int64_t rows, int64_t n) {
 // (col -1, value 0) load nothing and add fma(0, 0, p) = p exactly (p starts at
 // +0 and a sum never turns into -0), so the FMA chain needs no guard.
 // SMEM = false (rows too long for shared memory) gathers from global instead.
-constexpr int csr_stride(int R) { return (R & 1) ? R : R + 1; }
 constexpr int kCsrU = 4;  // entries in flight per lane; slice widths are padded to a multiple
 
-template <int R, bool SMEM>
-__global__ void __launch_bounds__(kCsrThreads) csr_step_kernel(DevSolve s, DevSell S) {
+template <int R, bool SMEM, int THREADS = kCsrThreads>
+__global__ void __launch_bounds__(THREADS) csr_step_kernel(DevSolve s, DevSell S) {
   constexpr int ST = csr_stride(R);
   if (s.state->done) return;
   const int jl = launch_index(s);
   extern __shared__ __align__(16) double sa[];  // [n][ST] staged rows of A_{j-1}
   __shared__ unsigned long long next_slice;
-  __shared__ double red[kCsrThreads / 32][R][2];
-  __shared__ double wred[kCsrThreads / 32][3];
+  __shared__ double red[THREADS / 32][R][2];
+  __shared__ double wred[THREADS / 32][3];
   const int64_t n = s.n, ld = s.ld, rows = s.rows;
   const int64_t il0 = int64_t(blockIdx.x) * R;
   const int nr = int(rows - il0 < R ? rows - il0 : R);
@@ -89,25 +104,35 @@ __global__ void __launch_bounds__(kCsrThreads) csr_step_kernel(DevSolve s, DevSe
   const double* __restrict__ ain = a_in + size_t(il0) * size_t(ld);  // SMEM = false: row r at ain + r * ld
 
   if (threadIdx.x == 0) next_slice = 0ull;
+  // Staged rows are indexed by POSITION: the image's columns are positions
+  // (S.perm[k] when the columns were relabelled for bank balance, else k).
+  const int32_t* __restrict__ perm = S.perm;
+  const int32_t* __restrict__ inv = S.inv;
   if constexpr (SMEM) {
     for (int r = 0; r < nr; ++r)
-      for (int64_t c = threadIdx.x; c < n; c += blockDim.x) sa[size_t(c) * ST + r] = ain[size_t(r) * size_t(ld) + size_t(c)];
+      for (int64_t c = threadIdx.x; c < n; c += blockDim.x) {
+        const int64_t p = perm ? int64_t(__ldg(perm + c)) : c;
+        sa[size_t(p) * ST + r] = ain[size_t(r) * size_t(ld) + size_t(c)];
+      }
   }
   __syncthreads();
-  auto A = [&](int r, int64_t c) -> double {
-    if constexpr (SMEM) return sa[size_t(c) * ST + r];
-    else return ain[size_t(r < nr ? r : 0) * size_t(ld) + size_t(c)];
+  auto A = [&](int r, int64_t p) -> double {  // element at position p of staged row r
+    if constexpr (SMEM) return sa[size_t(p) * ST + r];
+    else return ain[size_t(r < nr ? r : 0) * size_t(ld) + size_t(inv ? int64_t(__ldg(inv + p)) : p)];
   };
-  double ti[R], di[R], epsi[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int rr = r < nr ? r : 0;
-    ti[r] = s.theta[s.row0 + il0 + rr];
-    di[r] = d_in[il0 + rr];
-    epsi[r] = __dadd_rn(ti[r], __dmul_rn(lam, di[r]));
+  // per-row constants of the staged rows live in shared memory (registers go
+  // to the image prefetch below)
+  __shared__ double rowc[3][R];  // theta_i, d_{j-1}(i), eps_i
+  if (threadIdx.x < R) {
+    const int rr = int(threadIdx.x) < nr ? int(threadIdx.x) : 0;
+    const double ti = s.theta[s.row0 + il0 + rr], di = d_in[il0 + rr];
+    rowc[0][threadIdx.x] = ti;
+    rowc[1][threadIdx.x] = di;
+    rowc[2][threadIdx.x] = __dadd_rn(ti, __dmul_rn(lam, di));
   }
+  __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  constexpr int NW = kCsrThreads / 32;
+  constexpr int NW = THREADS / 32;
   double num[R], den[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) num[r] = den[r] = 0.0;
@@ -151,23 +176,24 @@ __global__ void __launch_bounds__(kCsrThreads) csr_step_kernel(DevSolve s, DevSe
     }
     if (j >= 0) {
       const double tj = s.theta[j];
+      const int64_t pj = perm ? int64_t(__ldg(perm + j)) : j;  // position of column j
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         if (r >= nr) break;
         const int64_t gi = s.row0 + il0 + r;
-        const double aij = A(r, j);
+        const double aij = A(r, pj);
         double val;
         if (gi == j) {
           val = 1.0;
         } else {
-          const double gg = s.gapmat ? s.gapmat[size_t(il0 + r) * size_t(ld) + size_t(j)] : 1.0 / __dsub_rn(ti[r], tj);
-          val = __dmul_rn(__dmul_rn(lam_k, gg), __dsub_rn(p[r], __dmul_rn(di[r], aij)));
+          const double gg = s.gapmat ? s.gapmat[size_t(il0 + r) * size_t(ld) + size_t(j)] : 1.0 / __dsub_rn(rowc[0][r], tj);
+          val = __dmul_rn(__dmul_rn(lam_k, gg), __dsub_rn(p[r], __dmul_rn(rowc[1][r], aij)));
         }
         a_out[size_t(il0 + r) * size_t(ld) + size_t(j)] = val;
         t_step = fmax(t_step, fabs(__dsub_rn(val, aij)));
         t_max = fmax(t_max, fabs(val));
         t_nonfin += isfinite(val) ? 0.0 : 1.0;
-        const double rr = __dadd_rn(__dmul_rn(__dsub_rn(tj, epsi[r]), aij), __dmul_rn(lam, p[r]));
+        const double rr = __dadd_rn(__dmul_rn(__dsub_rn(tj, rowc[2][r]), aij), __dmul_rn(lam, p[r]));
         num[r] = fmax(num[r], fabs(rr));
         den[r] = fmax(den[r], fabs(aij));
       }
@@ -205,7 +231,7 @@ __global__ void __launch_bounds__(kCsrThreads) csr_step_kernel(DevSolve s, DevSe
     for (int32_t q = lane; q < width; q += 32) {
       const int64_t idx = off + int64_t(q) * 32 + L;
       const int32_t c = __ldg(S.cols + idx);
-      if (c >= 0) part = __fma_rn(__ldg(S.vals + idx), arow_new[c], part);
+      if (c >= 0) part = __fma_rn(__ldg(S.vals + idx), arow_new[inv ? __ldg(inv + c) : c], part);
     }
     part = warp_sum(part);
     if (lane == 0) {
@@ -239,7 +265,7 @@ cudaError_t launch_csr_step(const DevSolve& s, const DevSell& d, cudaStream_t st
   const int use_smem = Rs > 0 ? 1 : 0;
   const int R = use_smem ? Rs : 1;
   const unsigned grid = unsigned((s.rows + R - 1) / R);
-  const size_t smem = use_smem ? size_t(csr_stride(R)) * size_t(s.n) * 8 : 0;
+  const size_t smem = use_smem ? size_t(csr_stride(R)) * size_t(d.npad > s.n ? d.npad : s.n) * 8 : 0;
   if (!use_smem) {
     csr_step_kernel<1, false><<<grid, kCsrThreads, 0, st>>>(s, d);
     return cudaGetLastError();
