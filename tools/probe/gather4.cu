@@ -11,6 +11,55 @@
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
 
+template <int M>
+__device__ __forceinline__ double ldz(const double* p) {
+  double v;
+  if constexpr (M == 0) v = __ldg(p);
+  else if constexpr (M == 1) asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  else if constexpr (M == 2) asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  else v = *p;
+  return v;
+}
+template <int M>
+__global__ void ldg_mode(const int* __restrict__ idx, const double* __restrict__ z, double* out, int64_t rows) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t r = t; r < rows; r += stride) {
+    const int4* ip = reinterpret_cast<const int4*>(idx + r * 16);
+    int c[16];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      int4 v = __ldg(ip + q);
+      c[4 * q] = v.x; c[4 * q + 1] = v.y; c[4 * q + 2] = v.z; c[4 * q + 3] = v.w;
+    }
+    double g[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) g[q] = ldz<M>(z + c[q]);
+    double acc = 0;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) acc += g[q];
+    out[r] = acc;
+  }
+}
+template <int M>
+void run_mode(const int* idx, const double* z, double* out, int64_t rows, const char* name) {
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  for (int bps : {4, 8}) {
+    int blocks = 148 * bps;
+    float ms;
+    ldg_mode<M><<<blocks, 256>>>(idx, z, out, rows);
+    cudaEventRecord(e0);
+    for (int r = 0; r < 10; ++r) ldg_mode<M><<<blocks, 256>>>(idx, z, out, rows);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&ms, e0, e1);
+    ms /= 10;
+    printf("%-26s blocks/SM %d: %.1f us  %.1f Ggather/s\n", name, bps, ms * 1e3, rows * 16 / ms / 1e6);
+  }
+}
+
 __global__ void ldg_gather(const int* __restrict__ idx, const double* __restrict__ z, double* out, int64_t rows) {
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -117,6 +166,11 @@ int main() {
     ms /= 10;
     printf("ldg  gather blocks/SM %d: %.1f us  %.1f Ggather/s\n", bps, ms * 1e3, nnz / ms / 1e6);
   }
+  run_mode<0>(idx, z, out, rows, "ldg (nc)");
+  run_mode<1>(idx, z, out, rows, "ld.global.cg");
+  run_mode<2>(idx, z, out, rows, "ld.nc.L1::no_allocate");
+  run_mode<3>(idx, z, out, rows, "ld (generic)");
+  if (getenv("NO_TMA")) return 0;
   void* fp = nullptr;
   cudaDriverEntryPointQueryResult q;
   cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fp, cudaEnableDefault, &q);
