@@ -144,31 +144,57 @@ __global__ void __launch_bounds__(kFoldThreads) fold_kernel(DevSolve s, int ntil
     bp[1] = a1;
     bp[2] = a2;
     bp[3] = rmax;
-    fence_acq_rel_gpu();
-    const unsigned prev = atomicAdd(s.counter, 1u);
-    last = (prev == gridDim.x - 1);
+    if (gridDim.x == 1) {
+      last = true;  // nothing to elect (the row map's fold is one block)
+    } else {
+      fence_acq_rel_gpu();
+      const unsigned prev = atomicAdd(s.counter, 1u);
+      last = (prev == gridDim.x - 1);
+    }
   }
   __syncthreads();
   if (!last) return;
   __shared__ dpt_sm_state dec;  // the decided state, for the precheck
-  if (threadIdx.x == 0) {
-    fence_acq_rel_gpu();
-    double r[4] = {0.0, 0.0, 0.0, 0.0};
-    if (gridDim.x == 1) {
-      r[0] = a0;  // this block's own maxima (already complete)
-      r[1] = a1;
-      r[2] = a2;
-      r[3] = rmax;
-    } else {
-      for (unsigned b = 0; b < gridDim.x; ++b) {  // __ldcg: L2, where the other blocks' stores landed
-        const double2 p01 = __ldcg(reinterpret_cast<const double2*>(s.blockpart + size_t(b) * 8));
-        const double2 p23 = __ldcg(reinterpret_cast<const double2*>(s.blockpart + size_t(b) * 8 + 2));
-        r[0] = fmax(r[0], p01.x);
-        r[1] = fmax(r[1], p01.y);
-        r[2] += p23.x;
-        r[3] = fmax(r[3], p23.y);
+  // The elected block folds the per-block maxima with all its threads (a
+  // single-thread loop over ~300 blocks was a chain of L2 round trips: c2's
+  // fold took 32 us).  Max is order-free and the nonfinite count is an exact
+  // integer sum, so the result does not depend on the reduction shape.
+  double r[4] = {a0, a1, a2, rmax};  // thread 0: this block's own maxima
+  if (gridDim.x > 1) {
+    if (threadIdx.x == 0) fence_acq_rel_gpu();  // acquire the other blocks' partials
+    __syncthreads();
+    r[0] = r[1] = r[2] = r[3] = 0.0;
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) {  // __ldcg: L2, where they landed
+      const double2 p01 = __ldcg(reinterpret_cast<const double2*>(s.blockpart + size_t(b) * 8));
+      const double2 p23 = __ldcg(reinterpret_cast<const double2*>(s.blockpart + size_t(b) * 8 + 2));
+      r[0] = fmax(r[0], p01.x);
+      r[1] = fmax(r[1], p01.y);
+      r[2] += p23.x;
+      r[3] = fmax(r[3], p23.y);
+    }
+    __shared__ double red5[kFoldThreads / 32][4];
+    r[0] = warp_max(r[0]);
+    r[1] = warp_max(r[1]);
+    r[2] = warp_sum(r[2]);
+    r[3] = warp_max(r[3]);
+    if (lane == 0) {
+      red5[threadIdx.x >> 5][0] = r[0];
+      red5[threadIdx.x >> 5][1] = r[1];
+      red5[threadIdx.x >> 5][2] = r[2];
+      red5[threadIdx.x >> 5][3] = r[3];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      r[0] = r[1] = r[2] = r[3] = 0.0;
+      for (int w = 0; w < int(blockDim.x >> 5); ++w) {
+        r[0] = fmax(r[0], red5[w][0]);
+        r[1] = fmax(r[1], red5[w][1]);
+        r[2] += red5[w][2];
+        r[3] = fmax(r[3], red5[w][3]);
       }
     }
+  }
+  if (threadIdx.x == 0) {
     s.stats[0] = r[0];
     s.stats[1] = r[1];
     s.stats[2] = r[2];
