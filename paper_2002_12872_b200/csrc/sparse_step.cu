@@ -315,6 +315,114 @@ struct RowGroup {
   static constexpr int G = MODE == 0 ? 4 : (MODE == 1 ? 1 : 32);
 };
 
+__device__ __forceinline__ bool gemv_vec_ok(const double* dense, const double* z, int64_t ld) {
+  return ((ld & 1) == 0) && ((reinterpret_cast<uintptr_t>(dense) | reinterpret_cast<uintptr_t>(z)) & 15) == 0;
+}
+
+// w[row] for the dense row map, by the whole block: warp q sums columns
+// [q n / NW, (q + 1) n / NW) (even boundaries), the warps' sums are added in
+// warp order -- one fixed order, the same in every block.  The warp that owns
+// row m = row uses this value too, so w[row] is bit-identical everywhere.
+template <int NW>
+__device__ __forceinline__ double gemv_block_dot(const double* __restrict__ dense, int64_t n, int64_t ld, int64_t row,
+                                                 const double* __restrict__ z, double* sh) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double* dr = dense + size_t(row) * size_t(ld);
+  double w = 0.0;
+  if (gemv_vec_ok(dense, z, ld)) {
+    const int64_t n2 = n >> 1;
+    const int64_t c0 = n2 * warp / NW, c1 = n2 * (warp + 1) / NW;
+    const double2* d2 = reinterpret_cast<const double2*>(dr);
+    const double2* z2 = reinterpret_cast<const double2*>(z);
+    double a0 = 0.0, a1 = 0.0;
+    for (int64_t c = c0 + lane; c < c1; c += 32) {
+      const double2 x = __ldg(d2 + c), y = z2[c];
+      a0 = __fma_rn(x.x, y.x, a0);
+      a1 = __fma_rn(x.y, y.y, a1);
+    }
+    if ((n & 1) && warp == NW - 1 && lane == 0) a0 = __fma_rn(dr[n - 1], z[n - 1], a0);
+    w = a0 + a1;
+  } else {
+    const int64_t c0 = n * warp / NW, c1 = n * (warp + 1) / NW;
+    for (int64_t c = c0 + lane; c < c1; c += 32) w = __fma_rn(dr[c], z[c], w);
+  }
+  w = warp_sum(w);
+  if (lane == 0) sh[warp] = w;
+  __syncthreads();
+  double t = 0.0;
+#pragma unroll
+  for (int q = 0; q < NW; ++q) t += sh[q];
+  return t;
+}
+
+// Rows per warp of the dense row map (measured, tools/gemv_time.py): one row
+// per warp keeps z in L1 only for small n; from n = 4096 two rows share each z
+// load, from 16384 four.
+constexpr int64_t kGemvRpw2 = 4096;
+constexpr int64_t kGemvRpw4 = 16384;
+// RPW rows per warp (dense row map, n large): rows m .. m+RPW-1 stream
+// together, 16-byte loads, four columns-chunks per lane in flight per row; per
+// row two accumulators (even / odd columns), one fixed order.  The row m = row
+// takes the block's w[row] (bit-identical to every block's).
+template <int RPW, class F>
+__device__ __forceinline__ void gemv_rows_loop(const double* __restrict__ dense, int64_t n, int64_t ld, int64_t row,
+                                               double wr, const double* __restrict__ z, int lane, F& finish_row) {
+  const int64_t nwarps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  const int64_t wid = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t n2 = n >> 1;
+  const double2* z2 = reinterpret_cast<const double2*>(z);
+  for (int64_t m0 = wid * RPW; m0 < n; m0 += nwarps * RPW) {
+    const double2* d2[RPW];
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) {
+      const int64_t m = m0 + r < n ? m0 + r : n - 1;
+      d2[r] = reinterpret_cast<const double2*>(dense + size_t(m) * size_t(ld));
+    }
+    double a0[RPW], a1[RPW];
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) a0[r] = a1[r] = 0.0;
+    int64_t c = lane;
+    for (; c + 96 < n2; c += 128) {
+      double2 y[4], x[RPW][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) y[u] = z2[c + 32 * u];
+#pragma unroll
+      for (int r = 0; r < RPW; ++r)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) x[r][u] = __ldg(d2[r] + c + 32 * u);
+#pragma unroll
+      for (int r = 0; r < RPW; ++r)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          a0[r] = __fma_rn(x[r][u].x, y[u].x, a0[r]);
+          a1[r] = __fma_rn(x[r][u].y, y[u].y, a1[r]);
+        }
+    }
+    for (; c < n2; c += 32) {
+      const double2 y = z2[c];
+#pragma unroll
+      for (int r = 0; r < RPW; ++r) {
+        const double2 x = __ldg(d2[r] + c);
+        a0[r] = __fma_rn(x.x, y.x, a0[r]);
+        a1[r] = __fma_rn(x.y, y.y, a1[r]);
+      }
+    }
+    if ((n & 1) && lane == 0) {
+#pragma unroll
+      for (int r = 0; r < RPW; ++r)
+        a0[r] = __fma_rn(reinterpret_cast<const double*>(d2[r])[n - 1], z[n - 1], a0[r]);
+    }
+    double w[RPW];
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) w[r] = warp_sum(a0[r] + a1[r]);
+    if (lane == 0) {
+#pragma unroll
+      for (int r = 0; r < RPW; ++r)
+        if (m0 + r < n) finish_row(m0 + r, m0 + r == row ? wr : w[r]);
+    }
+  }
+}
+
 template <int MODE>
 __device__ __forceinline__ double group_row_dot(const DevCsr& D, const double* __restrict__ dense, int64_t n,
                                                 int64_t ld, int64_t m, const double* __restrict__ z, int sub) {
@@ -334,8 +442,37 @@ __device__ __forceinline__ double group_row_dot(const DevCsr& D, const double* _
     const int64_t pb = D.rowptr[m], pe = D.rowptr[m + 1];
     for (int64_t q = pb; q < pe; ++q) w = __fma_rn(__ldg(D.vals + q), z[__ldg(D.cols + q)], w);
   } else {
+    // GEMV row: HBM-bound stream of Delta's row.  16-byte loads, eight per
+    // lane in flight, two accumulators (even / odd columns) -- a fixed order.
     const double* dr = dense + size_t(m) * size_t(ld);
-    for (int64_t c = sub; c < n; c += 32) w = __fma_rn(dr[c], z[c], w);
+    if (gemv_vec_ok(dense, z, ld)) {
+      const double2* d2 = reinterpret_cast<const double2*>(dr);
+      const double2* z2 = reinterpret_cast<const double2*>(z);
+      const int64_t n2 = n >> 1;
+      double a0 = 0.0, a1 = 0.0;
+      int64_t c = sub;
+      for (; c + 224 < n2; c += 256) {
+        double2 x[8], y[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x[u] = __ldg(d2 + c + 32 * u);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) y[u] = z2[c + 32 * u];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          a0 = __fma_rn(x[u].x, y[u].x, a0);
+          a1 = __fma_rn(x[u].y, y[u].y, a1);
+        }
+      }
+      for (; c < n2; c += 32) {
+        const double2 x = __ldg(d2 + c), y = z2[c];
+        a0 = __fma_rn(x.x, y.x, a0);
+        a1 = __fma_rn(x.y, y.y, a1);
+      }
+      if ((n & 1) && sub == 0) a0 = __fma_rn(dr[n - 1], z[n - 1], a0);
+      w = a0 + a1;
+    } else {
+      for (int64_t c = sub; c < n; c += 32) w = __fma_rn(dr[c], z[c], w);
+    }
     w = warp_sum(w);
   }
   return w;
@@ -356,7 +493,14 @@ __global__ void __launch_bounds__(kSingleThreads)
   const double lam_k = lam_of(s, jl), lam = s.lambda;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int sub = threadIdx.x % G;
-  if (warp == 0) {  // one code path for the whole warp (the group shuffles name all lanes)
+  if constexpr (MODE == 2) {  // the whole block streams row `row` once
+    __shared__ double wsh[kSingleThreads / 32];
+    const double wr = gemv_block_dot<kSingleThreads / 32>(dense, n, ld, row, z, wsh);
+    if (threadIdx.x == 0) {
+      wrow_s = wr;
+      if (blockIdx.x == 0) s.dvec[(jl - 1) & 1][0] = wr;  // w[row] of z_{j-1} for the fold's eps
+    }
+  } else if (warp == 0) {  // one code path for the whole warp (the group shuffles name all lanes)
     const double wr = (MODE == 1 && lane != 0) ? 0.0 : group_row_dot<MODE>(D, dense, n, ld, row, z, sub);
     if (lane == 0) {
       wrow_s = wr;
@@ -432,6 +576,14 @@ __global__ void __launch_bounds__(kSingleThreads)
           if (mm[u] < n) finish_row(mm[u], w[u]);
       }
     }
+  } else if (MODE == 2 && gemv_vec_ok(dense, z, ld) && n >= kGemvRpw2) {
+    // Dense Delta, large n: each warp streams RPW consecutive rows at once, so
+    // every z load (from L2 once z outgrows L1) serves RPW rows -- with one row
+    // per warp, z's re-reads matched Delta's own traffic (n^2 doubles each).
+    if (n >= kGemvRpw4)
+      gemv_rows_loop<4>(dense, n, ld, row, wr, z, lane, finish_row);
+    else
+      gemv_rows_loop<2>(dense, n, ld, row, wr, z, lane, finish_row);
   } else {
     constexpr int U = 2;
     for (int64_t m0 = int64_t(blockIdx.x) * ROWS_PER_ITER; m0 < n; m0 += U * stride) {
@@ -440,7 +592,7 @@ __global__ void __launch_bounds__(kSingleThreads)
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         mm[u] = m0 + u * stride + threadIdx.x / G;
-        w[u] = group_row_dot<MODE>(D, dense, n, ld, mm[u] < n ? mm[u] : n - 1, z, sub);
+        w[u] = (MODE == 2 && mm[u] == row) ? wr : group_row_dot<MODE>(D, dense, n, ld, mm[u] < n ? mm[u] : n - 1, z, sub);
       }
       if (sub == 0) {
 #pragma unroll

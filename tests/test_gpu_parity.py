@@ -229,6 +229,24 @@ def test_single_dense_vs_oracle():
         assert np.max(np.abs(g.z - r.z)) < VEC_ATOL
 
 
+@pytest.mark.parametrize("n", [4097, 4608, 16400])
+def test_single_dense_gemv_rows_per_warp_vs_oracle(n):
+    # dense row map at the sizes where each warp streams 2 (n >= 4096) or 4
+    # (n >= 16384) rows at once; odd n takes the scalar tail column
+    d = pr.theta_linear(n, 1.0 / n)
+    delta = np.random.default_rng(n).standard_normal((n, n))
+    np.fill_diagonal(delta, 0.0)
+    p = PartitionedProblem(d, delta, 0.5 / math.sqrt(n))
+    o = dict(tol=1e-12, max_iter=60)
+    for row in (n - 1, n // 3):
+        g = P.iterate_single(p, row, _o(o))
+        r = O.iterate_single(p, row, o)
+        assert int(g.status) == r.status and abs(g.iterations - r.iterations) <= 1, (row, g.status, r.status)
+        if int(r.status) != 2:
+            assert np.max(np.abs(g.z - r.z)) < VEC_ATOL
+            assert abs(g.eigenvalue - r.eigenvalue) <= EIG_RTOL * max(1.0, abs(r.eigenvalue))
+
+
 # --------------------------------------------- full BASELINE sizes ----
 def _row_sample_check(p, plan_rows, lam, k_rows, a_prev):
     want = O.step_rows(p, 0, a_prev[:k_rows], lam)
