@@ -1,3 +1,4 @@
+// (index loads coalesced across the warp: element q of thread t at idx[q NT + t])
 // Random FP64 gathers from distributed shared memory (a z-block spread over a
 // thread-block cluster) vs from L2.  Question for K3 (c4: 16.7 M random
 // gathers of an 8 MB vector per step): can a cluster-resident z block serve
@@ -23,12 +24,13 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(512, 1)
   cl.sync();
   const uint32_t base = uint32_t(__cvta_generic_to_shared(zs));
   const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  const uint32_t* my = idx + t * per_thread;
+  const int64_t NT = int64_t(gridDim.x) * blockDim.x;
+  const uint32_t* my = idx + t;
   double acc = 0.0;
   for (int64_t q = 0; q < per_thread; q += 16) {
     uint32_t c[16];
 #pragma unroll
-    for (int u = 0; u < 16; ++u) c[u] = __ldg(my + q + u);
+    for (int u = 0; u < 16; ++u) c[u] = __ldg(my + (q + u) * NT);
     double g[16];
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
@@ -47,12 +49,13 @@ __global__ void __cluster_dims__(CS, 1, 1) __launch_bounds__(512, 1)
 __global__ void __launch_bounds__(512, 1) l2_gather(const double* __restrict__ z, const uint32_t* __restrict__ idx,
                                                     int64_t per_thread, double* out) {
   const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  const uint32_t* my = idx + t * per_thread;
+  const int64_t NT = int64_t(gridDim.x) * blockDim.x;
+  const uint32_t* my = idx + t;
   double acc = 0.0;
   for (int64_t q = 0; q < per_thread; q += 16) {
     uint32_t c[16];
 #pragma unroll
-    for (int u = 0; u < 16; ++u) c[u] = __ldg(my + q + u);
+    for (int u = 0; u < 16; ++u) c[u] = __ldg(my + (q + u) * NT);
     double g[16];
 #pragma unroll
     for (int u = 0; u < 16; ++u) g[u] = __ldg(z + c[u]);
@@ -69,12 +72,13 @@ __global__ void __launch_bounds__(512, 1) smem_gather(const double* __restrict__
   for (int i = threadIdx.x; i < kPerCta; i += blockDim.x) zs[i] = zblk[i];
   __syncthreads();
   const int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  const uint32_t* my = idx + t * per_thread;
+  const int64_t NT = int64_t(gridDim.x) * blockDim.x;
+  const uint32_t* my = idx + t;
   double acc = 0.0;
   for (int64_t q = 0; q < per_thread; q += 16) {
     uint32_t c[16];
 #pragma unroll
-    for (int u = 0; u < 16; ++u) c[u] = __ldg(my + q + u) % kPerCta;
+    for (int u = 0; u < 16; ++u) c[u] = __ldg(my + (q + u) * NT) % kPerCta;
     double g[16];
 #pragma unroll
     for (int u = 0; u < 16; ++u) g[u] = zs[c[u]];
