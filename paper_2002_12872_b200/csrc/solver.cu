@@ -1047,8 +1047,21 @@ struct Guard {
 
 // Rank r owns rows [r*per, min(n, (r+1)*per)) of A (the paper's columns).
 void shard_rows(const dpt_ctx* ctx, int64_t n, int64_t* row0, int64_t* rows) {
-  const int64_t per = (n + ctx->world - 1) / ctx->world;
-  *row0 = std::min<int64_t>(n, per * ctx->rank);
+  int rank = ctx->rank, world = ctx->world;
+  // Development knob: DPT_SHARD_EMULATE=r/w gives a communicator-less context
+  // rank r's row shard of a w-way solve, to time and test the per-rank kernels
+  // at sharded shapes on one GPU (its decisions see only the local rows).
+  if (!ctx->comm) {
+    if (const char* e = std::getenv("DPT_SHARD_EMULATE")) {
+      int r = 0, wv = 1;
+      if (std::sscanf(e, "%d/%d", &r, &wv) == 2 && wv > 0 && r >= 0 && r < wv) {
+        rank = r;
+        world = wv;
+      }
+    }
+  }
+  const int64_t per = (n + world - 1) / world;
+  *row0 = std::min<int64_t>(n, per * rank);
   *rows = std::min<int64_t>(n, *row0 + per) - *row0;
 }
 
