@@ -729,12 +729,28 @@ int dense_tile_m(int cfg) { return cfg == 0 ? CfgSmall::BM : (cfg == 1 ? CfgBig:
 // Tile configuration for a problem size: 64x64 below n = 2048 (enough CTAs to
 // fill 148 SMs), otherwise 128x64 with two CTAs per SM (c2 n = 4096: 3.93 ms /
 // 94.3 % of the DMMA peak vs 4.21 ms / 87.8 % for 128x128 with one CTA per SM,
-// whose epilogue leaves the tensor pipe idle).  DPT_DENSE_CFG=1 forces 128x128.
-int dense_cfg_for(int64_t n) {
+// whose epilogue leaves the tensor pipe idle) -- unless the 64x64 tiles put
+// fewer 64x64 units on the busiest SM: a 1024-row shard of n = 4096 (the 4-way
+// sharded c2) has 512 128x64 tiles (4 on some SMs = 8 units) but 1024 64x64
+// tiles (7 units): 1.03 vs 1.15 ms per step (profiles/r01e_shard_times.txt).
+// DPT_DENSE_CFG=0/1/2 forces a configuration.
+int dense_cfg_for(int64_t n, int64_t rows) {
   if (n < 2048) return 0;
-  const char* e = getenv("DPT_DENSE_CFG");
-  const int v = e ? atoi(e) : 2;
-  return (v == 1 || v == 2) ? v : 2;
+  if (const char* e = getenv("DPT_DENSE_CFG")) {
+    const int v = atoi(e);
+    return (v == 0 || v == 1 || v == 2) ? v : 2;
+  }
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  const int64_t cols = (n + 63) / 64;
+  const int64_t t2 = (rows + CfgMid::BM - 1) / CfgMid::BM * cols, t0 = (rows + CfgSmall::BM - 1) / CfgSmall::BM * cols;
+  const int64_t u2 = 2 * ((t2 + sms - 1) / sms), u0 = (t0 + sms - 1) / sms;  // 64x64 units on the busiest SM
+  return u0 < u2 ? 0 : 2;
 }
 
 // Resident CTAs of the stream-K kernel (its persistent grid).

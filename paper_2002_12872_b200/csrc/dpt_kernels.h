@@ -11,7 +11,7 @@ namespace dpt {
 // dense_step.cu (K1)
 int make_tmap_rowmajor(CUtensorMap* out, const double* base, int64_t dim0, int64_t dim1, int64_t ld,
                        int box1);
-int dense_cfg_for(int64_t n);
+int dense_cfg_for(int64_t n, int64_t rows);
 int dense_tile_n(int cfg);
 int dense_tile_m(int cfg);
 int dense_step_ntiles(int64_t rows, int ntn, int cfg);

@@ -647,7 +647,7 @@ void make_work(Work& w, dpt_ctx* ctx, DevProblem& dp, Mode mode, int64_t row0, i
   s.fuse_decide = ctx->comm ? 0 : 1;  // with a communicator the stats are max-allreduced first
   int ntiles_aux = 1;
   if (mode == MODE_DENSE_FULL) {
-    dp.big = dense_cfg_for(dp.n);
+    dp.big = dense_cfg_for(dp.n, rows);
     s.ntn = int((dp.ncol + dense_tile_n(dp.big) - 1) / dense_tile_n(dp.big));
     w.ntiles_step = dense_step_ntiles(rows, s.ntn, dp.big);
     ntiles_aux = dense_init_ntiles(rows, s.ntn, dp.cplx);
