@@ -21,6 +21,7 @@ norm epilogue) + the fold/decision kernels.  Metric unit: iterations / s.
           /root/reference/proj/src) on a bounded row sample, all host threads.
 
 --impl reference times only the reference arm (rank 0; other ranks exit 0).
+--baselines prints the per-config reference-vs-B200 table.
 N > 1 (torchrun): rows of A sharded over ranks (strong scaling of the same
 n = 4096 solve), per-iteration NCCL max-allreduce of the step statistics.
 """
@@ -52,6 +53,10 @@ def parse():
     ap.add_argument("--n", type=int, default=N_DEFAULT, help="override n (testing only)")
     ap.add_argument("--e2e-calls", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--baselines", action="store_true",
+                    help="instead of the bench line: the reference's own CPU solver on every BASELINE config "
+                         "(time to its terminal status, one core) next to the B200 public call, plus the "
+                         "lambda-plane scan and Matrix Market legs (several minutes)")
     return ap.parse_args()
 
 
@@ -215,9 +220,130 @@ def run_reference(args):
     return 0
 
 
+# ------------------------------------------------------ baselines table ----
+def _timed(fn, reps=1):
+    best, out = None, None
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        out = fn()
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    return best, out
+
+
+def run_baselines():
+    """BASELINE.md §3's CPU baseline plan, measured on this box in one run: the
+    reference's own solver (oracle/_ref, one core -- it is single-threaded) to
+    its terminal status on c1 / c3 / c4 / c4b, one c2 iteration via
+    iterate_fixed, against the B200 public call (host arrays in and out; warm,
+    best of 3; and device-resident inputs).  Then the reference's threaded
+    scan_domain vs the batched scan, and its Matrix Market reader vs ours."""
+    if int(os.environ.get("RANK", "0")) != 0:
+        return 0
+    import torch
+    import paper_2002_12872_b200 as P
+    from oracle.bind import Checker, ComplexReference, ReferenceMatrixMarket, available
+    from paper_2002_12872_b200 import problems as pr
+    from paper_2002_12872_b200.dpt import CsrMatrix, IterationOptions, PartitionedProblem, ScanGrid, ScanMode
+    if not available("reference"):
+        print(json.dumps({"baselines": "unavailable", "why": "oracle/_ref not built"}))
+        return 0
+    R = Checker("reference")
+    host = {"cpu": os.cpu_count(), "model": platform_cpu()}
+
+    def dev_problem(p):
+        dv = torch.device("cuda")
+        d = torch.as_tensor(p.d, device=dv)
+        if hasattr(p.delta, "rowptr"):
+            delta = CsrMatrix(len(p.d), torch.as_tensor(p.delta.rowptr, device=dv),
+                              torch.as_tensor(p.delta.cols, device=dv), torch.as_tensor(p.delta.vals, device=dv))
+        else:
+            delta = torch.as_tensor(p.delta, device=dv)
+        return PartitionedProblem(d, delta, p.lam)
+
+    for name in ("c1", "c4", "c4b", "c3"):
+        p, o, desc = pr.config(name)
+        single = name.startswith("c4")
+        if single:
+            tr, r = _timed(lambda: R.dominant_eigenpair(p, o))
+            call = lambda q: P.dominant_eigenpair(q, IterationOptions(**o))  # noqa: E731
+        else:
+            tr, r = _timed(lambda: R.iterate_full(p, o))
+            call = lambda q: P.iterate_full(q, IterationOptions(**o))  # noqa: E731
+        tg, g = _timed(lambda: call(p), reps=3)
+        pd = dev_problem(p)
+        torch.cuda.synchronize()
+        td, gd = _timed(lambda: call(pd), reps=3)
+        print(json.dumps({"config": name, "workload": desc,
+                          "reference": {"status": STATUS_NAMES[r.status], "iterations": r.iterations, "s": tr,
+                                        "cores": 1, "host": host},
+                          "b200": {"status": P.to_string(g.status), "iterations": g.iterations,
+                                   "host_arrays_s": tg, "device_inputs_s": td},
+                          "speedup_host_arrays": tr / tg}), flush=True)
+    # c2: one reference iteration (a full c2 run is ~11 min on one core; it diverges at k = 4).
+    # iterate_fixed(1) only needs P(I) (the reference's matmul skips I's zeros); k = 2 adds the
+    # first full product, so the difference is one iteration.
+    p, o, desc = pr.config("c2")
+    t1, _ = _timed(lambda: R.iterate_fixed(p, 1, p.lam))
+    t2, _ = _timed(lambda: R.iterate_fixed(p, 2, p.lam))
+    tr = t2 - t1
+    plan = P.Plan(p)
+    plan.begin()
+    plan.steps(3)
+    torch.cuda.synchronize()
+    t_step = plan.steps(20, time_kernel=True) / 20 * 1e-3
+    plan.close()
+    print(json.dumps({"config": "c2", "workload": desc + "; one iteration (reference: iterate_fixed k = 2 minus k = 1)",
+                      "reference": {"s_per_iteration": tr, "cores": 1, "host": host},
+                      "b200": {"s_per_iteration_kernel": t_step}, "speedup": tr / t_step}), flush=True)
+    # lambda-plane scans (row f4): the reference's scan_domain on all host threads vs the batched kernel
+    C = ComplexReference()
+    threads = os.cpu_count() or 1
+    cases = [("two_by_two", pr.two_by_two(1.0), "Full", 0, (-1.2, 1.2, -1.0, 1.0)),
+             ("random_uniform n=16", PartitionedProblem(*pr.random_uniform(16, 3), 0.0), "Full", 0,
+              (-0.2, 0.2, -0.2, 0.2)),
+             ("oscillator n=64 row", PartitionedProblem(*pr.oscillator(64), 0.0), "SingleRow", 63, (0.0, 0.8, -0.3, 0.3))]
+    for name, p, mode, row, g in cases:
+        o = IterationOptions(max_iter=300)
+        P.scan_domain(p, ScanGrid(*g, 8, 8), ScanMode(mode, row), o)
+        tg, _ = _timed(lambda: P.scan_domain(p, ScanGrid(*g, 512, 512), ScanMode(mode, row), o))
+        tr, _ = _timed(lambda: C.scan_domain(p, ScanGrid(*g, 64, 64), mode, row, 0.0, {"max_iter": 300},
+                                              threads=threads))
+        print(json.dumps({"scan": name, "mode": mode, "b200_cells_per_s": 512 * 512 / tg,
+                          "reference_cells_per_s": 64 * 64 / tr, "reference_threads": threads,
+                          "speedup": (512 * 512 / tg) / (64 * 64 / tr)}), flush=True)
+    # Matrix Market (row f3): a c4-shaped file, the reference's reader vs ours
+    import tempfile
+    csr = pr.csr_fixed_per_row(1 << 20, 3, 16)
+    path = os.path.join(tempfile.mkdtemp(), "delta.mtx")
+    P.write_matrix_market(csr, path)
+    tg, m = _timed(lambda: P.read_matrix_market(path))
+    tr, (rc, _, ref) = _timed(lambda: ReferenceMatrixMarket().read(path))
+    assert rc == 0 and np.array_equal(m.rowptr, ref[1]) and np.array_equal(m.cols, csr.cols)
+    print(json.dumps({"matrix_market": "read c4-shaped file", "mb": os.path.getsize(path) / 1e6, "b200_lib_s": tg,
+                      "reference_s": tr, "speedup": tr / tg}), flush=True)
+    os.remove(path)
+    return 0
+
+
+STATUS_NAMES = ["Converged", "BoundedNonConverged", "Diverged", "MaxIterations"]
+
+
+def platform_cpu():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 # ------------------------------------------------------------ B200 arm ----
 def main():
     args = parse()
+    if args.baselines:
+        return run_baselines()
     if args.impl == "reference":
         return run_reference(args)
     import torch
