@@ -53,6 +53,7 @@ struct DenseCfg {
 
 using CfgBig = DenseCfg<128, 128, 2, 4>;      // cfg 1: one CTA per SM
 using CfgSmall = DenseCfg<64, 64, 2, 2, 3>;   // cfg 0: n < 2048 (enough CTAs for 148 SMs), 3 CTAs/SM
+using CfgSmall8 = DenseCfg<64, 64, 2, 4, 2>;  // cfg 0, real: the same tiles with 8 warps of 32x16
 using CfgMid = DenseCfg<128, 64, 4, 2, 2>;    // cfg 2: two CTAs per SM -> one CTA's epilogue
                                               //        overlaps the other's DMMA mainloop
 
@@ -806,7 +807,17 @@ static cudaError_t launch_cfg(const DevSolve& s, const CUtensorMap* amaps, const
 
 cudaError_t launch_dense_step(const DevSolve& s, const CUtensorMap* amaps, const CUtensorMap* dmap,
                               const double* delta, int cfg, cudaStream_t st) {
-  if (cfg == 0) return launch_cfg<CfgSmall>(s, amaps, dmap, delta, st);
+  if (cfg == 0) {
+    // real problems: 8 warps of 32x16 at 2 CTAs/SM (c1 K1 89.0 vs 91.1 us for
+    // 4 warps of 32x32 at 3 CTAs/SM: more independent DMMA chains per
+    // scheduler); DPT_SMALL8=0 selects the 4-warp layout
+    static const bool small8 = [] {
+      const char* e = getenv("DPT_SMALL8");
+      return !(e && e[0] == '0');
+    }();
+    if (small8 && !s.cplx) return launch_cfg<CfgSmall8>(s, amaps, dmap, delta, st);
+    return launch_cfg<CfgSmall>(s, amaps, dmap, delta, st);
+  }
   if (cfg == 2) return launch_cfg<CfgMid>(s, amaps, dmap, delta, st);
   return launch_cfg<CfgBig>(s, amaps, dmap, delta, st);
 }
