@@ -71,39 +71,53 @@ __device__ __forceinline__ double u16_dot_sel(const int4* crow, const double2* v
 // chunks of 4 columns are visited in the order k = (q + rot) & 3 (rot = the
 // row's lane), which makes the shared-memory reads conflict-free.  Every
 // evaluation of a given row -- including the w[row] that each block needs --
-// uses the same rot, so the value is bit-identical.
-__device__ __forceinline__ double u16_dot_rot(const int4* crow, const double2* vrow, int rot,
-                                              const double* __restrict__ z) {
+// uses the same rot, so the value is bit-identical.  Split into the staged
+// loads (u16_load_rot) and the gathers + FMA chain (u16_gather_dot) so the
+// per-warp pipeline can release its stage between the two.
+struct U16Row {
   int4 c[4];
   double2 va[4], vb[4];
+};
+
+__device__ __forceinline__ U16Row u16_load_rot(const int4* crow, const double2* vrow, int rot) {
+  U16Row r;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int k = (q + rot) & 3;
-    c[q] = crow[k];
+    r.c[q] = crow[k];
     // values 4k..4k+3 are 16-byte chunks 2k, 2k+1; alternate which one is read
     // first by (rot >> 2) & 1 so the 32 lanes spread over all 8 bank slots
     const int f = (rot >> 2) & 1;
     const double2 x0 = vrow[2 * k + f], x1 = vrow[2 * k + (f ^ 1)];
-    va[q] = f ? x1 : x0;
-    vb[q] = f ? x0 : x1;
+    r.va[q] = f ? x1 : x0;
+    r.vb[q] = f ? x0 : x1;
   }
+  return r;
+}
+
+__device__ __forceinline__ double u16_gather_dot(const U16Row& r, const double* __restrict__ z) {
   double zg[16];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    zg[4 * q + 0] = z[c[q].x];
-    zg[4 * q + 1] = z[c[q].y];
-    zg[4 * q + 2] = z[c[q].z];
-    zg[4 * q + 3] = z[c[q].w];
+    zg[4 * q + 0] = z[r.c[q].x];
+    zg[4 * q + 1] = z[r.c[q].y];
+    zg[4 * q + 2] = z[r.c[q].z];
+    zg[4 * q + 3] = z[r.c[q].w];
   }
   double w = 0.0;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    w = __fma_rn(va[q].x, zg[4 * q + 0], w);
-    w = __fma_rn(va[q].y, zg[4 * q + 1], w);
-    w = __fma_rn(vb[q].x, zg[4 * q + 2], w);
-    w = __fma_rn(vb[q].y, zg[4 * q + 3], w);
+    w = __fma_rn(r.va[q].x, zg[4 * q + 0], w);
+    w = __fma_rn(r.va[q].y, zg[4 * q + 1], w);
+    w = __fma_rn(r.vb[q].x, zg[4 * q + 2], w);
+    w = __fma_rn(r.vb[q].y, zg[4 * q + 3], w);
   }
   return w;
+}
+
+__device__ __forceinline__ double u16_dot_rot(const int4* crow, const double2* vrow, int rot,
+                                              const double* __restrict__ z) {
+  return u16_gather_dot(u16_load_rot(crow, vrow, rot), z);
 }
 
 template <int ROWS, int MINB, bool ROT>
@@ -217,12 +231,137 @@ __global__ void __launch_bounds__(ROWS, MINB)
   }
 }
 
+// Per-warp pipeline variant: each warp streams its own 32-row trips (2 KiB of
+// columns + 4 KiB of values per trip, one cp.async.bulk pair issued by lane 0)
+// through an S-deep private ring with its own mbarriers, and releases a stage
+// as soon as its lanes hold the row in registers (__syncwarp), before the
+// gathers.  No block-wide barrier inside the loop: warps drift freely, so the
+// L1's random-gather queue stays fed while other warps wait on L2.  Rows are
+// the same lane-rotated dots as above (trip = 32 rows, so rot = m & 31 = lane).
+template <int W, int S>
+struct U16W {
+  static constexpr int TripBytes = 32 * 16 * 12;  // 6 KiB
+  static constexpr int Smem = W * S * TripBytes;
+};
+
+template <int W, int S, int MINB>
+__global__ void __launch_bounds__(W * 32, MINB)
+    single_u16w_kernel(DevSolve s, DevCsr D, int64_t row, int64_t ntrips) {
+  constexpr int kTrip = U16W<W, S>::TripBytes;
+  if (s.state->done) return;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ uint64_t bar[W][S];
+  __shared__ double red[W][5];
+  const int jl = launch_index(s);
+  const int64_t n = s.n;
+  const double* __restrict__ z = s.slots + size_t((jl - 1) % s.nslots) * size_t(s.slot_elems);
+  double* __restrict__ zo = s.slots + size_t(jl % s.nslots) * size_t(s.slot_elems);
+  const double lam_k = lam_of(s, jl), lam = s.lambda;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint8_t* ring = smem + size_t(warp) * S * kTrip;
+  const int64_t stride = int64_t(gridDim.x) * W;
+  int64_t t = int64_t(blockIdx.x) * W + warp;
+
+  auto issue = [&](int64_t trip, int st) {
+    const int64_t r0 = trip * 32;
+    const int64_t nr = (n - r0) < 32 ? (n - r0) : 32;
+    uint8_t* base = ring + st * kTrip;
+    mbar_arrive_expect_tx(&bar[warp][st], uint32_t(nr * 16 * 12));
+    bulk_load(base, D.cols + 16 * r0, uint32_t(nr * 16 * 4), &bar[warp][st]);
+    bulk_load(base + 32 * 64, D.vals + 16 * r0, uint32_t(nr * 16 * 8), &bar[warp][st]);
+  };
+  if (lane == 0) {
+    for (int i = 0; i < S; ++i) mbar_init(&bar[warp][i], 1);
+    fence_mbar_init();
+    for (int i = 0; i < S; ++i)
+      if (t + i * stride < ntrips) issue(t + i * stride, i);
+  }
+  __syncwarp();
+  // w[row] of z_{j-1} in the rotation of the lane that owns row; every lane
+  // evaluates it (uniform addresses: one sector per load) while the first
+  // trips are in flight
+  const double wr = u16_dot_rot(reinterpret_cast<const int4*>(D.cols + 16 * row),
+                                reinterpret_cast<const double2*>(D.vals + 16 * row), int(row & 31), z);
+  if (blockIdx.x == 0 && threadIdx.x == 0) s.dvec[(jl - 1) & 1][0] = wr;  // for the fold's eps
+  const double trow = s.theta[row];
+  const double eps = __dadd_rn(trow, __dmul_rn(lam, wr));
+  double num = 0.0, den = 0.0, t_step = 0.0, t_max = 0.0, t_nonfin = 0.0;
+
+  for (int it = 0; t < ntrips; ++it, t += stride) {
+    const int st = it % S;
+    mbar_wait(&bar[warp][st], uint32_t(it / S) & 1u);
+    const int64_t m = t * 32 + lane;
+    const uint8_t* base = ring + st * kTrip;
+    U16Row rd;
+    if (m < n)
+      rd = u16_load_rot(reinterpret_cast<const int4*>(base + lane * 64),
+                        reinterpret_cast<const double2*>(base + 32 * 64 + lane * 128), lane);
+    __syncwarp();  // every lane holds its row: the stage can be refilled
+    if (lane == 0 && t + S * stride < ntrips) issue(t + S * stride, st);
+    if (m < n) {
+      const double zm = z[m];
+      const double tm = s.theta[m];
+      const double w = u16_gather_dot(rd, z);
+      double val;
+      if (m == row) {
+        val = 1.0;
+      } else {
+        const double g = s.gapmat ? s.gapmat[m] : 1.0 / __dsub_rn(trow, tm);  // build_gap_row, partition.cpp:83-96
+        val = __dmul_rn(__dmul_rn(lam_k, g), __dsub_rn(w, __dmul_rn(wr, zm)));
+      }
+      zo[m] = val;
+      t_step = fmax(t_step, fabs(__dsub_rn(val, zm)));
+      t_max = fmax(t_max, fabs(val));
+      t_nonfin += isfinite(val) ? 0.0 : 1.0;
+      const double r = __dadd_rn(__dmul_rn(__dsub_rn(tm, eps), zm), __dmul_rn(lam, w));
+      num = fmax(num, fabs(r));
+      den = fmax(den, fabs(zm));
+    }
+  }
+  num = warp_max(num);
+  den = warp_max(den);
+  t_step = warp_max(t_step);
+  t_max = warp_max(t_max);
+  t_nonfin = warp_sum(t_nonfin);
+  if (lane == 0) {
+    red[warp][0] = num;
+    red[warp][1] = den;
+    red[warp][2] = t_step;
+    red[warp][3] = t_max;
+    red[warp][4] = t_nonfin;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a[5] = {0, 0, 0, 0, 0};
+    for (int ww = 0; ww < W; ++ww) {
+      a[0] = fmax(a[0], red[ww][0]);
+      a[1] = fmax(a[1], red[ww][1]);
+      a[2] = fmax(a[2], red[ww][2]);
+      a[3] = fmax(a[3], red[ww][3]);
+      a[4] += red[ww][4];
+    }
+    const int tn = blockIdx.x, ntn = s.ntn;
+    s.rowpart[rp_index(0, 0, tn, 1, ntn)] = 0.0;
+    s.rowpart[rp_index(1, 0, tn, 1, ntn)] = a[0];
+    s.rowpart[rp_index(2, 0, tn, 1, ntn)] = a[1];
+    double* tp = s.tilepart + size_t(tn) * 4;
+    tp[0] = a[2];
+    tp[1] = a[3];
+    tp[2] = a[4];
+    tp[3] = 0.0;
+  }
+}
+
 // Variant table (DPT_U16_VARIANT selects one for tuning runs; default 1: measured
 // 98 us / step on c4 vs 109 us (0), 147-160 us (128-row trips), 143 us (64-row)).
 struct U16Variant {
   int rows, minb, rot;
 };
-static const U16Variant kU16Var[] = {{256, 2, 0}, {256, 2, 1}, {128, 4, 0}, {128, 4, 1}, {128, 6, 1}, {64, 8, 1}};
+static const U16Variant kU16Var[] = {{256, 2, 0}, {256, 2, 1}, {128, 4, 0}, {128, 4, 1}, {128, 6, 1}, {64, 8, 1},
+                                     // per-warp pipelines (rows = 32 * warps per block)
+                                     {256, 2, 1}, {192, 3, 1}, {512, 1, 1}, {128, 3, 1}, {160, 3, 1},
+                                     {256, 2, 1}, {192, 3, 1}, {160, 4, 1}, {128, 5, 1}, {128, 4, 1},
+                                     {512, 1, 1}, {160, 3, 1}, {128, 4, 1}};
 
 static int u16_variant() {
   const char* e = getenv("DPT_U16_VARIANT");
@@ -235,6 +374,22 @@ int u16_grid(int64_t n) {
   const int64_t trips = (n + V.rows - 1) / V.rows;
   const int64_t g = 148 * V.minb;  // resident blocks
   return int(trips < g ? (trips < 1 ? 1 : trips) : g);
+}
+
+template <int W, int S, int MINB>
+static cudaError_t launch_u16w(const DevSolve& s, const DevCsr& d, int64_t row, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(single_u16w_kernel<W, S, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         U16W<W, S>::Smem);
+    if (getenv("DPT_U16_CARVEOUT"))  // tuning: force the shared-memory carveout (percent)
+      cudaFuncSetAttribute(single_u16w_kernel<W, S, MINB>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           atoi(getenv("DPT_U16_CARVEOUT")));
+    attr = true;
+  }
+  const int64_t trips = (s.n + 31) / 32;
+  single_u16w_kernel<W, S, MINB><<<u16_grid(s.n), W * 32, U16W<W, S>::Smem, st>>>(s, d, row, trips);
+  return cudaGetLastError();
 }
 
 template <int ROWS, int MINB, bool ROT>
@@ -257,6 +412,19 @@ cudaError_t launch_single_u16(const DevSolve& s, const DevCsr& d, int64_t row, c
     case 3: return launch_u16<128, 4, true>(s, d, row, st);
     case 4: return launch_u16<128, 6, true>(s, d, row, st);
     case 5: return launch_u16<64, 8, true>(s, d, row, st);
+    case 6: return launch_u16w<8, 2, 2>(s, d, row, st);
+    case 7: return launch_u16w<6, 2, 3>(s, d, row, st);
+    case 8: return launch_u16w<16, 2, 1>(s, d, row, st);
+    case 9: return launch_u16w<4, 3, 3>(s, d, row, st);
+    case 10: return launch_u16w<5, 2, 3>(s, d, row, st);
+    case 11: return launch_u16w<8, 1, 2>(s, d, row, st);
+    case 12: return launch_u16w<6, 1, 3>(s, d, row, st);
+    case 13: return launch_u16w<5, 1, 4>(s, d, row, st);
+    case 14: return launch_u16w<4, 1, 5>(s, d, row, st);
+    case 15: return launch_u16w<4, 2, 4>(s, d, row, st);
+    case 16: return launch_u16w<16, 1, 1>(s, d, row, st);
+    case 17: return launch_u16w<5, 1, 3>(s, d, row, st);
+    case 18: return launch_u16w<4, 1, 4>(s, d, row, st);
     default: return launch_u16<256, 2, false>(s, d, row, st);
   }
 }

@@ -825,6 +825,20 @@ void key_add(std::vector<unsigned char>& k, const T& v) {
   k.insert(k.end(), p, p + sizeof(T));
 }
 
+// Development knobs that select kernels (tuning runs and tests switch them
+// between calls in one process): part of the loop-graph key, so a graph
+// captured under one selection is never replayed under another.
+static const char* const kKernelKnobs[] = {"DPT_U16_VARIANT", "DPT_DENSE_CFG", "DPT_SMALL8", "DPT_CSR_ROWS",
+                                           "DPT_SELL_SCHED", "DPT_SELL_RELABEL", "DPT_DENSE_SK", "DPT_SHARD_EMULATE"};
+
+void key_add_knobs(std::vector<unsigned char>& k) {
+  for (const char* name : kKernelKnobs) {
+    const char* v = std::getenv(name);
+    k.push_back(v ? 1 : 0);
+    if (v) k.insert(k.end(), v, v + std::strlen(v) + 1);
+  }
+}
+
 void drive_graph(dpt_ctx* ctx, Work& w, DevProblem& dp, Mode mode, int64_t row, int total, int issued,
                  int64_t cycle_elems, dpt_trace_fn trace, void* user, dpt_error_info* err) {
   cudaStream_t st = ctx->stream;
@@ -849,6 +863,7 @@ void drive_graph(dpt_ctx* ctx, Work& w, DevProblem& dp, Mode mode, int64_t row, 
   key_add(key, dp.uniform16);
   key_add(key, dp.csr());
   key_add(key, dp.sell());
+  key_add_knobs(key);
   dpt_ctx::LoopGraph* hit = nullptr;
   for (auto& lg : ctx->loop_graphs)
     if (lg.key == key) hit = &lg;

@@ -1,0 +1,45 @@
+"""GPU: every K3 (16-nonzeros-per-row row map) variant -- block-staged trips
+(DPT_U16_VARIANT 0-5) and per-warp pipelines (6-10) -- against the oracle,
+and the lane-rotated ones bit for bit against each other (same per-row
+accumulation order).  Sizes include a ragged last trip and n smaller than one
+warp-trip."""
+import os
+
+import numpy as np
+import pytest
+
+import paper_2002_12872_b200 as P
+from oracle.bind import Checker
+from paper_2002_12872_b200 import problems as pr
+
+pytestmark = pytest.mark.gpu
+
+ROTATED = [1, 3, 4, 5, 6, 7, 8, 9, 10]
+
+
+@pytest.fixture
+def variant_env():
+    old = os.environ.get("DPT_U16_VARIANT")
+    yield
+    if old is None:
+        os.environ.pop("DPT_U16_VARIANT", None)
+    else:
+        os.environ["DPT_U16_VARIANT"] = old
+
+
+@pytest.mark.parametrize("n", [20, 1000, 70001])
+def test_k3_variants_agree(variant_env, n):
+    p, o, _ = pr.config("c4b", n)
+    r = Checker("oracle").dominant_eigenpair(p, o)
+    ref = None
+    for v in [0, 2] + ROTATED:
+        os.environ["DPT_U16_VARIANT"] = str(v)
+        g = P.dominant_eigenpair(p, P.IterationOptions(**o))
+        assert int(g.status) == r.status and abs(g.iterations - r.iterations) <= 1, (v, g.status, g.iterations)
+        assert abs(g.eigenvalue - r.eigenvalue) <= 1e-10 * max(1.0, abs(r.eigenvalue)), v
+        assert np.max(np.abs(g.z_chart - r.z)) < 1e-9, v
+        if v in ROTATED:
+            if ref is None:
+                ref = g
+            else:
+                assert g.iterations == ref.iterations and np.array_equal(g.z_chart, ref.z_chart), v
