@@ -95,14 +95,29 @@ __device__ __forceinline__ U16Row u16_load_rot(const int4* crow, const double2* 
   return r;
 }
 
+// Gather through L1 without allocating a line (tuning variant).
+__device__ __forceinline__ double ld_na(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
+template <bool NA = false>
 __device__ __forceinline__ double u16_gather_dot(const U16Row& r, const double* __restrict__ z) {
   double zg[16];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    zg[4 * q + 0] = z[r.c[q].x];
-    zg[4 * q + 1] = z[r.c[q].y];
-    zg[4 * q + 2] = z[r.c[q].z];
-    zg[4 * q + 3] = z[r.c[q].w];
+    if (NA) {
+      zg[4 * q + 0] = ld_na(z + r.c[q].x);
+      zg[4 * q + 1] = ld_na(z + r.c[q].y);
+      zg[4 * q + 2] = ld_na(z + r.c[q].z);
+      zg[4 * q + 3] = ld_na(z + r.c[q].w);
+    } else {
+      zg[4 * q + 0] = z[r.c[q].x];
+      zg[4 * q + 1] = z[r.c[q].y];
+      zg[4 * q + 2] = z[r.c[q].z];
+      zg[4 * q + 3] = z[r.c[q].w];
+    }
   }
   double w = 0.0;
 #pragma unroll
@@ -244,7 +259,7 @@ struct U16W {
   static constexpr int Smem = W * S * TripBytes;
 };
 
-template <int W, int S, int MINB>
+template <int W, int S, int MINB, bool NA = false>
 __global__ void __launch_bounds__(W * 32, MINB)
     single_u16w_kernel(DevSolve s, DevCsr D, int64_t row, int64_t ntrips) {
   constexpr int kTrip = U16W<W, S>::TripBytes;
@@ -301,7 +316,7 @@ __global__ void __launch_bounds__(W * 32, MINB)
     if (m < n) {
       const double zm = z[m];
       const double tm = s.theta[m];
-      const double w = u16_gather_dot(rd, z);
+      const double w = u16_gather_dot<NA>(rd, z);
       double val;
       if (m == row) {
         val = 1.0;
@@ -352,8 +367,12 @@ __global__ void __launch_bounds__(W * 32, MINB)
   }
 }
 
-// Variant table (DPT_U16_VARIANT selects one for tuning runs; default 1: measured
-// 98 us / step on c4 vs 109 us (0), 147-160 us (128-row trips), 143 us (64-row)).
+// Variant table (DPT_U16_VARIANT selects one for tuning runs).  Measured on c4
+// (profiles/r01f_k3_sweep.txt): block-staged trips 98 us (1), 109 us (0); per-warp
+// rings with two stages 91-92 us (6, 8, 10), with one stage 83.4-84.3 us (11, 16-18;
+// default 11).  The binding unit is the L1: every byte of shared memory taken
+// from it costs in-flight gather capacity -- forcing the maximum shared carveout
+// slows every variant to ~146 us, as do configurations that need > 196 KB.
 struct U16Variant {
   int rows, minb, rot;
 };
@@ -361,11 +380,12 @@ static const U16Variant kU16Var[] = {{256, 2, 0}, {256, 2, 1}, {128, 4, 0}, {128
                                      // per-warp pipelines (rows = 32 * warps per block)
                                      {256, 2, 1}, {192, 3, 1}, {512, 1, 1}, {128, 3, 1}, {160, 3, 1},
                                      {256, 2, 1}, {192, 3, 1}, {160, 4, 1}, {128, 5, 1}, {128, 4, 1},
-                                     {512, 1, 1}, {160, 3, 1}, {128, 4, 1}};
+                                     {512, 1, 1}, {160, 3, 1}, {128, 4, 1},
+                                     {256, 2, 1}, {256, 2, 1}};
 
 static int u16_variant() {
   const char* e = getenv("DPT_U16_VARIANT");
-  const int v = e ? atoi(e) : 1;  // 256-row trips, lane-rotated dot: fastest on B200 (tools/u16_sweep.sh)
+  const int v = e ? atoi(e) : 11;  // per-warp pipeline, 8 warps x 2 blocks, one stage: fastest on B200 (tools/u16_sweep.sh)
   return (v >= 0 && v < int(sizeof(kU16Var) / sizeof(kU16Var[0]))) ? v : 0;
 }
 
@@ -376,19 +396,19 @@ int u16_grid(int64_t n) {
   return int(trips < g ? (trips < 1 ? 1 : trips) : g);
 }
 
-template <int W, int S, int MINB>
+template <int W, int S, int MINB, bool NA = false>
 static cudaError_t launch_u16w(const DevSolve& s, const DevCsr& d, int64_t row, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(single_u16w_kernel<W, S, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(single_u16w_kernel<W, S, MINB, NA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          U16W<W, S>::Smem);
     if (getenv("DPT_U16_CARVEOUT"))  // tuning: force the shared-memory carveout (percent)
-      cudaFuncSetAttribute(single_u16w_kernel<W, S, MINB>, cudaFuncAttributePreferredSharedMemoryCarveout,
+      cudaFuncSetAttribute(single_u16w_kernel<W, S, MINB, NA>, cudaFuncAttributePreferredSharedMemoryCarveout,
                            atoi(getenv("DPT_U16_CARVEOUT")));
     attr = true;
   }
   const int64_t trips = (s.n + 31) / 32;
-  single_u16w_kernel<W, S, MINB><<<u16_grid(s.n), W * 32, U16W<W, S>::Smem, st>>>(s, d, row, trips);
+  single_u16w_kernel<W, S, MINB, NA><<<u16_grid(s.n), W * 32, U16W<W, S>::Smem, st>>>(s, d, row, trips);
   return cudaGetLastError();
 }
 
@@ -425,6 +445,8 @@ cudaError_t launch_single_u16(const DevSolve& s, const DevCsr& d, int64_t row, c
     case 16: return launch_u16w<16, 1, 1>(s, d, row, st);
     case 17: return launch_u16w<5, 1, 3>(s, d, row, st);
     case 18: return launch_u16w<4, 1, 4>(s, d, row, st);
+    case 19: return launch_u16w<8, 1, 2, true>(s, d, row, st);
+    case 20: return launch_u16w<8, 2, 2, true>(s, d, row, st);
     default: return launch_u16<256, 2, false>(s, d, row, st);
   }
 }

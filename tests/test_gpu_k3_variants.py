@@ -14,7 +14,7 @@ from paper_2002_12872_b200 import problems as pr
 
 pytestmark = pytest.mark.gpu
 
-ROTATED = [1, 3, 4, 5, 6, 7, 8, 9, 10]
+ROTATED = [1, 3, 4, 5, 6, 7, 8, 9, 10, 11, 16, 17, 18, 19, 20]
 
 
 @pytest.fixture

@@ -1,3 +1,3 @@
-VARIANTS="11 15 16 17 18" bash tools/u16_sweep.sh > gpurun_out/k3v_sweep3.txt 2>&1
-echo "carveout 100" >> gpurun_out/k3v_sweep3.txt
-DPT_U16_CARVEOUT=100 VARIANTS="6 11 15 16 17 18" bash tools/u16_sweep.sh >> gpurun_out/k3v_sweep3.txt 2>&1
+VARIANTS="11 19 20" bash tools/u16_sweep.sh > gpurun_out/k3v_sweep4.txt 2>&1
+for c in 44 50; do echo "carveout $c" >> gpurun_out/k3v_sweep4.txt; DPT_U16_CARVEOUT=$c VARIANTS="11 19" bash tools/u16_sweep.sh >> gpurun_out/k3v_sweep4.txt 2>&1; done
+timeout 300 python -m pytest tests/test_gpu_k3_variants.py -x -q > gpurun_out/k3v_test2.log 2>&1
