@@ -109,11 +109,26 @@ __global__ void __launch_bounds__(THREADS) csr_step_kernel(DevSolve s, DevSell S
   const int32_t* __restrict__ perm = S.perm;
   const int32_t* __restrict__ inv = S.inv;
   if constexpr (SMEM) {
-    for (int r = 0; r < nr; ++r)
-      for (int64_t c = threadIdx.x; c < n; c += blockDim.x) {
-        const int64_t p = perm ? int64_t(__ldg(perm + c)) : c;
-        sa[size_t(p) * ST + r] = ain[size_t(r) * size_t(ld) + size_t(c)];
+    // all R rows of a column chunk are loaded before any is stored: R * kStageU
+    // independent loads in flight per thread (the loop is HBM-latency bound)
+    constexpr int kStageU = R <= 3 ? 4 : 2;
+    for (int64_t c0 = threadIdx.x; c0 < n; c0 += kStageU * int64_t(blockDim.x)) {
+      double v[kStageU][R];
+      int64_t p[kStageU];
+#pragma unroll
+      for (int u = 0; u < kStageU; ++u) {
+        const int64_t c = c0 + int64_t(u) * blockDim.x;
+        p[u] = c < n ? (perm ? int64_t(__ldg(perm + c)) : c) : -1;
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          if (c < n && r < nr) v[u][r] = ain[size_t(r) * size_t(ld) + size_t(c)];
       }
+#pragma unroll
+      for (int u = 0; u < kStageU; ++u)
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          if (p[u] >= 0 && r < nr) sa[size_t(p[u]) * ST + r] = v[u][r];
+    }
   }
   __syncthreads();
   auto A = [&](int r, int64_t p) -> double {  // element at position p of staged row r
