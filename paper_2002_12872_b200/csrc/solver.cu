@@ -33,6 +33,7 @@
 #include <memory>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/dpt_b200.h"
@@ -96,6 +97,9 @@ struct dpt_ctx {
   // pinned host snapshot buffers, kept across calls
   void* pinned = nullptr;
   size_t pinned_bytes = 0;
+  // staging ring for large copies to / from PAGEABLE host memory (stage_copy)
+  void* stage[2] = {nullptr, nullptr};
+  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
   // Instantiated device-loop graphs (drive_graph), keyed by every parameter
   // the captured launches depend on.  Repeated solves of one problem get the
   // same workspace blocks from the caching allocator, hence the same key, and
@@ -234,6 +238,149 @@ cudaError_t to_host_ordered(void* dst, const void* src, size_t bytes, cudaMemcpy
   cudaError_t e = cudaMemcpyAsync(dst, src, bytes, kind, st);
   if (e != cudaSuccess) return e;
   return cudaStreamSynchronize(st);
+}
+
+// ------------------------------------------------ staged host copies ----
+// Copies between the device and PAGEABLE host memory (numpy arrays, the
+// reference's std::vector / DenseMatrix storage) go through the driver's own
+// bounce buffers at ~5-8 GB/s.  Large ones are staged here instead: a
+// two-buffer pinned ring, the DMA of one chunk overlapping the host memcpy of
+// the other, the host side split over several threads (which also spreads the
+// first-touch page faults of a fresh destination).  Pinned / registered host
+// memory and small copies keep the plain cudaMemcpy*Async.
+constexpr size_t kStageBytes = size_t(32) << 20;
+constexpr size_t kStageMin = size_t(4) << 20;
+
+bool host_pageable(const void* q) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, q) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeUnregistered;
+}
+
+int copy_threads() {
+  static const int t = [] {
+    const unsigned h = std::thread::hardware_concurrency();
+    return int(std::max(1u, std::min(8u, h / 2)));
+  }();
+  return t;
+}
+
+void par_memcpy(void* dst, const void* src, size_t bytes) {
+  const int T = bytes >= (size_t(2) << 20) ? copy_threads() : 1;
+  if (T == 1) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  const size_t per = ((bytes + T - 1) / T + 4095) & ~size_t(4095);
+  std::thread th[8];
+  int nt = 0;
+  for (int t = 1; t < T; ++t) {
+    const size_t off = size_t(t) * per;
+    if (off >= bytes) break;
+    th[nt++] = std::thread(std::memcpy, static_cast<char*>(dst) + off, static_cast<const char*>(src) + off,
+                           std::min(per, bytes - off));
+  }
+  std::memcpy(dst, src, std::min(per, bytes));
+  for (int t = 0; t < nt; ++t) th[t].join();
+}
+
+cudaError_t stage_ready(dpt_ctx* ctx) {
+  for (int b = 0; b < 2; ++b) {
+    if (!ctx->stage[b]) {
+      cudaError_t e = cudaMallocHost(&ctx->stage[b], kStageBytes);
+      if (e != cudaSuccess) return e;
+      e = cudaEventCreateWithFlags(&ctx->stage_ev[b], cudaEventDisableTiming);
+      if (e != cudaSuccess) return e;
+    }
+    cudaError_t e = cudaEventSynchronize(ctx->stage_ev[b]);  // a previous staged upload may still read it
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+// height rows of width bytes; device rows at pitch dpitch_dev, host rows dense
+// (pitch = width).  Chunks are whole rows (or, for one long row, byte ranges).
+cudaError_t stage_copy(dpt_ctx* ctx, void* dst, size_t dpitch, const void* src, size_t spitch, size_t width,
+                       size_t height, cudaMemcpyKind kind) {
+  cudaStream_t st = ctx->stream;
+  const bool d2h = kind == cudaMemcpyDeviceToHost;
+  const size_t total = width * height;
+  cudaError_t e = stage_ready(ctx);
+  if (e != cudaSuccess) return e;
+  // chunk geometry: rows per chunk, or bytes per chunk of a single row
+  const bool by_rows = height > 1 && width <= kStageBytes;
+  const size_t rows_per = by_rows ? kStageBytes / width : 0;
+  const size_t nch = by_rows ? (height + rows_per - 1) / rows_per : (total + kStageBytes - 1) / kStageBytes;
+  auto dev_op = [&](size_t i) -> cudaError_t {
+    void* buf = ctx->stage[i & 1];
+    if (by_rows) {
+      const size_t r0 = i * rows_per, nr = std::min(rows_per, height - r0);
+      if (d2h)
+        e = cudaMemcpy2DAsync(buf, width, static_cast<const char*>(src) + r0 * spitch, spitch, width, nr, kind, st);
+      else
+        e = cudaMemcpy2DAsync(static_cast<char*>(dst) + r0 * dpitch, dpitch, buf, width, width, nr, kind, st);
+    } else {
+      const size_t o = i * kStageBytes, nb = std::min(kStageBytes, total - o);
+      if (d2h)
+        e = cudaMemcpyAsync(buf, static_cast<const char*>(src) + o, nb, kind, st);
+      else
+        e = cudaMemcpyAsync(static_cast<char*>(dst) + o, buf, nb, kind, st);
+    }
+    if (e != cudaSuccess) return e;
+    return cudaEventRecord(ctx->stage_ev[i & 1], st);
+  };
+  auto host_span = [&](size_t i, size_t* off) -> size_t {  // host byte range of chunk i
+    if (by_rows) {
+      const size_t r0 = i * rows_per;
+      *off = r0 * width;
+      return std::min(rows_per, height - r0) * width;
+    }
+    *off = i * kStageBytes;
+    return std::min(kStageBytes, total - *off);
+  };
+  if (d2h) {
+    for (size_t i = 0; i < nch && i < 2; ++i)
+      if ((e = dev_op(i)) != cudaSuccess) return e;
+    for (size_t i = 0; i < nch; ++i) {
+      if ((e = cudaEventSynchronize(ctx->stage_ev[i & 1])) != cudaSuccess) return e;
+      size_t off;
+      const size_t nb = host_span(i, &off);
+      par_memcpy(static_cast<char*>(dst) + off, ctx->stage[i & 1], nb);
+      if (i + 2 < nch && (e = dev_op(i + 2)) != cudaSuccess) return e;
+    }
+  } else {
+    for (size_t i = 0; i < nch; ++i) {
+      if (i >= 2 && (e = cudaEventSynchronize(ctx->stage_ev[i & 1])) != cudaSuccess) return e;
+      size_t off;
+      const size_t nb = host_span(i, &off);
+      par_memcpy(ctx->stage[i & 1], static_cast<const char*>(src) + off, nb);
+      if ((e = dev_op(i)) != cudaSuccess) return e;
+    }
+  }
+  return cudaSuccess;
+}
+
+// cudaMemcpyAsync / cudaMemcpy2DAsync on the context's stream, staged when the
+// host side is large and pageable.  Device-to-host copies return complete.
+cudaError_t copy_async(dpt_ctx* ctx, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind) {
+  if (bytes == 0) return cudaSuccess;
+  if ((kind == cudaMemcpyHostToDevice || kind == cudaMemcpyDeviceToHost) && bytes >= kStageMin &&
+      host_pageable(kind == cudaMemcpyHostToDevice ? src : dst))
+    return stage_copy(ctx, dst, bytes, src, bytes, bytes, 1, kind);
+  return cudaMemcpyAsync(dst, src, bytes, kind, ctx->stream);
+}
+
+cudaError_t copy2d_async(dpt_ctx* ctx, void* dst, size_t dpitch, const void* src, size_t spitch, size_t width,
+                         size_t height, cudaMemcpyKind kind) {
+  if (width == 0 || height == 0) return cudaSuccess;
+  const bool host_dense = kind == cudaMemcpyHostToDevice ? spitch == width : dpitch == width;
+  if ((kind == cudaMemcpyHostToDevice || kind == cudaMemcpyDeviceToHost) && host_dense &&
+      width * height >= kStageMin && host_pageable(kind == cudaMemcpyHostToDevice ? src : dst))
+    return stage_copy(ctx, dst, dpitch, src, spitch, width, height, kind);
+  return cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height, kind, ctx->stream);
 }
 
 void dalloc(DBuf& b, size_t bytes, dpt_error_info* err) {
@@ -537,7 +684,7 @@ void upload(DevProblem& dp, dpt_ctx* ctx, const dpt_problem* p, dpt_error_info* 
     dp.theta.view(p->d);
   } else {
     dalloc(dp.theta, size_t(cx * n) * 8, err);
-    if (n) CK(cudaMemcpyAsync(dp.theta.p, p->d, size_t(cx * n) * 8, k, st));
+    if (n) CK(copy_async(ctx, dp.theta.p, p->d, size_t(cx * n) * 8, k));
   }
   if (p->delta_kind == DPT_DELTA_DENSE) {
     if (dp.cplx) {
@@ -560,7 +707,7 @@ void upload(DevProblem& dp, dpt_ctx* ctx, const dpt_problem* p, dpt_error_info* 
         }
       }
       dalloc(dp.delta, B.size() * 8 + 64, err);
-      if (n) CK(cudaMemcpyAsync(dp.delta.p, B.data(), B.size() * 8, cudaMemcpyHostToDevice, st));
+      if (n) CK(copy_async(ctx, dp.delta.p, B.data(), B.size() * 8, cudaMemcpyHostToDevice));
       CK(cudaStreamSynchronize(st));  // B goes out of scope
     } else if (dev && n && dp.ld == n && aligned16(p->delta)) {
       dp.ldd = dp.ld;
@@ -570,9 +717,9 @@ void upload(DevProblem& dp, dpt_ctx* ctx, const dpt_problem* p, dpt_error_info* 
       dalloc(dp.delta, size_t(n) * size_t(dp.ldd) * 8 + 64, err);
       if (n) {
         if (dp.ldd == n)
-          CK(cudaMemcpyAsync(dp.delta.p, p->delta, size_t(n) * size_t(n) * 8, k, st));
+          CK(copy_async(ctx, dp.delta.p, p->delta, size_t(n) * size_t(n) * 8, k));
         else
-          CK(cudaMemcpy2DAsync(dp.delta.p, size_t(dp.ldd) * 8, p->delta, size_t(n) * 8, size_t(n) * 8, size_t(n), k, st));
+          CK(copy2d_async(ctx, dp.delta.p, size_t(dp.ldd) * 8, p->delta, size_t(n) * 8, size_t(n) * 8, size_t(n), k));
       }
     }
   } else {
@@ -591,10 +738,10 @@ void upload(DevProblem& dp, dpt_ctx* ctx, const dpt_problem* p, dpt_error_info* 
       dalloc(dp.rowptr, size_t(n + 1) * 8, err);
       dalloc(dp.cols, size_t(nnz) * 4, err);
       dalloc(dp.vals, size_t(cx * nnz) * 8, err);
-      CK(cudaMemcpyAsync(dp.rowptr.p, p->rowptr, size_t(n + 1) * 8, k, st));
+      CK(copy_async(ctx, dp.rowptr.p, p->rowptr, size_t(n + 1) * 8, k));
       if (nnz) {
-        CK(cudaMemcpyAsync(dp.cols.p, p->cols, size_t(nnz) * 4, k, st));
-        CK(cudaMemcpyAsync(dp.vals.p, p->vals, size_t(cx * nnz) * 8, k, st));
+        CK(copy_async(ctx, dp.cols.p, p->cols, size_t(nnz) * 4, k));
+        CK(copy_async(ctx, dp.vals.p, p->vals, size_t(cx * nnz) * 8, k));
       }
     }
     if (sell) {
@@ -1019,6 +1166,10 @@ void drive(dpt_ctx* ctx, Work& w, DevProblem& dp, Mode mode, int64_t row, int to
 
 void copy_out(double* dst, const double* src, size_t count, int out_mem, cudaStream_t st, dpt_error_info* err) {
   if (!dst || count == 0) return;
+  if (out_mem != DPT_MEM_DEVICE && t_ctx && st == t_ctx->stream) {
+    CK(copy_async(t_ctx, dst, src, count * 8, cudaMemcpyDeviceToHost));
+    return;
+  }
   CK(cudaMemcpyAsync(dst, src, count * 8, out_mem == DPT_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st));
 }
 
@@ -1027,6 +1178,10 @@ void copy_slot_out(double* dst, const Work& w, const DevProblem& dp, int slot, i
   if (!dst || dp.n == 0) return;
   const double* src = w.s.slots + size_t(slot) * size_t(w.s.slot_elems);
   const cudaMemcpyKind k = out_mem == DPT_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  if (k == cudaMemcpyDeviceToHost && t_ctx && st == t_ctx->stream) {  // staged when pageable
+    CK(copy2d_async(t_ctx, dst, size_t(dp.ncol) * 8, src, size_t(dp.ld) * 8, size_t(dp.ncol) * 8, size_t(w.s.rows), k));
+    return;
+  }
   if (dp.ld == dp.ncol)
     CK(cudaMemcpyAsync(dst, src, size_t(w.s.rows) * size_t(dp.ncol) * 8, k, st));
   else
@@ -1122,7 +1277,7 @@ void gather_rows(dpt_ctx* ctx, const Work& w, const DevProblem& dp, int slot, do
     throw Fail{DPT_ERR_NCCL};
   }
   const cudaMemcpyKind k = out_mem == DPT_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-  CK(cudaMemcpy2DAsync(dst, size_t(dp.ncol) * 8, all.p, size_t(dp.ld) * 8, size_t(dp.ncol) * 8, size_t(dp.n), k, st));
+  CK(copy2d_async(ctx, dst, size_t(dp.ncol) * 8, all.p, size_t(dp.ld) * 8, size_t(dp.ncol) * 8, size_t(dp.n), k));
   CK(cudaStreamSynchronize(st));
 }
 
@@ -1819,6 +1974,10 @@ void dpt_ctx_destroy(dpt_ctx* ctx) {
     for (auto& kv : ctx->free_blocks) cudaFree(kv.second);
     ctx->free_blocks.clear();
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    for (int b = 0; b < 2; ++b) {
+      if (ctx->stage_ev[b]) cudaEventSynchronize(ctx->stage_ev[b]), cudaEventDestroy(ctx->stage_ev[b]);
+      if (ctx->stage[b]) cudaFreeHost(ctx->stage[b]);
+    }
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
