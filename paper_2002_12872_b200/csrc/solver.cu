@@ -263,7 +263,11 @@ bool host_pageable(const void* q) {
 int copy_threads() {
   static const int t = [] {
     const unsigned h = std::thread::hardware_concurrency();
-    return int(std::max(1u, std::min(8u, h / 2)));
+    // measured on the GPU box (16 host threads, profiles/r01f_host_copy_threads.txt): a 537 MB
+    // download into fresh pages takes 34.7 / 24.6 / 21.1 / 26.8 ms with 4 / 8 / 12 / 16 threads
+    int v = int(std::max(1u, std::min(12u, h * 3 / 4)));
+    if (const char* e = std::getenv("DPT_COPY_THREADS")) v = std::max(1, std::min(16, atoi(e)));
+    return v;
   }();
   return t;
 }
@@ -275,7 +279,7 @@ void par_memcpy(void* dst, const void* src, size_t bytes) {
     return;
   }
   const size_t per = ((bytes + T - 1) / T + 4095) & ~size_t(4095);
-  std::thread th[8];
+  std::thread th[16];
   int nt = 0;
   for (int t = 1; t < T; ++t) {
     const size_t off = size_t(t) * per;
@@ -308,6 +312,27 @@ cudaError_t stage_copy(dpt_ctx* ctx, void* dst, size_t dpitch, const void* src, 
   cudaStream_t st = ctx->stream;
   const bool d2h = kind == cudaMemcpyDeviceToHost;
   const size_t total = width * height;
+  static const bool timing = std::getenv("DPT_TIMING") != nullptr;
+  const auto t_start = std::chrono::steady_clock::now();
+  double t_host = 0.0;  // seconds in host memcpys
+  struct Report {
+    bool on;
+    const std::chrono::steady_clock::time_point& t0;
+    const double& th;
+    size_t bytes;
+    bool d2h;
+    ~Report() {
+      if (!on) return;
+      const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      std::fprintf(stderr, "[dpt] staged %s %8.1f MB %8.1f us (%5.1f GB/s; host memcpy %8.1f us)\n", d2h ? "d2h" : "h2d",
+                   bytes / 1e6, s * 1e6, bytes / s / 1e9, th * 1e6);
+    }
+  } report{timing, t_start, t_host, total, d2h};
+  auto timed_memcpy = [&](void* dd, const void* ss, size_t nb) {
+    const auto a = std::chrono::steady_clock::now();
+    par_memcpy(dd, ss, nb);
+    if (timing) t_host += std::chrono::duration<double>(std::chrono::steady_clock::now() - a).count();
+  };
   cudaError_t e = stage_ready(ctx);
   if (e != cudaSuccess) return e;
   // chunk geometry: rows per chunk, or bytes per chunk of a single row
@@ -348,7 +373,7 @@ cudaError_t stage_copy(dpt_ctx* ctx, void* dst, size_t dpitch, const void* src, 
       if ((e = cudaEventSynchronize(ctx->stage_ev[i & 1])) != cudaSuccess) return e;
       size_t off;
       const size_t nb = host_span(i, &off);
-      par_memcpy(static_cast<char*>(dst) + off, ctx->stage[i & 1], nb);
+      timed_memcpy(static_cast<char*>(dst) + off, ctx->stage[i & 1], nb);
       if (i + 2 < nch && (e = dev_op(i + 2)) != cudaSuccess) return e;
     }
   } else {
@@ -356,7 +381,7 @@ cudaError_t stage_copy(dpt_ctx* ctx, void* dst, size_t dpitch, const void* src, 
       if (i >= 2 && (e = cudaEventSynchronize(ctx->stage_ev[i & 1])) != cudaSuccess) return e;
       size_t off;
       const size_t nb = host_span(i, &off);
-      par_memcpy(ctx->stage[i & 1], static_cast<const char*>(src) + off, nb);
+      timed_memcpy(ctx->stage[i & 1], static_cast<const char*>(src) + off, nb);
       if ((e = dev_op(i)) != cudaSuccess) return e;
     }
   }
@@ -2177,10 +2202,12 @@ int dpt_dominant_eigenpair(dpt_ctx* ctx, const dpt_problem* p, const dpt_options
     return run_single(ctx, p, best, &o, 0.0, nullptr, nullptr, z_chart, out_mem, rep, nullptr, 0, 0.0, nullptr,
                       z_unit, err);
   }
-  std::vector<double> d = host_levels(p, err);
+  std::vector<double> dcopy;  // device levels only: host levels are read in place
+  if (p->mem != DPT_MEM_HOST) dcopy = host_levels(p, err);
+  const double* dl = p->mem == DPT_MEM_HOST ? p->d : dcopy.data();
   pt.mark("dominant: host_levels");
   const int cx = p->is_complex ? 2 : 1;
-  auto re = [&](int64_t i) { return d[size_t(cx * i)]; };
+  auto re = [&](int64_t i) { return dl[size_t(cx * i)]; };
   int64_t best = 0;  // first argmax of Re d (dpt.cpp:404-406)
   for (int64_t i = 1; i < n; ++i)
     if (re(i) > re(best)) best = i;
@@ -2190,24 +2217,24 @@ int dpt_dominant_eigenpair(dpt_ctx* ctx, const dpt_problem* p, const dpt_options
       if (i == best) continue;
       if (re(i) > re(runner)) runner = i;
     }
-    const double thr = cx == 2 ? threshold_of_c(n, d.data(), o.degeneracy_tol) : threshold_of(n, d.data(), o.degeneracy_tol);
+    const double thr = cx == 2 ? threshold_of_c(n, dl, o.degeneracy_tol) : threshold_of(n, dl, o.degeneracy_tol);
     if (re(best) - re(runner) < thr) {
       if (err) {
         err->i = best;
         err->j = runner;
         err->ei = re(best);
         err->ej = re(runner);
-        err->ei_im = cx == 2 ? d[size_t(2 * best + 1)] : 0.0;
-        err->ej_im = cx == 2 ? d[size_t(2 * runner + 1)] : 0.0;
+        err->ei_im = cx == 2 ? dl[size_t(2 * best + 1)] : 0.0;
+        err->ej_im = cx == 2 ? dl[size_t(2 * runner + 1)] : 0.0;
       }
       set_err(err, DPT_ERR_DEGENERATE, "dominant_eigenpair: ambiguous dominant level");
       return DPT_ERR_DEGENERATE;
     }
   }
   int64_t bj;
-  const bool deg = cx == 2 ? find_degenerate_row_c(n, d.data(), best, o.degeneracy_tol, &bj)
-                           : find_degenerate_row(n, d.data(), best, o.degeneracy_tol, &bj);
-  if (deg) degenerate_error(err, best, bj, d.data(), cx == 2);
+  const bool deg = cx == 2 ? find_degenerate_row_c(n, dl, best, o.degeneracy_tol, &bj)
+                           : find_degenerate_row(n, dl, best, o.degeneracy_tol, &bj);
+  if (deg) degenerate_error(err, best, bj, dl, cx == 2);
   pt.mark("dominant: selection");
   return run_single(ctx, p, best, &o, 0.0, nullptr, nullptr, z_chart, out_mem, rep, nullptr, 0, 0.0, nullptr,
                     z_unit, err);
