@@ -68,7 +68,7 @@ __device__ __forceinline__ double u16_dot_sel(const int4* crow, const double2* v
 }
 
 // Row dot in the lane-rotated chunk order used everywhere for this row:
-// chunks of 4 columns are visited in the order k = (q + rot) & 3 (rot = the
+// chunks of 4 columns are visited in the order k = (q + rot / 2) & 3 (rot = the
 // row's lane), which makes the shared-memory reads conflict-free.  Every
 // evaluation of a given row -- including the w[row] that each block needs --
 // uses the same rot, so the value is bit-identical.  Split into the staged
@@ -83,11 +83,15 @@ __device__ __forceinline__ U16Row u16_load_rot(const int4* crow, const double2* 
   U16Row r;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const int k = (q + rot) & 3;
+    // A quarter-warp (8 lanes) shares one 128-byte wavefront of a 16-byte
+    // load.  Lanes l, l^1 have column rows 64 bytes apart, so chunk k = (q +
+    // l/2) & 3 puts the 8 lanes on 8 distinct 16-byte slots; values 4k..4k+3
+    // are 16-byte chunks 2k, 2k+1 of a 128-byte row, read first-chunk f = l & 1,
+    // again 8 distinct slots.  (Rotating by l itself left the column loads
+    // 2-way conflicted: 0.5 M extra wavefronts per c4 step.)
+    const int k = (q + (rot >> 1)) & 3;
     r.c[q] = crow[k];
-    // values 4k..4k+3 are 16-byte chunks 2k, 2k+1; alternate which one is read
-    // first by (rot >> 2) & 1 so the 32 lanes spread over all 8 bank slots
-    const int f = (rot >> 2) & 1;
+    const int f = rot & 1;
     const double2 x0 = vrow[2 * k + f], x1 = vrow[2 * k + (f ^ 1)];
     r.va[q] = f ? x1 : x0;
     r.vb[q] = f ? x0 : x1;

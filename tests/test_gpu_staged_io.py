@@ -13,6 +13,10 @@ from paper_2002_12872_b200 import problems as pr
 pytestmark = pytest.mark.gpu
 
 
+def _np(x):
+    return x.cpu().numpy() if torch.is_tensor(x) else np.asarray(x)
+
+
 def _dev(p):
     dev = torch.device("cuda")
     if hasattr(p.delta, "rowptr"):
@@ -29,8 +33,8 @@ def test_dense_host_arrays_match_device_inputs(n):
     h = P.iterate_full(p, P.IterationOptions(**o))
     d = P.iterate_full(_dev(p), P.IterationOptions(**o))
     assert int(h.status) == int(d.status) and h.iterations == d.iterations
-    assert np.array_equal(h.state.a, d.state.a)
-    assert np.array_equal(h.eigenvalues, d.eigenvalues) and np.array_equal(h.residuals, d.residuals)
+    assert np.array_equal(h.state.a, _np(d.state.a))
+    assert np.array_equal(h.eigenvalues, _np(d.eigenvalues)) and np.array_equal(h.residuals, _np(d.residuals))
     # pinned caller buffers take the direct path: same bits
     outs = (torch.empty((n, n), dtype=torch.float64, pin_memory=True).numpy(),
             torch.empty(n, dtype=torch.float64, pin_memory=True).numpy(),
@@ -44,4 +48,4 @@ def test_csr_host_arrays_match_device_inputs():
     h = P.dominant_eigenpair(p, P.IterationOptions(**o))
     d = P.dominant_eigenpair(_dev(p), P.IterationOptions(**o))
     assert int(h.status) == int(d.status) and h.iterations == d.iterations
-    assert np.array_equal(h.z_chart, d.z_chart) and h.eigenvalue == d.eigenvalue
+    assert np.array_equal(h.z_chart, _np(d.z_chart)) and h.eigenvalue == d.eigenvalue
