@@ -373,10 +373,13 @@ __global__ void __launch_bounds__(W * 32, MINB)
 
 // Variant table (DPT_U16_VARIANT selects one for tuning runs).  Measured on c4
 // (profiles/r01f_k3_sweep.txt): block-staged trips 98 us (1), 109 us (0); per-warp
-// rings with two stages 91-92 us (6, 8, 10), with one stage 83.4-84.3 us (11, 16-18;
-// default 11).  The binding unit is the L1: every byte of shared memory taken
-// from it costs in-flight gather capacity -- forcing the maximum shared carveout
-// slows every variant to ~146 us, as do configurations that need > 196 KB.
+// rings with two stages 91-92 us (6, 8, 10), with one stage 83.3-84.9 us (11,
+// 16-18; default 16).  Making the column loads bank-conflict-free (rotation by
+// lane / 2) removed 0.53 M shared wavefronts per step and left the time
+// unchanged.  The binding unit is the L1's sector rate for the gathers, and
+// every byte of shared memory taken from it costs in-flight gather capacity:
+// forcing the maximum shared carveout slows every variant to ~146 us, as do
+// configurations that need > 196 KB.
 struct U16Variant {
   int rows, minb, rot;
 };
@@ -389,7 +392,7 @@ static const U16Variant kU16Var[] = {{256, 2, 0}, {256, 2, 1}, {128, 4, 0}, {128
 
 static int u16_variant() {
   const char* e = getenv("DPT_U16_VARIANT");
-  const int v = e ? atoi(e) : 11;  // per-warp pipeline, 8 warps x 2 blocks, one stage: fastest on B200 (tools/u16_sweep.sh)
+  const int v = e ? atoi(e) : 16;  // per-warp pipeline, 16 warps x 1 block per SM, one stage: fastest on B200 (tools/u16_sweep.sh)
   return (v >= 0 && v < int(sizeof(kU16Var) / sizeof(kU16Var[0]))) ? v : 0;
 }
 
