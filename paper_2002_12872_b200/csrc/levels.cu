@@ -73,41 +73,48 @@ __global__ void __launch_bounds__(kLvThreads) levels_scan_kernel(const double* _
     const Top none{0.0, -1};
     merge2(t0, t1, c, none);
   }
-  // warp then block merge (fixed order)
-  for (int o = 16; o > 0; o >>= 1) {
-    Top u0{__shfl_xor_sync(0xffffffffu, t0.v, o), __shfl_xor_sync(0xffffffffu, t0.i, o)};
-    Top u1{__shfl_xor_sync(0xffffffffu, t1.v, o), __shfl_xor_sync(0xffffffffu, t1.i, o)};
-    merge2(t0, t1, u0, u1);
-    lr = fmin(lr, __shfl_xor_sync(0xffffffffu, lr, o));
-    hr = fmax(hr, __shfl_xor_sync(0xffffffffu, hr, o));
-    li = fmin(li, __shfl_xor_sync(0xffffffffu, li, o));
-    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-    nans += __shfl_xor_sync(0xffffffffu, nans, o);
-  }
-  __shared__ double sh[kLvThreads / 32][9];
-  const int w = threadIdx.x >> 5;
-  if ((threadIdx.x & 31) == 0) {
-    sh[w][0] = t0.v;
-    sh[w][1] = double(t0.i);
-    sh[w][2] = t1.v;
-    sh[w][3] = double(t1.i);
-    sh[w][4] = lr;
-    sh[w][5] = hr;
-    sh[w][6] = li;
-    sh[w][7] = hi;
-    sh[w][8] = nans;
-  }
-  __syncthreads();
+  // block merge (the order does not matter: top-2 under a total order, exact
+  // min / max, integer-valued counts), result in thread 0
+  auto block_merge = [&]() {
+    for (int o = 16; o > 0; o >>= 1) {
+      Top u0{__shfl_xor_sync(0xffffffffu, t0.v, o), __shfl_xor_sync(0xffffffffu, t0.i, o)};
+      Top u1{__shfl_xor_sync(0xffffffffu, t1.v, o), __shfl_xor_sync(0xffffffffu, t1.i, o)};
+      merge2(t0, t1, u0, u1);
+      lr = fmin(lr, __shfl_xor_sync(0xffffffffu, lr, o));
+      hr = fmax(hr, __shfl_xor_sync(0xffffffffu, hr, o));
+      li = fmin(li, __shfl_xor_sync(0xffffffffu, li, o));
+      hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+      nans += __shfl_xor_sync(0xffffffffu, nans, o);
+    }
+    __shared__ double sh[kLvThreads / 32][9];
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+      sh[w][0] = t0.v;
+      sh[w][1] = double(t0.i);
+      sh[w][2] = t1.v;
+      sh[w][3] = double(t1.i);
+      sh[w][4] = lr;
+      sh[w][5] = hr;
+      sh[w][6] = li;
+      sh[w][7] = hi;
+      sh[w][8] = nans;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int q = 1; q < kLvThreads / 32; ++q) {
+        merge2(t0, t1, Top{sh[q][0], int64_t(sh[q][1])}, Top{sh[q][2], int64_t(sh[q][3])});
+        lr = fmin(lr, sh[q][4]);
+        hr = fmax(hr, sh[q][5]);
+        li = fmin(li, sh[q][6]);
+        hi = fmax(hi, sh[q][7]);
+        nans += sh[q][8];
+      }
+    }
+    __syncthreads();
+  };
+  block_merge();
   __shared__ bool last;
   if (threadIdx.x == 0) {
-    for (int q = 1; q < kLvThreads / 32; ++q) {
-      merge2(t0, t1, Top{sh[q][0], int64_t(sh[q][1])}, Top{sh[q][2], int64_t(sh[q][3])});
-      lr = fmin(lr, sh[q][4]);
-      hr = fmax(hr, sh[q][5]);
-      li = fmin(li, sh[q][6]);
-      hi = fmax(hi, sh[q][7]);
-      nans += sh[q][8];
-    }
     double* bp = part + size_t(blockIdx.x) * 9;
     bp[0] = t0.v;
     bp[1] = double(t0.i);
@@ -122,26 +129,36 @@ __global__ void __launch_bounds__(kLvThreads) levels_scan_kernel(const double* _
     last = atomicAdd(counter, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (!last || threadIdx.x != 0) return;
-  fence_acq_rel_gpu();
-  Top g0{0.0, -1}, g1{0.0, -1};
-  double glr = INFINITY, ghr = -INFINITY, gli = INFINITY, ghi = -INFINITY, gn = 0.0;
-  for (unsigned b = 0; b < gridDim.x; ++b) {
+  if (!last) return;
+  // the elected block merges the per-block parts with all its threads (a
+  // serial loop over ~300 parts cost ~170 us of dependent L2 round trips)
+  if (threadIdx.x == 0) fence_acq_rel_gpu();
+  __syncthreads();
+  t0 = Top{0.0, -1};
+  t1 = Top{0.0, -1};
+  lr = INFINITY;
+  hr = -INFINITY;
+  li = INFINITY;
+  hi = -INFINITY;
+  nans = 0.0;
+  for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
     const double* bp = part + size_t(b) * 9;
-    merge2(g0, g1, Top{__ldcg(bp + 0), int64_t(__ldcg(bp + 1))}, Top{__ldcg(bp + 2), int64_t(__ldcg(bp + 3))});
-    glr = fmin(glr, __ldcg(bp + 4));
-    ghr = fmax(ghr, __ldcg(bp + 5));
-    gli = fmin(gli, __ldcg(bp + 6));
-    ghi = fmax(ghi, __ldcg(bp + 7));
-    gn += __ldcg(bp + 8);
+    merge2(t0, t1, Top{__ldcg(bp + 0), int64_t(__ldcg(bp + 1))}, Top{__ldcg(bp + 2), int64_t(__ldcg(bp + 3))});
+    lr = fmin(lr, __ldcg(bp + 4));
+    hr = fmax(hr, __ldcg(bp + 5));
+    li = fmin(li, __ldcg(bp + 6));
+    hi = fmax(hi, __ldcg(bp + 7));
+    nans += __ldcg(bp + 8);
   }
-  out[0] = double(g0.i);
-  out[1] = double(g1.i);
-  out[2] = glr;
-  out[3] = ghr;
-  out[4] = gli;
-  out[5] = ghi;
-  out[6] = gn;
+  block_merge();
+  if (threadIdx.x != 0) return;
+  out[0] = double(t0.i);
+  out[1] = double(t1.i);
+  out[2] = lr;
+  out[3] = hr;
+  out[4] = li;
+  out[5] = hi;
+  out[6] = nans;
   *counter = 0u;
 }
 
