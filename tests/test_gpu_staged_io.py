@@ -49,3 +49,26 @@ def test_csr_host_arrays_match_device_inputs():
     d = P.dominant_eigenpair(_dev(p), P.IterationOptions(**o))
     assert int(h.status) == int(d.status) and h.iterations == d.iterations
     assert np.array_equal(h.z_chart, _np(d.z_chart)) and h.eigenvalue == d.eigenvalue
+
+
+def test_dominant_selection_large_host_levels():
+    """n >= 2^16 host levels are scanned on the device (temporary copy): same
+    row, same ambiguity / degeneracy payloads as the host scans."""
+    n = 70000
+    d = np.linspace(0.0, 1.0, n)
+    z = P.CsrMatrix(n, np.zeros(n + 1, dtype=np.int64), np.zeros(0, dtype=np.int32), np.zeros(0))
+    r = P.dominant_eigenpair(P.PartitionedProblem(d, z, 0.5))
+    assert r.row == n - 1 and r.iterations == 1 and r.eigenvalue == 1.0
+    tie = d.copy()
+    tie[5] = 1.0  # runner-up equal to the maximum: ambiguous, payload (first max, runner-up)
+    with pytest.raises(P.DegenerateSpectrum) as e:
+        P.dominant_eigenpair(P.PartitionedProblem(tie, z, 0.5))
+    assert (e.value.first(), e.value.second()) == (5, n - 1)
+    # same pair from the device-resident levels
+    with pytest.raises(P.DegenerateSpectrum) as e2:
+        P.dominant_eigenpair(P.PartitionedProblem(torch.as_tensor(tie, device="cuda"), z, 0.5))
+    assert (e2.value.first(), e2.value.second()) == (5, n - 1)
+    nan = d.copy()
+    nan[7] = np.nan  # NaN levels take the host scans
+    r = P.dominant_eigenpair(P.PartitionedProblem(nan, z, 0.5))
+    assert r.row == n - 1
