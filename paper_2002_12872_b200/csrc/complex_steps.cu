@@ -337,15 +337,196 @@ __global__ void __launch_bounds__(kSingleCThreads)
   }
 }
 
-int single_cplx_ntiles(int64_t n, int dense) {
+// ---------------------------------------- complex row map, 16 per row ----
+// Complex CSR with exactly 16 nonzeros per row (c4 with complex data): the
+// per-warp pipeline of the real K3 (single_u16.cu) over a trip-major copy of
+// the CSR built once per problem (u16c_build_kernel): for 32-row trip t,
+// columns at cols_t[t][q/4][lane][4] and values at vals_t[t][q][lane] (one
+// complex each), so every stage read is a conflict-free 16-byte LDS and lane L
+// still owns row 32 t + L with its entries in CSR order q = 0..15 -- the same
+// complex products and sums, in the same order, as row_dot_c (bit-identical to
+// the general kernel, and to the w[row] each warp evaluates from the CSR).
+constexpr int kU16cWarps = 8;
+constexpr int kU16cTripBytes = 32 * 16 * 4 + 32 * 16 * 16;  // columns 2 KiB + values 8 KiB
+static_assert(kU16cTripBytes == 10240, "trip layout");
+
+__global__ void u16c_build_kernel(const int32_t* __restrict__ cols, const double* __restrict__ vals, int64_t n,
+                                  int32_t* __restrict__ ct, double* __restrict__ vt) {
+  const int64_t total = n * 16;
+  for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t m = e >> 4, q = e & 15, t = m >> 5, L = m & 31;
+    ct[t * 512 + (q >> 2) * 128 + L * 4 + (q & 3)] = cols[e];
+    const int64_t d = t * 512 + q * 32 + L;
+    vt[2 * d] = vals[2 * e];
+    vt[2 * d + 1] = vals[2 * e + 1];
+  }
+}
+
+cudaError_t launch_u16c_build(const int32_t* cols, const double* vals, int64_t n, int32_t* ct, double* vt,
+                              cudaStream_t st) {
+  const int64_t blocks = (n * 16 + 255) / 256;
+  u16c_build_kernel<<<unsigned(blocks < 148 * 16 ? (blocks > 0 ? blocks : 1) : 148 * 16), 256, 0, st>>>(cols, vals, n,
+                                                                                                     ct, vt);
+  return cudaGetLastError();
+}
+
+__global__ void __launch_bounds__(kU16cWarps * 32, 1)
+    single_cplx_u16w_kernel(DevSolve s, DevCsr D, const int32_t* __restrict__ ct, const double* __restrict__ vt,
+                            int64_t row, int64_t ntrips) {
+  if (s.state->done) return;
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ uint64_t bar[kU16cWarps];
+  __shared__ double red[kU16cWarps][5];
+  const int jl = launch_index(s);
+  const int64_t n = s.n;
+  const double* __restrict__ z = s.slots + size_t((jl - 1) % s.nslots) * size_t(s.slot_elems);
+  double* __restrict__ zo = s.slots + size_t(jl % s.nslots) * size_t(s.slot_elems);
+  const cd lamk = lamc_of(s, jl), lamc = cmake(s.lambda, s.lambda_im);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint8_t* stage = smem + size_t(warp) * kU16cTripBytes;
+  const int64_t stride = int64_t(gridDim.x) * kU16cWarps;
+  int64_t t = int64_t(blockIdx.x) * kU16cWarps + warp;
+  auto issue = [&](int64_t trip) {
+    const int64_t nr = (n - trip * 32) < 32 ? (n - trip * 32) : 32;
+    // a partial last trip is still laid out with 32 lanes (rows >= n absent):
+    // copy the whole trip slab the build wrote (cols / vals beyond the rows are
+    // never read)
+    (void)nr;
+    mbar_arrive_expect_tx(&bar[warp], uint32_t(kU16cTripBytes));
+    bulk_load(stage, ct + trip * 512, 2048u, &bar[warp]);
+    bulk_load(stage + 2048, vt + trip * 1024, 8192u, &bar[warp]);
+  };
+  if (lane == 0) {
+    mbar_init(&bar[warp], 1);
+    fence_mbar_init();
+    if (t < ntrips) issue(t);
+  }
+  __syncwarp();
+  const cd wr = row_dot_c<1>(D, nullptr, n, 0, row, z, 0);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    s.dvec[(jl - 1) & 1][0] = wr.x;  // w[row] of z_{j-1} for the fold's eps
+    s.dvec[(jl - 1) & 1][1] = wr.y;
+  }
+  const cd trow = cmake(s.theta[2 * row], s.theta[2 * row + 1]);
+  const cd eps = cadd(trow, cmul(lamc, wr));
+  double num = 0.0, den = 0.0, t_step = 0.0, t_max = 0.0, t_nonfin = 0.0;
+  for (int it = 0; t < ntrips; ++it, t += stride) {
+    mbar_wait(&bar[warp], uint32_t(it) & 1u);
+    const int64_t m = t * 32 + lane;
+    int4 c4[4];
+    double2 v[16];
+    const int4* cs = reinterpret_cast<const int4*>(stage) + lane;
+    const double2* vs = reinterpret_cast<const double2*>(stage + 2048) + lane;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) c4[k] = cs[k * 32];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = vs[q * 32];
+    {  // the stage is refilled right below: make every lane's reads land first
+      unsigned long long x = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) x ^= (unsigned long long)(unsigned)c4[k].x ^ c4[k].y ^ c4[k].z ^ c4[k].w;
+#pragma unroll
+      for (int q = 0; q < 16; ++q) x ^= __double_as_longlong(v[q].x) ^ __double_as_longlong(v[q].y);
+      if (x == 0x5bd1e9955bd1e995ull) red[warp][4] = 0.0;  // data-dependent: waits for the loads (red is rewritten below)
+    }
+    __syncwarp();  // every lane holds its row: refill the stage
+    if (lane == 0 && t + stride < ntrips) issue(t + stride);
+    if (m < n) {
+      const cd zm = cmake(z[2 * m], z[2 * m + 1]);
+      const cd tm = cmake(s.theta[2 * m], s.theta[2 * m + 1]);
+      const int32_t c[16] = {c4[0].x, c4[0].y, c4[0].z, c4[0].w, c4[1].x, c4[1].y, c4[1].z, c4[1].w,
+                             c4[2].x, c4[2].y, c4[2].z, c4[2].w, c4[3].x, c4[3].y, c4[3].z, c4[3].w};
+      double2 zg[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) zg[q] = *reinterpret_cast<const double2*>(z + 2 * size_t(c[q]));
+      cd w = cmake(0.0, 0.0);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) w = cadd(w, cmul(cmake(v[q].x, v[q].y), cmake(zg[q].x, zg[q].y)));
+      cd val;
+      if (m == row) {
+        val = cmake(1.0, 0.0);
+      } else {
+        const cd g = s.gapmat ? cmake(s.gapmat[2 * m], s.gapmat[2 * m + 1]) : crecip(csub(trow, tm));
+        val = cmul(cmul(lamk, g), csub(w, cmul(wr, zm)));
+      }
+      zo[2 * m] = val.x;
+      zo[2 * m + 1] = val.y;
+      t_step = fmax(t_step, cabs_(csub(val, zm)));
+      t_max = fmax(t_max, cabs_(val));
+      t_nonfin += cfinite(val) ? 0.0 : 1.0;
+      const cd r = cadd(cmul(csub(tm, eps), zm), cmul(lamc, w));
+      num = fmax(num, cabs_(r));
+      den = fmax(den, cabs_(zm));
+    }
+  }
+  num = warp_max(num);
+  den = warp_max(den);
+  t_step = warp_max(t_step);
+  t_max = warp_max(t_max);
+  t_nonfin = warp_sum(t_nonfin);
+  if (lane == 0) {
+    red[warp][0] = num;
+    red[warp][1] = den;
+    red[warp][2] = t_step;
+    red[warp][3] = t_max;
+    red[warp][4] = t_nonfin;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a[5] = {0, 0, 0, 0, 0};
+    for (int ww = 0; ww < kU16cWarps; ++ww) {
+      a[0] = fmax(a[0], red[ww][0]);
+      a[1] = fmax(a[1], red[ww][1]);
+      a[2] = fmax(a[2], red[ww][2]);
+      a[3] = fmax(a[3], red[ww][3]);
+      a[4] += red[ww][4];
+    }
+    const int tn = blockIdx.x, ntn = s.ntn;
+    s.rowpart[rp_index(0, 0, tn, 1, ntn)] = 0.0;
+    s.rowpart[rp_index(1, 0, tn, 1, ntn)] = a[0];
+    s.rowpart[rp_index(2, 0, tn, 1, ntn)] = a[1];
+    s.rowpart[rp_index(3, 0, tn, 1, ntn)] = 0.0;
+    double* tp = s.tilepart + size_t(tn) * 4;
+    tp[0] = a[2];
+    tp[1] = a[3];
+    tp[2] = a[4];
+    tp[3] = 0.0;
+  }
+}
+
+static bool u16c_enabled() {
+  const char* e = getenv("DPT_CPLX_U16");
+  return !(e && e[0] == '0');
+}
+
+int single_cplx_u16_grid(int64_t n) {
+  const int64_t trips = (n + 31) / 32;
+  const int64_t blocks = (trips + kU16cWarps - 1) / kU16cWarps;
+  return int(blocks < 148 ? (blocks > 0 ? blocks : 1) : 148);
+}
+
+int single_cplx_ntiles(int64_t n, int dense, int u16) {
+  if (u16 && !dense && u16c_enabled()) return single_cplx_u16_grid(n);
   const int rows_per_iter = kSingleCThreads / (dense ? 32 : 1);
   int64_t b = (n + rows_per_iter - 1) / rows_per_iter;
   if (b > 148 * 8) b = 148 * 8;
   return int(b < 1 ? 1 : b);
 }
 
-cudaError_t launch_single_cplx(const DevSolve& s, const DevCsr& d, const double* B, int64_t row, cudaStream_t st) {
-  const unsigned grid = unsigned(single_cplx_ntiles(s.n, B != nullptr));
+cudaError_t launch_single_cplx(const DevSolve& s, const DevCsr& d, const double* B, const int32_t* u16c_cols,
+                               const double* u16c_vals, int64_t row, cudaStream_t st) {
+  if (!B && u16c_cols && u16c_enabled()) {
+    constexpr int smem = kU16cWarps * kU16cTripBytes;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(single_cplx_u16w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      attr = true;
+    }
+    single_cplx_u16w_kernel<<<single_cplx_u16_grid(s.n), kU16cWarps * 32, smem, st>>>(s, d, u16c_cols, u16c_vals, row,
+                                                                                       (s.n + 31) / 32);
+    return cudaGetLastError();
+  }
+  const unsigned grid = unsigned(single_cplx_ntiles(s.n, B != nullptr, 0));
   if (B)
     single_cplx_kernel<2><<<grid, kSingleCThreads, 0, st>>>(s, d, B, row);
   else

@@ -54,8 +54,12 @@ cudaError_t launch_single_step(const DevSolve& s, const DevCsr& d, const double*
 // complex_steps.cu (complex K2 / K3)
 int csr_cplx_ntiles(int64_t rows, int64_t n);
 cudaError_t launch_csr_step_cplx(const DevSolve& s, const DevSell& d, cudaStream_t st);
-int single_cplx_ntiles(int64_t n, int dense);
-cudaError_t launch_single_cplx(const DevSolve& s, const DevCsr& d, const double* B, int64_t row, cudaStream_t st);
+int single_cplx_ntiles(int64_t n, int dense, int u16);
+// u16c_cols / u16c_vals: trip-major copy of a uniform-16 complex CSR (launch_u16c_build), or null
+cudaError_t launch_single_cplx(const DevSolve& s, const DevCsr& d, const double* B, const int32_t* u16c_cols,
+                               const double* u16c_vals, int64_t row, cudaStream_t st);
+cudaError_t launch_u16c_build(const int32_t* cols, const double* vals, int64_t n, int32_t* ct, double* vt,
+                              cudaStream_t st);
 
 // fold.cu (K4)
 int fold_blocks(int64_t rows);

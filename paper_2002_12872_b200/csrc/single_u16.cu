@@ -315,6 +315,15 @@ __global__ void __launch_bounds__(W * 32, MINB)
     if (m < n)
       rd = u16_load_rot(reinterpret_cast<const int4*>(base + lane * 64),
                         reinterpret_cast<const double2*>(base + 32 * 64 + lane * 128), lane);
+    {  // the stage is refilled right below: make every lane's reads land first
+      unsigned long long x = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        x ^= (unsigned long long)(unsigned)(rd.c[k].x ^ rd.c[k].y ^ rd.c[k].z ^ rd.c[k].w) ^
+             __double_as_longlong(rd.va[k].x) ^ __double_as_longlong(rd.va[k].y) ^
+             __double_as_longlong(rd.vb[k].x) ^ __double_as_longlong(rd.vb[k].y);
+      if (x == 0x5bd1e9955bd1e995ull) red[warp][4] = 0.0;  // data-dependent: waits for the loads (red is rewritten below)
+    }
     __syncwarp();  // every lane holds its row: the stage can be refilled
     if (lane == 0 && t + S * stride < ntrips) issue(t + S * stride, st);
     if (m < n) {

@@ -589,6 +589,7 @@ struct DevProblem {
   DBuf dmap;  // CUtensorMap for dense Delta
   int big = 1;  // dense tile configuration (dense_cfg_for)
   int uniform16 = 0;  // CSR with exactly 16 nonzeros per row (K3 fast path)
+  DBuf u16c_cols, u16c_vals;  // complex uniform-16: trip-major copy (complex_steps.cu)
   DBuf s_cols, s_vals, s_off, s_lcol, s_llen, s_pos;  // SELL-32 image (K2)
   DBuf s_perm, s_inv;                                 // column relabelling (bank balance), empty = identity
   int64_t nslices = 0, s_npad = 0;
@@ -771,7 +772,7 @@ void upload(DevProblem& dp, dpt_ctx* ctx, const dpt_problem* p, dpt_error_info* 
     }
     if (sell) {
       build_sell_device(dp, st, err);
-    } else if (n > 0 && !dp.cplx && nnz == 16 * n) {  // K3's uniform-16 fast path, tested on the device
+    } else if (n > 0 && nnz == 16 * n) {  // K3's uniform-16 fast path, tested on the device
       DBuf bad;
       dalloc(bad, 16, err);
       CK(cudaMemsetAsync(bad.p, 0, 4, st));
@@ -780,6 +781,15 @@ void upload(DevProblem& dp, dpt_ctx* ctx, const dpt_problem* p, dpt_error_info* 
       CK(cudaMemcpyAsync(&hb, bad.p, 4, cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
       dp.uniform16 = hb == 0 ? 1 : 0;
+      if (dp.uniform16 && dp.cplx) {  // complex: trip-major copy for the per-warp pipeline
+        const int64_t trips = (n + 31) / 32;
+        dalloc(dp.u16c_cols, size_t(trips) * 512 * 4, err);
+        dalloc(dp.u16c_vals, size_t(trips) * 512 * 16, err);
+        CK(cudaMemsetAsync(dp.u16c_cols.p, 0, size_t(trips) * 512 * 4, st));
+        CK(cudaMemsetAsync(dp.u16c_vals.p, 0, size_t(trips) * 512 * 16, st));
+        CK(launch_u16c_build(dp.cols.as<int32_t>(), dp.vals.as<double>(), n, dp.u16c_cols.as<int32_t>(),
+                             dp.u16c_vals.as<double>(), st));
+      }
     }
   }
 }
@@ -827,7 +837,7 @@ void make_work(Work& w, dpt_ctx* ctx, DevProblem& dp, Mode mode, int64_t row0, i
     s.ntn = csr_ntn(dp.n);
     w.ntiles_step = dp.cplx ? csr_cplx_ntiles(rows, dp.n) : csr_step_ntiles(rows, dp.n);
   } else if (dp.cplx) {
-    s.ntn = single_cplx_ntiles(dp.n, dp.kind == DPT_DELTA_DENSE);
+    s.ntn = single_cplx_ntiles(dp.n, dp.kind == DPT_DELTA_DENSE, dp.u16c_cols.p != nullptr);
     w.ntiles_step = s.ntn;
   } else {
     const int sm = single_mode(dp.kind == DPT_DELTA_DENSE, dp.uniform16);
@@ -961,8 +971,8 @@ void step_launch(dpt_ctx* ctx, Work& w, DevProblem& dp, Mode mode, int64_t row, 
   else if (mode == MODE_CSR_FULL)
     CK(launch_csr_step(w.s, dp.sell(), ctx->stream));
   else if (dp.cplx)
-    CK(launch_single_cplx(w.s, dp.csr(), dp.kind == DPT_DELTA_DENSE ? dp.delta.as<double>() : nullptr, row,
-                          ctx->stream));
+    CK(launch_single_cplx(w.s, dp.csr(), dp.kind == DPT_DELTA_DENSE ? dp.delta.as<double>() : nullptr,
+                          dp.u16c_cols.as<int32_t>(), dp.u16c_vals.as<double>(), row, ctx->stream));
   else
     CK(launch_single_step(w.s, dp.csr(), dp.kind == DPT_DELTA_DENSE ? dp.delta.as<double>() : nullptr, row,
                           single_mode(dp.kind == DPT_DELTA_DENSE, dp.uniform16), ctx->stream));
@@ -1001,7 +1011,7 @@ void key_add(std::vector<unsigned char>& k, const T& v) {
 // between calls in one process): part of the loop-graph key, so a graph
 // captured under one selection is never replayed under another.
 static const char* const kKernelKnobs[] = {"DPT_U16_VARIANT", "DPT_DENSE_CFG", "DPT_SMALL8", "DPT_CSR_ROWS",
-                                           "DPT_SELL_SCHED", "DPT_SELL_RELABEL", "DPT_DENSE_SK", "DPT_SHARD_EMULATE"};
+                                           "DPT_SELL_SCHED", "DPT_SELL_RELABEL", "DPT_CPLX_U16", "DPT_DENSE_SK", "DPT_SHARD_EMULATE"};
 
 void key_add_knobs(std::vector<unsigned char>& k) {
   for (const char* name : kKernelKnobs) {

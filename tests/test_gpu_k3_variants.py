@@ -43,3 +43,26 @@ def test_k3_variants_agree(variant_env, n):
                 ref = g
             else:
                 assert g.iterations == ref.iterations and np.array_equal(g.z_chart, ref.z_chart), v
+
+
+@pytest.mark.parametrize("n", [20, 1000, 70001])
+def test_complex_u16_pipeline_matches_general_kernel(variant_env, n):
+    """Complex data with 16 nonzeros per row: the per-warp pipeline over the
+    trip-major CSR copy is bit-identical to the general complex row map (same
+    products and sums in CSR order) and matches the reference's complex path."""
+    p, o, _ = pr.config("c4b", n)
+    p = P.PartitionedProblem(p.d, p.delta, p.lam * (1 + 0.5j))
+    outs = {}
+    for flag in ("0", "1"):
+        os.environ["DPT_CPLX_U16"] = flag
+        outs[flag] = P.dominant_eigenpair(p, P.IterationOptions(**o))
+    os.environ.pop("DPT_CPLX_U16", None)
+    a, b = outs["0"], outs["1"]
+    assert int(a.status) == int(b.status) and a.iterations == b.iterations
+    assert np.array_equal(a.z_chart, b.z_chart) and a.eigenvalue == b.eigenvalue
+    from oracle.bind import ComplexReference, available
+    if available("reference"):
+        r = ComplexReference().dominant_eigenpair(p, o)
+        assert int(b.status) == r.status and abs(b.iterations - r.iterations) <= 1
+        if r.status == 0:
+            assert abs(b.eigenvalue - r.eigenvalue) <= 1e-10 * max(1.0, abs(r.eigenvalue))
