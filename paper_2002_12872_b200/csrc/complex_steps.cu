@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(kSingleCThreads)
 // still owns row 32 t + L with its entries in CSR order q = 0..15 -- the same
 // complex products and sums, in the same order, as row_dot_c (bit-identical to
 // the general kernel, and to the w[row] each warp evaluates from the CSR).
-constexpr int kU16cWarps = 8;
+constexpr int kU16cWarps = 8;  // measured: 10 warps (100 KB of stages) 0.111 ms vs 0.108 ms
 constexpr int kU16cTripBytes = 32 * 16 * 4 + 32 * 16 * 16;  // columns 2 KiB + values 8 KiB
 static_assert(kU16cTripBytes == 10240, "trip layout");
 
