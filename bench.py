@@ -1,13 +1,20 @@
 #!/usr/bin/env python
 """bench.py -- DPT iteration throughput on B200 (BASELINE.json metric).
 
-Workload (N=1): BASELINE.json configs[1] -- dense unsymmetric full
-diagonalisation, n = 4096, FP64, seed 1, lambda = 0.5/sqrt(n) (SURVEY.md §8(d)
-recipe, synthetic).  Under reference semantics it terminates Diverged at k = 4,
-so, as BASELINE.md prescribes, throughput is timed over a fixed number of map
-applications (iterate_fixed semantics, dpt.hpp:94-96): one STEP = one DPT
-iteration = one fused K1 launch (P = A Delta^T GEMM + map + residual + step
-norm epilogue) + the fold/decision kernels.  Metric unit: iterations / s.
+Workloads (SURVEY.md §8(d) recipe, synthetic, seeded):
+  N = 1 (default): BASELINE.json configs[1] -- dense unsymmetric full
+          diagonalisation, n = 4096, FP64, seed 1, lambda = 0.5/sqrt(n).  Under
+          reference semantics it terminates Diverged at k = 4, so, as BASELINE.md
+          prescribes, throughput is timed over a fixed number of map applications
+          (iterate_fixed semantics, dpt.hpp:94-96).
+  N > 1:  BASELINE.json configs[4] -- dense symmetric n = 32768, seed 4, the
+          north_star's column-sharded multi-GPU config: rows of A (the paper's
+          columns) sharded over the ranks, Delta replicated, one NCCL
+          max-allreduce of the step statistics per iteration, final allgather.
+          (--workload c2|c5 overrides the choice.)
+One STEP = one DPT iteration = one fused K1 launch (P = A Delta^T GEMM + map +
+residual + step-norm epilogue) + the fold (+ allreduce + decision) kernels.
+Metric unit: iterations / s (whole job: every rank advances the same iteration).
 
   value   device-resident: inputs in HBM, CUDA events on the solver's stream
           around exactly K steps, max over ranks.
@@ -19,11 +26,14 @@ norm epilogue) + the fold/decision kernels.  Metric unit: iterations / s.
           peak measured in this run (DMMA probe; MEASURED_PEAKS.json has no FP64).
   cpu_baseline  the reference's own implementation (oracle/_ref, compiled from
           /root/reference/proj/src) on a bounded row sample, all host threads.
+  time_to_converge  (N = 1) the public iterate_full call, device-resident
+          inputs, to the terminal status: c2 (Diverged 4) and its converging
+          companion c2b (theta_i = i).
 
+--gpus N without torchrun re-launches itself under torch.distributed.run with
+N ranks (and fails if fewer than N GPUs are visible).
 --impl reference times only the reference arm (rank 0; other ranks exit 0).
 --baselines prints the per-config reference-vs-B200 table.
-N > 1 (torchrun): rows of A sharded over ranks (strong scaling of the same
-n = 4096 solve), per-iteration NCCL max-allreduce of the step statistics.
 """
 from __future__ import annotations
 
@@ -41,17 +51,16 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-N_DEFAULT = 4096
-
-
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--n", type=int, default=N_DEFAULT, help="override n (testing only)")
-    ap.add_argument("--e2e-calls", type=int, default=5)
+    ap.add_argument("--workload", default="auto", choices=["auto", "c2", "c5"],
+                    help="auto: c2 (configs[1]) at N = 1, c5 (configs[4]) at N > 1")
+    ap.add_argument("--size", type=int, default=0, help="override n (testing only)")
+    ap.add_argument("--e2e-calls", type=int, default=0, help="public calls timed for e2e (0: 5 for c2, 1 for c5)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--baselines", action="store_true",
                     help="instead of the bench line: the reference's own CPU solver on every BASELINE config "
@@ -60,23 +69,37 @@ def parse():
     return ap.parse_args()
 
 
-def workload_config(n, world):
+WORKLOADS = {
+    "c2": ("BASELINE configs[1]: dense unsymmetric DPT full diagonalisation, n={n}, FP64, seed 1, "
+           "theta ~ sorted U(0,n) with adjacent gaps >= 1e-3, Delta N(0,1) off-diagonal, "
+           "lambda=0.5/sqrt(n); step = one map application (iterate_fixed semantics)", 4096),
+    "c5": ("BASELINE configs[4]: dense symmetric DPT full diagonalisation, n={n}, FP64, seed 4, theta_i = i, "
+           "Delta symmetrised N(0,1) with zero diagonal, lambda=0.5/sqrt(n), tol 1e-12; rows of A column-"
+           "sharded over the ranks, Delta replicated; step = one map application (iterate_fixed semantics)", 32768),
+}
+
+
+def pick_workload(args, world):
+    wl = args.workload if args.workload != "auto" else ("c2" if world == 1 else "c5")
+    return wl, (args.size or WORKLOADS[wl][1])
+
+
+def workload_config(wl, n, world):
     return {
-        "workload": f"BASELINE configs[1]: dense unsymmetric DPT full diagonalisation, n={n}, FP64, seed 1, "
-                    "theta ~ sorted U(0,n) with adjacent gaps >= 1e-3, Delta N(0,1) off-diagonal, "
-                    "lambda=0.5/sqrt(n); step = one map application (iterate_fixed semantics)",
+        "workload": WORKLOADS[wl][0].format(n=n),
         "n": n,
         "lambda": 0.5 / math.sqrt(n),
         "flop_per_step": 2.0 * n ** 3,
-        "l2": "inputs larger than L2: A_k 128 MiB + Delta 128 MiB per step vs 126 MB L2 (no flush needed)",
-        "parallelism": f"rows of A sharded over {world} rank(s), NCCL max-allreduce per iteration" if world > 1
-        else "single GPU",
+        "l2": f"inputs larger than L2: A_k {n * n * 8 / 2**20 / world:.0f} MiB per rank + Delta "
+              f"{n * n * 8 / 2**20:.0f} MiB per step vs 126 MB L2 (no flush needed)",
+        "parallelism": f"rows of A sharded over {world} rank(s) (dp{world}), Delta replicated, NCCL max-allreduce "
+                       "per iteration" if world > 1 else "single GPU",
     }
 
 
-def make_inputs(n, pinned=False):
+def make_inputs(wl, n, pinned=False):
     from paper_2002_12872_b200 import problems as pr
-    p, o, desc = pr.config("c2", n)
+    p, o, desc = pr.config(wl, n)
     if pinned:
         import torch
         d = torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
@@ -184,40 +207,57 @@ def first_iterate_rows(p, rows):
     return out
 
 
+def reference_inputs(wl, n):
+    """The reference arm's inputs, built by oracle/gen.py (numpy restatement of
+    the same recipe) so the arm maps none of this repo's shared libraries."""
+    from types import SimpleNamespace
+    from oracle import gen
+    d, delta, lam = gen.dense_config(wl, n)
+    return SimpleNamespace(d=d, delta=delta, lam=lam)
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(max(args.gpus, 1))))
     if rank != 0:
         return 0
     from oracle.bind import available
-    n = args.n
-    cfg = workload_config(n, 1)
+    wl, n = pick_workload(args, world)
+    cfg = workload_config(wl, n, world)
     if not available("reference"):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libdynspec_ref.so not built"}))
         return 0
-    p, _ = make_inputs(n)
+    p = reference_inputs(wl, n)
     threads = os.cpu_count() or 1
-    rpt = 4
+    rpt = 4 if wl == "c2" else 1  # c5: one reference row is n^2 = 1.1e9 complex MACs (~4 s)
     a_rows = first_iterate_rows(p, threads * rpt)
-    for _ in range(max(args.warmup, 0)):
+    for _ in range(max(min(args.warmup, 1), 0)):
         reference_sample(p, a_rows, threads, rpt, p.lam)
     secs = []
-    for _ in range(args.steps):
+    for _ in range(args.steps if wl == "c2" else min(args.steps, 2)):
         s, rows, _ = reference_sample(p, a_rows, threads, rpt, p.lam)
         secs.append(s)
     t = float(np.mean(secs))
-    it_s = (threads * rpt / n) / t
-    sample = (f"{threads * rpt} of {n} rows of one c2 iteration per step (reference matmul(A_rows, delta_t) "
+    rows = threads * rpt
+    it_s = (rows / n) / t
+    sample = (f"{rows} of {n} rows of one {wl} iteration per step (reference matmul(A_rows, delta_t) "
               f"+ map, complex<double> as in the reference), {threads} threads x {rpt} rows; "
-              "iterations/s = sampled fraction / wall time")
+              f"iterations/s = sampled fraction / wall time (time per iteration extrapolated x{n / rows:.1f}); "
+              "inputs from oracle/gen.py")
     print(json.dumps({
-        "impl": "reference", "metric": "DPT iterations/s (dense n=4096 FP64 step)", "value": it_s,
-        "unit": "iter/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 / it_s, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64 (complex<double>)", "data": "synthetic", "config": cfg,
+        "impl": "reference", "metric": metric_name(n), "value": it_s,
+        "unit": "iter/s", "n_gpus": 0, "steps": len(secs), "warmup": args.warmup,
+        "ms_per_step": 1e3 / it_s, "higher_is_better": True, "scaling": "weak" if world == 1 else "strong",
+        "vs_baseline": None, "dtype": "f64 (complex<double>)", "data": "synthetic", "config": cfg,
+        "sample_rows": rows, "extrapolation_factor": n / rows, "sample_wall_s_per_step": t,
         "cpu_baseline": {"value": it_s, "unit": "iter/s", "cores": threads, "kind": "reference", "sample": sample},
         "e2e": {"value": it_s, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
     return 0
+
+
+def metric_name(n):
+    return f"DPT iterations/s (dense n={n} FP64 step)"
 
 
 # ------------------------------------------------------ baselines table ----
@@ -340,10 +380,32 @@ def platform_cpu():
 
 
 # ------------------------------------------------------------ B200 arm ----
+def spawn(args):
+    """--gpus N outside torchrun: re-launch this script with N ranks (one per GPU)."""
+    import socket
+    if args.impl == "b200":
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} requested but only {have} GPU(s) are visible", file=sys.stderr)
+            return 2
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # keep NCCL's init lines (nranks) visible
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     args = parse()
     if args.baselines:
         return run_baselines()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return spawn(args)
     if args.impl == "reference":
         return run_reference(args)
     import torch
@@ -353,10 +415,19 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr)
+        return 2
+    if torch.cuda.device_count() < world:
+        print(f"bench.py: {world} ranks but only {torch.cuda.device_count()} GPU(s) visible", file=sys.stderr)
+        return 2
     torch.cuda.set_device(local)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    n = args.n
+    wl, n = pick_workload(args, world)
+    e2e_calls = args.e2e_calls or (5 if wl == "c2" else 1)
     ctx = P.Context(local)
     if world > 1:
         uid = [P.Context.nccl_unique_id() if rank == 0 else None]
@@ -375,7 +446,9 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    p, opts = make_inputs(n)
+    t_gen = time.perf_counter()
+    p, opts = make_inputs(wl, n)
+    t_gen = time.perf_counter() - t_gen
     stream = torch.cuda.ExternalStream(ctx.stream_ptr)
     plan = P.Plan(p, ctx=ctx)
     plan.begin()
@@ -398,44 +471,69 @@ def main():
     ms_per_step = ms_total / args.steps
     value = 1e3 / ms_per_step  # whole-job iterations per second (all ranks advance the same iteration)
 
-    # roofline: the dense step kernel alone, events on its own stream
-    kernel_steps = min(args.steps, 50)
-    kms = plan.steps(kernel_steps, time_kernel=True) / kernel_steps
+    # roofline: the dense step kernel alone, events on its own stream (max over ranks)
+    kernel_steps = min(args.steps, 50 if wl == "c2" else 3)
+    kms = max_over_ranks(plan.steps(kernel_steps, time_kernel=True) / kernel_steps)
     rows_local = (n + world - 1) // world
     flop_launch = 2.0 * rows_local * n * n
     achieved = flop_launch / (kms * 1e-3) / 1e12
     peak = P.fp64_peak_tflops(local)
-    traffic = None
+    traffic, traffic_src = None, None
     prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
-    if os.path.exists(prof):
+    if os.path.exists(prof) and wl == "c2" and world == 1:
         try:
-            traffic = json.load(open(prof)).get("latest:prof_dense_c2", {}).get("dram_bytes_per_launch")
+            rec = json.load(open(prof)).get("latest:prof_dense_c2", {})
+            traffic, traffic_src = rec.get("dram_bytes_per_launch"), rec.get("source")
         except Exception:
             traffic = None
     plan.close()
 
     # e2e: the public API on pinned host arrays, solve to the terminal status
-    e2e = None
-    if rank == 0 or world > 1:
-        pe, oe = make_inputs(n, pinned=True)
-        io = P.IterationOptions(**oe)
-        outs = (torch.empty((n, n), dtype=torch.float64, pin_memory=True).numpy(),
-                torch.empty(n, dtype=torch.float64, pin_memory=True).numpy(),
-                torch.empty(n, dtype=torch.float64, pin_memory=True).numpy())
-        r = P.iterate_full(pe, io, ctx=ctx, out=outs)  # warm-up (first-call allocations)
-        barrier()
-        t0 = time.perf_counter()
-        iters = 0
-        for _ in range(args.e2e_calls):
-            r = P.iterate_full(pe, io, ctx=ctx, out=outs)
-            iters += r.iterations
-        barrier()
-        wall = max_over_ranks(time.perf_counter() - t0)
-        e2e = {"value": iters / wall, "unit": "iter/s",
-               "h2d_bytes_per_step": int((n * n + n) * 8 / max(r.iterations, 1)),
-               "d2h_bytes_per_step": int((n * n + 2 * n) * 8 / max(r.iterations, 1)),
-               "call": f"iterate_full(c2) pinned host arrays in and out -> {P.to_string(r.status)} at k={r.iterations}, "
-                       f"{wall / args.e2e_calls * 1e3:.2f} ms per call (upload, solve, download)"}
+    pe, oe = make_inputs(wl, n, pinned=True)
+    io = P.IterationOptions(**oe)
+    outs = (torch.empty((n, n), dtype=torch.float64, pin_memory=True).numpy(),
+            torch.empty(n, dtype=torch.float64, pin_memory=True).numpy(),
+            torch.empty(n, dtype=torch.float64, pin_memory=True).numpy())
+    if wl == "c2":
+        P.iterate_full(pe, io, ctx=ctx, out=outs)  # warm-up (first-call allocations)
+    barrier()
+    t0 = time.perf_counter()
+    iters = 0
+    for _ in range(e2e_calls):
+        r = P.iterate_full(pe, io, ctx=ctx, out=outs)
+        iters += r.iterations
+    barrier()
+    wall = max_over_ranks(time.perf_counter() - t0)
+    e2e = {"value": iters / wall, "unit": "iter/s",
+           "h2d_bytes_per_step": int((n * n + n) * 8 / max(r.iterations, 1)),
+           "d2h_bytes_per_step": int((n * n + 2 * n) * 8 / max(r.iterations, 1)),
+           "call": f"iterate_full({wl}) pinned host arrays in and out -> {P.to_string(r.status)} at "
+                   f"k={r.iterations}, {wall / e2e_calls * 1e3:.2f} ms per call (upload, solve, download)"
+                   + (f", {world} ranks (allgather of A to every rank)" if world > 1 else "")}
+    del pe, outs
+
+    # time to the terminal status through the public call, device-resident inputs
+    ttc = None
+    if world == 1 and wl == "c2":
+        ttc = {}
+        for name in ("c2", "c2b"):
+            from paper_2002_12872_b200 import problems as pr
+            q, oq, _ = pr.config(name, n)
+            dv = torch.device("cuda", local)
+            qd = P.PartitionedProblem(torch.as_tensor(q.d, device=dv), torch.as_tensor(q.delta, device=dv), q.lam)
+            P.iterate_full(qd, P.IterationOptions(**oq), ctx=ctx)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            rr = P.iterate_full(qd, P.IterationOptions(**oq), ctx=ctx)
+            torch.cuda.synchronize()
+            ttc[name] = {"status": P.to_string(rr.status), "iterations": rr.iterations,
+                         "wall_ms": (time.perf_counter() - t0) * 1e3, "device_ms": rr.device_ms}
+            del qd
+        ttc["how"] = ("public iterate_full, device-resident theta/Delta, results on the device; warm call; "
+                      "c2b = c2 with theta_i = i (the converging companion, SURVEY.md §8(d))")
+    elif world > 1 or wl == "c5":
+        ttc = {wl: {"status": P.to_string(r.status), "iterations": r.iterations,
+                    "wall_ms_with_host_copies": wall / e2e_calls * 1e3}}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -443,29 +541,37 @@ def main():
             from oracle.bind import available
             if available("reference"):
                 threads = os.cpu_count() or 1
-                rpt = 8
+                rpt = 8 if wl == "c2" else 1
                 a_rows = first_iterate_rows(p, threads * rpt)
                 s, rows, _ = reference_sample(p, a_rows, threads, rpt, p.lam)
                 cpu = {"value": (rows / n) / s, "unit": "iter/s", "cores": threads, "kind": "reference",
-                       "sample": f"{rows} of {n} rows of one c2 iteration (reference matmul(A_rows, delta_t) + map, "
-                                 f"complex<double>), {threads} threads; iter/s = fraction / wall"}
+                       "sample": f"{rows} of {n} rows of one {wl} iteration (reference matmul(A_rows, delta_t) + map, "
+                                 f"complex<double>), {threads} threads; iter/s = fraction / wall "
+                                 f"(extrapolated x{n / rows:.1f})"}
         except Exception as e:  # the baseline is reported, never required
             cpu = {"value": None, "unit": "iter/s", "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
 
     if rank == 0:
         line = {
-            "metric": "DPT iterations/s (dense n=4096 FP64 step)", "value": value, "unit": "iter/s",
+            "metric": metric_name(n), "value": value, "unit": "iter/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic (SURVEY.md §8(d) recipe, seeded)", "config": workload_config(n, world),
+            "dtype": "f64", "data": "synthetic (SURVEY.md §8(d) recipe, seeded)",
+            "config": workload_config(wl, n, world),
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": traffic,
+                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                          "kernel": "dense_step_kernel (K1)", "kernel_ms": kms,
+                         "flop_per_launch": flop_launch,
                          "peak_source": "FP64 DMMA probe measured in this run (MEASURED_PEAKS.json has no FP64 entry)"},
-            "e2e": e2e, "cpu_baseline": cpu, "clocks": clk, "gpu_launches": int(launches),
+            "e2e": e2e, "time_to_converge": ttc, "cpu_baseline": cpu, "clocks": clk, "gpu_launches": int(launches),
             "tflops_per_step": 2.0 * n ** 3 / (ms_per_step * 1e-3) / 1e12,
+            "input_gen_s": t_gen,
         }
-        print(json.dumps(line))
+        if world > 1:
+            line["per_rank"] = {"k1_ms_max": kms, "step_ms": ms_per_step,
+                                "fold_allreduce_decide_ms": ms_per_step - kms,
+                                "rows_per_rank": rows_local}
+        print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0

@@ -139,6 +139,9 @@ int dpt_nccl_unique_id(void* out, size_t bytes, dpt_error_info* err);
 void* dpt_ctx_stream(dpt_ctx* ctx);
 /* Kernel launches issued by this context so far (for gpu_launches accounting). */
 int64_t dpt_ctx_launch_count(const dpt_ctx* ctx);
+/* Device-loop graph cache of this context: replays of a cached graph (hits)
+ * and captures (misses) so far (tests of the cache key). */
+void dpt_ctx_graph_stats(const dpt_ctx* ctx, int64_t* hits, int64_t* misses);
 
 void dpt_options_default(dpt_options* o);
 const char* dpt_status_string(int status); /* to_string, dpt.cpp:297-309 */

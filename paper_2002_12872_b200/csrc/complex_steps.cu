@@ -203,12 +203,11 @@ cudaError_t launch_csr_step_cplx(const DevSolve& s, const DevSell& d, cudaStream
   const size_t smem = use_smem ? size_t(R) * size_t(s.n) * 16 : 0;
 #define DPT_CSRC_CASE(RR)                                                                         \
   case RR: {                                                                                      \
-    static bool attr = false;                                                                     \
-    if (!attr) {                                                                                  \
+    static DeviceAttrOnce attr;                                                                   \
+    attr([] {                                                                                     \
       cudaFuncSetAttribute(csr_step_cplx_kernel<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                            kCsrCSmemBudget + 1024);                                               \
-      attr = true;                                                                                \
-    }                                                                                             \
+    });                                                                                           \
     csr_step_cplx_kernel<RR><<<grid, kCsrCThreads, smem, st>>>(s, d, use_smem);                   \
     break;                                                                                        \
   }
@@ -375,7 +374,8 @@ __global__ void __launch_bounds__(kU16cWarps * 32, 1)
                             int64_t row, int64_t ntrips) {
   if (s.state->done) return;
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ uint64_t bar[kU16cWarps];
+  __shared__ uint64_t bar[kU16cWarps];    // full: the trip landed
+  __shared__ uint64_t empty[kU16cWarps];  // empty: all 32 lanes hold the trip in registers
   __shared__ double red[kU16cWarps][5];
   const int jl = launch_index(s);
   const int64_t n = s.n;
@@ -398,6 +398,7 @@ __global__ void __launch_bounds__(kU16cWarps * 32, 1)
   };
   if (lane == 0) {
     mbar_init(&bar[warp], 1);
+    mbar_init(&empty[warp], 32);
     fence_mbar_init();
     if (t < ntrips) issue(t);
   }
@@ -421,16 +422,14 @@ __global__ void __launch_bounds__(kU16cWarps * 32, 1)
     for (int k = 0; k < 4; ++k) c4[k] = cs[k * 32];
 #pragma unroll
     for (int q = 0; q < 16; ++q) v[q] = vs[q * 32];
-    {  // the stage is refilled right below: make every lane's reads land first
-      unsigned long long x = 0;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) x ^= (unsigned long long)(unsigned)c4[k].x ^ c4[k].y ^ c4[k].z ^ c4[k].w;
-#pragma unroll
-      for (int q = 0; q < 16; ++q) x ^= __double_as_longlong(v[q].x) ^ __double_as_longlong(v[q].y);
-      if (x == 0x5bd1e9955bd1e995ull) red[warp][4] = 0.0;  // data-dependent: waits for the loads (red is rewritten below)
+    // WAR handshake (as single_u16w_kernel): release after the reads, lane 0
+    // acquires the phase and fences generic -> async proxy before the refill
+    mbar_arrive_release(&empty[warp]);
+    if (lane == 0 && t + stride < ntrips) {
+      mbar_wait(&empty[warp], uint32_t(it) & 1u);
+      fence_proxy_async_smem();
+      issue(t + stride);
     }
-    __syncwarp();  // every lane holds its row: refill the stage
-    if (lane == 0 && t + stride < ntrips) issue(t + stride);
     if (m < n) {
       const cd zm = cmake(z[2 * m], z[2 * m + 1]);
       const cd tm = cmake(s.theta[2 * m], s.theta[2 * m + 1]);
@@ -517,11 +516,8 @@ cudaError_t launch_single_cplx(const DevSolve& s, const DevCsr& d, const double*
                                const double* u16c_vals, int64_t row, cudaStream_t st) {
   if (!B && u16c_cols && u16c_enabled()) {
     constexpr int smem = kU16cWarps * kU16cTripBytes;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(single_cplx_u16w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      attr = true;
-    }
+    static DeviceAttrOnce attr;
+    attr([] { cudaFuncSetAttribute(single_cplx_u16w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); });
     single_cplx_u16w_kernel<<<single_cplx_u16_grid(s.n), kU16cWarps * 32, smem, st>>>(s, d, u16c_cols, u16c_vals, row,
                                                                                        (s.n + 31) / 32);
     return cudaGetLastError();

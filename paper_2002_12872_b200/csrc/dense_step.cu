@@ -788,18 +788,12 @@ static cudaError_t launch_cfg(const DevSolve& s, const CUtensorMap* amaps, const
     }
   }
   if (s.cplx) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(dense_step_kernel<C, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-      attr = true;
-    }
+    static DeviceAttrOnce attr;
+    attr([] { cudaFuncSetAttribute(dense_step_kernel<C, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM); });
     dense_step_kernel<C, true><<<ntm * s.ntn, C::THREADS, C::SMEM, st>>>(s, amaps, dmap, delta, ntm);
   } else {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(dense_step_kernel<C, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-      attr = true;
-    }
+    static DeviceAttrOnce attr;
+    attr([] { cudaFuncSetAttribute(dense_step_kernel<C, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM); });
     dense_step_kernel<C, false><<<ntm * s.ntn, C::THREADS, C::SMEM, st>>>(s, amaps, dmap, delta, ntm);
   }
   return cudaGetLastError();

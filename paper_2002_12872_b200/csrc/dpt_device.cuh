@@ -5,9 +5,28 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "dpt_state.h"
 
 namespace dpt {
+
+// Function attributes (cudaFuncSetAttribute) are per device, and one process
+// may drive several devices (dpt_ctx_create(device)): `mask` holds one bit per
+// device ordinal on which the attributes were already set. The bit is set only
+// after the attributes, so a concurrent caller can at worst set them twice.
+struct DeviceAttrOnce {
+  std::atomic<unsigned long long> mask{0};
+  template <class F>
+  void operator()(F&& set) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (mask.load(std::memory_order_acquire) & bit) return;
+    set();
+    mask.fetch_or(bit, std::memory_order_release);
+  }
+};
 
 // Everything a launch needs that may change from iteration to iteration is
 // read from device memory (the state / tables below), so one captured CUDA
@@ -132,6 +151,20 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Consumer release of a stage (WAR handshake before an async-proxy refill):
+// mbarrier.arrive is a release at CTA scope, so this lane's preceding shared
+// reads are ordered before the producer's acquire (mbar_wait) of the phase.
+__device__ __forceinline__ void mbar_arrive_release(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Orders the generic-proxy shared accesses made visible to this thread (the
+// consumers' reads acquired through the empty barrier) before its subsequent
+// async-proxy (cp.async.bulk) writes to shared memory.
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {

@@ -455,11 +455,8 @@ cudaError_t launch_relabel(const int64_t* rp, const int32_t* cl, int64_t n, int6
   relabel_scan_kernel<<<1, 1024, 0, st>>>(ccount, n, start);
   relabel_fill_kernel<<<blocks, 256, 0, st>>>(rp, cl, n, slot_of, start, cfill, cgroups);
   const size_t smem = relabel_smem_bytes(nslices);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(relabel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  static DeviceAttrOnce attr;
+  attr([] { cudaFuncSetAttribute(relabel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); });
   relabel_kernel<<<1, 1024, smem, st>>>(start, cgroups, n, int(2 * nslices), cap, passes, bank, pos, inv, npad_alloc,
                                         npad_out);
   (void)nnz;

@@ -269,7 +269,8 @@ __global__ void __launch_bounds__(W * 32, MINB)
   constexpr int kTrip = U16W<W, S>::TripBytes;
   if (s.state->done) return;
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ uint64_t bar[W][S];
+  __shared__ uint64_t bar[W][S];    // full: the trip's bulk copies landed
+  __shared__ uint64_t empty[W][S];  // empty: all 32 lanes hold the trip in registers
   __shared__ double red[W][5];
   const int jl = launch_index(s);
   const int64_t n = s.n;
@@ -290,7 +291,10 @@ __global__ void __launch_bounds__(W * 32, MINB)
     bulk_load(base + 32 * 64, D.vals + 16 * r0, uint32_t(nr * 16 * 8), &bar[warp][st]);
   };
   if (lane == 0) {
-    for (int i = 0; i < S; ++i) mbar_init(&bar[warp][i], 1);
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&bar[warp][i], 1);
+      mbar_init(&empty[warp][i], 32);
+    }
     fence_mbar_init();
     for (int i = 0; i < S; ++i)
       if (t + i * stride < ntrips) issue(t + i * stride, i);
@@ -311,21 +315,18 @@ __global__ void __launch_bounds__(W * 32, MINB)
     mbar_wait(&bar[warp][st], uint32_t(it / S) & 1u);
     const int64_t m = t * 32 + lane;
     const uint8_t* base = ring + st * kTrip;
-    U16Row rd;
+    U16Row rd = {};
     if (m < n)
       rd = u16_load_rot(reinterpret_cast<const int4*>(base + lane * 64),
                         reinterpret_cast<const double2*>(base + 32 * 64 + lane * 128), lane);
-    {  // the stage is refilled right below: make every lane's reads land first
-      unsigned long long x = 0;
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        x ^= (unsigned long long)(unsigned)(rd.c[k].x ^ rd.c[k].y ^ rd.c[k].z ^ rd.c[k].w) ^
-             __double_as_longlong(rd.va[k].x) ^ __double_as_longlong(rd.va[k].y) ^
-             __double_as_longlong(rd.vb[k].x) ^ __double_as_longlong(rd.vb[k].y);
-      if (x == 0x5bd1e9955bd1e995ull) red[warp][4] = 0.0;  // data-dependent: waits for the loads (red is rewritten below)
+    // WAR handshake: every lane releases the stage after its reads; lane 0
+    // acquires that phase, then fences generic -> async proxy before the refill
+    mbar_arrive_release(&empty[warp][st]);
+    if (lane == 0 && t + S * stride < ntrips) {
+      mbar_wait(&empty[warp][st], uint32_t(it / S) & 1u);
+      fence_proxy_async_smem();
+      issue(t + S * stride, st);
     }
-    __syncwarp();  // every lane holds its row: the stage can be refilled
-    if (lane == 0 && t + S * stride < ntrips) issue(t + S * stride, st);
     if (m < n) {
       const double zm = z[m];
       const double tm = s.theta[m];
@@ -414,15 +415,14 @@ int u16_grid(int64_t n) {
 
 template <int W, int S, int MINB, bool NA = false>
 static cudaError_t launch_u16w(const DevSolve& s, const DevCsr& d, int64_t row, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
+  static DeviceAttrOnce attr;
+  attr([] {
     cudaFuncSetAttribute(single_u16w_kernel<W, S, MINB, NA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          U16W<W, S>::Smem);
     if (getenv("DPT_U16_CARVEOUT"))  // tuning: force the shared-memory carveout (percent)
       cudaFuncSetAttribute(single_u16w_kernel<W, S, MINB, NA>, cudaFuncAttributePreferredSharedMemoryCarveout,
                            atoi(getenv("DPT_U16_CARVEOUT")));
-    attr = true;
-  }
+  });
   const int64_t trips = (s.n + 31) / 32;
   single_u16w_kernel<W, S, MINB, NA><<<u16_grid(s.n), W * 32, U16W<W, S>::Smem, st>>>(s, d, row, trips);
   return cudaGetLastError();
@@ -430,12 +430,11 @@ static cudaError_t launch_u16w(const DevSolve& s, const DevCsr& d, int64_t row, 
 
 template <int ROWS, int MINB, bool ROT>
 static cudaError_t launch_u16(const DevSolve& s, const DevCsr& d, int64_t row, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
+  static DeviceAttrOnce attr;
+  attr([] {
     cudaFuncSetAttribute(single_u16_kernel<ROWS, MINB, ROT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          U16<ROWS>::Smem);
-    attr = true;
-  }
+  });
   const int64_t trips = (s.n + ROWS - 1) / ROWS;
   single_u16_kernel<ROWS, MINB, ROT><<<u16_grid(s.n), ROWS, U16<ROWS>::Smem, st>>>(s, d, row, trips);
   return cudaGetLastError();

@@ -112,6 +112,7 @@ struct dpt_ctx {
     int64_t per_body = 0;
   };
   std::vector<LoopGraph> loop_graphs;  // most recent last, at most kMaxLoopGraphs
+  int64_t graph_hits = 0, graph_misses = 0;
   // library handles for the homotopy's plain GEMM / LU (created on first use)
   cublasHandle_t cublas = nullptr;
   cusolverDnHandle_t cusolver = nullptr;
@@ -1037,20 +1038,26 @@ void drive_graph(dpt_ctx* ctx, Work& w, DevProblem& dp, Mode mode, int64_t row, 
   key_add(key, cycle_elems);
   key_add(key, w.ntiles_step);
   key_add(key, w.amaps.p);
-  key_add(key, dp.delta.p);
-  key_add(key, dp.dmap.p);
+  // every device buffer and scalar of the problem, so no buffer a launch reads
+  // can be left out of the key (a cache block handed out again at another
+  // address must never replay a graph holding the old one)
+  for (const DBuf* b : {&dp.theta, &dp.delta, &dp.rowptr, &dp.cols, &dp.vals, &dp.dmap, &dp.u16c_cols,
+                        &dp.u16c_vals, &dp.s_cols, &dp.s_vals, &dp.s_off, &dp.s_lcol, &dp.s_llen, &dp.s_pos,
+                        &dp.s_perm, &dp.s_inv})
+    key_add(key, b->p);
+  for (int64_t v : {dp.n, dp.ld, dp.nnz, dp.ncol, dp.ldd, dp.nslices, dp.s_npad}) key_add(key, v);
+  key_add(key, dp.lambda_im);
   key_add(key, dp.big);
   key_add(key, dp.cplx);
   key_add(key, dp.kind);
   key_add(key, dp.uniform16);
-  key_add(key, dp.csr());
-  key_add(key, dp.sell());
   key_add_knobs(key);
   dpt_ctx::LoopGraph* hit = nullptr;
   for (auto& lg : ctx->loop_graphs)
     if (lg.key == key) hit = &lg;
   static const bool dbg = std::getenv("DPT_GRAPH_DEBUG") != nullptr;
   if (dbg) std::fprintf(stderr, "[dpt] loop graph %s (%zu cached)\n", hit ? "hit" : "miss", ctx->loop_graphs.size());
+  ++(hit ? ctx->graph_hits : ctx->graph_misses);
   if (!hit) {
     dpt_ctx::LoopGraph lg;
     lg.key = key;
@@ -2069,6 +2076,11 @@ int dpt_ctx_set_comm(dpt_ctx* ctx, int rank, int world, const void* id, size_t b
 
 void* dpt_ctx_stream(dpt_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
 int64_t dpt_ctx_launch_count(const dpt_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+void dpt_ctx_graph_stats(const dpt_ctx* ctx, int64_t* hits, int64_t* misses) {
+  if (hits) *hits = ctx ? ctx->graph_hits : 0;
+  if (misses) *misses = ctx ? ctx->graph_misses : 0;
+}
 
 int dpt_iterate_full(dpt_ctx* ctx, const dpt_problem* p, const dpt_options* opts, dpt_trace_fn trace, void* user,
                      double* a_out, double* eig_out, double* res_out, int out_mem, dpt_report* rep,

@@ -287,12 +287,11 @@ cudaError_t launch_csr_step(const DevSolve& s, const DevSell& d, cudaStream_t st
   }
 #define DPT_CSR_CASE(RR)                                                                          \
   case RR: {                                                                                      \
-    static bool attr = false;                                                                     \
-    if (!attr) {                                                                                  \
+    static DeviceAttrOnce attr;                                                                   \
+    attr([] {                                                                                     \
       cudaFuncSetAttribute(csr_step_kernel<RR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                            kCsrSmemBudget + 1024);                                                \
-      attr = true;                                                                                \
-    }                                                                                             \
+    });                                                                                           \
     csr_step_kernel<RR, true><<<grid, kCsrThreads, smem, st>>>(s, d);                             \
     break;                                                                                        \
   }

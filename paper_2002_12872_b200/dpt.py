@@ -198,6 +198,13 @@ class Context:
     def launches(self) -> int:
         return int(N.lib().dpt_ctx_launch_count(self.handle))
 
+    @property
+    def graph_stats(self):
+        """(hits, misses) of this context's device-loop graph cache."""
+        h, m = ctypes.c_int64(0), ctypes.c_int64(0)
+        N.lib().dpt_ctx_graph_stats(self.handle, ctypes.byref(h), ctypes.byref(m))
+        return int(h.value), int(m.value)
+
     def close(self):
         if self.handle:
             N.lib().dpt_ctx_destroy(self.handle)

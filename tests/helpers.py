@@ -58,8 +58,15 @@ def assert_full_parity(g, status, iterations, a, eig, res, exact_iters=False):
     if int(status) == 2:  # Diverged: NaN read-offs, state carries the escaping iterate
         assert np.all(np.isnan(g.eigenvalues)) and np.all(np.isnan(g.residuals))
         return
+    if g.iterations != iterations and int(status) != 0:
+        # Bounded (a cycle) / MaxIterations one iterate apart: different points
+        # of the orbit, no value bound follows from the reference's rules
+        return
+    # Equal counts, or Converged one iteration apart: consecutive iterates of a
+    # converged run differ by less than tol <= 1e-12 (the convergence test), so
+    # the same bounds hold either way -- values are always compared.
+    assert eig_rel_err(g.eigenvalues, eig) < EIG_RTOL
+    assert float(np.max(np.abs(g.state.a - a))) < VEC_ATOL
     if g.iterations == iterations:
-        assert eig_rel_err(g.eigenvalues, eig) < EIG_RTOL
-        assert float(np.max(np.abs(g.state.a - a))) < VEC_ATOL
         ok = np.isfinite(res)
         assert np.allclose(g.residuals[ok], res[ok], rtol=1e-3, atol=1e-13)

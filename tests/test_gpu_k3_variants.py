@@ -66,3 +66,34 @@ def test_complex_u16_pipeline_matches_general_kernel(variant_env, n):
         assert int(b.status) == r.status and abs(b.iterations - r.iterations) <= 1
         if r.status == 0:
             assert abs(b.eigenvalue - r.eigenvalue) <= 1e-10 * max(1.0, abs(r.eigenvalue))
+
+
+def test_complex_u16_graph_cache_churn():
+    """the loop-graph key must cover every buffer a captured launch
+    reads.  Solve P1 (complex, 16 per row, device-resident CSR views), then a
+    same-n problem from host arrays (churns the context's block cache, so the
+    trip-major copies may land elsewhere), then P1 again: the last result is
+    bit-identical to the first, and the cache was exercised (hits and misses)."""
+    import torch
+    ctx = P.Context(0)
+    n = 70001
+    p1, o, _ = pr.config("c4b", n)
+    dv = torch.device("cuda")
+    p1 = P.PartitionedProblem(torch.as_tensor(p1.d, device=dv),
+                              P.CsrMatrix(n, torch.as_tensor(p1.delta.rowptr, device=dv),
+                                          torch.as_tensor(p1.delta.cols, device=dv),
+                                          torch.as_tensor(p1.delta.vals, device=dv)),
+                              p1.lam * (1 + 0.5j))
+    p2, _, _ = pr.config("c4b", n)
+    p2 = P.PartitionedProblem(p2.d, P.CsrMatrix(n, p2.delta.rowptr, p2.delta.cols, -p2.delta.vals),
+                              p2.lam * (1 - 0.25j))
+    io = P.IterationOptions(**o)
+    a = P.dominant_eigenpair(p1, io, ctx=ctx)
+    P.dominant_eigenpair(p2, io, ctx=ctx)
+    P.dominant_eigenpair(p2, io, ctx=ctx)
+    b = P.dominant_eigenpair(p1, io, ctx=ctx)
+    hits, misses = ctx.graph_stats
+    assert misses >= 1 and hits + misses >= 4, (hits, misses)
+    assert int(a.status) == int(b.status) and a.iterations == b.iterations
+    assert a.eigenvalue == b.eigenvalue and np.array_equal(a.z_chart, b.z_chart)
+    ctx.close()

@@ -306,3 +306,69 @@ def test_c4_full_size_vs_oracle():
     assert int(g.status) == r.status == 0 and abs(g.iterations - r.iterations) <= 1
     assert abs(g.eigenvalue - r.eigenvalue) <= EIG_RTOL * max(1, abs(r.eigenvalue))
     assert np.max(np.abs(g.z_chart - r.z)) < VEC_ATOL and np.max(np.abs(g.z_unit - r.z_unit)) < VEC_ATOL
+
+
+def _step_rows_threaded(p, row0, a_rows, lam, chunk=4):
+    """The oracle's step_rows over row chunks on the host cores (rows of the
+    map are independent, dpt.cpp:136-144; ctypes releases the GIL)."""
+    import concurrent.futures as cf
+    import os
+    out = np.empty_like(a_rows)
+    starts = list(range(0, a_rows.shape[0], chunk))
+
+    def one(s):
+        out[s:s + chunk] = O.step_rows(p, row0 + s, a_rows[s:s + chunk], lam)
+
+    with cf.ThreadPoolExecutor(max_workers=min(len(starts), os.cpu_count() or 1)) as ex:
+        list(ex.map(one, starts))
+    return out
+
+
+def test_c5_full_size():
+    """BASELINE configs[4]: dense symmetric n = 32768 (the north_star's
+    multi-GPU config; the reference cannot run it: >= 103 GB of complex n^2
+    buffers).  Size-independent properties against the oracle: two 64-row
+    blocks of A_1 and A_2 (rows are independent), the residual gate, the exact
+    unit diagonal, a fixed-point row sample of the final iterate, and the same
+    solve through the 1-rank NCCL collective path, bit for bit."""
+    p, o, _ = pr.config("c5")
+    n = 32768
+    blocks = (0, 20000)
+    plan = P.Plan(p)
+    plan.begin()
+    full1 = plan.read()
+    a1 = {r0: full1[r0:r0 + 64].copy() for r0 in blocks}
+    del full1
+    plan.steps(1)
+    full2 = plan.read()
+    a2 = {r0: full2[r0:r0 + 64].copy() for r0 in blocks}
+    del full2
+    plan.close()
+    eye = np.eye(n)
+    for r0 in blocks:
+        want1 = O.step_rows(p, r0, eye[r0:r0 + 64], p.lam)  # k = 1 from A_0 = I
+        assert np.max(np.abs(a1[r0] - want1)) < 1e-15, r0
+        want2 = _step_rows_threaded(p, r0, a1[r0], p.lam)  # k = 2: a full dense row product
+        assert np.max(np.abs(a2[r0] - want2)) < 1e-12, r0
+    del eye
+    g = P.iterate_full(p, _o(o))
+    assert g.status == P.ConvergenceStatus.Converged and g.iterations <= 12, (g.status, g.iterations)
+    assert np.max(g.residuals) < 1e-10
+    assert np.all(np.diag(g.state.a) == 1.0)
+    assert np.all(np.isfinite(g.eigenvalues))
+    # eigenvalues are theta_i + lambda (Delta A)_ii: a row sample from the oracle's own read-off
+    for r0 in blocks:
+        rows = slice(r0, r0 + 16)
+        nxt = _step_rows_threaded(p, r0, g.state.a[rows], p.lam)
+        assert np.max(np.abs(nxt - g.state.a[rows])) < 1e-11, r0
+    iters, a_g, eig_g = g.iterations, g.state.a, g.eigenvalues
+    del g
+    ctx = P.Context(0)
+    try:
+        ctx.set_comm(0, 1, P.Context.nccl_unique_id())
+        h = P.iterate_full(p, _o(o), ctx=ctx)
+        assert int(h.status) == 0 and h.iterations == iters
+        assert np.array_equal(h.eigenvalues, eig_g)
+        assert np.array_equal(h.state.a, a_g)
+    finally:
+        ctx.close()

@@ -200,3 +200,19 @@ def test_effective_window():  # dpt.cpp:83-90
     assert L.orc_effective_window(16, 100) == 16
     assert L.orc_effective_window(1, 10) == 0
     assert L.orc_effective_window(0, 10) == 0
+
+
+@pytest.mark.parametrize("name,n", [("c2", 300), ("c5", 700)])
+def test_gen_matches_inputs(name, n):
+    """oracle/gen.py (the reference arm's input builder, numpy) restates the
+    §8(d) recipe: the integer stream is bit-identical to csrc/problems.cpp, so
+    theta is identical and Delta agrees to the last ulp of numpy's log/cos."""
+    from oracle import gen
+    from paper_2002_12872_b200 import problems as pr
+    t, a, lam = gen.dense_config(name, n)
+    p, _, _ = pr.config(name, n)
+    assert np.array_equal(t, p.d) and lam == p.lam
+    assert np.max(np.abs(a - p.delta)) <= 4 * np.finfo(float).eps * max(1.0, np.max(np.abs(p.delta)))
+    assert np.array_equal(a == 0, p.delta == 0)
+    if name == "c5":
+        assert np.array_equal(a, a.T)
