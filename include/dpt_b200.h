@@ -135,6 +135,15 @@ void dpt_ctx_destroy(dpt_ctx* ctx);
 int dpt_ctx_set_comm(dpt_ctx* ctx, int rank, int world, const void* nccl_id, size_t id_bytes,
                      dpt_error_info* err);
 int dpt_nccl_unique_id(void* out, size_t bytes, dpt_error_info* err);
+/* TEST-ONLY loopback communicator: makes ctxs[0..world-1] (distinct contexts
+ * of ONE device, no NCCL communicator) ranks 0..world-1 of one sharded group.
+ * Each rank must then be driven by its own host thread making the same
+ * sequence of calls; the collectives (max-allreduce of the statistics, the
+ * final all-gathers) are host rendezvous plus stream-event dependencies and
+ * device copies -- no kernel waits on another rank's kernel.  Lets the
+ * world > 1 path (shard_rows -> per-rank step -> allreduce -> decide ->
+ * gather) run on a single GPU.  world <= 8. */
+int dpt_ctx_set_loopback(dpt_ctx** ctxs, int world, dpt_error_info* err);
 /* CUDA stream used by the context (cudaStream_t as void*). */
 void* dpt_ctx_stream(dpt_ctx* ctx);
 /* Kernel launches issued by this context so far (for gpu_launches accounting). */

@@ -84,6 +84,8 @@ def lib() -> ctypes.CDLL:
         L.dpt_ctx_launch_count.restype = c_int64
         L.dpt_ctx_graph_stats.argtypes = [c_void_p, P(c_int64), P(c_int64)]
         L.dpt_ctx_graph_stats.restype = None
+        L.dpt_ctx_set_loopback.argtypes = [P(c_void_p), c_int, P(dpt_error_info)]
+        L.dpt_ctx_set_loopback.restype = c_int
         L.dpt_options_default.argtypes = [P(dpt_options)]
         L.dpt_status_string.argtypes = [c_int]
         L.dpt_status_string.restype = ctypes.c_char_p

@@ -21,7 +21,10 @@
 #include <string.h>
 
 #include <algorithm>
+#include <exception>
 #include <chrono>
+#include <condition_variable>
+#include <mutex>
 #include <complex>
 #include <cstring>
 #include <set>
@@ -78,11 +81,62 @@ static NcclApi* nccl_api() {
 }
 static const int kNcclFloat64 = 8, kNcclMax = 2;
 
+// Test-only stand-in for NCCL when several ranks share ONE device in one
+// process (the pool gives one GPU per call): each rank is a dpt_ctx driven by
+// its own host thread.  A collective is a host rendezvous at ENQUEUE time plus
+// stream-ordered dependencies: every rank records an event after its input is
+// produced, all ranks meet, each waits (cudaStreamWaitEvent) on every peer's
+// event and reads the peers' buffers with a kernel / device copies, records a
+// second event, all meet again, and each waits on every peer's second event
+// before it may overwrite its input.  No kernel ever waits on another rank's
+// kernel (no spin flags), so the ranks' work may run in any order on the GPU.
+constexpr int kMaxLoopbackRanks = 8;
+
+struct LoopbackGroup {
+  ~LoopbackGroup() {
+    for (cudaEvent_t e : ev_in) cudaEventDestroy(e);
+    for (cudaEvent_t e : ev_out) cudaEventDestroy(e);
+  }
+  int world = 0;
+  std::mutex m;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  bool broken = false;
+  std::vector<const void*> src;
+  std::vector<cudaEvent_t> ev_in, ev_out;
+  // Host barrier of the ranks' threads; false (and the group marked broken) on a
+  // 120 s timeout or after another rank failed, so no rank hangs forever.
+  bool barrier() {
+    std::unique_lock<std::mutex> lk(m);
+    if (broken) return false;
+    const uint64_t g = gen;
+    if (++arrived == world) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+      return true;
+    }
+    if (!cv.wait_for(lk, std::chrono::seconds(120), [&] { return gen != g || broken; }) || broken) {
+      broken = true;
+      cv.notify_all();
+      return false;
+    }
+    return true;
+  }
+  void fail() {
+    std::lock_guard<std::mutex> lk(m);
+    broken = true;
+    cv.notify_all();
+  }
+};
+
 struct dpt_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   int rank = 0, world = 1;
   ncclComm_t comm = nullptr;
+  std::shared_ptr<LoopbackGroup> loop;  // test-only loopback communicator (dpt_ctx_set_loopback)
   int64_t launches = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   // Caching allocator: device blocks released by a call are kept for the next
@@ -578,6 +632,9 @@ void degenerate_error(dpt_error_info* err, int64_t i, int64_t j, const double* d
   throw Fail{DPT_ERR_DEGENERATE};
 }
 
+// with a communicator (NCCL or the test loopback) the solve is row-sharded
+bool sharded(const dpt_ctx* ctx) { return ctx->comm != nullptr || ctx->loop != nullptr; }
+
 // ------------------------------------------------------ device problem ----
 struct DevProblem {
   int64_t n = 0, ld = 0, nnz = 0;
@@ -827,7 +884,7 @@ void make_work(Work& w, dpt_ctx* ctx, DevProblem& dp, Mode mode, int64_t row0, i
   s.lambda = lambda;
   s.opts = so;
   s.fixed_mode = fixed_mode;
-  s.fuse_decide = ctx->comm ? 0 : 1;  // with a communicator the stats are max-allreduced first
+  s.fuse_decide = sharded(ctx) ? 0 : 1;  // with a communicator the stats are max-allreduced first
   int ntiles_aux = 1;
   if (mode == MODE_DENSE_FULL) {
     dp.big = dense_cfg_for(dp.n, rows);
@@ -939,7 +996,90 @@ void make_work(Work& w, dpt_ctx* ctx, DevProblem& dp, Mode mode, int64_t row0, i
   }
 }
 
+// ---- loopback collectives (LoopbackGroup) ----
+struct PeerPtrs {
+  const double* p[kMaxLoopbackRanks];
+};
+
+__global__ void loop_max_kernel(PeerPtrs in, int world, int count, double* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  double v = in.p[0][i];
+  for (int r = 1; r < world; ++r) v = fmax(v, in.p[r][i]);  // ncclMax of the statistics
+  out[i] = v;
+}
+
+void loop_meet(dpt_ctx* ctx, dpt_error_info* err) {
+  if (!ctx->loop->barrier()) {
+    set_err(err, DPT_ERR_NCCL, "loopback collective: a peer rank failed or timed out");
+    throw Fail{DPT_ERR_NCCL};
+  }
+}
+
+// in-place max-allreduce of `count` doubles (count <= 1024)
+void loop_allreduce_max(dpt_ctx* ctx, double* buf, int count, dpt_error_info* err) {
+  LoopbackGroup& G = *ctx->loop;
+  const int r = ctx->rank;
+  cudaStream_t st = ctx->stream;
+  DBuf tmp;
+  dalloc(tmp, size_t(count) * 8, err);
+  G.src[r] = buf;
+  CK(cudaEventRecord(G.ev_in[r], st));
+  loop_meet(ctx, err);
+  PeerPtrs pp{};
+  for (int q = 0; q < G.world; ++q) {
+    if (q != r) CK(cudaStreamWaitEvent(st, G.ev_in[q], 0));
+    pp.p[q] = static_cast<const double*>(G.src[q]);
+  }
+  loop_max_kernel<<<(count + 255) / 256, 256, 0, st>>>(pp, G.world, count, tmp.as<double>());
+  CK(cudaGetLastError());
+  ctx->launches += 1;
+  CK(cudaEventRecord(G.ev_out[r], st));
+  loop_meet(ctx, err);
+  for (int q = 0; q < G.world; ++q)
+    if (q != r) CK(cudaStreamWaitEvent(st, G.ev_out[q], 0));  // every peer has read `buf`
+  CK(cudaMemcpyAsync(buf, tmp.p, size_t(count) * 8, cudaMemcpyDeviceToDevice, st));
+  loop_meet(ctx, err);  // the exchange slots (src, events) are free again
+}
+
+// all-gather of `count` doubles per rank into dst[world * count]
+void loop_all_gather(dpt_ctx* ctx, const double* src, double* dst, size_t count, dpt_error_info* err) {
+  LoopbackGroup& G = *ctx->loop;
+  const int r = ctx->rank;
+  cudaStream_t st = ctx->stream;
+  G.src[r] = src;
+  CK(cudaEventRecord(G.ev_in[r], st));
+  loop_meet(ctx, err);
+  for (int q = 0; q < G.world; ++q) {
+    if (q != r) CK(cudaStreamWaitEvent(st, G.ev_in[q], 0));
+    CK(cudaMemcpyAsync(dst + size_t(q) * count, G.src[q], count * 8, cudaMemcpyDeviceToDevice, st));
+  }
+  CK(cudaEventRecord(G.ev_out[r], st));
+  loop_meet(ctx, err);
+  for (int q = 0; q < G.world; ++q)
+    if (q != r) CK(cudaStreamWaitEvent(st, G.ev_out[q], 0));  // every peer has copied `src`
+  loop_meet(ctx, err);
+}
+
+// C2 all-gather through NCCL or the loopback group
+void comm_all_gather(dpt_ctx* ctx, const double* src, double* dst, size_t count, const char* what,
+                     dpt_error_info* err) {
+  if (ctx->loop) {
+    loop_all_gather(ctx, src, dst, count, err);
+    return;
+  }
+  NcclApi* api = nccl_api();
+  if (!api || api->all_gather(src, dst, count, kNcclFloat64, ctx->comm, ctx->stream) != 0) {
+    set_err(err, DPT_ERR_NCCL, std::string("ncclAllGather of ") + what + " failed");
+    throw Fail{DPT_ERR_NCCL};
+  }
+}
+
 void allreduce_stats(dpt_ctx* ctx, Work& w, dpt_error_info* err) {
+  if (ctx->loop) {
+    loop_allreduce_max(ctx, w.s.stats, DPT_NSTATS, err);
+    return;
+  }
   if (!ctx->comm) return;
   NcclApi* api = nccl_api();
   if (!api || api->all_reduce(w.s.stats, w.s.stats, DPT_NSTATS, kNcclFloat64, kNcclMax, ctx->comm, ctx->stream) != 0) {
@@ -1252,6 +1392,9 @@ struct Guard {
     t_ctx = c;
   }
   ~Guard() {
+    // a rank leaving a call by an exception releases its loopback peers
+    // (they would otherwise wait at the next collective until the timeout)
+    if (ctx->loop && std::uncaught_exceptions() > 0) ctx->loop->fail();
     t_ctx = prev_ctx;
     if (old >= 0) cudaSetDevice(old);
   }
@@ -1263,7 +1406,7 @@ void shard_rows(const dpt_ctx* ctx, int64_t n, int64_t* row0, int64_t* rows) {
   // Development knob: DPT_SHARD_EMULATE=r/w gives a communicator-less context
   // rank r's row shard of a w-way solve, to time and test the per-rank kernels
   // at sharded shapes on one GPU (its decisions see only the local rows).
-  if (!ctx->comm) {
+  if (!sharded(ctx)) {
     if (const char* e = std::getenv("DPT_SHARD_EMULATE")) {
       int r = 0, wv = 1;
       if (std::sscanf(e, "%d/%d", &r, &wv) == 2 && wv > 0 && r >= 0 && r < wv) {
@@ -1305,19 +1448,15 @@ void gather_rows(dpt_ctx* ctx, const Work& w, const DevProblem& dp, int slot, do
                  dpt_error_info* err) {
   if (!dst) return;
   cudaStream_t st = ctx->stream;
-  if (!ctx->comm) {
+  if (!sharded(ctx)) {
     copy_slot_out(dst, w, dp, slot, out_mem, st, err);
     return;
   }
-  // C2: the final eigenvector gather (one ncclAllGather of the row shards)
-  NcclApi* api = nccl_api();
+  // C2: the final eigenvector gather (one all-gather of the row shards)
   DBuf all;
   dalloc(all, size_t(ctx->world) * size_t(w.s.slot_elems) * 8, err);
   const double* src = w.s.slots + size_t(slot) * size_t(w.s.slot_elems);
-  if (!api || api->all_gather(src, all.p, size_t(w.s.slot_elems), kNcclFloat64, ctx->comm, st) != 0) {
-    set_err(err, DPT_ERR_NCCL, "ncclAllGather of the iterate shards failed");
-    throw Fail{DPT_ERR_NCCL};
-  }
+  comm_all_gather(ctx, src, all.as<double>(), size_t(w.s.slot_elems), "the iterate shards", err);
   const cudaMemcpyKind k = out_mem == DPT_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
   CK(copy2d_async(ctx, dst, size_t(dp.ncol) * 8, all.p, size_t(dp.ld) * 8, size_t(dp.ncol) * 8, size_t(dp.n), k));
   CK(cudaStreamSynchronize(st));
@@ -1331,11 +1470,7 @@ void gather_vec(dpt_ctx* ctx, const Work& w, const double* src, double* dst, int
   n *= width;
   DBuf all;
   dalloc(all, size_t(ctx->world) * size_t(per) * 8, err);
-  NcclApi* api = nccl_api();
-  if (!api || api->all_gather(src, all.p, size_t(per), kNcclFloat64, ctx->comm, st) != 0) {
-    set_err(err, DPT_ERR_NCCL, "ncclAllGather of the read-offs failed");
-    throw Fail{DPT_ERR_NCCL};
-  }
+  comm_all_gather(ctx, src, all.as<double>(), size_t(per), "the read-offs", err);
   copy_out(dst, all.as<double>(), size_t(n), out_mem, st, err);
   CK(cudaStreamSynchronize(st));
 }
@@ -1567,7 +1702,7 @@ int run_full(dpt_ctx* ctx, const dpt_problem* p, const dpt_options* opts_in, boo
   if (n > 0) {
     gather_rows(ctx, w, dp, final_iter % nslots, a_out, out_mem, err);
     if (readoffs) {
-      if (ctx->comm) {
+      if (sharded(ctx)) {
         gather_vec(ctx, w, w.s.eps, eig_out, out_mem, n, err, cx);
         gather_vec(ctx, w, w.s.res, res_out, out_mem, n, err);
       } else {
@@ -1593,7 +1728,7 @@ int run_step_full(dpt_ctx* ctx, const dpt_problem* p, const double* a, const dou
                   double lambda_im = 0.0) {
   Guard g(ctx);
   validate(p, err);
-  if (ctx->comm) {
+  if (sharded(ctx)) {
     set_err(err, DPT_ERR_UNSUPPORTED, "step_full is a single-device call");
     throw Fail{DPT_ERR_UNSUPPORTED};
   }
@@ -2070,6 +2205,39 @@ int dpt_ctx_set_comm(dpt_ctx* ctx, int rank, int world, const void* id, size_t b
   }
   ctx->rank = rank;
   ctx->world = world;
+  return DPT_OK;
+  DPT_API_END
+}
+
+int dpt_ctx_set_loopback(dpt_ctx** ctxs, int world, dpt_error_info* err) {
+  DPT_API_BEGIN
+  if (!ctxs || world < 1 || world > kMaxLoopbackRanks) {
+    set_err(err, DPT_ERR_INVALID_ARG, "loopback group: 1..8 contexts");
+    return DPT_ERR_INVALID_ARG;
+  }
+  for (int r = 0; r < world; ++r)
+    if (!ctxs[r] || ctxs[r]->comm || ctxs[r]->device != ctxs[0]->device) {
+      set_err(err, DPT_ERR_INVALID_ARG, "loopback group: distinct contexts of one device, no NCCL communicator");
+      return DPT_ERR_INVALID_ARG;
+    }
+  auto g = std::make_shared<LoopbackGroup>();
+  g->world = world;
+  g->src.assign(size_t(world), nullptr);
+  {
+    Guard gd(ctxs[0]);
+    for (int r = 0; r < world; ++r) {
+      cudaEvent_t a, b;
+      CK(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+      g->ev_in.push_back(a);
+      g->ev_out.push_back(b);
+    }
+  }
+  for (int r = 0; r < world; ++r) {
+    ctxs[r]->loop = g;
+    ctxs[r]->rank = r;
+    ctxs[r]->world = world;
+  }
   return DPT_OK;
   DPT_API_END
 }
@@ -2710,7 +2878,7 @@ int dpt_plan_steps(dpt_plan* pl, int k, double* kernel_ms, dpt_error_info* err) 
 int dpt_plan_read(dpt_plan* pl, double* out, int out_mem, dpt_error_info* err) {
   DPT_API_BEGIN
   Guard g(pl->ctx);
-  if (pl->mode == MODE_SINGLE || !pl->ctx->comm)
+  if (pl->mode == MODE_SINGLE || !sharded(pl->ctx))
     copy_slot_out(out, pl->w, pl->dp, pl->issued % 2, out_mem, pl->ctx->stream, err);
   else
     gather_rows(pl->ctx, pl->w, pl->dp, pl->issued % 2, out, out_mem, err);

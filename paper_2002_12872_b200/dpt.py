@@ -184,6 +184,15 @@ class Context:
         _raise(N.lib().dpt_ctx_set_comm(self.handle, rank, world, buf, len(nccl_id), ctypes.byref(err)), err)
 
     @staticmethod
+    def set_loopback(ctxs) -> None:
+        """TEST-ONLY: make these contexts (one device) ranks 0..len-1 of a
+        sharded group whose collectives are in-process (dpt_ctx_set_loopback);
+        drive each rank from its own thread with the same calls."""
+        arr = (ctypes.c_void_p * len(ctxs))(*[c.handle for c in ctxs])
+        err = N.dpt_error_info()
+        _raise(N.lib().dpt_ctx_set_loopback(arr, len(ctxs), ctypes.byref(err)), err)
+
+    @staticmethod
     def nccl_unique_id() -> bytes:
         err = N.dpt_error_info()
         buf = ctypes.create_string_buffer(128)

@@ -3,6 +3,7 @@
 oracle/Makefile).  Run in the build container (where /root/reference exists):
 
     make -C oracle && python tests/golden/make_golden.py
+    python tests/golden/make_golden.py c3full     # c3 at n = 8192 (~2 min)
 
 The fixtures are small (n <= 96) so they travel with the repo; the tests check
 both the C restatement and the CUDA path against them.
@@ -60,5 +61,28 @@ def main():
         print(name, n, r.status, r.iterations)
 
 
+C3_ROWS = ((0, 64), (4000, 4064))
+
+
+def c3_full():
+    """BASELINE configs[2] at its full size (n = 8192 CSR, ~92 s in the
+    reference): status, iterations, all eigenvalues and residuals, and two
+    64-row blocks of the final eigenvector matrix.  The inputs are regenerated
+    by the tests from the recipe; their fingerprint is stored to pin them."""
+    R = Checker("reference")
+    p, o, _ = pr.config("c3")
+    r = R.iterate_full(p, o)
+    rec = dict(status=r.status, iterations=r.iterations, step_norm=r.step_norm, eig=r.eig, res=r.res,
+               nnz=p.delta.nnz, vals_sum=np.sum(p.delta.vals), cols_sum=np.sum(p.delta.cols.astype(np.int64)),
+               lam=p.lam)
+    for a, b in C3_ROWS:
+        rec[f"a_{a}_{b}"] = r.a[a:b]
+    np.savez_compressed(os.path.join(OUT, "c3full_n8192.npz"), **rec)
+    print("c3 full", r.status, r.iterations)
+
+
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "c3full":
+        c3_full()
+    else:
+        main()

@@ -279,6 +279,30 @@ def test_c2_full_size_status_and_row_slices():
     assert np.max(np.abs(a2[rows] - want)) < 1e-12
 
 
+def test_c3_full_size_vs_reference_golden():
+    """BASELINE configs[2] at full size against the REFERENCE's own solve
+    (tests/golden/c3full_n8192.npz, written by make_golden.py c3full from
+    oracle/_ref): status, iterations, all 8192 eigenvalues (1e-10 relative),
+    residuals, and two 64-row blocks of the eigenvector matrix (1e-9)."""
+    import os
+    from helpers import GOLDEN
+    z = np.load(os.path.join(GOLDEN, "c3full_n8192.npz"))
+    p, o, _ = pr.config("c3")  # n = 8192 CSR, nnz = 336,376 with the recipe
+    assert p.delta.nnz == 336376 == int(z["nnz"])
+    assert np.sum(p.delta.vals) == float(z["vals_sum"]) and np.sum(p.delta.cols.astype(np.int64)) == int(z["cols_sum"])
+    g = P.iterate_full(p, _o(o))
+    assert int(g.status) == int(z["status"]) == 0 and abs(g.iterations - int(z["iterations"])) <= 1
+    assert int(z["iterations"]) == 18  # SURVEY.md App. C
+    assert eig_rel_err(g.eigenvalues, z["eig"]) < EIG_RTOL
+    for key in z.files:
+        if key.startswith("a_"):
+            a, b = (int(x) for x in key.split("_")[1:])
+            assert np.max(np.abs(g.state.a[a:b] - z[key])) < VEC_ATOL, key
+    assert np.max(g.residuals) < 1e-10
+    assert np.allclose(g.residuals, z["res"], rtol=1e-3, atol=1e-13)
+    assert np.all(np.diag(g.state.a) == 1.0)
+
+
 def test_c3_full_size_properties():
     p, o, _ = pr.config("c3")  # n = 8192 CSR, nnz = 336,376 with the recipe
     assert p.delta.nnz == 336376
