@@ -39,6 +39,8 @@
 #include <thread>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/dpt_b200.h"
 #include "dpt_kernels.h"
 #include "dpt_state.h"
@@ -230,6 +232,15 @@ using namespace dpt;
 
 struct Fail {
   int code;
+};
+
+// NVTX range of one host phase (header-only NVTX v3: a no-op unless a tool
+// such as nsys / ncu --nvtx is attached)
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+  Nvtx(const Nvtx&) = delete;
+  Nvtx& operator=(const Nvtx&) = delete;
 };
 
 void set_err(dpt_error_info* e, int code, const std::string& msg) {
@@ -748,6 +759,7 @@ void validate(const dpt_problem* p, dpt_error_info* err) {
 }
 
 void upload(DevProblem& dp, dpt_ctx* ctx, const dpt_problem* p, dpt_error_info* err, bool sell = false) {
+  Nvtx nvtx_range("dpt.upload");
   validate(p, err);
   const int64_t n = p->n;
   const int cx = p->is_complex ? 2 : 1;  // doubles per scalar
@@ -1164,6 +1176,7 @@ void key_add_knobs(std::vector<unsigned char>& k) {
 
 void drive_graph(dpt_ctx* ctx, Work& w, DevProblem& dp, Mode mode, int64_t row, int total, int issued,
                  int64_t cycle_elems, dpt_trace_fn trace, void* user, dpt_error_info* err) {
+  Nvtx nvtx_range("dpt.device_loop");
   cudaStream_t st = ctx->stream;
   struct LoopReset {
     DevSolve* s;
@@ -1270,6 +1283,7 @@ void drive_graph(dpt_ctx* ctx, Work& w, DevProblem& dp, Mode mode, int64_t row, 
 // launches queued after a terminal decision are no-ops.
 void drive(dpt_ctx* ctx, Work& w, DevProblem& dp, Mode mode, int64_t row, int total, bool first_is_init,
            dpt_trace_fn trace, void* user, dpt_error_info* err) {
+  Nvtx nvtx_range("dpt.drive");
   cudaStream_t st = ctx->stream;
   const int64_t cycle_elems = (mode == MODE_SINGLE) ? dp.ncol : w.s.rows * dp.ncol;
   int issued = 0;
@@ -1279,7 +1293,11 @@ void drive(dpt_ctx* ctx, Work& w, DevProblem& dp, Mode mode, int64_t row, int to
     post_step(ctx, w, dense_init_ntiles(w.s.rows, w.s.ntn, w.s.cplx), cycle_elems, err);
     issued = 1;
   }
-  if (w.s.fuse_decide && issued < total && graph_loop_enabled()) {
+  // With a TraceSink the host chunk driver runs instead of the device loop: the
+  // sink is then called while the solve is in flight (after each chunk, in k
+  // order) and a sink that aborts stops the device within one chunk, as the
+  // reference's sink -- called inside its loop, dpt.cpp:153-157 -- stops it.
+  if (w.s.fuse_decide && issued < total && graph_loop_enabled() && !trace) {
     drive_graph(ctx, w, dp, mode, row, total, issued, cycle_elems, trace, user, err);
     return;
   }
@@ -1326,7 +1344,7 @@ void drive(dpt_ctx* ctx, Work& w, DevProblem& dp, Mode mode, int64_t row, int to
     if (pending) done = consume(slot ^ 1);
     pending = true;
     ++c;
-    chunk = std::min(chunk * 2, 64);
+    chunk = std::min(chunk * 2, trace ? 8 : 64);  // a sink sees every iteration within <= 8 launches
   }
   if (pending && !done) done = consume((c - 1) & 1);
   CK(cudaStreamSynchronize(st));
@@ -1446,6 +1464,7 @@ void put_identity(dpt_ctx* ctx, Work& w, DevProblem& dp, dpt_error_info* err) {
 
 void gather_rows(dpt_ctx* ctx, const Work& w, const DevProblem& dp, int slot, double* dst, int out_mem,
                  dpt_error_info* err) {
+  Nvtx nvtx_range("dpt.gather_rows");
   if (!dst) return;
   cudaStream_t st = ctx->stream;
   if (!sharded(ctx)) {
@@ -1594,6 +1613,7 @@ int run_full(dpt_ctx* ctx, const dpt_problem* p, const dpt_options* opts_in, boo
              int fixed_k, double fixed_lambda, dpt_trace_fn trace, void* user, double* a_out,
              double* eig_out, double* res_out, int out_mem, dpt_report* rep, dpt_error_info* err,
              double fixed_lambda_im = 0.0) {
+  Nvtx nvtx_range("dpt.run_full");
   const dpt_options o = opts_or_default(opts_in);
   Guard g(ctx);
   validate(p, err);
@@ -1726,6 +1746,7 @@ int run_full(dpt_ctx* ctx, const dpt_problem* p, const dpt_options* opts_in, boo
 int run_step_full(dpt_ctx* ctx, const dpt_problem* p, const double* a, const double* gap, double lambda,
                   double* out, int io_mem, double* eig_out, double* res_out, dpt_error_info* err,
                   double lambda_im = 0.0) {
+  Nvtx nvtx_range("dpt.step_full");
   Guard g(ctx);
   validate(p, err);
   if (sharded(ctx)) {
@@ -1769,6 +1790,7 @@ int run_single(dpt_ctx* ctx, const dpt_problem* p, int64_t row, const dpt_option
                dpt_trace_fn trace, void* user, double* z_out, int out_mem, dpt_report* rep,
                const double* z_in, int z_mem, double fixed_lambda, double* eig_fixed, double* z_unit,
                dpt_error_info* err, const double* gap_row = nullptr, double fixed_lambda_im = 0.0) {
+  Nvtx nvtx_range("dpt.run_single");
   const dpt_options o = opts_or_default(opts_in);
   Guard g(ctx);
   validate(p, err);
@@ -1931,6 +1953,7 @@ void gemm_rm(dpt_ctx* ctx, int cx, int64_t n, const double* A, const double* B, 
 
 int run_homotopy(dpt_ctx* ctx, const dpt_problem* p, int stages, const dpt_options* opts_in, double* a_out,
                  double* eig_out, double* res_out, int out_mem, dpt_report* rep, dpt_error_info* err) {
+  Nvtx nvtx_range("dpt.homotopy_solve");
   Guard g(ctx);
   validate(p, err);
   if (stages < 1) {

@@ -112,6 +112,27 @@ def test_trace_exception_propagates():
         P.iterate_full(pr.two_by_two(0.3), trace=sink)
 
 
+def test_trace_abort_stops_the_device():
+    """A sink that aborts at k = 3 stops the solve within one chunk of launches
+    (the reference calls the sink inside its loop, dpt.cpp:153-157): a run
+    with max_iter 1000 that never terminates on its own (lambda = 0.88 with
+    the cycle window off) issues at most a few chunks, and the sink is never
+    called again after it raised."""
+    ctx = P.Context(0)
+    seen = []
+
+    def sink(k, s, r):
+        seen.append(k)
+        if k == 3:
+            raise KeyError("stop")
+    l0 = ctx.launches
+    with pytest.raises(KeyError):
+        P.iterate_full(pr.two_by_two(0.88), P.IterationOptions(cycle_window=0, max_iter=1000), trace=sink, ctx=ctx)
+    assert seen == [1, 2, 3]
+    assert ctx.launches - l0 < 3 * (4 + 8 + 8), ctx.launches - l0
+    ctx.close()
+
+
 # ------------------------------------------- known answers (test_dpt.cpp) ----
 def test_known_answers_full():
     s = math.sqrt(1 + 4 * 0.09)
