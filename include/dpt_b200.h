@@ -267,12 +267,22 @@ int dpt_effective_window(int requested, int64_t n); /* dpt.cpp:83-90 */
  * homotopy_solve, dpt.hpp:145-152 / dpt.cpp:505-556: `stages` solves along
  * lambda_s = lambda s / stages, each on the problem rebased by the product W of
  * the converged bases (R = W^-1 (lambda_s Delta + diag d) W, re-split with
- * lambda 1), all on the device (cuBLAS GEMM / cuSOLVER LU for the basis
- * algebra, the solver's kernels for the stage solves).  Outputs as
+ * lambda 1), all on the device (the basis algebra on the library-free DMMA
+ * GEMM and cluster LU of linalg.cu, the stage solves on the solver's kernels).  Outputs as
  * dpt_iterate_full: a = the normalised eigenvector matrix, read-offs against
  * the original problem, rep.iterations = the sum over stages, rep.status = the
  * last stage's.  Errors: stages < 1 -> DPT_ERR_INVALID_ARG; a singular basis
  * -> DPT_ERR_UNSUPPORTED (the reference's std::runtime_error). */
+/* matmul(DenseMatrix, DenseMatrix), matrix.cpp:130-143: c (m x n) = a (m x k)
+ * b (k x n), row-major, complex interleaved when is_complex (the DMMA GEMM). */
+int dpt_matmul_dense(dpt_ctx* ctx, int64_t m, int64_t k, int64_t n, int is_complex, const double* a, const double* b,
+                     double* c, int mem, dpt_error_info* err);
+/* solve_linear_multi(a, b), matrix.cpp:519-533: x (n x nrhs) = a^-1 b by LU
+ * with partial pivoting (first row of maximal |a(i,k)|), on the device.  An
+ * exactly-zero pivot -> DPT_ERR_UNSUPPORTED ("solve_linear: singular matrix",
+ * the reference's std::runtime_error). */
+int dpt_solve_linear_multi(dpt_ctx* ctx, int64_t n, int64_t nrhs, int is_complex, const double* a, const double* b,
+                           double* x, int mem, dpt_error_info* err);
 int dpt_homotopy_solve(dpt_ctx* ctx, const dpt_problem* p, int stages, const dpt_options* opts, double* a_out,
                        double* eig_out, double* res_out, int out_mem, dpt_report* rep, dpt_error_info* err);
 

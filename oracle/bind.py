@@ -269,6 +269,8 @@ class ComplexReference:
         L.ref_c_check_degenerate.argtypes = [c_int64, c_void_p, c_double, P(c_int64), P(c_int64)]
         L.ref_c_homotopy.argtypes = [P(orc_cproblem), c_int, P(orc_options), c_void_p, c_void_p, c_void_p,
                                      P(orc_report)]
+        L.ref_c_matmul.argtypes = [c_int64, c_int64, c_int64, c_void_p, c_void_p, c_void_p]
+        L.ref_c_solve_linear_multi.argtypes = [c_int64, c_int64, c_void_p, c_void_p, c_void_p]
         L.ref_scan_domain.argtypes = [P(orc_cproblem), c_double, c_double, c_double, c_double, c_int64, c_int64, c_int,
                                       c_int64, c_double, P(orc_options), c_int, c_void_p, c_void_p, P(c_int64),
                                       P(c_int64)]
@@ -379,6 +381,23 @@ class ComplexReference:
         rc = self.L.ref_c_homotopy(ctypes.byref(pr), int(stages), ctypes.byref(Checker._opts(opts)), a.ctypes.data,
                                    eig.ctypes.data, res.ctypes.data, ctypes.byref(rep))
         return FullResult(rc, rep.status, rep.iterations, rep.step_norm, a, eig, res)
+
+    def matmul(self, a, b):
+        """The reference's matmul(DenseMatrix, DenseMatrix) (matrix.cpp:130-143)."""
+        a = np.ascontiguousarray(a, dtype=np.complex128)
+        b = np.ascontiguousarray(b, dtype=np.complex128)
+        c = np.zeros((a.shape[0], b.shape[1]), np.complex128)
+        assert self.L.ref_c_matmul(a.shape[0], a.shape[1], b.shape[1], a.ctypes.data, b.ctypes.data,
+                                   c.ctypes.data) == 0
+        return c
+
+    def solve_linear_multi(self, a, b):
+        """The reference's solve_linear_multi (matrix.cpp:519-533): (rc, x); rc 8 = singular."""
+        a = np.ascontiguousarray(a, dtype=np.complex128)
+        b = np.ascontiguousarray(b, dtype=np.complex128)
+        x = np.zeros(b.shape, np.complex128)
+        rc = self.L.ref_c_solve_linear_multi(a.shape[0], b.shape[1], a.ctypes.data, b.ctypes.data, x.ctypes.data)
+        return rc, x
 
     def scan_domain(self, p, grid, mode="Full", row=0, ramp_alpha=0.0, opts=None, threads=0):
         """The reference's scan_domain: (rc, classes[res_im, res_re] uint8, iterations int32, degenerate)."""

@@ -567,3 +567,39 @@ extern "C" int ref_c_homotopy(const orc_cproblem* p, int stages, const orc_optio
     return 9;
   }
 }
+
+// matmul (matrix.cpp:130-143) and solve_linear_multi (matrix.cpp:519-533) of the
+// reference on interleaved complex row-major arrays (the device linear algebra's checkers).
+namespace {
+DenseMatrix get_cdense(const double* a, std::size_t r, std::size_t c) {
+  DenseMatrix m(r, c);
+  for (std::size_t i = 0; i < r * c; ++i) m.data()[i] = cdouble{a[2 * i], a[2 * i + 1]};
+  return m;
+}
+void put_cdense_rc(const DenseMatrix& m, double* out) {
+  for (std::size_t i = 0; i < m.rows() * m.cols(); ++i) {
+    out[2 * i] = m.data()[i].real();
+    out[2 * i + 1] = m.data()[i].imag();
+  }
+}
+}  // namespace
+
+extern "C" int ref_c_matmul(int64_t m, int64_t k, int64_t n, const double* a, const double* b, double* c) {
+  try {
+    put_cdense_rc(matmul(get_cdense(a, size_t(m), size_t(k)), get_cdense(b, size_t(k), size_t(n))), c);
+    return ORC_OK;
+  } catch (...) {
+    return 9;
+  }
+}
+
+extern "C" int ref_c_solve_linear_multi(int64_t n, int64_t nrhs, const double* a, const double* b, double* x) {
+  try {
+    put_cdense_rc(solve_linear_multi(get_cdense(a, size_t(n), size_t(n)), get_cdense(b, size_t(n), size_t(nrhs))), x);
+    return ORC_OK;
+  } catch (const std::runtime_error&) {
+    return 8;  // "solve_linear: singular matrix"
+  } catch (...) {
+    return 9;
+  }
+}

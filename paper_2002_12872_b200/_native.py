@@ -132,6 +132,10 @@ def lib() -> ctypes.CDLL:
         L.dpt_spectral_spread.argtypes = [I64, c_void_p]
         L.dpt_spectral_spread.restype = D
         L.dpt_effective_window.argtypes = [c_int, I64]
+        L.dpt_matmul_dense.argtypes = [c_void_p, c_int64, c_int64, c_int64, c_int, c_void_p, c_void_p, c_void_p,
+                                       c_int, P(dpt_error_info)]
+        L.dpt_solve_linear_multi.argtypes = [c_void_p, c_int64, c_int64, c_int, c_void_p, c_void_p, c_void_p, c_int,
+                                             P(dpt_error_info)]
         L.dpt_homotopy_solve.argtypes = [c_void_p, P(dpt_problem), c_int, P(dpt_options), c_void_p, c_void_p,
                                          c_void_p, c_int, P(dpt_report), P(dpt_error_info)]
         L.dpt_mm_read.argtypes = [ctypes.c_char_p, c_int, P(dpt_mm_matrix), P(dpt_error_info)]

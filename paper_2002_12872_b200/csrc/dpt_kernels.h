@@ -71,14 +71,28 @@ cudaError_t launch_identity(const DevSolve& s, cudaStream_t st);
 int dense_sk_grid(int cplx);          // stream-K K1: resident CTAs (persistent grid)
 size_t dense_sk_part_doubles();       // stream-K K1: doubles per partial tile
 cudaError_t launch_hom_stage_matrix(const double* D, const double* d, double lr, double li, int cx, int64_t n,
-                                    double* M, cudaStream_t st);
-cudaError_t launch_hom_transpose(const double* src, double* dst, int cx, int64_t n, cudaStream_t st);
-cudaError_t launch_hom_partition(const double* R, double* dlev, double* Dp, int cx, int64_t n, cudaStream_t st);
-cudaError_t launch_hom_normalise(const double* W, double* a, int cx, int64_t n, unsigned* singular, cudaStream_t st);
-cudaError_t launch_hom_densify(const int64_t* rp, const int32_t* cl, const double* vl, int cx, int64_t n, double* D,
-                               cudaStream_t st);
-cudaError_t launch_hom_identity(double* W, int cx, int64_t n, cudaStream_t st);
+                                    int64_t ld, double* M, cudaStream_t st);
+cudaError_t launch_hom_partition(const double* R, int64_t ld, double* dlev, double* Dp, int cx, int64_t n,
+                                 cudaStream_t st);
+cudaError_t launch_hom_normalise(const double* W, int64_t ld, double* a, int cx, int64_t n, unsigned* singular,
+                                 cudaStream_t st);
+cudaError_t launch_hom_densify(const int64_t* rp, const int32_t* cl, const double* vl, int cx, int64_t n, int64_t ld,
+                               double* D, cudaStream_t st);
+cudaError_t launch_hom_identity(double* W, int cx, int64_t n, int64_t ld, cudaStream_t st);
 cudaError_t launch_hom_nonfinite(const double* a, int64_t count, unsigned* bad, cudaStream_t st);
+// linalg.cu: library-free dense linear algebra of the device homotopy (row-major
+// FP64, leading dims in doubles, complex interleaved when cx = 2)
+cudaError_t launch_gemm_nt(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, const double* B,
+                           int64_t ldb, double alpha, double beta, double* Cm, int64_t ldc, cudaStream_t st);
+cudaError_t launch_gemm_bop(int cx, bool trans, const double* S, int64_t lds, int64_t N, int64_t K, double* out,
+                            int64_t ldo, cudaStream_t st);
+cudaError_t launch_lu_factor(int cx, double* A, int64_t lda, int64_t n, int64_t* piv, int* info, double* scratch,
+                             int* launches, cudaStream_t st);
+cudaError_t launch_lu_solve(int cx, const double* A, int64_t lda, int64_t n, double* X, int64_t ldx, int64_t nrhs,
+                            double* scratch, int* launches, cudaStream_t st);
+cudaError_t launch_gather_rows(const double* src, int64_t ld, const int64_t* perm, int64_t n, int64_t width,
+                               double* dst, cudaStream_t st);
+int64_t lu_max_n(int cx);
 
 // scan.cu: batched scan_domain, one warp per lambda cell (complex arithmetic in
 // the reference's operation order).  All arrays complex interleaved unless noted.

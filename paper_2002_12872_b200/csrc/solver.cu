@@ -12,8 +12,6 @@
 // trace log to the TraceSink in k order, and stops.
 #include <cuda.h>
 #include <cuda_runtime.h>
-#include <cublas_v2.h>
-#include <cusolverDn.h>
 #include <dlfcn.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -169,9 +167,6 @@ struct dpt_ctx {
   };
   std::vector<LoopGraph> loop_graphs;  // most recent last, at most kMaxLoopGraphs
   int64_t graph_hits = 0, graph_misses = 0;
-  // library handles for the homotopy's plain GEMM / LU (created on first use)
-  cublasHandle_t cublas = nullptr;
-  cusolverDnHandle_t cusolver = nullptr;
 };
 
 namespace {
@@ -1913,44 +1908,13 @@ int run_single(dpt_ctx* ctx, const dpt_problem* p, int64_t row, const dpt_option
 
 
 // ------------------------------------------------------ homotopy_solve ----
-// dpt.cpp:505-556 on the device.  Per stage s: M_s = lam_s Delta + diag(d),
-// R = W^-1 (M_s W) (cuBLAS GEMM + cuSOLVER LU -- plain library linear algebra),
-// partition(R) -> d', Delta' (lambda 1), the DPT solve of that problem in the
-// solver's kernels (A_s stays in HBM), W <- W A_s^T.  Then a(i, m) =
-// W(m, i) / W(i, i) and the read-offs of a against the original problem.
-#define CB(x)                                                                                   \
-  do {                                                                                          \
-    const cublasStatus_t s_ = (x);                                                              \
-    if (s_ != CUBLAS_STATUS_SUCCESS) {                                                          \
-      set_err(err, DPT_ERR_CUDA, std::string("cuBLAS status ") + std::to_string(int(s_)) + ": " #x); \
-      throw Fail{DPT_ERR_CUDA};                                                                 \
-    }                                                                                           \
-  } while (0)
-#define CSV(x)                                                                                    \
-  do {                                                                                            \
-    const cusolverStatus_t s_ = (x);                                                              \
-    if (s_ != CUSOLVER_STATUS_SUCCESS) {                                                          \
-      set_err(err, DPT_ERR_CUDA, std::string("cuSOLVER status ") + std::to_string(int(s_)) + ": " #x); \
-      throw Fail{DPT_ERR_CUDA};                                                                   \
-    }                                                                                             \
-  } while (0)
-
-// row-major C = A B (n x n): the column-major product B^T-view x A^T-view
-void gemm_rm(dpt_ctx* ctx, int cx, int64_t n, const double* A, const double* B, double* C, bool b_transposed,
-             dpt_error_info* err) {
-  const int nn = int(n);
-  // row-major buffers are column-major transposes: C^T = B^T A^T (or A B^T -> C^T = B A^T)
-  const cublasOperation_t opA = b_transposed ? CUBLAS_OP_T : CUBLAS_OP_N;
-  if (cx == 2) {
-    const cuDoubleComplex one = make_cuDoubleComplex(1.0, 0.0), zero = make_cuDoubleComplex(0.0, 0.0);
-    CB(cublasZgemm(ctx->cublas, opA, CUBLAS_OP_N, nn, nn, nn, &one, reinterpret_cast<const cuDoubleComplex*>(B), nn,
-                   reinterpret_cast<const cuDoubleComplex*>(A), nn, &zero, reinterpret_cast<cuDoubleComplex*>(C), nn));
-  } else {
-    const double one = 1.0, zero = 0.0;
-    CB(cublasDgemm(ctx->cublas, opA, CUBLAS_OP_N, nn, nn, nn, &one, B, nn, A, nn, &zero, C, nn));
-  }
-}
-
+// dpt.cpp:505-556 on the device, no libraries.  Per stage s:
+// M_s = lam_s Delta + diag(d); R = W^-1 (M_s W) -- the product on the DMMA
+// GEMM, the solve as an LU of W with partial pivoting (cluster panels + GEMM
+// trailing updates) and blocked triangular solves over the n right-hand sides
+// (linalg.cu); partition(R) -> d', Delta' (lambda 1), the DPT solve of that
+// problem in the solver's kernels (A_s stays in HBM), W <- W A_s^T.  Then
+// a(i, m) = W(m, i) / W(i, i) and the read-offs of a against the original problem.
 int run_homotopy(dpt_ctx* ctx, const dpt_problem* p, int stages, const dpt_options* opts_in, double* a_out,
                  double* eig_out, double* res_out, int out_mem, dpt_report* rep, dpt_error_info* err) {
   Nvtx nvtx_range("dpt.homotopy_solve");
@@ -1963,81 +1927,86 @@ int run_homotopy(dpt_ctx* ctx, const dpt_problem* p, int stages, const dpt_optio
   const dpt_options o = opts_or_default(opts_in);
   const int64_t n = p->n;
   const int cx = p->is_complex ? 2 : 1;
+  if (n > lu_max_n(cx)) {
+    set_err(err, DPT_ERR_UNSUPPORTED, "homotopy_solve: n exceeds the device LU's cluster panel capacity (" +
+                                          std::to_string(lu_max_n(cx)) + ")");
+    return DPT_ERR_UNSUPPORTED;
+  }
   cudaStream_t st = ctx->stream;
-  if (!ctx->cublas) CB(cublasCreate(&ctx->cublas));
-  if (!ctx->cusolver) CSV(cusolverDnCreate(&ctx->cusolver));
-  CB(cublasSetStream(ctx->cublas, st));
-  CSV(cusolverDnSetStream(ctx->cusolver, st));
-  const size_t mat = size_t(cx) * size_t(n) * size_t(n) * 8;
+  const int64_t ld = (cx * n + 1) & ~int64_t(1);  // doubles per row, even (TMA strides)
+  const size_t mat = size_t(n) * size_t(ld) * 8;  // padded row-major matrix
+  const size_t cmat = size_t(cx) * size_t(n) * size_t(n) * 8;  // contiguous (the stage problem / its result)
+  const int64_t ldop = 2 * n;  // B-operand rows: n (real) or the 2n x 2n image (complex), 2n >= cx n, even
+  const size_t opbytes = size_t(cx * n) * size_t(ldop) * 8;
   const cudaMemcpyKind k = p->mem == DPT_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-  DBuf bd, bD, bW, bM, bT1, bT2, bA, bdl, bDp, bpiv, binfo, bflag;
+  DBuf bd, bD, bW, bWn, bM, bMW, bLU, bX, bA, bdl, bDp, bop, bscr, bpiv, bperm, binfo, bflag;
   dalloc(bd, size_t(cx * n) * 8, err);
   dalloc(bD, mat, err);
   dalloc(bW, mat, err);
+  dalloc(bWn, mat, err);
   dalloc(bM, mat, err);
-  dalloc(bT1, mat, err);
-  dalloc(bT2, mat, err);
-  dalloc(bA, mat, err);
+  dalloc(bMW, mat, err);
+  dalloc(bLU, mat, err);
+  dalloc(bX, mat, err);
+  dalloc(bA, cmat, err);
   dalloc(bdl, size_t(cx * n) * 8, err);
-  dalloc(bDp, mat, err);
-  dalloc(bpiv, size_t(n) * 4 + 16, err);
+  dalloc(bDp, cmat, err);
+  dalloc(bop, opbytes, err);
+  dalloc(bscr, size_t(4) * size_t(n) * 32 * 8 + 64, err);
+  dalloc(bpiv, size_t(n) * 8 + 16, err);
+  dalloc(bperm, size_t(n) * 8 + 16, err);
   dalloc(binfo, 16, err);
   dalloc(bflag, 16, err);
   if (n) CK(cudaMemcpyAsync(bd.p, p->d, size_t(cx * n) * 8, k, st));
   if (p->delta_kind == DPT_DELTA_DENSE) {  // densify(p.delta) (dpt.cpp:510)
-    if (n) CK(cudaMemcpyAsync(bD.p, p->delta, mat, k, st));
+    if (n) CK(copy2d_async(ctx, bD.p, size_t(ld) * 8, p->delta, size_t(cx * n) * 8, size_t(cx * n) * 8, size_t(n), k));
   } else {
     DevProblem dp;
     upload(dp, ctx, p, err);
     CK(cudaMemsetAsync(bD.p, 0, mat, st));
-    CK(launch_hom_densify(dp.rowptr.as<int64_t>(), dp.cols.as<int32_t>(), dp.vals.as<double>(), cx, n,
+    CK(launch_hom_densify(dp.rowptr.as<int64_t>(), dp.cols.as<int32_t>(), dp.vals.as<double>(), cx, n, ld,
                           bD.as<double>(), st));
     CK(cudaStreamSynchronize(st));  // dp's buffers go out of scope
   }
-  CK(launch_hom_identity(bW.as<double>(), cx, n, st));
-  int lwork = 0;
-  if (cx == 2)
-    CSV(cusolverDnZgetrf_bufferSize(ctx->cusolver, int(n), int(n), reinterpret_cast<cuDoubleComplex*>(bT1.p),
-                                    int(n), &lwork));
-  else
-    CSV(cusolverDnDgetrf_bufferSize(ctx->cusolver, int(n), int(n), bT1.as<double>(), int(n), &lwork));
-  DBuf bwork;
-  dalloc(bwork, size_t(std::max(lwork, 1)) * size_t(cx) * 8, err);
+  CK(launch_hom_identity(bW.as<double>(), cx, n, ld, st));
+  ctx->launches += 1;
+  std::vector<int64_t> hpiv(static_cast<size_t>(n)), hperm(static_cast<size_t>(n));
   dpt_report last{};
   int total = 0;
   double* W = bW.as<double>();
-  double* Wn = bT2.as<double>();
-  for (int s = 1; s <= stages; ++s) {
+  double* Wn = bWn.as<double>();
+  for (int s = 1; s <= stages && n > 0; ++s) {
     const double f = double(s) / double(stages);  // lam_s = lambda * (s / stages), complex * double
     const double lr = p->lambda * f, li = (p->is_complex ? p->lambda_im : 0.0) * f;
-    CK(launch_hom_stage_matrix(bD.as<double>(), bd.as<double>(), lr, li, cx, n, bM.as<double>(), st));
-    gemm_rm(ctx, cx, n, bM.as<double>(), W, bT1.as<double>(), false, err);  // M W
-    // R = W^-1 (M W): column-major LU of W, solve against (M W), back to row-major
-    CK(launch_hom_transpose(W, bA.as<double>(), cx, n, st));                  // W (column-major)
-    CK(launch_hom_transpose(bT1.as<double>(), bDp.as<double>(), cx, n, st));  // M W (column-major)
-    int* piv = bpiv.as<int>();
-    int* info = binfo.as<int>();
-    if (cx == 2) {
-      CSV(cusolverDnZgetrf(ctx->cusolver, int(n), int(n), reinterpret_cast<cuDoubleComplex*>(bA.p), int(n),
-                           reinterpret_cast<cuDoubleComplex*>(bwork.p), piv, info));
-    } else {
-      CSV(cusolverDnDgetrf(ctx->cusolver, int(n), int(n), bA.as<double>(), int(n), bwork.as<double>(), piv, info));
-    }
+    CK(launch_hom_stage_matrix(bD.as<double>(), bd.as<double>(), lr, li, cx, n, ld, bM.as<double>(), st));
+    // M W: B operand = W^T (real) or its image (complex)
+    CK(launch_gemm_bop(cx, true, W, ld / cx, n, n, bop.as<double>(), ldop, st));
+    CK(launch_gemm_nt(n, cx * n, cx * n, bM.as<double>(), ld, bop.as<double>(), ldop, 1.0, 0.0, bMW.as<double>(), ld,
+                      st));
+    ctx->launches += 3;
+    // R = W^-1 (M W): LU of a copy of W (lu_factor, matrix.cpp:468-494)
+    CK(cudaMemcpyAsync(bLU.p, W, mat, cudaMemcpyDeviceToDevice, st));
+    int nl = 0;
+    CK(launch_lu_factor(cx, bLU.as<double>(), ld, n, bpiv.as<int64_t>(), binfo.as<int>(), bscr.as<double>(), &nl, st));
     int hinfo = 0;
-    CK(cudaMemcpyAsync(&hinfo, info, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&hinfo, binfo.p, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hpiv.data(), bpiv.p, size_t(n) * 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    if (hinfo > 0) {  // lu_factor's exact-zero pivot (matrix.cpp:485)
+    ctx->launches += nl;
+    if (hinfo >= 1 && hinfo <= n) {  // lu_factor's exact-zero pivot (matrix.cpp:485)
       set_err(err, DPT_ERR_UNSUPPORTED, "solve_linear: singular matrix");
       throw Fail{DPT_ERR_UNSUPPORTED};
     }
-    if (cx == 2)
-      CSV(cusolverDnZgetrs(ctx->cusolver, CUBLAS_OP_N, int(n), int(n), reinterpret_cast<cuDoubleComplex*>(bA.p),
-                           int(n), piv, reinterpret_cast<cuDoubleComplex*>(bDp.p), int(n), info));
-    else
-      CSV(cusolverDnDgetrs(ctx->cusolver, CUBLAS_OP_N, int(n), int(n), bA.as<double>(), int(n), piv, bDp.as<double>(),
-                           int(n), info));
-    CK(launch_hom_transpose(bDp.as<double>(), bM.as<double>(), cx, n, st));  // R (row-major)
-    CK(launch_hom_partition(bM.as<double>(), bdl.as<double>(), bDp.as<double>(), cx, n, st));
+    // lu_solve's b[perm[i]] (matrix.cpp:501): the row permutation of the pivot sequence
+    for (int64_t i = 0; i < n; ++i) hperm[size_t(i)] = i;
+    for (int64_t i = 0; i < n; ++i) std::swap(hperm[size_t(i)], hperm[size_t(hpiv[size_t(i)])]);
+    CK(cudaMemcpyAsync(bperm.p, hperm.data(), size_t(n) * 8, cudaMemcpyHostToDevice, st));
+    CK(launch_gather_rows(bMW.as<double>(), ld, bperm.as<int64_t>(), n, ld, bX.as<double>(), st));
+    nl = 0;
+    CK(launch_lu_solve(cx, bLU.as<double>(), ld, n, bX.as<double>(), ld, n, bscr.as<double>(), &nl, st));
+    CK(launch_hom_partition(bX.as<double>(), ld, bdl.as<double>(), bDp.as<double>(), cx, n, st));
+    ctx->launches += nl + 2;
+    CK(cudaStreamSynchronize(st));  // hperm (host) is rewritten next stage
     dpt_problem sp{};
     sp.n = n;
     sp.d = bdl.as<double>();
@@ -2053,13 +2022,19 @@ int run_homotopy(dpt_ctx* ctx, const dpt_problem* p, int stages, const dpt_optio
     if (rc != DPT_OK) return rc;
     total += last.iterations;
     if (last.status != DPT_CONVERGED) break;
-    gemm_rm(ctx, cx, n, W, bA.as<double>(), Wn, true, err);  // W V, V = A^T (no conjugation)
+    // W V with V = A_s^T (no conjugation): the NT product against A_s itself
+    CK(launch_gemm_bop(cx, false, bA.as<double>(), n, n, n, bop.as<double>(), ldop, st));
+    CK(launch_gemm_nt(n, cx * n, cx * n, W, ld, bop.as<double>(), ldop, 1.0, 0.0, Wn, ld, st));
+    ctx->launches += 2;
     std::swap(W, Wn);
   }
   // a(i, m) = W(m, i) / W(i, i)
   CK(cudaMemsetAsync(bflag.p, 0, 8, st));
-  CK(launch_hom_normalise(W, bA.as<double>(), cx, n, bflag.as<unsigned>(), st));
-  CK(launch_hom_nonfinite(bA.as<double>(), int64_t(cx) * n * n, bflag.as<unsigned>() + 1, st));
+  if (n) {
+    CK(launch_hom_normalise(W, ld, bA.as<double>(), cx, n, bflag.as<unsigned>(), st));
+    CK(launch_hom_nonfinite(bA.as<double>(), int64_t(cx) * n * n, bflag.as<unsigned>() + 1, st));
+    ctx->launches += 2;
+  }
   unsigned hf[2] = {0, 0};
   CK(cudaMemcpyAsync(hf, bflag.p, 8, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -2164,8 +2139,6 @@ void dpt_ctx_destroy(dpt_ctx* ctx) {
     Guard g(ctx);
     if (ctx->comm && nccl_api() && nccl_api()->comm_destroy) nccl_api()->comm_destroy(ctx->comm);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-    if (ctx->cublas) cublasDestroy(ctx->cublas);
-    if (ctx->cusolver) cusolverDnDestroy(ctx->cusolver);
     for (auto& lg : ctx->loop_graphs) {
       if (lg.ge) cudaGraphExecDestroy(lg.ge);
       if (lg.g) cudaGraphDestroy(lg.g);
@@ -2552,6 +2525,103 @@ int dpt_homotopy_solve(dpt_ctx* ctx, const dpt_problem* p, int stages, const dpt
                        double* eig_out, double* res_out, int out_mem, dpt_report* rep, dpt_error_info* err) {
   DPT_API_BEGIN
   return run_homotopy(ctx, p, stages, opts, a_out, eig_out, res_out, out_mem, rep, err);
+  DPT_API_END
+}
+
+// ---------------------------------------------- dense linear algebra ----
+// matmul(Dense, Dense) (matrix.cpp:130-143) and solve_linear_multi
+// (matrix.cpp:519-533) on the device kernels of the homotopy (linalg.cu).
+namespace {
+void put_padded(dpt_ctx* ctx, DBuf& b, const double* src, int64_t rows, int64_t cols_d, int64_t ld, int mem,
+                dpt_error_info* err) {
+  dalloc(b, size_t(std::max<int64_t>(rows, 1)) * size_t(ld) * 8, err);
+  CK(cudaMemsetAsync(b.p, 0, size_t(std::max<int64_t>(rows, 1)) * size_t(ld) * 8, ctx->stream));
+  if (rows && cols_d)
+    CK(copy2d_async(ctx, b.p, size_t(ld) * 8, src, size_t(cols_d) * 8, size_t(cols_d) * 8, size_t(rows),
+                    mem == DPT_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+}
+void get_padded(dpt_ctx* ctx, double* dst, const DBuf& b, int64_t rows, int64_t cols_d, int64_t ld, int mem,
+                dpt_error_info* err) {
+  if (rows && cols_d)
+    CK(copy2d_async(ctx, dst, size_t(cols_d) * 8, b.p, size_t(ld) * 8, size_t(cols_d) * 8, size_t(rows),
+                    mem == DPT_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost));
+  CK(cudaStreamSynchronize(ctx->stream));
+}
+int64_t even_ld(int64_t v) { return (v + 1) & ~int64_t(1); }
+}  // namespace
+
+int dpt_matmul_dense(dpt_ctx* ctx, int64_t m, int64_t k, int64_t n, int is_complex, const double* a, const double* b,
+                     double* c, int mem, dpt_error_info* err) {
+  DPT_API_BEGIN
+  Guard g(ctx);
+  if (m < 0 || k < 0 || n < 0) {
+    set_err(err, DPT_ERR_SHAPE, "matmul shape mismatch");
+    return DPT_ERR_SHAPE;
+  }
+  const int cx = is_complex ? 2 : 1;
+  cudaStream_t st = ctx->stream;
+  DBuf ba, bb, bop, bc;
+  const int64_t lda = even_ld(cx * k), ldc = even_ld(cx * n), ldop = even_ld(cx * k);
+  put_padded(ctx, ba, a, m, cx * k, lda, mem, err);
+  put_padded(ctx, bb, b, k, cx * n, even_ld(cx * n), mem, err);
+  dalloc(bop, size_t(std::max<int64_t>(cx * n, 1)) * size_t(std::max<int64_t>(ldop, 2)) * 8, err);
+  dalloc(bc, size_t(std::max<int64_t>(m, 1)) * size_t(ldc) * 8, err);
+  if (k == 0) {
+    CK(cudaMemsetAsync(bc.p, 0, size_t(std::max<int64_t>(m, 1)) * size_t(ldc) * 8, st));
+  } else if (m && n) {
+    CK(launch_gemm_bop(cx, true, bb.as<double>(), even_ld(cx * n) / cx, n, k, bop.as<double>(), ldop, st));
+    CK(launch_gemm_nt(m, cx * n, cx * k, ba.as<double>(), lda, bop.as<double>(), ldop, 1.0, 0.0, bc.as<double>(), ldc,
+                      st));
+    ctx->launches += 2;
+  }
+  get_padded(ctx, c, bc, m, cx * n, ldc, mem, err);
+  return DPT_OK;
+  DPT_API_END
+}
+
+int dpt_solve_linear_multi(dpt_ctx* ctx, int64_t n, int64_t nrhs, int is_complex, const double* a, const double* b,
+                           double* x, int mem, dpt_error_info* err) {
+  DPT_API_BEGIN
+  Guard g(ctx);
+  const int cx = is_complex ? 2 : 1;
+  if (n < 0 || nrhs < 0) {
+    set_err(err, DPT_ERR_SHAPE, "solve_linear_multi shape mismatch");
+    return DPT_ERR_SHAPE;
+  }
+  if (n > lu_max_n(cx)) {
+    set_err(err, DPT_ERR_UNSUPPORTED, "solve_linear_multi: n exceeds the device LU's cluster panel capacity");
+    return DPT_ERR_UNSUPPORTED;
+  }
+  if (n == 0) return DPT_OK;
+  cudaStream_t st = ctx->stream;
+  const int64_t lda = even_ld(cx * n), ldx = even_ld(cx * std::max<int64_t>(nrhs, 1));
+  DBuf ba, bb, bx, bpiv, bperm, binfo, bscr;
+  put_padded(ctx, ba, a, n, cx * n, lda, mem, err);
+  put_padded(ctx, bb, b, n, cx * nrhs, ldx, mem, err);
+  dalloc(bx, size_t(n) * size_t(ldx) * 8, err);
+  dalloc(bpiv, size_t(n) * 8, err);
+  dalloc(bperm, size_t(n) * 8, err);
+  dalloc(binfo, 16, err);
+  dalloc(bscr, size_t(4) * size_t(std::max(n, nrhs)) * 32 * 8 + 64, err);
+  int nl = 0;
+  CK(launch_lu_factor(cx, ba.as<double>(), lda, n, bpiv.as<int64_t>(), binfo.as<int>(), bscr.as<double>(), &nl, st));
+  int hinfo = 0;
+  std::vector<int64_t> hpiv(static_cast<size_t>(n)), hperm(static_cast<size_t>(n));
+  CK(cudaMemcpyAsync(&hinfo, binfo.p, 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(hpiv.data(), bpiv.p, size_t(n) * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (hinfo >= 1 && hinfo <= n) {
+    set_err(err, DPT_ERR_UNSUPPORTED, "solve_linear: singular matrix");
+    return DPT_ERR_UNSUPPORTED;
+  }
+  for (int64_t i = 0; i < n; ++i) hperm[size_t(i)] = i;
+  for (int64_t i = 0; i < n; ++i) std::swap(hperm[size_t(i)], hperm[size_t(hpiv[size_t(i)])]);
+  CK(cudaMemcpyAsync(bperm.p, hperm.data(), size_t(n) * 8, cudaMemcpyHostToDevice, st));
+  CK(launch_gather_rows(bb.as<double>(), ldx, bperm.as<int64_t>(), n, ldx, bx.as<double>(), st));
+  if (nrhs) CK(launch_lu_solve(cx, ba.as<double>(), lda, n, bx.as<double>(), ldx, nrhs, bscr.as<double>(), &nl, st));
+  ctx->launches += nl + 1;
+  get_padded(ctx, x, bx, n, cx * nrhs, ldx, mem, err);
+  return DPT_OK;
   DPT_API_END
 }
 

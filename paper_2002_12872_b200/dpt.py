@@ -471,6 +471,52 @@ def homotopy_solve(p: PartitionedProblem, stages: int, opts: Optional[IterationO
                              rep.iterations, res, rep.step_norm, rep.device_ms)
 
 
+def _dense_host(x):
+    x = np.asarray(x)
+    cplx = np.iscomplexobj(x)
+    return np.ascontiguousarray(x, dtype=np.complex128 if cplx else np.float64), cplx
+
+
+def matmul_dense(a, b, ctx: Context = None) -> np.ndarray:
+    """matmul(DenseMatrix, DenseMatrix) (matrix.cpp:130-143) on the device DMMA
+    GEMM: a (m x k) @ b (k x n), real or complex host arrays."""
+    ctx = ctx or default_context()
+    a, ca = _dense_host(a)
+    b, cb = _dense_host(b)
+    if a.ndim != 2 or b.ndim != 2 or a.shape[1] != b.shape[0]:
+        raise ShapeError("matmul shape mismatch")
+    cplx = ca or cb
+    if cplx:
+        a, b = a.astype(np.complex128), b.astype(np.complex128)
+    c = np.zeros((a.shape[0], b.shape[1]), dtype=np.complex128 if cplx else np.float64)
+    err = N.dpt_error_info()
+    _raise(N.lib().dpt_matmul_dense(ctx.handle, a.shape[0], a.shape[1], b.shape[1], int(cplx), a.ctypes.data,
+                                    b.ctypes.data, c.ctypes.data, N.DPT_MEM_HOST, ctypes.byref(err)), err)
+    return c
+
+
+def solve_linear_multi(a, b, ctx: Context = None) -> np.ndarray:
+    """solve_linear_multi (matrix.cpp:519-533) on the device: a^-1 b by LU with
+    partial pivoting (cluster panels + DMMA updates).  Raises RuntimeError
+    ("solve_linear: singular matrix") on an exactly-zero pivot, as the reference."""
+    ctx = ctx or default_context()
+    a, ca = _dense_host(a)
+    b, cb = _dense_host(b)
+    if a.ndim != 2 or a.shape[0] != a.shape[1] or b.ndim != 2 or b.shape[0] != a.shape[0]:
+        raise ShapeError("solve_linear_multi shape mismatch")
+    cplx = ca or cb
+    if cplx:
+        a, b = a.astype(np.complex128), b.astype(np.complex128)
+    x = np.zeros(b.shape, dtype=np.complex128 if cplx else np.float64)
+    err = N.dpt_error_info()
+    rc = N.lib().dpt_solve_linear_multi(ctx.handle, a.shape[0], b.shape[1], int(cplx), a.ctypes.data, b.ctypes.data,
+                                        x.ctypes.data, N.DPT_MEM_HOST, ctypes.byref(err))
+    if rc == N.DPT_ERR_UNSUPPORTED and b"singular" in err.message:
+        raise RuntimeError(err.message.decode())
+    _raise(rc, err)
+    return x
+
+
 def iterate_ramped(p: PartitionedProblem, alpha: float, opts: Optional[IterationOptions] = None,
                    trace=None, ctx: Context = None):
     """lambda_k = lambda (1 - alpha^(k-1)) (dpt.hpp:85-92); alpha in [0, 1)."""

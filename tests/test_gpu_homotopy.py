@@ -1,6 +1,6 @@
 """GPU: staged continuation homotopy_solve on the device (SURVEY.md §8(f) row
 f2) against the reference's homotopy_solve (proj/src/dpt.cpp:505-556, in
-oracle/_ref).  The basis algebra runs in cuBLAS / cuSOLVER and each stage in
+oracle/_ref).  The basis algebra runs in the library-free DMMA GEMM + cluster LU (csrc/linalg.cu) and each stage in
 the solver's kernels, so parity is numerical: same status, iterations within
 +-1 per stage, eigenvalues 1e-10 relative, eigenvectors 1e-9 max-abs.  Plus
 the reference's own homotopy tests (proj/tests/test_dpt.cpp:336-359)."""
@@ -99,7 +99,7 @@ def test_csr_delta_and_stalled_stage(R):
 
 
 def test_c1_scale(R):
-    """n = 1024 (c1), 2 stages: the stage solves are K1 launches, the basis algebra cuBLAS/cuSOLVER."""
+    """n = 1024 (c1), 2 stages: the stage solves are K1 launches, the basis algebra csrc/linalg.cu."""
     p, o, _ = pr.config("c1", 1024)
     g = P.homotopy_solve(p, 2, IterationOptions(**o))
     assert g.status == P.ConvergenceStatus.Converged

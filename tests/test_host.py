@@ -180,3 +180,13 @@ def test_sharded_two_ranks_gloo(name):
     if int(z["status"]) != 2:
         assert np.max(np.abs(full - z["a"])) < 1e-9
         assert np.max(np.abs(eig - z["eig"]) / np.maximum(1, np.abs(z["eig"]))) < 1e-10
+
+
+def test_library_needs_no_linear_algebra_libraries():
+    """Row f2 runs on the repo's own kernels: libdpt_b200.so links neither
+    cuBLAS nor cuSOLVER (the homotopy's GEMM / LU are csrc/linalg.cu)."""
+    import subprocess
+    so = os.path.join(ROOT, "paper_2002_12872_b200", "libdpt_b200.so")
+    out = subprocess.run(["readelf", "-d", so], capture_output=True, text=True, check=True).stdout
+    needed = [ln for ln in out.splitlines() if "NEEDED" in ln]
+    assert needed and not any("cublas" in ln or "cusolver" in ln for ln in needed), needed
