@@ -39,14 +39,6 @@ struct DevSell {
   const int32_t* perm;      // [n] shared-memory position of column k (bank balance), null = identity
   const int32_t* inv;       // [npad] column at position p (-1 = unused), null = identity
   int64_t npad;             // staged row length in positions (>= n)
-  // split staging (csr_step_parts_kernel): positions cut into `parts` ranges of
-  // hpos; bnd[sl * (parts + 1) + h] = first step of range h in slice sl
-  int parts;
-  int64_t hpos;
-  const int32_t* bnd;
-  double* pbuf;             // [nslot][R][nslices * 32] partial dots between ranges
-  int* pflags;              // [nslot] slot ownership (0 free)
-  int nslot;
 };
 int csr_step_ntiles(int64_t rows, int64_t n);
 int csr_ntn(int64_t n);
@@ -130,18 +122,11 @@ cudaError_t launch_scan(const ScanArgs& a, int warps_total, cudaStream_t st);
 cudaError_t launch_sell_perm(const int64_t* rp, int64_t n, int32_t* lane_col, int32_t* lane_len, int64_t* pos_of,
                              cudaStream_t st);
 cudaError_t launch_sell_widths(const int64_t* rp, const int32_t* cl, int64_t nslices, const int32_t* lane_col, int G,
-                               int sched, const int32_t* perm, int parts, int64_t hpos, int32_t* bnd, int64_t* widths,
-                               cudaStream_t st);
+                               int sched, const int32_t* perm, int64_t* widths, cudaStream_t st);
 cudaError_t launch_sell_scan(int64_t* widths, int64_t nslices, int64_t* total, cudaStream_t st);
 cudaError_t launch_sell_fill(const int64_t* rp, const int32_t* cl, const double* vl, int cx, int64_t nslices,
-                             const int32_t* lane_col, int G, int sched, const int32_t* perm, int parts, int64_t hpos,
-                             const int64_t* off, int32_t* s_cols, double* s_vals, cudaStream_t st);
-// K2 split staging: parts (1 = whole rows) for an n x n CSR full map with npad
-// staged positions, the positions per part, and the rows a CTA stages
-int csr_parts_for(int64_t n, int64_t npad, int cplx, int sched);
-int64_t csr_part_positions(int64_t npad, int parts);
-int csr_parts_rows(int64_t hpos);
-int csr_step_ntiles_sell(int64_t rows, int64_t n, const DevSell& d);
+                             const int32_t* lane_col, int G, int sched, const int32_t* perm, const int64_t* off,
+                             int32_t* s_cols, double* s_vals, cudaStream_t st);
 // column relabelling for bank balance (real K2): pos / inv permutation, padded staged-row length
 size_t relabel_smem_bytes(int64_t nslices);
 cudaError_t launch_relabel(const int64_t* rp, const int32_t* cl, int64_t n, int64_t nnz, int64_t nslices,

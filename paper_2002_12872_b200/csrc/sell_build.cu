@@ -123,20 +123,11 @@ __global__ void sell_sched_kernel(const int64_t* __restrict__ rp, const int32_t*
 // schedule's order: deterministic (both passes make the same choices), the
 // same for every staging variant R, within rounding of the reference's
 // CSR-order sum.  Counts and cursors live in registers (unrolled bank loops).
-//
-// Parts (K2's split staging, csr_step_parts_kernel): with parts > 1 the staged
-// positions are cut into ranges of hpos; a lane issues all its entries of
-// range 0, then of range 1, ... -- each range scheduled by the same auction and
-// padded to kSellPad steps; bnd[sl * (parts + 1) + h] is the first step of
-// range h (bnd[.. + parts] = the width).  A kernel that streams the whole width
-// (csr_step_kernel) accumulates in exactly this order too, so every staging
-// variant gives bit-identical sums.
 template <bool WRITE>
 __global__ void __launch_bounds__(256)
     sell_free_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ cl, const double* __restrict__ vl,
                      int cx, int64_t nslices, const int32_t* __restrict__ lane_col, int G,
-                     const int32_t* __restrict__ perm, int parts, int64_t hpos, int32_t* bnd, int64_t* width_or_off,
-                     int32_t* s_cols, double* s_vals) {
+                     const int32_t* __restrict__ perm, int64_t* width_or_off, int32_t* s_cols, double* s_vals) {
   const int lane = threadIdx.x & 31;
   const int64_t sl = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   if (sl >= nslices) return;  // warp-uniform
@@ -149,22 +140,13 @@ __global__ void __launch_bounds__(256)
   // relabelled for bank balance (sell_relabel_kernel), else k
   auto colpos = [&](int64_t q) -> int32_t { return perm ? perm[cl[q]] : cl[q]; };
   int cnt[16], pos[16];
-  int64_t step = 0;
-  if (lane == 0 && bnd) bnd[sl * (parts + 1)] = 0;
-  for (int h = 0; h < parts; ++h) {
-  const int64_t lo = parts > 1 ? h * hpos : 0, hi = parts > 1 ? (h + 1) * hpos : INT64_MAX;
-  auto inpart = [&](int32_t p) { return p >= lo && p < hi; };
 #pragma unroll
   for (int b = 0; b < 16; ++b) {
     cnt[b] = 0;
     pos[b] = len;
   }
-  int rem = 0;
   for (int q = 0; q < len; ++q) {
-    const int32_t cp = colpos(beg + q);
-    if (!inpart(cp)) continue;
-    const int bk = int(uint32_t(cp) & gm);
-    ++rem;
+    const int bk = int(uint32_t(colpos(beg + q)) & gm);
 #pragma unroll
     for (int b = 0; b < 16; ++b)
       if (b == bk) {
@@ -172,6 +154,8 @@ __global__ void __launch_bounds__(256)
         ++cnt[b];
       }
   }
+  int rem = len;
+  int64_t step = 0;
   while (__any_sync(0xffffffffu, rem > 0)) {
     unsigned taken = 0;  // banks won in this step (uniform within a group)
     int mybank = -1;
@@ -215,11 +199,7 @@ __global__ void __launch_bounds__(256)
       --rem;
       if (left > 0) {
         int q2 = q + 1;
-        while (true) {
-          const int32_t cp = colpos(beg + q2);
-          if (inpart(cp) && int(uint32_t(cp) & gm) == mybank) break;
-          ++q2;
-        }
+        while (int(uint32_t(colpos(beg + q2)) & gm) != mybank) ++q2;
 #pragma unroll
         for (int b = 0; b < 16; ++b)
           if (b == mybank) pos[b] = q2;
@@ -227,10 +207,7 @@ __global__ void __launch_bounds__(256)
     }
     ++step;
   }
-  step = (step + kSellPad - 1) / kSellPad * kSellPad;  // every range starts on a kSellPad boundary
-  if (lane == 0 && bnd) bnd[sl * (parts + 1) + h + 1] = int32_t(step);
-  }
-  if (!WRITE && lane == 0) width_or_off[sl] = step;
+  if (!WRITE && lane == 0) width_or_off[sl] = (step + kSellPad - 1) / kSellPad * kSellPad;
 }
 
 // exclusive scan of widths (in steps) into entry offsets (x 32), one block
@@ -432,12 +409,11 @@ cudaError_t launch_sell_perm(const int64_t* rp, int64_t n, int32_t* lane_col, in
 }
 
 cudaError_t launch_sell_widths(const int64_t* rp, const int32_t* cl, int64_t nslices, const int32_t* lane_col, int G,
-                               int sched, const int32_t* perm, int parts, int64_t hpos, int32_t* bnd, int64_t* widths,
-                               cudaStream_t st) {
+                               int sched, const int32_t* perm, int64_t* widths, cudaStream_t st) {
   const int64_t blocks = (nslices * 32 + 255) / 256;
   if (blocks > 0 && sched == 2)
     sell_free_kernel<false><<<unsigned(blocks), 256, 0, st>>>(rp, cl, nullptr, 1, nslices, lane_col, G, perm,
-                                                              parts, hpos, bnd, widths, nullptr, nullptr);
+                                                                         widths, nullptr, nullptr);
   else if (blocks > 0)
     sell_sched_kernel<false><<<unsigned(blocks), 256, 0, st>>>(rp, cl, nullptr, 1, nslices, lane_col, G, sched,
                                                                 widths, nullptr, nullptr);
@@ -450,12 +426,12 @@ cudaError_t launch_sell_scan(int64_t* widths, int64_t nslices, int64_t* total, c
 }
 
 cudaError_t launch_sell_fill(const int64_t* rp, const int32_t* cl, const double* vl, int cx, int64_t nslices,
-                             const int32_t* lane_col, int G, int sched, const int32_t* perm, int parts, int64_t hpos,
-                             const int64_t* off, int32_t* s_cols, double* s_vals, cudaStream_t st) {
+                             const int32_t* lane_col, int G, int sched, const int32_t* perm, const int64_t* off,
+                             int32_t* s_cols, double* s_vals, cudaStream_t st) {
   const int64_t blocks = (nslices * 32 + 255) / 256;
   if (blocks > 0 && sched == 2)
-    sell_free_kernel<true><<<unsigned(blocks), 256, 0, st>>>(rp, cl, vl, cx, nslices, lane_col, G, perm, parts, hpos,
-                                                             nullptr, const_cast<int64_t*>(off), s_cols, s_vals);
+    sell_free_kernel<true><<<unsigned(blocks), 256, 0, st>>>(rp, cl, vl, cx, nslices, lane_col, G, perm,
+                                                                        const_cast<int64_t*>(off), s_cols, s_vals);
   else if (blocks > 0)
     sell_sched_kernel<true><<<unsigned(blocks), 256, 0, st>>>(rp, cl, vl, cx, nslices, lane_col, G, sched,
                                                                const_cast<int64_t*>(off), s_cols, s_vals);

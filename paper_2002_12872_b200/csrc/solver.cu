@@ -656,15 +656,12 @@ struct DevProblem {
   DBuf u16c_cols, u16c_vals;  // complex uniform-16: trip-major copy (complex_steps.cu)
   DBuf s_cols, s_vals, s_off, s_lcol, s_llen, s_pos;  // SELL-32 image (K2)
   DBuf s_perm, s_inv;                                 // column relabelling (bank balance), empty = identity
-  DBuf s_bnd, s_pbuf, s_pflags;                       // split staging: range bounds, parked dots, slot flags
-  int s_parts = 1, s_nslot = 0;
-  int64_t s_hpos = 0;
   int64_t nslices = 0, s_npad = 0;
   DevCsr csr() const { return DevCsr{rowptr.as<int64_t>(), cols.as<int32_t>(), vals.as<double>(), nnz}; }
   DevSell sell() const {
     return DevSell{s_cols.as<int32_t>(), s_vals.as<double>(), s_off.as<int64_t>(), s_lcol.as<int32_t>(),
                    s_llen.as<int32_t>(), s_pos.as<int64_t>(), nslices, s_perm.as<int32_t>(), s_inv.as<int32_t>(),
-                   s_npad, s_parts, s_hpos, s_bnd.as<int32_t>(), s_pbuf.as<double>(), s_pflags.as<int>(), s_nslot};
+                   s_npad};
   }
 };
 
@@ -707,45 +704,25 @@ void build_sell_device(DevProblem& dp, cudaStream_t st, dpt_error_info* err) {
                       3, scratch.as<int32_t>(), bankb.as<int32_t>(), dp.s_perm.as<int32_t>(), dp.s_inv.as<int32_t>(),
                       16 * cap, tot.as<int32_t>() + 2, st));
   }
-  int32_t npad = 0;
-  if (relabel) {
-    CK(cudaMemcpyAsync(&npad, tot.as<int32_t>() + 2, 4, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    dp.s_npad = std::max<int64_t>(npad, n);
-  }
-  // split staging of K2 (sparse_step.cu, csr_step_parts_kernel): the image's
-  // entries are scheduled range by range of staged positions
-  dp.s_parts = csr_parts_for(n, dp.s_npad, dp.cplx, sched);
-  if (dp.s_parts > 1) {
-    dp.s_hpos = csr_part_positions(dp.s_npad, dp.s_parts);
-    dalloc(dp.s_bnd, size_t(ns) * size_t(dp.s_parts + 1) * 4, err);
-    int dev = 0, sms = 0;
-    CK(cudaGetDevice(&dev));
-    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    dp.s_nslot = std::max(sms, 1) + 8;  // > resident CTAs (one per SM)
-    dalloc(dp.s_pbuf, size_t(dp.s_nslot) * size_t(csr_parts_rows(dp.s_hpos)) * size_t(ns * 32) * 8, err);
-    dalloc(dp.s_pflags, size_t(dp.s_nslot) * 4, err);
-    CK(cudaMemsetAsync(dp.s_pflags.p, 0, size_t(dp.s_nslot) * 4, st));
-  }
   CK(launch_sell_widths(dp.rowptr.as<int64_t>(), dp.cols.as<int32_t>(), ns, dp.s_lcol.as<int32_t>(), G, sched,
-                        dp.s_perm.as<int32_t>(), dp.s_parts, dp.s_hpos, dp.s_bnd.as<int32_t>(),
-                        dp.s_off.as<int64_t>(), st));
+                        dp.s_perm.as<int32_t>(), dp.s_off.as<int64_t>(), st));
   CK(launch_sell_scan(dp.s_off.as<int64_t>(), ns, tot.as<int64_t>(), st));
   int64_t total = 0;
+  int32_t npad = 0;
   CK(cudaMemcpyAsync(&total, tot.p, 8, cudaMemcpyDeviceToHost, st));
+  if (relabel) CK(cudaMemcpyAsync(&npad, tot.as<int32_t>() + 2, 4, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  if (relabel) dp.s_npad = std::max<int64_t>(npad, n);
   if (std::getenv("DPT_SELL_DEBUG"))
-    std::fprintf(stderr, "[dpt] SELL image: n=%lld slices=%lld steps=%lld sched=%d relabel=%d npad=%lld parts=%d\n",
-                 (long long)n, (long long)ns, (long long)(total / 32), sched, int(relabel), (long long)dp.s_npad,
-                 dp.s_parts);
+    std::fprintf(stderr, "[dpt] SELL image: n=%lld slices=%lld steps=%lld sched=%d relabel=%d npad=%lld\n",
+                 (long long)n, (long long)ns, (long long)(total / 32), sched, int(relabel), (long long)dp.s_npad);
   const int64_t alloc = std::max<int64_t>(total, 1);
   dalloc(dp.s_cols, size_t(alloc) * 4, err);
   dalloc(dp.s_vals, size_t(cx * alloc) * 8, err);
   CK(cudaMemsetAsync(dp.s_cols.p, 0xff, size_t(alloc) * 4, st));
   CK(cudaMemsetAsync(dp.s_vals.p, 0, size_t(cx * alloc) * 8, st));
   CK(launch_sell_fill(dp.rowptr.as<int64_t>(), dp.cols.as<int32_t>(), dp.vals.as<double>(), cx, ns,
-                      dp.s_lcol.as<int32_t>(), G, sched, dp.s_perm.as<int32_t>(), dp.s_parts, dp.s_hpos,
-                      dp.s_off.as<int64_t>(),
+                      dp.s_lcol.as<int32_t>(), G, sched, dp.s_perm.as<int32_t>(), dp.s_off.as<int64_t>(),
                       dp.s_cols.as<int32_t>(),
                       dp.s_vals.as<double>(), st));
   dp.nslices = ns;
@@ -923,7 +900,7 @@ void make_work(Work& w, dpt_ctx* ctx, DevProblem& dp, Mode mode, int64_t row0, i
     ntiles_aux = dense_init_ntiles(rows, s.ntn, dp.cplx);
   } else if (mode == MODE_CSR_FULL) {
     s.ntn = csr_ntn(dp.n);
-    w.ntiles_step = dp.cplx ? csr_cplx_ntiles(rows, dp.n) : csr_step_ntiles_sell(rows, dp.n, dp.sell());
+    w.ntiles_step = dp.cplx ? csr_cplx_ntiles(rows, dp.n) : csr_step_ntiles(rows, dp.n);
   } else if (dp.cplx) {
     s.ntn = single_cplx_ntiles(dp.n, dp.kind == DPT_DELTA_DENSE, dp.u16c_cols.p != nullptr);
     w.ntiles_step = s.ntn;
@@ -1181,7 +1158,7 @@ void key_add(std::vector<unsigned char>& k, const T& v) {
 // Development knobs that select kernels (tuning runs and tests switch them
 // between calls in one process): part of the loop-graph key, so a graph
 // captured under one selection is never replayed under another.
-static const char* const kKernelKnobs[] = {"DPT_U16_VARIANT", "DPT_DENSE_CFG", "DPT_SMALL8", "DPT_CSR_ROWS", "DPT_CSR_PARTS",
+static const char* const kKernelKnobs[] = {"DPT_U16_VARIANT", "DPT_DENSE_CFG", "DPT_SMALL8", "DPT_CSR_ROWS",
                                            "DPT_SELL_SCHED", "DPT_SELL_RELABEL", "DPT_CPLX_U16", "DPT_DENSE_SK", "DPT_SHARD_EMULATE"};
 
 void key_add_knobs(std::vector<unsigned char>& k) {
@@ -1214,10 +1191,9 @@ void drive_graph(dpt_ctx* ctx, Work& w, DevProblem& dp, Mode mode, int64_t row, 
   // address must never replay a graph holding the old one)
   for (const DBuf* b : {&dp.theta, &dp.delta, &dp.rowptr, &dp.cols, &dp.vals, &dp.dmap, &dp.u16c_cols,
                         &dp.u16c_vals, &dp.s_cols, &dp.s_vals, &dp.s_off, &dp.s_lcol, &dp.s_llen, &dp.s_pos,
-                        &dp.s_perm, &dp.s_inv, &dp.s_bnd, &dp.s_pbuf, &dp.s_pflags})
+                        &dp.s_perm, &dp.s_inv})
     key_add(key, b->p);
-  for (int64_t v : {dp.n, dp.ld, dp.nnz, dp.ncol, dp.ldd, dp.nslices, dp.s_npad, dp.s_hpos}) key_add(key, v);
-  key_add(key, dp.s_parts);
+  for (int64_t v : {dp.n, dp.ld, dp.nnz, dp.ncol, dp.ldd, dp.nslices, dp.s_npad}) key_add(key, v);
   key_add(key, dp.lambda_im);
   key_add(key, dp.big);
   key_add(key, dp.cplx);

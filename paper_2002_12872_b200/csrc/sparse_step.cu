@@ -275,270 +275,7 @@ __global__ void __launch_bounds__(THREADS) csr_step_kernel(DevSolve s, DevSell S
   }
 }
 
-// ---------------------------------------------------------- split staging ----
-// K2 with the staged rows cut into position ranges (csr_step_parts_kernel).
-// The binding resource of csr_step_kernel is the L1/shared data pipe: per SELL
-// image step a warp issues 3 wavefronts of image loads (columns + values) and 2
-// per staged row of gathers, and every CTA streams the whole image.  Staging R'
-// = 2R rows of HALF the positions (the same shared memory) halves the image
-// traffic per FMA.  Range h of every lane's entries is scheduled contiguously
-// (sell_free_kernel, `parts`), so a CTA stages range 0 of its rows, runs every
-// slice's range-0 steps, parks each lane's R' partial dots in a per-CTA slot of
-// global memory (L2-resident: <= one CTA per SM holds a slot), restages range 1,
-// continues the SAME FMA chains from the parked values, and finishes with the
-// map epilogue.  The chain order is the image's order, identical to the unsplit
-// kernel's over the same image: results are bit-identical.
-// Planar staging: position p of range h of row r at sa[r * H + p - h H] (H is a
-// multiple of 16, so the bank of every gather is p mod 16, as the schedule assumes).
-int64_t csr_part_positions(int64_t npad, int parts) {
-  const int64_t h = (npad + parts - 1) / parts;
-  return (h + 15) / 16 * 16;
-}
-
-constexpr int kPartsMaxRows = 8;
-
-int csr_parts_rows(int64_t hpos) {
-  int64_t r = kCsrSmemBudget / (8 * hpos);
-  return int(r > kPartsMaxRows ? kPartsMaxRows : r);
-}
-
-int csr_parts_for(int64_t n, int64_t npad, int cplx, int sched) {
-  if (cplx || sched != 2 || n < 64) return 1;
-  if (const char* e = getenv("DPT_CSR_PARTS")) {  // A/B and tests: force the range count
-    const int v = atoi(e);
-    if (v >= 1 && v <= 4 && csr_parts_rows(csr_part_positions(npad, v)) >= 2) return v;
-    return 1;
-  }
-  // whole rows fit at most 3 to a CTA: split them in two (c3: 3 -> 6 rows)
-  return (n >= 4096 && csr_rows_natural(n) <= 3 && csr_parts_rows(csr_part_positions(npad, 2)) >= 4) ? 2 : 1;
-}
-
-static bool csr_use_parts(const DevSell& d) { return d.parts > 1 && getenv("DPT_CSR_ROWS") == nullptr; }
-
-int csr_step_ntiles_sell(int64_t rows, int64_t n, const DevSell& d) {
-  if (!csr_use_parts(d)) return csr_step_ntiles(rows, n);
-  const int R = csr_parts_rows(d.hpos);
-  return int((rows + R - 1) / R);
-}
-
-template <int R, int THREADS, int U>
-__global__ void __launch_bounds__(THREADS) csr_step_parts_kernel(DevSolve s, DevSell S) {
-  if (s.state->done) return;
-  const int jl = launch_index(s);
-  extern __shared__ __align__(16) double sa[];  // [R][H] planar
-  __shared__ unsigned long long next_slice[4];
-  __shared__ double red[THREADS / 32][R][2];
-  __shared__ double wred[THREADS / 32][3];
-  __shared__ double rowc[3][R];  // theta_i, d_{j-1}(i), eps_i
-  __shared__ int slot;
-  constexpr int NW = THREADS / 32;
-  const int64_t n = s.n, ld = s.ld, rows = s.rows;
-  const int64_t il0 = int64_t(blockIdx.x) * R;
-  const int nr = int(rows - il0 < R ? rows - il0 : R);
-  const int slot_in = (jl - 1) % s.nslots, slot_out = jl % s.nslots;
-  const double* __restrict__ ain = s.slots + size_t(slot_in) * size_t(s.slot_elems) + size_t(il0) * size_t(ld);
-  double* a_out = s.slots + size_t(slot_out) * size_t(s.slot_elems);
-  const double lam_k = lam_of(s, jl), lam = s.lambda;
-  const double* d_in = s.dvec[(jl - 1) & 1];
-  const int32_t* __restrict__ perm = S.perm;
-  const int32_t* __restrict__ inv = S.inv;
-  const int64_t H = S.hpos, NT = S.nslices * 32;
-  const int parts = S.parts;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) {
-    for (int h = 0; h < 4; ++h) next_slice[h] = 0ull;
-    // claim a parking slot: at most one CTA per SM is resident (shared memory),
-    // and there are 2 x SMs slots, so a free one is always found
-    int sl = int(blockIdx.x % unsigned(S.nslot));
-    while (atomicCAS(S.pflags + sl, 0, 1) != 0) sl = (sl + 1) % S.nslot;
-    slot = sl;
-  }
-  if (threadIdx.x < R) {
-    const int rr = int(threadIdx.x) < nr ? int(threadIdx.x) : 0;
-    const double ti = s.theta[s.row0 + il0 + rr], di = d_in[il0 + rr];
-    rowc[0][threadIdx.x] = ti;
-    rowc[1][threadIdx.x] = di;
-    rowc[2][threadIdx.x] = __dadd_rn(ti, __dmul_rn(lam, di));
-  }
-  __syncthreads();
-  double* __restrict__ pb = S.pbuf + size_t(slot) * size_t(R) * size_t(NT);
-  // residual maxima per (warp, row) live in shared memory (registers go to the
-  // R-wide FMA chains): each slice's values are warp-reduced, lane 0 folds them
-  if (lane < R) red[warp][lane][0] = red[warp][lane][1] = 0.0;
-  double t_step = 0.0, t_max = 0.0, t_nonfin = 0.0;
-
-  for (int h = 0; h < parts; ++h) {
-    const int64_t lo = int64_t(h) * H;
-    if (h) __syncthreads();  // every warp is done with range h - 1 (and its parked dots are visible)
-    // stage range h: read the rows coalesced, keep the columns whose position falls in it
-    constexpr int kStageU = 2;
-    for (int64_t c0 = threadIdx.x; c0 < n; c0 += kStageU * int64_t(THREADS)) {
-      double v[kStageU][R];
-      int64_t p[kStageU];
-#pragma unroll
-      for (int u = 0; u < kStageU; ++u) {
-        const int64_t c = c0 + int64_t(u) * THREADS;
-        p[u] = c < n ? (perm ? int64_t(__ldg(perm + c)) : c) - lo : -1;
-        if (p[u] >= H) p[u] = -1;
-#pragma unroll
-        for (int r = 0; r < R; ++r)
-          if (p[u] >= 0 && r < nr) v[u][r] = ain[size_t(r) * size_t(ld) + size_t(c)];
-      }
-#pragma unroll
-      for (int u = 0; u < kStageU; ++u)
-#pragma unroll
-        for (int r = 0; r < R; ++r)
-          if (p[u] >= 0 && r < nr) sa[size_t(r) * size_t(H) + size_t(p[u])] = v[u][r];
-    }
-    __syncthreads();
-    while (true) {
-      int64_t sl = 0;
-      if (lane == 0) sl = atomicAdd(&next_slice[h], 1);
-      sl = __shfl_sync(0xffffffffu, sl, 0);
-      if (sl >= S.nslices) break;
-      const int64_t t = sl * 32 + lane;
-      const int32_t qb = S.bnd[sl * (parts + 1) + h], qe = S.bnd[sl * (parts + 1) + h + 1];
-      const int64_t off = S.slice_off[sl];
-      const int32_t* __restrict__ sc = S.cols + off + lane;
-      const double* __restrict__ sv = S.vals + off + lane;
-      double p[R];
-#pragma unroll
-      for (int r = 0; r < R; ++r) p[r] = h ? pb[size_t(r) * size_t(NT) + size_t(t)] : 0.0;
-      for (int32_t q0 = qb; q0 < qe; q0 += U) {
-        int32_t c[U];
-        double v[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          c[u] = __ldg(sc + (q0 + u) * 32);
-          v[u] = __ldg(sv + (q0 + u) * 32);
-        }
-        double g[U][R];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const double* col = sa + (c[u] - lo);
-#pragma unroll
-          for (int r = 0; r < R; ++r) g[u][r] = c[u] >= 0 ? col[size_t(r) * size_t(H)] : 0.0;  // bubbles: no load
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-#pragma unroll
-          for (int r = 0; r < R; ++r) p[r] = __fma_rn(v[u], g[u][r], p[r]);
-      }
-      if (h + 1 < parts) {  // park the dots for range h + 1 (coalesced: index = SELL lane)
-#pragma unroll
-        for (int r = 0; r < R; ++r) pb[size_t(r) * size_t(NT) + size_t(t)] = p[r];
-        continue;
-      }
-      const int32_t j = S.lane_col[t];
-      const double tj = j >= 0 ? s.theta[j] : 0.0;
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        if (r >= nr) break;
-        double nu = 0.0, de = 0.0;
-        if (j >= 0) {
-          const int64_t gi = s.row0 + il0 + r;
-          const double aij = ain[size_t(r) * size_t(ld) + size_t(j)];
-          double val;
-          if (gi == j) {
-            val = 1.0;
-          } else {
-            const double gg =
-                s.gapmat ? s.gapmat[size_t(il0 + r) * size_t(ld) + size_t(j)] : 1.0 / __dsub_rn(rowc[0][r], tj);
-            val = __dmul_rn(__dmul_rn(lam_k, gg), __dsub_rn(p[r], __dmul_rn(rowc[1][r], aij)));
-          }
-          a_out[size_t(il0 + r) * size_t(ld) + size_t(j)] = val;
-          t_step = fmax(t_step, fabs(__dsub_rn(val, aij)));
-          t_max = fmax(t_max, fabs(val));
-          t_nonfin += isfinite(val) ? 0.0 : 1.0;
-          nu = fabs(__dadd_rn(__dmul_rn(__dsub_rn(tj, rowc[2][r]), aij), __dmul_rn(lam, p[r])));
-          de = fabs(aij);
-        }
-        nu = warp_max(nu);
-        de = warp_max(de);
-        if (lane == 0) {
-          red[warp][r][0] = fmax(red[warp][r][0], nu);
-          red[warp][r][1] = fmax(red[warp][r][1], de);
-        }
-      }
-    }
-  }
-
-  t_step = warp_max(t_step);
-  t_max = warp_max(t_max);
-  t_nonfin = warp_sum(t_nonfin);
-  if (lane == 0) {
-    wred[warp][0] = t_step;
-    wred[warp][1] = t_max;
-    wred[warp][2] = t_nonfin;
-  }
-  __syncthreads();  // also orders this CTA's A' stores (and parked-dot reads) before what follows
-  if (threadIdx.x == 0) atomicExch(S.pflags + slot, 0);  // the slot's last reads are done
-  // d_j(i) = P(A_j)(i,i) for the next launch, as csr_step_kernel
-  for (int r = warp; r < nr; r += NW) {
-    const int64_t il = il0 + r, gi = s.row0 + il;
-    const int64_t t = S.pos_of[gi];
-    const int L = int(t & 31);
-    const int64_t off = S.slice_off[t >> 5];
-    const int32_t width = int32_t((S.slice_off[(t >> 5) + 1] - off) >> 5);
-    const double* arow_new = a_out + size_t(il) * size_t(ld);
-    double part = 0.0;
-    for (int32_t q = lane; q < width; q += 32) {
-      const int64_t idx = off + int64_t(q) * 32 + L;
-      const int32_t c = __ldg(S.cols + idx);
-      if (c >= 0) part = __fma_rn(__ldg(S.vals + idx), arow_new[inv ? __ldg(inv + c) : c], part);
-    }
-    part = warp_sum(part);
-    if (lane == 0) {
-      double nu = 0.0, de = 0.0;
-      for (int ww = 0; ww < NW; ++ww) {
-        nu = fmax(nu, red[ww][r][0]);
-        de = fmax(de, red[ww][r][1]);
-      }
-      s.rowpart[rp_index(0, il, 0, rows, 1)] = part;
-      s.rowpart[rp_index(1, il, 0, rows, 1)] = nu;
-      s.rowpart[rp_index(2, il, 0, rows, 1)] = de;
-    }
-  }
-  if (threadIdx.x == 0) {
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-    for (int ww = 0; ww < NW; ++ww) {
-      a0 = fmax(a0, wred[ww][0]);
-      a1 = fmax(a1, wred[ww][1]);
-      a2 += wred[ww][2];
-    }
-    double* tp = s.tilepart + size_t(blockIdx.x) * 4;
-    tp[0] = a0;
-    tp[1] = a1;
-    tp[2] = a2;
-    tp[3] = 0.0;
-  }
-}
-
-template <int R, int THREADS, int U>
-static cudaError_t launch_parts(const DevSolve& s, const DevSell& d, cudaStream_t st) {
-  static DeviceAttrOnce attr;
-  attr([] {
-    cudaFuncSetAttribute(csr_step_parts_kernel<R, THREADS, U>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kCsrSmemBudget + 1024);
-  });
-  const unsigned grid = unsigned((s.rows + R - 1) / R);
-  const size_t smem = size_t(R) * size_t(d.hpos) * 8;
-  csr_step_parts_kernel<R, THREADS, U><<<grid, THREADS, smem, st>>>(s, d);
-  return cudaGetLastError();
-}
-
 cudaError_t launch_csr_step(const DevSolve& s, const DevSell& d, cudaStream_t st) {
-  if (csr_use_parts(d)) {
-    switch (csr_parts_rows(d.hpos)) {
-      case 2: return launch_parts<2, 1024, 4>(s, d, st);
-      case 3: return launch_parts<3, 512, 4>(s, d, st);
-      case 4: return launch_parts<4, 512, 4>(s, d, st);
-      case 5: return launch_parts<5, 512, 2>(s, d, st);
-      case 6: return launch_parts<6, 512, 2>(s, d, st);
-      case 7: return launch_parts<7, 512, 2>(s, d, st);
-      default: return launch_parts<8, 512, 2>(s, d, st);
-    }
-  }
   const int Rs = csr_rows_per_cta(s.n);
   const int use_smem = Rs > 0 ? 1 : 0;
   const int R = use_smem ? Rs : 1;
