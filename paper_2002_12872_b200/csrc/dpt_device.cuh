@@ -64,7 +64,6 @@ struct DevSolve {
   double* cyclepart;    // [fold_blocks][DPT_MAX_WINDOW]
   int fixed_mode;       // iterate_fixed: no decisions, step every launch
   int fuse_decide;      // single rank: the fold's last block also runs the decision
-  int fold_in_step;     // the step kernel's last block runs the fold itself (K3: no fold launch)
   double* sk_ws;        // stream-K K1 (small n): per-CTA partial-tile slots, or null
   unsigned* sk_cnt;     // stream-K K1: per-tile part counters
   // device-side iteration loop (CUDA graph WHILE node, solver.cu drive_graph):

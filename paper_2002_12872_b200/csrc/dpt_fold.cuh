@@ -59,7 +59,7 @@ static __device__ void decide_now(const DevSolve& s);
 // decision: if the first entries already differ by >= tol from every window
 // entry, within_tol is false for all of them and the cycle kernel has nothing
 // to do (exact early-out, dpt.cpp:60-79).
-static __device__ void cycle_sample_precheck(const DevSolve& s, const dpt_sm_state& dec, unsigned* block_bits) {
+static __device__ void cycle_sample_precheck(const DevSolve& s, const dpt_sm_state& dec) {
   dpt_sm_state* st = s.state;
   if (dec.done || !dec.cycle_pending) return;
   const int j = dec.j;
@@ -90,12 +90,13 @@ static __device__ void cycle_sample_precheck(const DevSolve& s, const dpt_sm_sta
 #pragma unroll
   for (int p = 0; p < DPT_MAX_WINDOW; ++p) bits |= (fabs(cv - pv[p]) >= s.opts.tol) ? (1u << p) : 0u;
   bits = __reduce_or_sync(0xffffffffu, bits);
-  if (threadIdx.x == 0) *block_bits = 0u;
+  __shared__ unsigned block_bits;
+  if (threadIdx.x == 0) block_bits = 0u;
   __syncthreads();
-  if ((threadIdx.x & 31) == 0) atomicOr(block_bits, bits);
+  if ((threadIdx.x & 31) == 0) atomicOr(&block_bits, bits);
   __syncthreads();
   const unsigned need = npast >= 32 ? 0xffffffffu : ((1u << npast) - 1u);
-  if (threadIdx.x == 0 && (*block_bits & need) == need) {
+  if (threadIdx.x == 0 && (block_bits & need) == need) {
     st->cycle_pending = 0;  // refuted for every entry: the stats keep "not within"
 #pragma unroll
     for (int p = 0; p < DPT_MAX_WINDOW; ++p) s.stats[DPT_STATS_CYCLE0 + p] = 1.0;
@@ -130,73 +131,6 @@ static __device__ dpt_sm_state decide_local(const DevSolve& s, const double* sta
 }
 
 static __device__ void decide_now(const DevSolve& s) { (void)decide_local(s, nullptr); }
-
-// The one-row fold (the row map: rows = 1) run by the LAST block of the step
-// kernel itself (fold_in_step): the same reductions as fold_kernel's
-// block-per-row path and its elected tail -- the row partials of the ntn step
-// blocks, the launch maxima, stats[0..3], and on a single rank the decision,
-// the loop condition and the cycle pre-check -- without a fold launch.  The
-// residual maxima are order-free and rowpart[0] (the row map's d) is 0, so the
-// result equals fold_kernel's bit for bit.  `scratch` is shared memory the
-// caller no longer uses (>= 4 * warps + 8 doubles + a dpt_sm_state).  Not
-// inlined: the step kernel's main loop keeps its registers.
-static __device__ __noinline__ void fold_row_map_in_block(const DevSolve& s, int ntn, double* scratch) {
-  const int j = launch_index(s);
-  const int nw = int(blockDim.x >> 5), lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const double* dprev = s.dvec[(j - 1) & 1];
-  double* dnext = s.dvec[j & 1];
-  double d = 0.0, num = 0.0, den = 0.0, a0 = 0.0, a1 = 0.0, a2 = 0.0;
-  for (int tn = threadIdx.x; tn < ntn; tn += blockDim.x) {
-    d += __ldcg(s.rowpart + rp_index(0, 0, tn, 1, ntn));
-    num = fmax(num, __ldcg(s.rowpart + rp_index(1, 0, tn, 1, ntn)));
-    den = fmax(den, __ldcg(s.rowpart + rp_index(2, 0, tn, 1, ntn)));
-    const double2 t01 = __ldcg(reinterpret_cast<const double2*>(s.tilepart + size_t(tn) * 4));
-    a0 = fmax(a0, t01.x);
-    a1 = fmax(a1, t01.y);
-    a2 += __ldcg(s.tilepart + size_t(tn) * 4 + 2);
-  }
-  d = warp_sum(d);
-  num = warp_max(num);
-  den = warp_max(den);
-  a0 = warp_max(a0);
-  a1 = warp_max(a1);
-  a2 = warp_sum(a2);
-  double* red = scratch;  // [nw][6]
-  if (lane == 0) {
-    red[warp * 6 + 0] = d;
-    red[warp * 6 + 1] = num;
-    red[warp * 6 + 2] = den;
-    red[warp * 6 + 3] = a0;
-    red[warp * 6 + 4] = a1;
-    red[warp * 6 + 5] = a2;
-  }
-  __syncthreads();
-  dpt_sm_state* dec = reinterpret_cast<dpt_sm_state*>(scratch + 6 * nw + 2);
-  if (threadIdx.x == 0) {
-    double dd = 0.0, nn = 0.0, ee = 0.0, r[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int w = 0; w < nw; ++w) {
-      dd += red[w * 6 + 0];
-      nn = fmax(nn, red[w * 6 + 1]);
-      ee = fmax(ee, red[w * 6 + 2]);
-      r[0] = fmax(r[0], red[w * 6 + 3]);
-      r[1] = fmax(r[1], red[w * 6 + 4]);
-      r[2] += red[w * 6 + 5];
-    }
-    r[3] = fold_row_store(s, 0, dd, 0.0, nn, ee, dprev, dnext);
-    s.stats[0] = r[0];
-    s.stats[1] = r[1];
-    s.stats[2] = r[2];
-    s.stats[3] = r[3];
-    if (s.fuse_decide) {
-      *dec = decide_local(s, r);
-      if (s.has_loop && (dec->done || dec->j >= s.loop_total)) cudaGraphSetConditional(s.loop_cond, 0u);
-    }
-  }
-  if (s.fuse_decide) {
-    __syncthreads();
-    cycle_sample_precheck(s, *dec, reinterpret_cast<unsigned*>(scratch + 6 * nw));
-  }
-}
 
 
 }  // namespace dpt

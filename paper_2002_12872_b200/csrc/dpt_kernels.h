@@ -41,7 +41,6 @@ struct DevSell {
   int64_t npad;             // staged row length in positions (>= n)
 };
 int csr_step_ntiles(int64_t rows, int64_t n);
-bool u16_fuses_fold();  // K3's per-warp pipeline folds in its last block (fold_in_step)
 int csr_ntn(int64_t n);
 cudaError_t launch_csr_step(const DevSolve& s, const DevSell& d, cudaStream_t st);
 

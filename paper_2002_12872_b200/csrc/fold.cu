@@ -206,9 +206,8 @@ __global__ void __launch_bounds__(kFoldThreads) fold_kernel(DevSolve s, int ntil
     }
   }
   if (s.fuse_decide) {
-    __shared__ unsigned block_bits;
     __syncthreads();
-    cycle_sample_precheck(s, dec, &block_bits);
+    cycle_sample_precheck(s, dec);
   }
 }
 

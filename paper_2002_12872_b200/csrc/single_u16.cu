@@ -16,7 +16,6 @@
 #include <stdlib.h>
 
 #include "dpt_device.cuh"
-#include "dpt_fold.cuh"
 #include "dpt_kernels.h"
 
 namespace dpt {
@@ -380,24 +379,6 @@ __global__ void __launch_bounds__(W * 32, MINB)
     tp[2] = a[4];
     tp[3] = 0.0;
   }
-  if (s.fold_in_step) {
-    // the last block to finish runs the fold (fold_row_map_in_block) in the
-    // stage ring, which no bulk copy targets any more: no fold launch, no extra
-    // static shared memory (the L1 keeps its gather capacity)
-    unsigned* flag = reinterpret_cast<unsigned*>(smem);
-    if (threadIdx.x == 0) {
-      fence_acq_rel_gpu();  // release this block's partials
-      *flag = (atomicAdd(s.counter, 1u) == gridDim.x - 1) ? 1u : 0u;
-    }
-    __syncthreads();
-    if (*flag == 0u) return;
-    if (threadIdx.x == 0) {
-      fence_acq_rel_gpu();  // acquire every block's partials
-      *s.counter = 0u;
-    }
-    __syncthreads();
-    fold_row_map_in_block(s, int(gridDim.x), reinterpret_cast<double*>(smem) + 2);
-  }
 }
 
 // Variant table (DPT_U16_VARIANT selects one for tuning runs).  Measured on c4
@@ -418,15 +399,6 @@ static const U16Variant kU16Var[] = {{256, 2, 0}, {256, 2, 1}, {128, 4, 0}, {128
                                      {256, 2, 1}, {192, 3, 1}, {160, 4, 1}, {128, 5, 1}, {128, 4, 1},
                                      {512, 1, 1}, {160, 3, 1}, {128, 4, 1},
                                      {256, 2, 1}, {256, 2, 1}};
-
-static int u16_variant();
-
-// The per-warp pipelines (variants >= 6) fold in their last block
-// (fold_in_step); DPT_FOLD_SPLIT=1 keeps the separate fold launch (A/B).
-bool u16_fuses_fold() {
-  const char* e = getenv("DPT_FOLD_SPLIT");
-  return u16_variant() >= 6 && !(e && e[0] == '1');
-}
 
 static int u16_variant() {
   const char* e = getenv("DPT_U16_VARIANT");

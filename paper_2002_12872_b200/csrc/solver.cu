@@ -908,7 +908,6 @@ void make_work(Work& w, dpt_ctx* ctx, DevProblem& dp, Mode mode, int64_t row0, i
     const int sm = single_mode(dp.kind == DPT_DELTA_DENSE, dp.uniform16);
     s.ntn = single_ntn(dp.n, sm);
     w.ntiles_step = single_ntiles(dp.n, sm);
-    s.fold_in_step = (sm == 0 && u16_fuses_fold()) ? 1 : 0;  // K3 folds in its last block
   }
   s.ntiles = std::max(w.ntiles_step, ntiles_aux);
   const size_t slot_elems = size_t(std::max<int64_t>(rows_alloc, 1)) * size_t(dp.ld);
@@ -1098,10 +1097,8 @@ void allreduce_stats(dpt_ctx* ctx, Work& w, dpt_error_info* err) {
 
 // One iteration's device work after the step kernel.
 void post_step(dpt_ctx* ctx, Work& w, int ntiles, int64_t cycle_elems, dpt_error_info* err) {
-  if (!w.s.fold_in_step) {  // (K3 folds in its own last block)
-    CK(launch_fold(w.s, ntiles, ctx->stream));
-    ctx->launches += 1;
-  }
+  CK(launch_fold(w.s, ntiles, ctx->stream));
+  ctx->launches += 1;
   if (!w.s.fuse_decide) {  // sharded: cross-rank max of the statistics, then the decision
     allreduce_stats(ctx, w, err);
     CK(launch_decide(w.s, ctx->stream));
@@ -1161,7 +1158,7 @@ void key_add(std::vector<unsigned char>& k, const T& v) {
 // Development knobs that select kernels (tuning runs and tests switch them
 // between calls in one process): part of the loop-graph key, so a graph
 // captured under one selection is never replayed under another.
-static const char* const kKernelKnobs[] = {"DPT_U16_VARIANT", "DPT_FOLD_SPLIT", "DPT_DENSE_CFG", "DPT_SMALL8", "DPT_CSR_ROWS",
+static const char* const kKernelKnobs[] = {"DPT_U16_VARIANT", "DPT_DENSE_CFG", "DPT_SMALL8", "DPT_CSR_ROWS",
                                            "DPT_SELL_SCHED", "DPT_SELL_RELABEL", "DPT_CPLX_U16", "DPT_DENSE_SK", "DPT_SHARD_EMULATE"};
 
 void key_add_knobs(std::vector<unsigned char>& k) {
