@@ -25,7 +25,9 @@ def kernels(fn):
     for e in prof.events():
         if e.device_type != torch.autograd.DeviceType.CUDA or "Memcpy" in e.name or "Memset" in e.name:
             continue
-        k = e.name.split("(")[0].split("<")[0][-40:]
+        import re
+        m = re.search(r"(\w+_kernel)", e.name)
+        k = m.group(1) if m else e.name[:40]
         c, t = out.get(k, (0, 0.0))
         out[k] = (c + 1, t + e.time_range.elapsed_us())
     return {k: {"n": c, "us": round(t, 1)} for k, (c, t) in out.items()}
