@@ -483,7 +483,10 @@ def main():
     if os.path.exists(prof) and wl == "c2" and world == 1:
         try:
             rec = json.load(open(prof)).get("latest:prof_dense_c2", {})
-            traffic, traffic_src = rec.get("dram_bytes_per_launch"), rec.get("source")
+            traffic = rec.get("dram_bytes_per_launch")
+            traffic_src = (f"ncu --set full capture {rec.get('capture')} of the same kernel at this workload "
+                           f"(profiles/ncu_summary.json; dram__bytes_read.sum + dram__bytes_write.sum per launch, "
+                           f"cold-cache replay) -- not measured inside this run") if traffic else None
         except Exception:
             traffic = None
     plan.close()

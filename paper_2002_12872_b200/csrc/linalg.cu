@@ -171,7 +171,7 @@ constexpr int kPanelMaxNb = 32;
 template <int CX>
 __global__ void __launch_bounds__(kPanelThreads)
     lu_panel_kernel(double* __restrict__ A, int64_t lde, int64_t n, int64_t kb, int nb, int64_t R,
-                    int64_t* __restrict__ piv, int* __restrict__ info) {
+                    int64_t* __restrict__ piv, int* __restrict__ info, int64_t* __restrict__ swmap) {
   cg::cluster_group cl = cg::this_cluster();
   const int rank = int(cl.block_rank());
   extern __shared__ __align__(16) double sp[];
@@ -265,22 +265,12 @@ __global__ void __launch_bounds__(kPanelThreads)
     const int64_t i = q / nb, c = q % nb;
     st_e<CX>(A, (kb + r0 + i) * lde + kb + c, ld_e<CX>(sp, c * R + i));
   }
-  cl.sync();  // no CTA exits while a peer could still read its shared memory
-}
-
-// The panel's row interchanges applied to the columns outside it ([0, kb) and
-// [kb + nb, n)): the composite permutation of the touched rows is rebuilt per
-// block, the rows read into shared memory, then written to their targets.
-constexpr int kSwapThreads = 64;
-
-template <int CX>
-__global__ void __launch_bounds__(kSwapThreads)
-    lu_swap_rest_kernel(double* __restrict__ A, int64_t lde, int64_t n, int64_t kb, int nb,
-                        const int64_t* __restrict__ piv) {
-  __shared__ int64_t rows[2 * kPanelMaxNb], src[2 * kPanelMaxNb];
-  __shared__ int cnt;
-  extern __shared__ __align__(16) double buf[];  // [2 nb][kSwapThreads] elements
-  if (threadIdx.x == 0) {
+  if (rank == 0 && tid == 0) {
+    // the panel's interchanges as one permutation of the touched rows, for the
+    // other columns (lu_swap_rest_kernel): swmap = {count, rows[], src[]};
+    // piv[kb ..] was written by this thread
+    int64_t* rows = swmap + 1;
+    int64_t* src = swmap + 1 + 2 * kPanelMaxNb;
     int k = 0;
     auto slot = [&](int64_t r) {
       for (int q = 0; q < k; ++q)
@@ -295,7 +285,27 @@ __global__ void __launch_bounds__(kSwapThreads)
       src[a] = src[b];
       src[b] = t;
     }
-    cnt = k;
+    swmap[0] = k;
+  }
+  cl.sync();  // no CTA exits while a peer could still read its shared memory
+}
+
+// The panel's row interchanges applied to the columns outside it ([0, kb) and
+// [kb + nb, n)): the composite permutation of the touched rows is rebuilt per
+// block, the rows read into shared memory, then written to their targets.
+constexpr int kSwapThreads = 64;
+constexpr int64_t kSwapMapDoubles = 256;  // scratch head holding the panel's swap map (1 + 4 kPanelMaxNb)
+
+template <int CX>
+__global__ void __launch_bounds__(kSwapThreads)
+    lu_swap_rest_kernel(double* __restrict__ A, int64_t lde, int64_t n, int64_t kb, int nb,
+                        const int64_t* __restrict__ swmap) {
+  __shared__ int64_t rows[2 * kPanelMaxNb], src[2 * kPanelMaxNb];
+  extern __shared__ __align__(16) double buf[];  // [2 nb][kSwapThreads] elements
+  const int cnt = int(swmap[0]);
+  for (int q = threadIdx.x; q < cnt; q += blockDim.x) {
+    rows[q] = swmap[1 + q];
+    src[q] = swmap[1 + 2 * kPanelMaxNb + q];
   }
   __syncthreads();
   const int64_t rest = n - nb;  // columns outside the panel
@@ -442,7 +452,7 @@ int64_t lu_max_n(int cx) { return int64_t(kPanelCluster) * (kPanelSmem / (8 * 8 
 
 template <int CX>
 static cudaError_t lu_panel(double* A, int64_t lde, int64_t n, int64_t kb, int nb, int64_t* piv, int* info,
-                            cudaStream_t st) {
+                            int64_t* swmap, cudaStream_t st) {
   const int64_t m = n - kb;
   const int64_t R = (m + kPanelCluster - 1) / kPanelCluster;
   const size_t smem = size_t(R) * size_t(nb) * 8 * CX;
@@ -462,7 +472,7 @@ static cudaError_t lu_panel(double* A, int64_t lde, int64_t n, int64_t kb, int n
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, lu_panel_kernel<CX>, A, lde, n, kb, nb, R, piv, info);
+  return cudaLaunchKernelEx(&cfg, lu_panel_kernel<CX>, A, lde, n, kb, nb, R, piv, info, swmap);
 }
 
 template <int CX>
@@ -486,7 +496,7 @@ static cudaError_t trsm_block(bool lower, const double* LU, int64_t lde, int64_t
 // In-place LU with partial pivoting of the n x n matrix A (row-major, leading
 // dim lda doubles, complex interleaved when cx = 2).  piv[k] = the row swapped
 // with row k at step k (absolute); *info = first singular column + 1, or 0.
-// scratch: >= 4 * n * kPanelMaxNb doubles (the U12 operand / its complex image).
+// scratch: >= 4 * n * kPanelMaxNb + 256 doubles (the swap map, then the U12 operand / its complex image).
 cudaError_t launch_lu_factor(int cx, double* A, int64_t lda, int64_t n, int64_t* piv, int* info, double* scratch,
                              int* launches, cudaStream_t st) {
   const int nb = panel_nb(cx, n);
@@ -495,7 +505,9 @@ cudaError_t launch_lu_factor(int cx, double* A, int64_t lda, int64_t n, int64_t*
   LA_CK(cudaMemsetAsync(info, 0x7f, sizeof(int), st));  // INT_MAX-ish: "none"
   for (int64_t kb = 0; kb < n; kb += nb) {
     const int w = int(n - kb < nb ? n - kb : nb);
-    LA_CK(cx == 2 ? lu_panel<2>(A, lde, n, kb, w, piv, info, st) : lu_panel<1>(A, lde, n, kb, w, piv, info, st));
+    int64_t* swmap = reinterpret_cast<int64_t*>(scratch);  // {count, rows[64], src[64]}, then the operand
+    LA_CK(cx == 2 ? lu_panel<2>(A, lde, n, kb, w, piv, info, swmap, st)
+                  : lu_panel<1>(A, lde, n, kb, w, piv, info, swmap, st));
     const int64_t rest = n - w;
     if (rest > 0) {
       const unsigned g = unsigned((rest + kSwapThreads - 1) / kSwapThreads);
@@ -506,9 +518,9 @@ cudaError_t launch_lu_factor(int cx, double* A, int64_t lda, int64_t n, int64_t*
         cudaFuncSetAttribute(lu_swap_rest_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
       });
       if (cx == 2)
-        lu_swap_rest_kernel<2><<<g, kSwapThreads, sm, st>>>(A, lde, n, kb, w, piv);
+        lu_swap_rest_kernel<2><<<g, kSwapThreads, sm, st>>>(A, lde, n, kb, w, swmap);
       else
-        lu_swap_rest_kernel<1><<<g, kSwapThreads, sm, st>>>(A, lde, n, kb, w, piv);
+        lu_swap_rest_kernel<1><<<g, kSwapThreads, sm, st>>>(A, lde, n, kb, w, swmap);
       LA_CK(cudaGetLastError());
       *launches += 1;
     }
@@ -519,8 +531,9 @@ cudaError_t launch_lu_factor(int cx, double* A, int64_t lda, int64_t n, int64_t*
     LA_CK(cx == 2 ? trsm_block<2>(true, A, lde, kb, w, A, lde, c0, m2, st)
                   : trsm_block<1>(true, A, lde, kb, w, A, lde, c0, m2, st));
     const int64_t ldo = even(cx * w);
-    LA_CK(launch_gemm_bop(cx, true, A + (kb * lde + c0) * cx, lde, m2, w, scratch, ldo, st));
-    LA_CK(gemm_e(cx, m2, m2, w, A + (c0 * lde + kb) * cx, lda, scratch, ldo, -1.0, 1.0, A + (c0 * lde + c0) * cx,
+    double* bop = scratch + kSwapMapDoubles;
+    LA_CK(launch_gemm_bop(cx, true, A + (kb * lde + c0) * cx, lde, m2, w, bop, ldo, st));
+    LA_CK(gemm_e(cx, m2, m2, w, A + (c0 * lde + kb) * cx, lda, bop, ldo, -1.0, 1.0, A + (c0 * lde + c0) * cx,
                  lda, st));
     *launches += 3;
   }
