@@ -265,12 +265,13 @@ __global__ void __launch_bounds__(kPanelThreads)
     const int64_t i = q / nb, c = q % nb;
     st_e<CX>(A, (kb + r0 + i) * lde + kb + c, ld_e<CX>(sp, c * R + i));
   }
+  __shared__ int64_t rows[2 * kPanelMaxNb], src[2 * kPanelMaxNb];
+  __shared__ int nrows;
   if (rank == 0 && tid == 0) {
     // the panel's interchanges as one permutation of the touched rows, for the
-    // other columns (lu_swap_rest_kernel): swmap = {count, rows[], src[]};
+    // other columns (lu_swap_rest_kernel): swmap = {count, rows[], src[]},
+    // built in shared memory (a chain of dependent global round trips is slow);
     // piv[kb ..] was written by this thread
-    int64_t* rows = swmap + 1;
-    int64_t* src = swmap + 1 + 2 * kPanelMaxNb;
     int k = 0;
     auto slot = [&](int64_t r) {
       for (int q = 0; q < k; ++q)
@@ -285,7 +286,15 @@ __global__ void __launch_bounds__(kPanelThreads)
       src[a] = src[b];
       src[b] = t;
     }
-    swmap[0] = k;
+    nrows = k;
+  }
+  if (rank == 0) {
+    __syncthreads();
+    for (int q = tid; q < nrows; q += kPanelThreads) {
+      swmap[1 + q] = rows[q];
+      swmap[1 + 2 * kPanelMaxNb + q] = src[q];
+    }
+    if (tid == 0) swmap[0] = nrows;
   }
   cl.sync();  // no CTA exits while a peer could still read its shared memory
 }
