@@ -1,31 +1,34 @@
 """Per-rank step time of the sharded dense solve, emulated on one GPU
 (DPT_SHARD_EMULATE=r/w: rank r's row shard, no communicator).  Development /
-profiles helper: python tools/shard_times.py [worlds] (env DPT_DENSE_VARCOLS)."""
+profiles helper:  python tools/shard_times.py [--config c2|c5] [--worlds 1,2,4,8]
+Rank 0 holds the largest shard (ceil(n / w) rows), so its time is the step's."""
+import argparse
 import json
 import os
-import subprocess
 import sys
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-SCRIPT = r"""
-import sys, json
-sys.path.insert(0, ".")
-import paper_2002_12872_b200 as P
-from paper_2002_12872_b200 import problems as pr
-p, o, _ = pr.config("c2")
-plan = P.Plan(p)
-plan.begin(); plan.steps(3)
-k = 20
-kms = plan.steps(k, time_kernel=True) / k
-print(json.dumps({"kernel_ms": kms}))
-"""
-worlds = [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "1,2,4,8").split(",")]
-for w in worlds:
-    env = dict(os.environ, DPT_SHARD_EMULATE=f"0/{w}")
-    out = subprocess.run([sys.executable, "-c", SCRIPT], cwd=ROOT, env=env, capture_output=True, text=True)
-    rec = json.loads(out.stdout.strip().splitlines()[-1]) if out.returncode == 0 else {"error": out.stderr[-300:]}
-    rec.update(world=w, varcols=os.environ.get("DPT_DENSE_VARCOLS", "auto"))
-    if "kernel_ms" in rec:
-        rows = -(-4096 // w)
-        rec["tflops"] = 2.0 * rows * 4096 * 4096 / (rec["kernel_ms"] * 1e-3) / 1e12
-    print(json.dumps(rec))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2002_12872_b200 as P  # noqa: E402
+from paper_2002_12872_b200 import problems as pr  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="c2")
+ap.add_argument("--worlds", default="1,2,4,8")
+ap.add_argument("--steps", type=int, default=0)
+a = ap.parse_args()
+p, o, _ = pr.config(a.config)
+n = len(p.d)
+k = a.steps or (20 if n <= 8192 else 2)
+peak = P.fp64_peak_tflops(0)
+for w in [int(x) for x in a.worlds.split(",")]:
+    os.environ["DPT_SHARD_EMULATE"] = f"0/{w}"
+    plan = P.Plan(p)
+    plan.begin()
+    plan.steps(1 if n > 8192 else 3)
+    kms = plan.steps(k, time_kernel=True) / k
+    plan.close()
+    rows = -(-n // w)
+    tf = 2.0 * rows * n * n / (kms * 1e-3) / 1e12
+    print(json.dumps({"config": a.config, "n": n, "world": w, "rows_rank0": rows, "kernel_ms": kms, "tflops": tf,
+                      "fp64_frac": tf / peak, "share_of_1gpu_ideal": None}), flush=True)
+os.environ.pop("DPT_SHARD_EMULATE", None)
