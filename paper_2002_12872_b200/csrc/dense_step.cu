@@ -315,6 +315,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
     if (producer && kt + C::STAGES < KT) {  // refill this stage once every warp released it
       const int kn = kt + C::STAGES;
       mbar_wait(&empty[st], (kt / C::STAGES) & 1);
+      fence_proxy_async_smem();  // the consumers' generic reads of the stage before the async-proxy refill
       mbar_arrive_expect_tx(&full[st], C::STAGE_BYTES);
       tma_load_2d(sA + st * C::A_BYTES, am, &full[st], kn * C::BK, tm * C::BM);
       tma_load_2d(sB + st * C::B_BYTES, dmap, &full[st], kn * C::BK, tn * C::BN);
@@ -422,6 +423,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
       if (lane == 0) mbar_arrive(&empty[st]);
       if (producer && u0 + it + C::STAGES < u1) {  // refill this stage with the unit STAGES ahead
         mbar_wait(&empty[st], uint32_t((it / C::STAGES) & 1));
+        fence_proxy_async_smem();  // the consumers' generic reads of the stage before the async-proxy refill
         issue(u0 + it + C::STAGES, st);
       }
       __syncwarp();

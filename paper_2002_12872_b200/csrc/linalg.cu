@@ -86,6 +86,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
     if (producer && kt + C::STAGES < KT) {
       const int kn = kt + C::STAGES;
       mbar_wait(&empty[st], (kt / C::STAGES) & 1);
+      fence_proxy_async_smem();  // the consumers' generic reads of the stage before the async-proxy refill
       mbar_arrive_expect_tx(&full[st], C::STAGE_BYTES);
       tma_load_2d(sA + st * C::A_BYTES, &am, &full[st], kn * C::BK, tm * C::BM);
       tma_load_2d(sB + st * C::B_BYTES, &bm, &full[st], kn * C::BK, tn * C::BN);
@@ -265,36 +266,48 @@ __global__ void __launch_bounds__(kPanelThreads)
     const int64_t i = q / nb, c = q % nb;
     st_e<CX>(A, (kb + r0 + i) * lde + kb + c, ld_e<CX>(sp, c * R + i));
   }
-  __shared__ int64_t rows[2 * kPanelMaxNb], src[2 * kPanelMaxNb];
-  __shared__ int nrows;
-  if (rank == 0 && tid == 0) {
-    // the panel's interchanges as one permutation of the touched rows, for the
-    // other columns (lu_swap_rest_kernel): swmap = {count, rows[], src[]},
-    // built in shared memory (a chain of dependent global round trips is slow);
-    // piv[kb ..] was written by this thread
-    int k = 0;
-    auto slot = [&](int64_t r) {
-      for (int q = 0; q < k; ++q)
-        if (rows[q] == r) return q;
-      rows[k] = r;
-      src[k] = r;
-      return k++;
-    };
-    for (int j = 0; j < nb; ++j) {
-      const int a = slot(kb + j), b = slot(piv[kb + j]);
-      const int64_t t = src[a];
-      src[a] = src[b];
-      src[b] = t;
-    }
-    nrows = k;
-  }
+  // The panel's interchanges as one permutation of the touched rows, for the
+  // other columns (lu_swap_rest_kernel): swmap = {count, rows[], src[]}.
+  // Warp 0 of rank 0 replays the swaps: positions kb .. kb+nb-1 are indexed
+  // directly (cur), pivot rows below the panel live in a short list found by
+  // one ballot per column.
+  __shared__ int64_t cur[kPanelMaxNb], extpos[kPanelMaxNb], extval[kPanelMaxNb];
   if (rank == 0) {
-    __syncthreads();
-    for (int q = tid; q < nrows; q += kPanelThreads) {
-      swmap[1 + q] = rows[q];
-      swmap[1 + 2 * kPanelMaxNb + q] = src[q];
+    __syncthreads();  // piv[kb ..] was written by thread 0 of this block
+    if (warp == 0) {
+      if (lane < nb) cur[lane] = kb + lane;
+      int next = 0;
+      __syncwarp();
+      for (int j = 0; j < nb; ++j) {
+        const int64_t p = piv[kb + j];
+        if (p < kb + nb) {
+          if (lane == 0) {
+            const int64_t t = cur[j];
+            cur[j] = cur[p - kb];
+            cur[p - kb] = t;
+          }
+        } else {
+          const unsigned hit = __ballot_sync(0xffffffffu, lane < next && extpos[lane] == p);
+          if (lane == 0) {
+            int q = hit ? __ffs(hit) - 1 : next;
+            if (!hit) {
+              extpos[q] = p;
+              extval[q] = p;
+            }
+            const int64_t t = cur[j];
+            cur[j] = extval[q];
+            extval[q] = t;
+          }
+          next += hit ? 0 : 1;
+        }
+        __syncwarp();
+      }
+      for (int q = lane; q < nb + next; q += 32) {
+        swmap[1 + q] = q < nb ? kb + q : extpos[q - nb];
+        swmap[1 + 2 * kPanelMaxNb + q] = q < nb ? cur[q] : extval[q - nb];
+      }
+      if (lane == 0) swmap[0] = nb + next;
     }
-    if (tid == 0) swmap[0] = nrows;
   }
   cl.sync();  // no CTA exits while a peer could still read its shared memory
 }
