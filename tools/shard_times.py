@@ -30,5 +30,5 @@ for w in [int(x) for x in a.worlds.split(",")]:
     rows = -(-n // w)
     tf = 2.0 * rows * n * n / (kms * 1e-3) / 1e12
     print(json.dumps({"config": a.config, "n": n, "world": w, "rows_rank0": rows, "kernel_ms": kms, "tflops": tf,
-                      "fp64_frac": tf / peak, "share_of_1gpu_ideal": None}), flush=True)
+                      "fp64_frac": tf / peak}), flush=True)
 os.environ.pop("DPT_SHARD_EMULATE", None)
