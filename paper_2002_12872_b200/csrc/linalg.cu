@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(kPanelThreads)
     if (tid == 0) {
       double gb = -1.0;
       int64_t gi = INT64_MAX;
-      for (int r = 0; r < kPanelCluster; ++r) {
+      for (int r = 0; r < int(cl.num_blocks()); ++r) {
         const double v = *cl.map_shared_rank(&cand_v, r);
         const int64_t i = *cl.map_shared_rank(&cand_i, r);
         if (v > gb || (v == gb && i < gi)) gb = v, gi = i;
@@ -476,20 +476,24 @@ template <int CX>
 static cudaError_t lu_panel(double* A, int64_t lde, int64_t n, int64_t kb, int nb, int64_t* piv, int* info,
                             int64_t* swmap, cudaStream_t st) {
   const int64_t m = n - kb;
-  const int64_t R = (m + kPanelCluster - 1) / kPanelCluster;
+  // the smallest cluster whose shared memories hold the panel: a short panel
+  // stays in one CTA (its "cluster barriers" are block barriers)
+  int cs = 1;
+  while (cs < kPanelCluster && (m + cs - 1) / cs * nb * 8 * CX > kPanelSmem) cs *= 2;
+  const int64_t R = (m + cs - 1) / cs;
   const size_t smem = size_t(R) * size_t(nb) * 8 * CX;
   static DeviceAttrOnce attr;
   attr([] {
     cudaFuncSetAttribute(lu_panel_kernel<CX>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kPanelSmem));
   });
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(kPanelCluster);
+  cfg.gridDim = dim3(cs);
   cfg.blockDim = dim3(kPanelThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = kPanelCluster;
+  at[0].val.clusterDim.x = cs;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
@@ -515,83 +519,147 @@ static cudaError_t trsm_block(bool lower, const double* LU, int64_t lde, int64_t
     if (e_ != cudaSuccess) return e_;     \
   } while (0)
 
+// Two-level blocking: panels of nb <= 32 columns (the cluster kernel) inside
+// outer blocks of kOuter columns.  Inside an outer block each panel's update
+// only reaches the block's own columns (K = nb GEMMs on narrow strips); the
+// columns right of the block get ONE update per outer block with K = kOuter,
+// where the DMMA GEMM runs near its peak (a K = 32 update is bound by reading
+// and writing C).
+constexpr int kOuter = 128;
+
+// B operand of the update "rows r0..r0+k of S (k x ncols elements at S, element
+// ld lds) times ..." into the scratch operand area; returns its leading dim.
+static int64_t bop_of_rows(int cx, const double* S, int64_t lds, int64_t ncols, int k, double* out, cudaStream_t st,
+                           cudaError_t* e) {
+  const int64_t ldo = even(cx * k);
+  *e = launch_gemm_bop(cx, true, S, lds, ncols, k, out, ldo, st);
+  return ldo;
+}
+
 // In-place LU with partial pivoting of the n x n matrix A (row-major, leading
 // dim lda doubles, complex interleaved when cx = 2).  piv[k] = the row swapped
-// with row k at step k (absolute); *info = first singular column + 1, or 0.
-// scratch: >= 4 * n * kPanelMaxNb + 256 doubles (the swap map, then the U12 operand / its complex image).
+// with row k at step k (absolute); *info = first singular column + 1, or a
+// large value.  scratch: >= 4 * n * kOuter + kSwapMapDoubles doubles.
 cudaError_t launch_lu_factor(int cx, double* A, int64_t lda, int64_t n, int64_t* piv, int* info, double* scratch,
                              int* launches, cudaStream_t st) {
   const int nb = panel_nb(cx, n);
   if (nb == 0) return cudaErrorInvalidValue;
+  const int outer = kOuter / nb * nb;
   const int64_t lde = lda / cx;  // element leading dim
+  int64_t* swmap = reinterpret_cast<int64_t*>(scratch);  // {count, rows[64], src[64]}
+  double* bop = scratch + kSwapMapDoubles;
+  auto at = [&](int64_t r, int64_t c) { return A + (r * lde + c) * cx; };
+  cudaError_t e = cudaSuccess;
   LA_CK(cudaMemsetAsync(info, 0x7f, sizeof(int), st));  // INT_MAX-ish: "none"
-  for (int64_t kb = 0; kb < n; kb += nb) {
-    const int w = int(n - kb < nb ? n - kb : nb);
-    int64_t* swmap = reinterpret_cast<int64_t*>(scratch);  // {count, rows[64], src[64]}, then the operand
-    LA_CK(cx == 2 ? lu_panel<2>(A, lde, n, kb, w, piv, info, swmap, st)
-                  : lu_panel<1>(A, lde, n, kb, w, piv, info, swmap, st));
-    const int64_t rest = n - w;
-    if (rest > 0) {
-      const unsigned g = unsigned((rest + kSwapThreads - 1) / kSwapThreads);
-      const size_t sm = size_t(2 * w) * kSwapThreads * 8 * cx;
-      static DeviceAttrOnce attr;
-      attr([] {
-        cudaFuncSetAttribute(lu_swap_rest_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-        cudaFuncSetAttribute(lu_swap_rest_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-      });
-      if (cx == 2)
-        lu_swap_rest_kernel<2><<<g, kSwapThreads, sm, st>>>(A, lde, n, kb, w, swmap);
-      else
-        lu_swap_rest_kernel<1><<<g, kSwapThreads, sm, st>>>(A, lde, n, kb, w, swmap);
-      LA_CK(cudaGetLastError());
+  for (int64_t ob = 0; ob < n; ob += outer) {
+    const int64_t oe = ob + outer < n ? ob + outer : n;  // outer block columns [ob, oe)
+    for (int64_t kb = ob; kb < oe; kb += nb) {
+      const int w = int(oe - kb < nb ? oe - kb : nb);
+      LA_CK(cx == 2 ? lu_panel<2>(A, lde, n, kb, w, piv, info, swmap, st)
+                    : lu_panel<1>(A, lde, n, kb, w, piv, info, swmap, st));
       *launches += 1;
+      const int64_t rest = n - w;
+      if (rest > 0) {  // the panel's interchanges on every other column
+        const unsigned g = unsigned((rest + kSwapThreads - 1) / kSwapThreads);
+        const size_t sm = size_t(2 * w) * kSwapThreads * 8 * cx;
+        static DeviceAttrOnce attr;
+        attr([] {
+          cudaFuncSetAttribute(lu_swap_rest_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+          cudaFuncSetAttribute(lu_swap_rest_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+        });
+        if (cx == 2)
+          lu_swap_rest_kernel<2><<<g, kSwapThreads, sm, st>>>(A, lde, n, kb, w, swmap);
+        else
+          lu_swap_rest_kernel<1><<<g, kSwapThreads, sm, st>>>(A, lde, n, kb, w, swmap);
+        LA_CK(cudaGetLastError());
+        *launches += 1;
+      }
+      // inside the outer block: U = L11^-1 A for its remaining columns, then
+      // the rows below -= L21 U (K = w)
+      const int64_t c0 = kb + w, wc = oe - c0;
+      if (wc <= 0) continue;
+      LA_CK(cx == 2 ? trsm_block<2>(true, A, lde, kb, w, A, lde, c0, wc, st)
+                    : trsm_block<1>(true, A, lde, kb, w, A, lde, c0, wc, st));
+      const int64_t ldo = bop_of_rows(cx, at(kb, c0), lde, wc, w, bop, st, &e);
+      LA_CK(e);
+      LA_CK(gemm_e(cx, n - c0, wc, w, at(c0, kb), lda, bop, ldo, -1.0, 1.0, at(c0, c0), lda, st));
+      *launches += 3;
     }
-    *launches += 1;
-    const int64_t c0 = kb + w, m2 = n - c0;
+    const int64_t c2 = oe, m2 = n - c2;
     if (m2 <= 0) continue;
-    // U12 = L11^-1 A12, then A22 -= L21 U12
-    LA_CK(cx == 2 ? trsm_block<2>(true, A, lde, kb, w, A, lde, c0, m2, st)
-                  : trsm_block<1>(true, A, lde, kb, w, A, lde, c0, m2, st));
-    const int64_t ldo = even(cx * w);
-    double* bop = scratch + kSwapMapDoubles;
-    LA_CK(launch_gemm_bop(cx, true, A + (kb * lde + c0) * cx, lde, m2, w, bop, ldo, st));
-    LA_CK(gemm_e(cx, m2, m2, w, A + (c0 * lde + kb) * cx, lda, bop, ldo, -1.0, 1.0, A + (c0 * lde + c0) * cx,
-                 lda, st));
-    *launches += 3;
+    // right of the outer block: U12 = L11^-1 A12 (L11 = the block's unit lower
+    // triangle, blocked by the panels), then the trailing A22 -= L21 U12 (K = outer)
+    for (int64_t kb = ob; kb < oe; kb += nb) {
+      const int w = int(oe - kb < nb ? oe - kb : nb);
+      LA_CK(cx == 2 ? trsm_block<2>(true, A, lde, kb, w, A, lde, c2, m2, st)
+                    : trsm_block<1>(true, A, lde, kb, w, A, lde, c2, m2, st));
+      *launches += 1;
+      const int64_t r1 = kb + w;
+      if (r1 >= oe) continue;
+      const int64_t ldo = bop_of_rows(cx, at(kb, c2), lde, m2, w, bop, st, &e);
+      LA_CK(e);
+      LA_CK(gemm_e(cx, oe - r1, m2, w, at(r1, kb), lda, bop, ldo, -1.0, 1.0, at(r1, c2), lda, st));
+      *launches += 2;
+    }
+    const int64_t ldo = bop_of_rows(cx, at(ob, c2), lde, m2, int(oe - ob), bop, st, &e);
+    LA_CK(e);
+    LA_CK(gemm_e(cx, m2, m2, oe - ob, at(c2, ob), lda, bop, ldo, -1.0, 1.0, at(c2, c2), lda, st));
+    *launches += 2;
   }
   return cudaSuccess;
 }
 
 // X <- U^-1 L^-1 X for the LU in A (after the caller permuted X's rows):
-// nrhs columns, blocked by kPanelMaxNb rows; off-diagonal updates are gemm_nt.
-// scratch: >= 4 * nrhs * kPanelMaxNb doubles.
+// nrhs columns; 32-row diagonal blocks (one thread per right-hand side),
+// off-diagonal updates by gemm_nt -- within an outer block of kOuter rows with
+// K = 32, beyond it once per outer block with K = kOuter.
+// scratch: >= 4 * nrhs * kOuter doubles.
 cudaError_t launch_lu_solve(int cx, const double* A, int64_t lda, int64_t n, double* X, int64_t ldx, int64_t nrhs,
                             double* scratch, int* launches, cudaStream_t st) {
   const int nb = kPanelMaxNb;
   const int64_t lde = lda / cx, ldxe = ldx / cx;
-  for (int64_t kb = 0; kb < n; kb += nb) {  // forward: L Y = X (unit lower)
-    const int w = int(n - kb < nb ? n - kb : nb);
-    LA_CK(cx == 2 ? trsm_block<2>(true, A, lde, kb, w, X, ldxe, 0, nrhs, st)
-                  : trsm_block<1>(true, A, lde, kb, w, X, ldxe, 0, nrhs, st));
-    const int64_t r1 = kb + w, m2 = n - r1;
-    *launches += 1;
-    if (m2 <= 0) continue;
-    const int64_t ldo = even(cx * w);
-    LA_CK(launch_gemm_bop(cx, true, X + kb * ldx, ldxe, nrhs, w, scratch, ldo, st));
-    LA_CK(gemm_e(cx, m2, nrhs, w, A + (r1 * lde + kb) * cx, lda, scratch, ldo, -1.0, 1.0, X + r1 * ldx, ldx, st));
+  auto at = [&](int64_t r, int64_t c) { return A + (r * lde + c) * cx; };
+  cudaError_t e = cudaSuccess;
+  for (int64_t ob = 0; ob < n; ob += kOuter) {  // forward: L Y = X (unit lower)
+    const int64_t oe = ob + kOuter < n ? ob + kOuter : n;
+    for (int64_t kb = ob; kb < oe; kb += nb) {
+      const int w = int(oe - kb < nb ? oe - kb : nb);
+      LA_CK(cx == 2 ? trsm_block<2>(true, A, lde, kb, w, X, ldxe, 0, nrhs, st)
+                    : trsm_block<1>(true, A, lde, kb, w, X, ldxe, 0, nrhs, st));
+      *launches += 1;
+      const int64_t r1 = kb + w;
+      if (r1 >= oe) continue;
+      const int64_t ldo = bop_of_rows(cx, X + kb * ldx, ldxe, nrhs, w, scratch, st, &e);
+      LA_CK(e);
+      LA_CK(gemm_e(cx, oe - r1, nrhs, w, at(r1, kb), lda, scratch, ldo, -1.0, 1.0, X + r1 * ldx, ldx, st));
+      *launches += 2;
+    }
+    if (oe >= n) continue;
+    const int64_t ldo = bop_of_rows(cx, X + ob * ldx, ldxe, nrhs, int(oe - ob), scratch, st, &e);
+    LA_CK(e);
+    LA_CK(gemm_e(cx, n - oe, nrhs, oe - ob, at(oe, ob), lda, scratch, ldo, -1.0, 1.0, X + oe * ldx, ldx, st));
     *launches += 2;
   }
-  const int64_t nblk = (n + nb - 1) / nb;
-  for (int64_t b = nblk - 1; b >= 0; --b) {  // backward: U R = Y
-    const int64_t kb = b * nb;
-    const int w = int(n - kb < nb ? n - kb : nb);
-    LA_CK(cx == 2 ? trsm_block<2>(false, A, lde, kb, w, X, ldxe, 0, nrhs, st)
-                  : trsm_block<1>(false, A, lde, kb, w, X, ldxe, 0, nrhs, st));
-    *launches += 1;
-    if (kb == 0) continue;
-    const int64_t ldo = even(cx * w);
-    LA_CK(launch_gemm_bop(cx, true, X + kb * ldx, ldxe, nrhs, w, scratch, ldo, st));
-    LA_CK(gemm_e(cx, kb, nrhs, w, A + kb * cx, lda, scratch, ldo, -1.0, 1.0, X, ldx, st));
+  const int64_t nob = (n + kOuter - 1) / kOuter;
+  for (int64_t o = nob - 1; o >= 0; --o) {  // backward: U R = Y
+    const int64_t ob = o * kOuter, oe = ob + kOuter < n ? ob + kOuter : n;
+    const int64_t nblk = (oe - ob + nb - 1) / nb;
+    for (int64_t b = nblk - 1; b >= 0; --b) {
+      const int64_t kb = ob + b * nb;
+      const int w = int(oe - kb < nb ? oe - kb : nb);
+      LA_CK(cx == 2 ? trsm_block<2>(false, A, lde, kb, w, X, ldxe, 0, nrhs, st)
+                    : trsm_block<1>(false, A, lde, kb, w, X, ldxe, 0, nrhs, st));
+      *launches += 1;
+      if (kb == ob) continue;
+      const int64_t ldo = bop_of_rows(cx, X + kb * ldx, ldxe, nrhs, w, scratch, st, &e);
+      LA_CK(e);
+      LA_CK(gemm_e(cx, kb - ob, nrhs, w, at(ob, kb), lda, scratch, ldo, -1.0, 1.0, X + ob * ldx, ldx, st));
+      *launches += 2;
+    }
+    if (ob == 0) continue;
+    const int64_t ldo = bop_of_rows(cx, X + ob * ldx, ldxe, nrhs, int(oe - ob), scratch, st, &e);
+    LA_CK(e);
+    LA_CK(gemm_e(cx, ob, nrhs, oe - ob, at(0, ob), lda, scratch, ldo, -1.0, 1.0, X, ldx, st));
     *launches += 2;
   }
   return cudaSuccess;

@@ -189,7 +189,10 @@ __global__ void __launch_bounds__(ROWS, MINB)
   for (int it = 0; trip < ntrips; ++it, trip += gridDim.x) {
     const int st = it & 1;
     const int64_t next = trip + gridDim.x;
-    if (tid == 0 && next < ntrips) issue(next, st ^ 1);  // stage st^1 was released by the barrier below
+    if (tid == 0 && next < ntrips) {  // stage st^1 was released by the barrier below
+      fence_proxy_async_smem();          // its generic reads before the async-proxy refill
+      issue(next, st ^ 1);
+    }
     mbar_wait(&bar[st], (it >> 1) & 1);
     const int64_t m = trip * kU16Rows + tid;
     if (m < n) {

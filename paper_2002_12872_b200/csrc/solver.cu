@@ -1952,7 +1952,7 @@ int run_homotopy(dpt_ctx* ctx, const dpt_problem* p, int stages, const dpt_optio
   dalloc(bdl, size_t(cx * n) * 8, err);
   dalloc(bDp, cmat, err);
   dalloc(bop, opbytes, err);
-  dalloc(bscr, size_t(4) * size_t(n) * 32 * 8 + 4096, err);
+  dalloc(bscr, size_t(4) * size_t(n) * 128 * 8 + 4096, err);
   dalloc(bpiv, size_t(n) * 8 + 16, err);
   dalloc(bperm, size_t(n) * 8 + 16, err);
   dalloc(binfo, 16, err);
@@ -2602,7 +2602,7 @@ int dpt_solve_linear_multi(dpt_ctx* ctx, int64_t n, int64_t nrhs, int is_complex
   dalloc(bpiv, size_t(n) * 8, err);
   dalloc(bperm, size_t(n) * 8, err);
   dalloc(binfo, 16, err);
-  dalloc(bscr, size_t(4) * size_t(std::max(n, nrhs)) * 32 * 8 + 4096, err);
+  dalloc(bscr, size_t(4) * size_t(std::max(n, nrhs)) * 128 * 8 + 4096, err);
   int nl = 0;
   CK(launch_lu_factor(cx, ba.as<double>(), lda, n, bpiv.as<int64_t>(), binfo.as<int>(), bscr.as<double>(), &nl, st));
   int hinfo = 0;
