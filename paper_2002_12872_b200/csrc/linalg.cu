@@ -210,25 +210,37 @@ __global__ void __launch_bounds__(kPanelThreads)
     }
     if (lane == 0) wv[warp] = best, wi[warp] = bi;
     __syncthreads();
-    if (tid == 0) {
-      for (int w = 1; w < kPanelThreads / 32; ++w)
-        if (wv[w] > best || (wv[w] == best && wi[w] < bi)) best = wv[w], bi = wi[w];
-      cand_v = best;
-      cand_i = bi;
+    if (warp == 0) {  // the block's candidate: one more shuffle tree over the warps' winners
+      best = lane < kPanelThreads / 32 ? wv[lane] : -1.0;
+      bi = lane < kPanelThreads / 32 ? wi[lane] : INT64_MAX;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_down_sync(0xffffffffu, best, o);
+        const int64_t oi = __shfl_down_sync(0xffffffffu, bi, o);
+        if (ov > best || (ov == best && oi < bi)) best = ov, bi = oi;
+      }
+      if (lane == 0) {
+        cand_v = best;
+        cand_i = bi;
+      }
     }
     cl.sync();  // [A] every CTA's candidate is published
-    if (tid == 0) {
-      double gb = -1.0;
-      int64_t gi = INT64_MAX;
-      for (int r = 0; r < int(cl.num_blocks()); ++r) {
-        const double v = *cl.map_shared_rank(&cand_v, r);
-        const int64_t i = *cl.map_shared_rank(&cand_i, r);
-        if (v > gb || (v == gb && i < gi)) gb = v, gi = i;
+    if (warp == 0) {  // lanes read the cluster's candidates in parallel (DSMEM), then one tree
+      const int nblk = int(cl.num_blocks());
+      double gb = lane < nblk ? *cl.map_shared_rank(&cand_v, lane) : -1.0;
+      int64_t gi = lane < nblk ? *cl.map_shared_rank(&cand_i, lane) : INT64_MAX;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_down_sync(0xffffffffu, gb, o);
+        const int64_t oi = __shfl_down_sync(0xffffffffu, gi, o);
+        if (ov > gb || (ov == gb && oi < gi)) gb = ov, gi = oi;
       }
-      s_p = gi;
-      s_sing = !(gb > 0.0);  // exactly-zero column: lu_factor's singular test (matrix.cpp:485)
-      if (s_sing && rank == 0) atomicMin(info, int(kb + j + 1));
-      if (rank == 0) piv[kb + j] = kb + (s_sing ? j : gi);
+      if (lane == 0) {
+        s_p = gi;
+        s_sing = !(gb > 0.0);  // exactly-zero column: lu_factor's singular test (matrix.cpp:485)
+        if (s_sing && rank == 0) atomicMin(info, int(kb + j + 1));
+        if (rank == 0) piv[kb + j] = kb + (s_sing ? j : gi);
+      }
     }
     __syncthreads();
     const int64_t p = s_sing ? j : s_p;
@@ -476,10 +488,9 @@ template <int CX>
 static cudaError_t lu_panel(double* A, int64_t lde, int64_t n, int64_t kb, int nb, int64_t* piv, int* info,
                             int64_t* swmap, cudaStream_t st) {
   const int64_t m = n - kb;
-  // the smallest cluster whose shared memories hold the panel: a short panel
-  // stays in one CTA (its "cluster barriers" are block barriers)
-  int cs = 1;
-  while (cs < kPanelCluster && (m + cs - 1) / cs * nb * 8 * CX > kPanelSmem) cs *= 2;
+  // always the full cluster: fewer CTAs hold short panels too, but the
+  // per-column elimination then runs on fewer SMs (measured slower)
+  const int cs = kPanelCluster;
   const int64_t R = (m + cs - 1) / cs;
   const size_t smem = size_t(R) * size_t(nb) * 8 * CX;
   static DeviceAttrOnce attr;
