@@ -491,6 +491,30 @@ def main():
             traffic = None
     plan.close()
 
+    # N > 1: the same workload's one-GPU step on rank 0 (the others wait), so the
+    # line carries its own single-GPU point of the c5 scaling curve
+    one_gpu = None
+    if world > 1:
+        if rank == 0:
+            c1 = P.Context(local)
+            pl1 = P.Plan(p, ctx=c1)
+            pl1.begin()
+            pl1.steps(1)
+            k1 = min(args.steps, 3)
+            ms1 = pl1.steps(k1, time_kernel=True) / k1
+            s1 = torch.cuda.ExternalStream(c1.stream_ptr)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s1)
+            pl1.steps(k1)
+            e1.record(s1)
+            e1.synchronize()
+            step1 = e0.elapsed_time(e1) / k1
+            pl1.close()
+            c1.close()
+            one_gpu = {"value": 1e3 / step1, "unit": "iter/s", "ms_per_step": step1, "k1_ms": ms1,
+                       "how": "rank 0 alone, unsharded plan of the same problem, events on its stream"}
+        barrier()
+
     # e2e: the public API on pinned host arrays, solve to the terminal status
     pe, oe = make_inputs(wl, n, pinned=True)
     io = P.IterationOptions(**oe)
@@ -574,9 +598,15 @@ def main():
             line["per_rank"] = {"k1_ms_max": kms, "step_ms": ms_per_step,
                                 "fold_allreduce_decide_ms": ms_per_step - kms,
                                 "rows_per_rank": rows_local}
-        print(json.dumps(line), flush=True)
+            line["same_workload_1gpu"] = one_gpu
+    # tear the communicators down BEFORE printing: with NCCL_DEBUG=INFO their
+    # shutdown lines would otherwise follow the JSON line
+    ctx.close()
     if world > 1:
         dist.destroy_process_group()
+    if rank == 0:
+        sys.stdout.flush()
+        print(json.dumps(line), flush=True)
     return 0
 
 
