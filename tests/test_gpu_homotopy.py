@@ -66,8 +66,9 @@ def test_reference_known_answers():
     assert np.max(np.abs(h.state.a - d.state.a)) < 1e-10
 
 
-@pytest.mark.parametrize("n,seed,lam,stages", [(6, 3, 0.2, 3), (16, 5, 0.1, 4), (40, 1, 0.05, 2), (40, 2, 0.05, 2),
-                                               (130, 2, 0.02, 3)])
+@pytest.mark.parametrize("n,seed,lam,stages", [(6, 3, 0.2, 3), (7, 4, 0.2, 2), (16, 5, 0.1, 4), (33, 6, 0.08, 2),
+                                               (40, 1, 0.05, 2), (40, 2, 0.05, 2), (130, 2, 0.02, 3),
+                                               (161, 3, 0.02, 2)])
 def test_random_uniform_vs_reference(R, n, seed, lam, stages):
     t, d = pr.random_uniform(n, seed)
     compare(R, PartitionedProblem(t, d, lam), stages)

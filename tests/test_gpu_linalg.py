@@ -99,3 +99,17 @@ def test_large_solve_residual():
     x = P.solve_linear_multi(a, b)
     assert np.max(np.abs(a @ x - b)) <= 1e-10 * np.max(np.abs(b)) * np.sqrt(n)
     assert np.max(np.abs(x - np.linalg.solve(a, b))) <= 1e-11
+
+
+def test_empty_and_degenerate_shapes(R):
+    """n = 0 / k = 0 / nrhs = 0 (the reference returns empty or zero
+    matrices) and 1 x 1 systems."""
+    assert P.matmul_dense(np.zeros((0, 3)), np.zeros((3, 4))).shape == (0, 4)
+    z = P.matmul_dense(np.zeros((3, 0)), np.zeros((0, 5)))
+    assert z.shape == (3, 5) and np.all(z == 0.0)
+    assert P.solve_linear_multi(np.zeros((0, 0)), np.zeros((0, 2))).shape == (0, 2)
+    assert P.solve_linear_multi(np.eye(4), np.zeros((4, 0))).shape == (4, 0)
+    x = P.solve_linear_multi(np.array([[4.0]]), np.array([[2.0, -8.0]]))
+    assert np.array_equal(x, np.array([[0.5, -2.0]]))
+    with pytest.raises(ValueError):
+        P.solve_linear_multi(np.eye(3), np.ones((4, 1)))

@@ -56,8 +56,8 @@ def assert_same_report(g, h):
     assert np.array_equal(g.residuals, h.residuals, equal_nan=True)
 
 
-@pytest.mark.parametrize("name,n,world", [("c1", 300, 2), ("c1", 301, 3), ("c2b", 1024, 2), ("c2", 256, 2),
-                                          ("c3", 512, 2), ("c3", 515, 3)])
+@pytest.mark.parametrize("name,n,world", [("c1", 300, 2), ("c1", 301, 3), ("c1", 301, 4), ("c2b", 1024, 2),
+                                          ("c2", 256, 2), ("c2b", 777, 8), ("c3", 512, 2), ("c3", 515, 3)])
 def test_sharded_solve_equals_unsharded(name, n, world):
     p, o, _ = pr.config(name, n)
     io = P.IterationOptions(**o)
