@@ -1,4 +1,4 @@
-"""GPU: the world > 1 CUDA path on ONE device.  Two (or three) contexts on
+"""GPU: the world > 1 CUDA path on ONE device.  Two to eight contexts on
 device 0 form a loopback group (dpt_ctx_set_loopback, test-only): each rank
 is driven by its own host thread through the public calls, so the real sharded
 code runs -- shard_rows -> per-rank step kernel on its row block -> max-
