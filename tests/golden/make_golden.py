@@ -4,6 +4,7 @@ oracle/Makefile).  Run in the build container (where /root/reference exists):
 
     make -C oracle && python tests/golden/make_golden.py
     python tests/golden/make_golden.py c3full     # c3 at n = 8192 (~2 min)
+    python tests/golden/make_golden.py c2bfull    # c2b at n = 4096 (~20 min)
 
 The fixtures are small (n <= 96) so they travel with the repo; the tests check
 both the C restatement and the CUDA path against them.
@@ -81,8 +82,29 @@ def c3_full():
     print("c3 full", r.status, r.iterations)
 
 
+C2B_ROWS = ((0, 64), (2000, 2064))
+
+
+def c2b_full():
+    """The bench family at its full size: c2b (BASELINE configs[1] with theta_i
+    = i, the converging companion; n = 4096 dense unsymmetric, ~20 min in the
+    reference).  Status, iterations, all eigenvalues and residuals, two 64-row
+    blocks of the eigenvector matrix, and the inputs' fingerprint."""
+    R = Checker("reference")
+    p, o, _ = pr.config("c2b")
+    r = R.iterate_full(p, o)
+    rec = dict(status=r.status, iterations=r.iterations, step_norm=r.step_norm, eig=r.eig, res=r.res,
+               delta_sum=np.sum(p.delta), delta_sq=np.sum(p.delta * p.delta), lam=p.lam)
+    for a, b in C2B_ROWS:
+        rec[f"a_{a}_{b}"] = r.a[a:b]
+    np.savez_compressed(os.path.join(OUT, "c2bfull_n4096.npz"), **rec)
+    print("c2b full", r.status, r.iterations)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "c3full":
         c3_full()
+    elif len(sys.argv) > 1 and sys.argv[1] == "c2bfull":
+        c2b_full()
     else:
         main()

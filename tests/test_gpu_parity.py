@@ -324,6 +324,28 @@ def test_c3_full_size_vs_reference_golden():
     assert np.all(np.diag(g.state.a) == 1.0)
 
 
+def test_c2b_full_size_vs_reference_golden():
+    """The bench's config family at full size, converging: c2b (BASELINE
+    configs[1] with theta_i = i; n = 4096 dense unsymmetric) against the
+    REFERENCE's own solve (tests/golden/c2bfull_n4096.npz, make_golden.py
+    c2bfull, ~20 min in oracle/_ref): status, iterations, all eigenvalues,
+    residuals and two 64-row blocks of the eigenvector matrix."""
+    import os
+    from helpers import GOLDEN
+    z = np.load(os.path.join(GOLDEN, "c2bfull_n4096.npz"))
+    p, o, _ = pr.config("c2b")
+    assert np.sum(p.delta) == float(z["delta_sum"]) and np.sum(p.delta * p.delta) == float(z["delta_sq"])
+    g = P.iterate_full(p, _o(o))
+    assert int(g.status) == int(z["status"]) == 0 and abs(g.iterations - int(z["iterations"])) <= 1
+    assert eig_rel_err(g.eigenvalues, z["eig"]) < EIG_RTOL
+    for key in z.files:
+        if key.startswith("a_"):
+            a, b = (int(x) for x in key.split("_")[1:])
+            assert np.max(np.abs(g.state.a[a:b] - z[key])) < VEC_ATOL, key
+    assert np.max(g.residuals) < 1e-10
+    assert np.allclose(g.residuals, z["res"], rtol=1e-3, atol=1e-13)
+
+
 def test_c3_full_size_properties():
     p, o, _ = pr.config("c3")  # n = 8192 CSR, nnz = 336,376 with the recipe
     assert p.delta.nnz == 336376
