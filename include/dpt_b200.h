@@ -64,7 +64,10 @@ typedef enum dpt_error {
 /* Where the pointers of a call live. */
 typedef enum dpt_mem { DPT_MEM_HOST = 0, DPT_MEM_DEVICE = 1 } dpt_mem;
 
-typedef enum dpt_delta_kind { DPT_DELTA_DENSE = 0, DPT_DELTA_CSR = 1 } dpt_delta_kind;
+/* DPT_DELTA_DENSE_T: dense, but `delta` holds Delta^T (the reference's cached
+ * PartitionedProblem::delta_t, partition.hpp:43-50); accepted by the
+ * single-step entry points (step_full), transposed on the device. */
+typedef enum dpt_delta_kind { DPT_DELTA_DENSE = 0, DPT_DELTA_CSR = 1, DPT_DELTA_DENSE_T = 2 } dpt_delta_kind;
 
 /* IterationOptions, dpt.hpp:22-31 -- field for field, same defaults
  * (dpt_options_default). */

@@ -754,6 +754,48 @@ cudaError_t launch_dense_step(const DevSolve& s, const CUtensorMap* amaps, const
   return launch_cfg<CfgBig>(s, amaps, dmap, delta, st);
 }
 
+// K1's dense B operand from the caller's Delta (src, n x n, row-major; complex
+// interleaved when cx = 2), optionally given transposed (the reference's
+// cached delta_t): real -> dst[j][k] = Delta(j, k) (ld ldd); complex -> the
+// 2n x 2n real image (rows 2j, 2j+1 = (Re, -Im), (Im, Re) of Delta(j, k)).
+// 32 x 32 tiles through shared memory, so both the transposed reads and the
+// writes are coalesced.
+__global__ void __launch_bounds__(256) delta_image_kernel(const double* __restrict__ src, int64_t n, int cx,
+                                                            int transposed, double* __restrict__ dst, int64_t ldd) {
+  __shared__ double2 tile[32][33];
+  const int64_t j0 = int64_t(blockIdx.y) * 32, k0 = int64_t(blockIdx.x) * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  for (int r = ty; r < 32; r += 8) {
+    // element (j, k) of Delta = src[j][k], or src[k][j] when transposed; stage it at tile[jj][kk]
+    const int64_t a = transposed ? k0 + r : j0 + r, b = transposed ? j0 + tx : k0 + tx;  // src row a, col b
+    double2 v = make_double2(0.0, 0.0);
+    if (a < n && b < n) v = cx == 2 ? reinterpret_cast<const double2*>(src)[a * n + b] : make_double2(src[a * n + b], 0.0);
+    if (transposed)
+      tile[tx][r] = v;  // src (k0 + r, j0 + tx) = Delta(j0 + tx, k0 + r)
+    else
+      tile[r][tx] = v;
+  }
+  __syncthreads();
+  for (int r = ty; r < 32; r += 8) {
+    const int64_t j = j0 + r, kk = k0 + tx;
+    if (j >= n || kk >= n) continue;
+    const double2 v = tile[r][tx];
+    if (cx == 2) {
+      *reinterpret_cast<double2*>(dst + (2 * j) * ldd + 2 * kk) = make_double2(v.x, -v.y);
+      *reinterpret_cast<double2*>(dst + (2 * j + 1) * ldd + 2 * kk) = make_double2(v.y, v.x);
+    } else {
+      dst[j * ldd + kk] = v.x;
+    }
+  }
+}
+
+cudaError_t launch_delta_image(const double* src, int64_t n, int cx, int transposed, double* dst, int64_t ldd,
+                               cudaStream_t st) {
+  const dim3 grid(unsigned((n + 31) / 32), unsigned((n + 31) / 32));
+  delta_image_kernel<<<grid, 256, 0, st>>>(src, n, cx, transposed, dst, ldd);
+  return cudaGetLastError();
+}
+
 int dense_step_ntiles(int64_t rows, int ntn, int cfg) {
   const int bm = dense_tile_m(cfg);
   return int((rows + bm - 1) / bm) * ntn;

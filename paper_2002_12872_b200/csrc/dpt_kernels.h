@@ -14,6 +14,8 @@ int make_tmap_rowmajor(CUtensorMap* out, const double* base, int64_t dim0, int64
 int dense_cfg_for(int64_t n, int64_t rows);
 int dense_tile_n(int cfg);
 int dense_tile_m(int cfg);
+cudaError_t launch_delta_image(const double* src, int64_t n, int cx, int transposed, double* dst, int64_t ldd,
+                               cudaStream_t st);
 int dense_step_ntiles(int64_t rows, int ntn, int cfg);
 int dense_init_ntiles(int64_t rows, int ntn, int cplx);
 cudaError_t launch_dense_step(const DevSolve& s, const CUtensorMap* amaps, const CUtensorMap* dmap,

@@ -728,7 +728,9 @@ void build_sell_device(DevProblem& dp, cudaStream_t st, dpt_error_info* err) {
   dp.nslices = ns;
 }
 
-void validate(const dpt_problem* p, dpt_error_info* err) {
+// allow_transposed: DPT_DELTA_DENSE_T (the caller passes Delta^T, the
+// reference's cached delta_t) is accepted by the single-step entry points only.
+void validate(const dpt_problem* p, dpt_error_info* err, bool allow_transposed = false) {
   if (!p || p->n < 0) {
     set_err(err, DPT_ERR_SHAPE, "problem: bad size");
     throw Fail{DPT_ERR_SHAPE};
@@ -737,7 +739,7 @@ void validate(const dpt_problem* p, dpt_error_info* err) {
     set_err(err, DPT_ERR_SHAPE, "problem: missing levels");
     throw Fail{DPT_ERR_SHAPE};
   }
-  if (p->delta_kind == DPT_DELTA_DENSE) {
+  if (p->delta_kind == DPT_DELTA_DENSE || (p->delta_kind == DPT_DELTA_DENSE_T && allow_transposed)) {
     if (p->n > 0 && !p->delta) {
       set_err(err, DPT_ERR_SHAPE, "problem: missing dense delta");
       throw Fail{DPT_ERR_SHAPE};
@@ -755,7 +757,7 @@ void validate(const dpt_problem* p, dpt_error_info* err) {
 
 void upload(DevProblem& dp, dpt_ctx* ctx, const dpt_problem* p, dpt_error_info* err, bool sell = false) {
   Nvtx nvtx_range("dpt.upload");
-  validate(p, err);
+  validate(p, err, true);
   const int64_t n = p->n;
   const int cx = p->is_complex ? 2 : 1;  // doubles per scalar
   dp.n = n;
@@ -763,9 +765,9 @@ void upload(DevProblem& dp, dpt_ctx* ctx, const dpt_problem* p, dpt_error_info* 
   dp.lambda_im = p->is_complex ? p->lambda_im : 0.0;
   dp.ncol = cx * n;
   dp.ld = (dp.ncol + 1) & ~int64_t(1);
-  dp.kind = p->delta_kind;
+  dp.kind = p->delta_kind == DPT_DELTA_CSR ? DPT_DELTA_CSR : DPT_DELTA_DENSE;  // Delta^T input is transposed below
+  const bool dense_t = p->delta_kind == DPT_DELTA_DENSE_T;
   const cudaMemcpyKind k = p->mem == DPT_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-  const cudaMemcpyKind hk = p->mem == DPT_MEM_DEVICE ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost;
   cudaStream_t st = ctx->stream;
   // Device-resident inputs whose layout the kernels take as is are used in
   // place (views); host inputs and re-laid-out arrays are copied.
@@ -777,29 +779,25 @@ void upload(DevProblem& dp, dpt_ctx* ctx, const dpt_problem* p, dpt_error_info* 
     dalloc(dp.theta, size_t(cx * n) * 8, err);
     if (n) CK(copy_async(ctx, dp.theta.p, p->d, size_t(cx * n) * 8, k));
   }
-  if (p->delta_kind == DPT_DELTA_DENSE) {
-    if (dp.cplx) {
-      // real image B (2n x 2n): row 2j = (Re D(j,k), -Im D(j,k))_k, row 2j+1 = (Im D(j,k), Re D(j,k))_k,
-      // so the real NT GEMM of the interleaved iterate with B yields (Re P, Im P) pairs.
-      dp.ldd = 2 * n;
-      std::vector<double> D(size_t(2 * n) * size_t(n));
-      if (n) CK(to_host_ordered(D.data(), p->delta, size_t(2 * n) * size_t(n) * 8, hk));
-      std::vector<double> B(size_t(2 * n) * size_t(2 * n));
-      for (int64_t j = 0; j < n; ++j) {
-        double* r0 = B.data() + size_t(2 * j) * size_t(2 * n);
-        double* r1 = r0 + 2 * n;
-        const double* src = D.data() + size_t(j) * size_t(2 * n);
-        for (int64_t q = 0; q < n; ++q) {
-          const double re = src[2 * q], im = src[2 * q + 1];
-          r0[2 * q] = re;
-          r0[2 * q + 1] = -im;
-          r1[2 * q] = im;
-          r1[2 * q + 1] = re;
-        }
+  if (p->delta_kind != DPT_DELTA_CSR) {
+    if (dp.cplx || dense_t) {
+      // Complex: the real image B (2n x 2n): row 2j = (Re D(j,k), -Im D(j,k))_k,
+      // row 2j+1 = (Im D(j,k), Re D(j,k))_k, so the real NT GEMM of the
+      // interleaved iterate with B yields (Re P, Im P) pairs.  Delta^T input:
+      // transposed on the way.  Both are built on the device (delta_image_kernel)
+      // from the caller's array, used in place when device-resident.
+      dp.ldd = dp.cplx ? 2 * n : dp.ld;
+      dalloc(dp.delta, size_t(dp.cplx ? 2 * n : n) * size_t(dp.ldd) * 8 + 64, err);
+      DBuf raw;
+      const double* src = p->delta;
+      if (!dev && n) {
+        dalloc(raw, size_t(cx) * size_t(n) * size_t(n) * 8, err);
+        CK(copy_async(ctx, raw.p, p->delta, size_t(cx) * size_t(n) * size_t(n) * 8, k));
+        src = raw.as<double>();
       }
-      dalloc(dp.delta, B.size() * 8 + 64, err);
-      if (n) CK(copy_async(ctx, dp.delta.p, B.data(), B.size() * 8, cudaMemcpyHostToDevice));
-      CK(cudaStreamSynchronize(st));  // B goes out of scope
+      if (n) CK(launch_delta_image(src, n, cx, dense_t ? 1 : 0, dp.delta.as<double>(), dp.ldd, st));
+      ctx->launches += 1;
+      CK(cudaStreamSynchronize(st));  // raw goes out of scope
     } else if (dev && n && dp.ld == n && aligned16(p->delta)) {
       dp.ldd = dp.ld;
       dp.delta.view(p->delta);  // TMA-ready as is: 16-byte aligned, even leading dimension
@@ -1743,7 +1741,7 @@ int run_step_full(dpt_ctx* ctx, const dpt_problem* p, const double* a, const dou
                   double lambda_im = 0.0) {
   Nvtx nvtx_range("dpt.step_full");
   Guard g(ctx);
-  validate(p, err);
+  validate(p, err, true);
   if (sharded(ctx)) {
     set_err(err, DPT_ERR_UNSUPPORTED, "step_full is a single-device call");
     throw Fail{DPT_ERR_UNSUPPORTED};
@@ -1752,7 +1750,7 @@ int run_step_full(dpt_ctx* ctx, const dpt_problem* p, const double* a, const dou
   if (n == 0) return DPT_OK;
   DevProblem dp;
   upload(dp, ctx, p, err, p->delta_kind == DPT_DELTA_CSR);
-  const Mode mode = p->delta_kind == DPT_DELTA_DENSE ? MODE_DENSE_FULL : MODE_CSR_FULL;
+  const Mode mode = p->delta_kind == DPT_DELTA_CSR ? MODE_CSR_FULL : MODE_DENSE_FULL;
   dpt_sm_options so{};
   so.max_iter = 1;
   Work w;

@@ -270,10 +270,13 @@ std::string to_string(ConvergenceStatus s) { return dpt_status_string(int(s)); }
 DenseMatrix step_full(const DenseMatrix& a, const GapMatrix& theta, const MatrixVariant& delta_t, cdouble lambda) {
   const std::size_t n = a.rows();
   if (a.cols() != n || theta.theta.rows() != n) throw ShapeError("step_full: dimension mismatch");
-  // the C ABI takes Delta; recover it from the cached transpose (no conjugation)
-  const MatrixVariant delta = transpose(delta_t);
   DiagonalMatrix zeros(std::vector<cdouble>(n, cdouble{}));  // levels unused with an explicit gap matrix
-  auto P = to_c(zeros, delta, lambda, has_imag(a) || has_imag(theta.theta));
+  // The C ABI takes Delta.  A dense delta_t goes in as is (DPT_DELTA_DENSE_T:
+  // transposed on the device); a sparse one is transposed here (no conjugation).
+  const bool dense_t = std::holds_alternative<DenseMatrix>(delta_t);
+  const MatrixVariant delta = dense_t ? MatrixVariant{} : transpose(delta_t);
+  auto P = to_c(zeros, dense_t ? delta_t : delta, lambda, has_imag(a) || has_imag(theta.theta));
+  if (dense_t) P->c.delta_kind = DPT_DELTA_DENSE_T;
   const InBuf ab(a.data(), n * n, P->cplx), gb(theta.theta.data(), n * n, P->cplx);
   DenseMatrix out(n, n);
   OutBuf ob(out.data(), n * n, P->cplx);
