@@ -120,3 +120,16 @@ def test_sharded_plan_steps():
     single = steps(None)
     for a in run_ranks(2, steps):
         assert np.array_equal(a, single)
+
+
+def test_row_map_replicas():
+    """The single-vector mode does not shard (one SpMV chain): with a
+    communicator every rank runs the whole row map as a replica, the
+    statistics all-reduce over identical values, and every rank returns the
+    single-device answer bit for bit ("replicas only")."""
+    p, o, _ = pr.config("c4b", 20000)
+    io = P.IterationOptions(**o)
+    h = P.dominant_eigenpair(p, io)
+    for g in run_ranks(2, lambda ctx: P.dominant_eigenpair(p, io, ctx=ctx)):
+        assert int(g.status) == int(h.status) and g.iterations == h.iterations and g.row == h.row
+        assert g.eigenvalue == h.eigenvalue and np.array_equal(g.z_chart, h.z_chart)
