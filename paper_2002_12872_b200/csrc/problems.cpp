@@ -13,6 +13,7 @@
 #include <cstdint>
 #include <cstring>
 #include <numeric>
+#include <thread>
 #include <vector>
 
 namespace {
@@ -89,19 +90,37 @@ int dpt_gen_theta_uniform_sorted(int64_t n, uint64_t seed, double hi, double min
 // Dense N(0,1) perturbation, drawn row-major from stream(seed, tag).
 // symmetric != 0: Delta(i,j) = (X(i,j) + X(j,i)) / 2 off the diagonal (c1, c5).
 // Either way the diagonal is zero (drawn, then zeroed: c2).
+// splitmix64's k-th output depends only on state0 + (k+1) gamma, so rows are
+// drawn in parallel (row i starts at draw 2 i n): the same values as one
+// sequential stream.  The symmetrisation pair (i, j), i < j, is read and
+// written only by the thread owning row i.
 void dpt_gen_dense_normal(int64_t n, uint64_t seed, const char* tag, int symmetric,
                           double* delta) {
-  Rng r = Rng::stream(seed, tag);
+  const Rng base = Rng::stream(seed, tag);
   const size_t nn = size_t(n);
-  for (size_t i = 0; i < nn; ++i)
-    for (size_t j = 0; j < nn; ++j) delta[i * nn + j] = r.normal();
+  const unsigned hw = std::thread::hardware_concurrency();
+  const int T = int(std::max(1u, std::min(hw ? hw : 1u, nn * nn >= (size_t(1) << 22) ? 32u : 1u)));
+  auto run = [&](auto&& body) {
+    std::vector<std::thread> th;
+    for (int t = 1; t < T; ++t) th.emplace_back(body, t);
+    body(0);
+    for (auto& x : th) x.join();
+  };
+  run([&](int t) {
+    for (size_t i = size_t(t); i < nn; i += size_t(T)) {
+      Rng r(base.s + 0x9E3779B97F4A7C15ull * (2 * i * nn));  // skip the 2 i n draws of rows < i
+      for (size_t j = 0; j < nn; ++j) delta[i * nn + j] = r.normal();
+    }
+  });
   if (symmetric) {
-    for (size_t i = 0; i < nn; ++i)
-      for (size_t j = i + 1; j < nn; ++j) {
-        const double v = (delta[i * nn + j] + delta[j * nn + i]) / 2.0;
-        delta[i * nn + j] = v;
-        delta[j * nn + i] = v;
-      }
+    run([&](int t) {
+      for (size_t i = size_t(t); i < nn; i += size_t(T))
+        for (size_t j = i + 1; j < nn; ++j) {
+          const double v = (delta[i * nn + j] + delta[j * nn + i]) / 2.0;
+          delta[i * nn + j] = v;
+          delta[j * nn + i] = v;
+        }
+    });
   }
   for (size_t i = 0; i < nn; ++i) delta[i * nn + i] = 0.0;
 }
