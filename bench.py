@@ -382,6 +382,67 @@ def platform_cpu():
 
 
 # ------------------------------------------------------------ B200 arm ----
+def other_configs(P, torch, ctx, local, fp64_peak):
+    """c1 / c3 / c4 / c4b next to the bench line: event-timed step kernel over
+    20 fixed steps (c1 / c3: K1 / K2, c4: K3) with its roofline fraction (FP64
+    against the DMMA peak for dense, algorithmic HBM bytes against
+    MEASURED_PEAKS.json for CSR / row map), and the public call to the terminal
+    status with device-resident inputs (best of 3)."""
+    from paper_2002_12872_b200 import problems as pr
+    hbm = 6551.0
+    try:
+        hbm = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        pass
+    dev = torch.device("cuda", local)
+    out = {}
+    for name in ("c1", "c3", "c4", "c4b"):
+        p, o, desc = pr.config(name)
+        n = len(p.d)
+        if hasattr(p.delta, "rowptr"):
+            delta = P.CsrMatrix(n, torch.as_tensor(p.delta.rowptr, device=dev), torch.as_tensor(p.delta.cols, device=dev),
+                                torch.as_tensor(p.delta.vals, device=dev))
+        else:
+            delta = torch.as_tensor(p.delta, device=dev)
+        pd = P.PartitionedProblem(torch.as_tensor(p.d, device=dev), delta, p.lam)
+        single = name.startswith("c4")
+        plan = P.Plan(pd, single=single, row=n - 1, ctx=ctx)
+        plan.begin()
+        plan.steps(3)
+        kms = plan.steps(20, time_kernel=True) / 20
+        plan.close()
+        rec = {"workload": desc, "kernel_ms": kms}
+        if single:
+            byts = 12 * p.delta.nnz + 8 * (n + 1) + 24 * n
+            rec.update(kernel="single_u16w_kernel (K3)", bound="hbm", gbs=byts / (kms * 1e-3) / 1e9,
+                       frac=byts / (kms * 1e-3) / 1e9 / hbm, algorithmic_bytes=byts)
+        elif hasattr(p.delta, "rowptr"):
+            byts = 16 * n * n + 12 * p.delta.nnz + 8 * (n + 1) + 8 * n
+            rec.update(kernel="csr_step_kernel (K2)", bound="hbm", gbs=byts / (kms * 1e-3) / 1e9,
+                       frac=byts / (kms * 1e-3) / 1e9 / hbm, algorithmic_bytes=byts)
+        else:
+            tf = 2.0 * n ** 3 / (kms * 1e-3) / 1e12
+            rec.update(kernel="dense_step_kernel (K1)", bound="tensor", tflops=tf, frac=tf / fp64_peak)
+        call = (lambda: P.dominant_eigenpair(pd, P.IterationOptions(**o), ctx=ctx)) if single else \
+            (lambda: P.iterate_full(pd, P.IterationOptions(**o), ctx=ctx))
+        call()
+        best, r = None, None
+        for _ in range(3):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            r = call()
+            torch.cuda.synchronize()
+            dt = (time.perf_counter() - t0) * 1e3
+            best = dt if best is None else min(best, dt)
+        rec.update(status=P.to_string(r.status), iterations=r.iterations, solve_wall_ms=best,
+                   solve_device_ms=r.device_ms)
+        out[name] = rec
+        del pd, delta
+    out["how"] = ("kernel: CUDA events around each of 20 fixed steps on the solver stream; solve: public call, "
+                  "device-resident inputs, warm, best of 3")
+    return out
+
+
 def spawn(args):
     """--gpus N outside torchrun: re-launch this script with N ranks (one per GPU)."""
     import socket
@@ -564,6 +625,13 @@ def main():
         ttc = {wl: {"status": P.to_string(r.status), "iterations": r.iterations,
                     "wall_ms_with_host_copies": wall / e2e_calls * 1e3}}
 
+    # N = 1: the other BASELINE configs in the same run (kernel per step with its
+    # roofline fraction, and time to the terminal status through the public call
+    # with device-resident inputs), so the driver's record covers every config
+    others = None
+    if world == 1 and wl == "c2" and not args.size:
+        others = other_configs(P, torch, ctx, local, peak)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -593,6 +661,7 @@ def main():
                          "flop_per_launch": flop_launch,
                          "peak_source": "FP64 DMMA probe measured in this run (MEASURED_PEAKS.json has no FP64 entry)"},
             "e2e": e2e, "time_to_converge": ttc, "cpu_baseline": cpu, "clocks": clk, "gpu_launches": int(launches),
+            "other_configs": others,
             "tflops_per_step": 2.0 * n ** 3 / (ms_per_step * 1e-3) / 1e12,
             "input_gen_s": t_gen,
         }
