@@ -674,11 +674,11 @@ int dense_tile_m(int cfg) { return cfg == 0 ? CfgSmall::BM : (cfg == 1 ? CfgBig:
 // tiles (7 units): 1.03 vs 1.15 ms per step (profiles/r01e_shard_times.txt).
 // DPT_DENSE_CFG=0/1/2 forces a configuration.
 int dense_cfg_for(int64_t n, int64_t rows) {
-  if (n < 2048) return 0;
   if (const char* e = getenv("DPT_DENSE_CFG")) {
     const int v = atoi(e);
     return (v == 0 || v == 1 || v == 2) ? v : 2;
   }
+  if (n < 2048) return 0;
   static int sms = 0;
   if (!sms) {
     int dev = 0;

@@ -44,3 +44,51 @@ def test_shim_matches_reference_callers():
             assert r == g, (k, r, g)
         else:
             assert abs(r - g) <= 1e-9 * max(1.0, abs(r)), (k, r, g)
+
+
+AREF = os.path.join(ROOT, "build", "accept_ref")
+AB200 = os.path.join(ROOT, "build", "accept_b200")
+
+
+@pytest.mark.skipif(not (os.path.exists(AREF) and os.path.exists(AB200)),
+                    reason="build/accept_* not built (needs /root/reference at build time)")
+def test_acceptance_criteria_match_reference():
+    """tests/cpp/accept.cpp: the reference's acceptance criteria 1, 2, 5, 6, 8, 9
+    (proj/tests/acceptance.cpp) at their own sizes -- 200 + 100 small complex
+    solves, the N = 50 ensemble, the N = 100 oscillator comparison and the
+    N = 100000 sparse dominant pair -- through the drop-in on the GPU, against
+    the same program linked with the reference's dpt.cpp, plus the criteria's
+    own thresholds on the GPU numbers."""
+    ref, got = run(AREF), run(AB200)
+    assert ref.keys() == got.keys()
+    for k, rv in ref.items():
+        gv = got[k]
+        if k.endswith(".status") or k == "done":
+            assert gv == rv, k
+            continue
+        r, g = float(rv), float(gv)
+        if k.endswith("iterations") or k.endswith(".k_d") or k.endswith(".k_rs"):
+            assert abs(r - g) <= 1, (k, r, g)
+        elif k.endswith("converged") or k.endswith("evaluated") or k.endswith(".row"):
+            assert r == g, (k, r, g)
+        elif k.endswith("defect") or k.endswith("residual") or k.endswith("error"):
+            assert g <= max(10.0 * r, 1e-10), (k, r, g)  # quality figures: thresholds, below
+        else:  # eigenvalue sums (n <= 50 terms), eigenvalues, vector entries
+            assert abs(r - g) <= 1e-9 * max(1.0, abs(r)), (k, r, g)
+    f = {k: float(v) for k, v in got.items() if not k.endswith(".status") and k != "done"}
+    # criterion 1: >= 195 evaluated, all converged, worst eigenpair defect < 1e-10
+    assert f["c1.evaluated"] >= 195 and f["c1.n_converged"] == f["c1.evaluated"] and f["c1.worst_defect"] < 1e-10
+    # criterion 2: all converged, closed-form eigenvalues to 1e-10, series converges iff lambda < 0.5
+    assert f["c2.worst_closed_form_error"] < 1e-10
+    for lam in ("0.10", "0.30", "0.45", "0.60", "0.80"):
+        assert got[f"c2[{lam}].status"] == "Converged"
+        assert f[f"c2[{lam}].rs_converged"] == (1.0 if float(lam) < 0.5 else 0.0)
+    # criterion 5: the iteration converges inside and outside, the series only inside and later
+    assert f["c5.inside.d_converged"] == 1 and f["c5.inside.rs_converged"] == 1
+    assert f["c5.inside.k_rs"] > f["c5.inside.k_d"]
+    assert f["c5.outside.d_converged"] == 1 and f["c5.outside.rs_converged"] == 0
+    # criterion 8: all 100 converge below the coupling bound
+    assert f["c8.n_converged"] == 100
+    # criterion 9: Converged within 20 iterations, residual < 1e-10, real eigenvalue
+    assert got["c9.status"] == "Converged" and f["c9.iterations"] <= 20
+    assert f["c9.residual"] < 1e-10 and abs(f["c9.eig.im"]) < 1e-12
