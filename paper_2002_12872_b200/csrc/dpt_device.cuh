@@ -210,6 +210,15 @@ __device__ __forceinline__ double2 lds128(uint32_t addr) {
   return v;
 }
 
+// 8-byte shared-memory load from a 32-bit shared address (LDS.64 with an
+// immediate offset; the address is data-dependent at every use, so the load
+// cannot move above the barrier that publishes the data).
+__device__ __forceinline__ double lds64(uint32_t addr) {
+  double v;
+  asm("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(addr));
+  return v;
+}
+
 // D(8x8) += A(8x4, row) * B(4x8, col), FP64 tensor core (SASS DMMA.8x8x4).
 // Fragments: a = A[lane>>2][lane&3], b = B[lane&3][lane>>2],
 // d = {D[lane>>2][2(lane&3)], D[lane>>2][2(lane&3)+1]}.

@@ -41,6 +41,11 @@ struct DevSell {
   const int32_t* perm;      // [n] shared-memory position of column k (bank balance), null = identity
   const int32_t* inv;       // [npad] column at position p (-1 = unused), null = identity
   int64_t npad;             // staged row length in positions (>= n)
+  // K2's shared-memory kernel reads a packed copy (launch_sell_pack), null when not built:
+  const uint16_t* cols16;   // [padded] the columns as 16-bit positions, trip-major: entry (step q, lane L)
+                            //          of a slice at slice_off + (q / 4) * 128 + 4 L + (q & 3); 0xffff = bubble
+  const int32_t* lane_pos;  // [nslices * 32] position of each lane's own column j (perm[j], or j), -1 = padding
+  const double* lane_theta; // [nslices * 32] theta[j] of each lane's column
 };
 int csr_step_ntiles(int64_t rows, int64_t n);
 int csr_ntn(int64_t n);
@@ -131,6 +136,9 @@ cudaError_t launch_sell_fill(const int64_t* rp, const int32_t* cl, const double*
                              int32_t* s_cols, double* s_vals, cudaStream_t st);
 // column relabelling for bank balance (real K2): pos / inv permutation, padded staged-row length
 size_t relabel_smem_bytes(int64_t nslices);
+cudaError_t launch_sell_pack(const int32_t* s_cols, const int64_t* off, int64_t nslices, const int32_t* lane_col,
+                             const int32_t* perm, const double* theta, uint16_t* cols16, int32_t* lane_pos,
+                             double* lane_theta, cudaStream_t st);
 cudaError_t launch_relabel(const int64_t* rp, const int32_t* cl, int64_t n, int64_t nnz, int64_t nslices,
                            const int64_t* slot_of, int cap, int passes, int32_t* scratch, int32_t* bank, int32_t* pos,
                            int32_t* inv, int64_t npad_alloc, int32_t* npad_out, cudaStream_t st);

@@ -438,6 +438,45 @@ cudaError_t launch_sell_fill(const int64_t* rp, const int32_t* cl, const double*
   return cudaGetLastError();
 }
 
+namespace {
+// Packed copy for K2's shared-memory kernel: 16-bit positions, four steps of a
+// lane adjacent (one 8-byte load per lane per trip instead of four 4-byte
+// ones), and the per-lane epilogue constants (the position and level of the
+// lane's own column j) in slice order, so the epilogue reads them coalesced
+// instead of gathering perm[j] / theta[j].  One warp per slice.
+__global__ void __launch_bounds__(256)
+    sell_pack_kernel(const int32_t* __restrict__ s_cols, const int64_t* __restrict__ off, int64_t nslices,
+                     const int32_t* __restrict__ lane_col, const int32_t* __restrict__ perm,
+                     const double* __restrict__ theta, uint16_t* cols16, int32_t* lane_pos, double* lane_theta) {
+  const int lane = threadIdx.x & 31;
+  const int64_t sl = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (sl >= nslices) return;
+  const int32_t j = lane_col[sl * 32 + lane];
+  lane_pos[sl * 32 + lane] = j < 0 ? -1 : (perm ? perm[j] : j);
+  lane_theta[sl * 32 + lane] = j < 0 ? 0.0 : theta[j];
+  const int64_t o = off[sl];
+  const int64_t width = (off[sl + 1] - o) >> 5;  // multiple of kSellPad = 4
+  uint2* dst = reinterpret_cast<uint2*>(cols16) + (o >> 2) + lane;
+  for (int64_t q0 = 0; q0 < width; q0 += 4) {
+    uint32_t c[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) c[u] = uint32_t(s_cols[o + (q0 + u) * 32 + lane]) & 0xffffu;  // -1 -> 0xffff
+    dst[(q0 >> 2) * 32] = make_uint2(c[0] | (c[1] << 16), c[2] | (c[3] << 16));
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_sell_pack(const int32_t* s_cols, const int64_t* off, int64_t nslices, const int32_t* lane_col,
+                             const int32_t* perm, const double* theta, uint16_t* cols16, int32_t* lane_pos,
+                             double* lane_theta, cudaStream_t st) {
+  const int64_t blocks = (nslices * 32 + 255) / 256;
+  if (blocks > 0)
+    sell_pack_kernel<<<unsigned(blocks), 256, 0, st>>>(s_cols, off, nslices, lane_col, perm, theta, cols16, lane_pos,
+                                                       lane_theta);
+  return cudaGetLastError();
+}
+
 size_t relabel_smem_bytes(int64_t nslices) { return size_t(2 * nslices) * 16 * 4; }
 
 cudaError_t launch_relabel(const int64_t* rp, const int32_t* cl, int64_t n, int64_t nnz, int64_t nslices,

@@ -656,12 +656,13 @@ struct DevProblem {
   DBuf u16c_cols, u16c_vals;  // complex uniform-16: trip-major copy (complex_steps.cu)
   DBuf s_cols, s_vals, s_off, s_lcol, s_llen, s_pos;  // SELL-32 image (K2)
   DBuf s_perm, s_inv;                                 // column relabelling (bank balance), empty = identity
+  DBuf s_cols16, s_lpos, s_ltheta;                    // packed copy for K2's shared-memory kernel (launch_sell_pack)
   int64_t nslices = 0, s_npad = 0;
   DevCsr csr() const { return DevCsr{rowptr.as<int64_t>(), cols.as<int32_t>(), vals.as<double>(), nnz}; }
   DevSell sell() const {
     return DevSell{s_cols.as<int32_t>(), s_vals.as<double>(), s_off.as<int64_t>(), s_lcol.as<int32_t>(),
                    s_llen.as<int32_t>(), s_pos.as<int64_t>(), nslices, s_perm.as<int32_t>(), s_inv.as<int32_t>(),
-                   s_npad};
+                   s_npad, s_cols16.as<uint16_t>(), s_lpos.as<int32_t>(), s_ltheta.as<double>()};
   }
 };
 
@@ -725,6 +726,14 @@ void build_sell_device(DevProblem& dp, cudaStream_t st, dpt_error_info* err) {
                       dp.s_lcol.as<int32_t>(), G, sched, dp.s_perm.as<int32_t>(), dp.s_off.as<int64_t>(),
                       dp.s_cols.as<int32_t>(),
                       dp.s_vals.as<double>(), st));
+  if (!dp.cplx && csr_staged_cols_max(n) > 0) {  // real rows that fit shared memory: positions < 65535
+    dalloc(dp.s_cols16, size_t(alloc) * 2, err);
+    dalloc(dp.s_lpos, size_t(ns * 32) * 4, err);
+    dalloc(dp.s_ltheta, size_t(ns * 32) * 8, err);
+    CK(launch_sell_pack(dp.s_cols.as<int32_t>(), dp.s_off.as<int64_t>(), ns, dp.s_lcol.as<int32_t>(),
+                        dp.s_perm.as<int32_t>(), dp.theta.as<double>(), dp.s_cols16.as<uint16_t>(),
+                        dp.s_lpos.as<int32_t>(), dp.s_ltheta.as<double>(), st));
+  }
   dp.nslices = ns;
 }
 
@@ -1189,7 +1198,7 @@ void drive_graph(dpt_ctx* ctx, Work& w, DevProblem& dp, Mode mode, int64_t row, 
   // address must never replay a graph holding the old one)
   for (const DBuf* b : {&dp.theta, &dp.delta, &dp.rowptr, &dp.cols, &dp.vals, &dp.dmap, &dp.u16c_cols,
                         &dp.u16c_vals, &dp.s_cols, &dp.s_vals, &dp.s_off, &dp.s_lcol, &dp.s_llen, &dp.s_pos,
-                        &dp.s_perm, &dp.s_inv})
+                        &dp.s_perm, &dp.s_inv, &dp.s_cols16, &dp.s_lpos, &dp.s_ltheta})
     key_add(key, b->p);
   for (int64_t v : {dp.n, dp.ld, dp.nnz, dp.ncol, dp.ldd, dp.nslices, dp.s_npad}) key_add(key, v);
   key_add(key, dp.lambda_im);

@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(THREADS) csr_step_kernel(DevSolve s, DevSell S
   if (s.state->done) return;
   const int jl = launch_index(s);
   extern __shared__ __align__(16) double sa[];  // [n][ST] staged rows of A_{j-1}
-  __shared__ unsigned long long next_slice;
+  __shared__ unsigned int next_slice;  // 32-bit: one ATOMS.ADD (a 64-bit shared atomicAdd is a CAS loop)
   __shared__ double red[THREADS / 32][R][2];
   __shared__ double wred[THREADS / 32][3];
   const int64_t n = s.n, ld = s.ld, rows = s.rows;
@@ -103,14 +103,17 @@ __global__ void __launch_bounds__(THREADS) csr_step_kernel(DevSolve s, DevSell S
   const double* d_in = s.dvec[(jl - 1) & 1];
   const double* __restrict__ ain = a_in + size_t(il0) * size_t(ld);  // SMEM = false: row r at ain + r * ld
 
-  if (threadIdx.x == 0) next_slice = 0ull;
+  if (threadIdx.x == 0) next_slice = 0u;
   // Staged rows are indexed by POSITION: the image's columns are positions
   // (S.perm[k] when the columns were relabelled for bank balance, else k).
   const int32_t* __restrict__ perm = S.perm;
   const int32_t* __restrict__ inv = S.inv;
   if constexpr (SMEM) {
     // all R rows of a column chunk are loaded before any is stored: R * kStageU
-    // independent loads in flight per thread (the loop is HBM-latency bound)
+    // independent loads in flight per thread (the loop is HBM-latency bound).
+    // (Filling by position instead -- conflict-free stores, reads through inv --
+    // was measured: the relabelled columns of 32 consecutive positions spread
+    // over ~12 lines, 17 M more global wavefronts for 8.5 M fewer shared ones.)
     constexpr int kStageU = R <= 3 ? 4 : 2;
     for (int64_t c0 = threadIdx.x; c0 < n; c0 += kStageU * int64_t(blockDim.x)) {
       double v[kStageU][R];
@@ -131,8 +134,12 @@ __global__ void __launch_bounds__(THREADS) csr_step_kernel(DevSolve s, DevSell S
     }
   }
   __syncthreads();
+  // 32-bit shared address of the staged rows, kept in a register: left to
+  // itself ptxas rematerialises it at every gather (S2R SR_CgaCtaId + LEA)
+  uint32_t sab = smem_u32(sa);
+  asm volatile("mov.u32 %0, %0;" : "+r"(sab));
   auto A = [&](int r, int64_t p) -> double {  // element at position p of staged row r
-    if constexpr (SMEM) return sa[size_t(p) * ST + r];
+    if constexpr (SMEM) return lds64(sab + uint32_t(p) * uint32_t(ST * 8) + uint32_t(r * 8));
     else return ain[size_t(r < nr ? r : 0) * size_t(ld) + size_t(inv ? int64_t(__ldg(inv + p)) : p)];
   };
   // per-row constants of the staged rows live in shared memory (registers go
@@ -159,39 +166,63 @@ __global__ void __launch_bounds__(THREADS) csr_step_kernel(DevSolve s, DevSell S
   // which warp computes a column.
   while (true) {
     int64_t sl = 0;
-    if (lane == 0) sl = atomicAdd(&next_slice, 1);
+    if (lane == 0) sl = int64_t(atomicAdd(&next_slice, 1u));
     sl = __shfl_sync(0xffffffffu, sl, 0);
     if (sl >= S.nslices) break;
     const int64_t t = sl * 32 + lane;
     const int32_t j = S.lane_col[t];
     const int64_t off = S.slice_off[sl];
     const int32_t width = int32_t((S.slice_off[sl + 1] - off) >> 5);  // multiple of kCsrU
-    const int32_t* __restrict__ sc = S.cols + off + lane;
     const double* __restrict__ sv = S.vals + off + lane;
     double p[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) p[r] = 0.0;
-    for (int32_t q0 = 0; q0 < width; q0 += kCsrU) {
-      int32_t c[kCsrU];
-      double v[kCsrU];
+    if constexpr (SMEM) {
+      // packed image (launch_sell_pack): the four 16-bit positions of a trip in
+      // one 8-byte load per lane; 0xffff = bubble
+      static_assert(kCsrU == 4, "the packed image holds four steps per trip");
+      const uint2* __restrict__ sc16 = reinterpret_cast<const uint2*>(S.cols16) + (off >> 2) + lane;
+      for (int32_t q0 = 0; q0 < width; q0 += kCsrU) {
+        const uint2 cc = __ldg(sc16 + (q0 >> 2) * 32);
+        uint32_t c[kCsrU] = {cc.x & 0xffffu, cc.x >> 16, cc.y & 0xffffu, cc.y >> 16};
+        double v[kCsrU];
 #pragma unroll
-      for (int u = 0; u < kCsrU; ++u) {
-        c[u] = __ldg(sc + (q0 + u) * 32);
-        v[u] = __ldg(sv + (q0 + u) * 32);
+        for (int u = 0; u < kCsrU; ++u) v[u] = __ldg(sv + (q0 + u) * 32);
+        double g[kCsrU][R];
+#pragma unroll
+        for (int u = 0; u < kCsrU; ++u)
+#pragma unroll
+          for (int r = 0; r < R; ++r) g[u][r] = c[u] != 0xffffu ? A(r, c[u]) : 0.0;  // bubbles issue no load
+#pragma unroll
+        for (int u = 0; u < kCsrU; ++u)
+#pragma unroll
+          for (int r = 0; r < R; ++r) p[r] = __fma_rn(v[u], g[u][r], p[r]);
       }
-      double g[kCsrU][R];
+    } else {
+      const int32_t* __restrict__ sc = S.cols + off + lane;
+      for (int32_t q0 = 0; q0 < width; q0 += kCsrU) {
+        int32_t c[kCsrU];
+        double v[kCsrU];
 #pragma unroll
-      for (int u = 0; u < kCsrU; ++u)
+        for (int u = 0; u < kCsrU; ++u) {
+          c[u] = __ldg(sc + (q0 + u) * 32);
+          v[u] = __ldg(sv + (q0 + u) * 32);
+        }
+        double g[kCsrU][R];
 #pragma unroll
-        for (int r = 0; r < R; ++r) g[u][r] = c[u] >= 0 ? A(r, c[u]) : 0.0;  // bubbles issue no load
+        for (int u = 0; u < kCsrU; ++u)
 #pragma unroll
-      for (int u = 0; u < kCsrU; ++u)
+          for (int r = 0; r < R; ++r) g[u][r] = c[u] >= 0 ? A(r, c[u]) : 0.0;  // bubbles issue no load
 #pragma unroll
-        for (int r = 0; r < R; ++r) p[r] = __fma_rn(v[u], g[u][r], p[r]);
+        for (int u = 0; u < kCsrU; ++u)
+#pragma unroll
+          for (int r = 0; r < R; ++r) p[r] = __fma_rn(v[u], g[u][r], p[r]);
+      }
     }
     if (j >= 0) {
-      const double tj = s.theta[j];
-      const int64_t pj = perm ? int64_t(__ldg(perm + j)) : j;  // position of column j
+      // the lane's own column: level and position, in slice order when packed
+      const double tj = SMEM ? __ldg(S.lane_theta + t) : s.theta[j];
+      const int64_t pj = SMEM ? int64_t(__ldg(S.lane_pos + t)) : (perm ? int64_t(__ldg(perm + j)) : j);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         if (r >= nr) break;
@@ -285,6 +316,7 @@ cudaError_t launch_csr_step(const DevSolve& s, const DevSell& d, cudaStream_t st
     csr_step_kernel<1, false><<<grid, kCsrThreads, 0, st>>>(s, d);
     return cudaGetLastError();
   }
+  if (!d.cols16 || !d.lane_pos || !d.lane_theta) return cudaErrorInvalidValue;  // the packed image was not built
 #define DPT_CSR_CASE(RR)                                                                          \
   case RR: {                                                                                      \
     static DeviceAttrOnce attr;                                                                   \
