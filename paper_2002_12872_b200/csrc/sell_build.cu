@@ -31,6 +31,7 @@ namespace {
 
 constexpr int kWin = 256;
 constexpr int kSellPad = 4;
+constexpr int kBankStage = 124;  // entries per row whose banks sell_free_kernel stages in shared memory
 
 // stable descending rank of each row's length inside its 256-row window
 __global__ void __launch_bounds__(kWin) sell_perm_kernel(const int64_t* __restrict__ rp, int64_t n,
@@ -139,6 +140,27 @@ __global__ void __launch_bounds__(256)
   // the image holds shared-memory positions: perm[k] when the columns were
   // relabelled for bank balance (sell_relabel_kernel), else k
   auto colpos = [&](int64_t q) -> int32_t { return perm ? perm[cl[q]] : cl[q]; };
+  // The bank of every entry of the slice's rows, staged in shared memory by the
+  // whole warp (row r's entries loaded by consecutive lanes: coalesced, and the
+  // 32 rows' loads are independent).  The schedule below walks a row's entries
+  // bank by bank; reading each bank through cl -> perm from global memory made
+  // every step a chain of dependent L2 round trips (c3: 0.58 ms per pass).
+  // Rows longer than the stage keep the global reads.  Same schedule either way.
+  __shared__ uint8_t sbank[8][32][kBankStage + 4];  // [warp][row][entry], padded: conflict-free per-lane reads
+  const int wib = (threadIdx.x >> 5) & 7;
+  const bool use_stage = __all_sync(0xffffffffu, len <= kBankStage);
+  if (use_stage) {
+#pragma unroll 8
+    for (int r = 0; r < 32; ++r) {  // unrolled: the rows' load chains (cl -> perm) overlap
+      const int64_t beg_r = __shfl_sync(0xffffffffu, beg, r);
+      const int len_r = __shfl_sync(0xffffffffu, len, r);
+      for (int q = lane; q < len_r; q += 32) sbank[wib][r][q] = uint8_t(uint32_t(colpos(beg_r + q)) & gm);
+    }
+    __syncwarp();
+  }
+  auto bankof = [&](int q) -> int {
+    return use_stage ? int(sbank[wib][lane][q]) : int(uint32_t(colpos(beg + q)) & gm);
+  };
   int cnt[16], pos[16];
 #pragma unroll
   for (int b = 0; b < 16; ++b) {
@@ -146,7 +168,7 @@ __global__ void __launch_bounds__(256)
     pos[b] = len;
   }
   for (int q = 0; q < len; ++q) {
-    const int bk = int(uint32_t(colpos(beg + q)) & gm);
+    const int bk = bankof(q);
 #pragma unroll
     for (int b = 0; b < 16; ++b)
       if (b == bk) {
@@ -171,12 +193,22 @@ __global__ void __launch_bounds__(256)
           }
       }
       if (!__any_sync(0xffffffffu, choice >= 0)) break;
-      const int key = choice >= 0 ? ((lane & ~int(gm)) << 5) + choice : 4096 + lane;
-      const unsigned peers = __match_any_sync(0xffffffffu, key);
-      const unsigned prio = choice >= 0 ? unsigned(rem) * 32u + unsigned(31 - lane) : 0u;
-      const unsigned top = __reduce_max_sync(peers, prio);
+      // the top bidder of each contested bank: every lane compares its bid with
+      // the G - 1 others of its group (xor-shuffles stay inside the aligned
+      // group).  Priorities are distinct (the lane is part of them), so exactly
+      // one bidder per bank wins.  (__match_any_sync + a masked
+      // __reduce_max_sync did the same at ~2000 cycles per round: both
+      // serialise over the distinct keys / masks of the warp.)
+      const unsigned remc = rem < (1 << 22) ? unsigned(rem) : (1u << 22) - 1u;  // 27-bit priority field
+      const unsigned prio = choice >= 0 ? remc * 32u + unsigned(31 - lane) : 0u;
+      const unsigned bid = choice >= 0 ? (unsigned(choice) << 27) | prio : 0xffffffffu;
+      bool top = choice >= 0;
+      for (int o = 1; o < G; ++o) {
+        const unsigned other = __shfl_xor_sync(0xffffffffu, bid, o);
+        if (other != 0xffffffffu && (other >> 27) == unsigned(choice) && (other & 0x7ffffffu) > prio) top = false;
+      }
       unsigned won = 0;
-      if (choice >= 0 && prio == top) {
+      if (top) {
         mybank = choice;
         won = 1u << choice;
       }
@@ -199,7 +231,7 @@ __global__ void __launch_bounds__(256)
       --rem;
       if (left > 0) {
         int q2 = q + 1;
-        while (int(uint32_t(colpos(beg + q2)) & gm) != mybank) ++q2;
+        while (bankof(q2) != mybank) ++q2;
 #pragma unroll
         for (int b = 0; b < 16; ++b)
           if (b == mybank) pos[b] = q2;
@@ -304,7 +336,12 @@ __global__ void relabel_fill_kernel(const int64_t* __restrict__ rp, const int32_
 }
 
 constexpr int kRelabelBatch = 64;
+constexpr int kRelabelStage = 4096;  // group-list entries of a batch staged in shared memory (2 x 16 KB)
 // One block.  L lives in shared memory: ng x 16 int32 (the caller checks it fits).
+// The group lists of a batch's columns are one contiguous range of cgroups,
+// staged in shared memory (double-buffered, see the batch loop); a batch whose
+// lists exceed the stage reads them from global memory.  Same arithmetic in
+// the same order as the unstaged kernel.
 __global__ void __launch_bounds__(1024) relabel_kernel(const int32_t* __restrict__ start,
                                                        const int32_t* __restrict__ cgroups, int64_t n, int ng,
                                                        int cap, int passes, int32_t* bank, int32_t* pos,
@@ -312,6 +349,8 @@ __global__ void __launch_bounds__(1024) relabel_kernel(const int32_t* __restrict
   extern __shared__ int32_t L[];  // [ng][16]
   __shared__ int32_t size[16];
   __shared__ int32_t prop[kRelabelBatch], acc[kRelabelBatch], oldb[kRelabelBatch];
+  __shared__ int32_t stage[2][kRelabelStage];
+  __shared__ int32_t sstart[2][kRelabelBatch + 1], sbk[2][kRelabelBatch];
   const int tid = threadIdx.x, c = tid >> 4, t = tid & 15;
   for (int64_t e = tid; e < int64_t(ng) * 16; e += blockDim.x) L[e] = 0;
   if (tid < 16) size[tid] = 0;
@@ -322,54 +361,105 @@ __global__ void __launch_bounds__(1024) relabel_kernel(const int32_t* __restrict
     for (int32_t q = start[k]; q < start[k + 1]; ++q) atomicAdd(&L[cgroups[q] * 16 + int(k & 15)], 1);
   }
   __syncthreads();
-  for (int pass = 0; pass < passes; ++pass) {
-    for (int64_t b0 = 0; b0 < n; b0 += kRelabelBatch) {
-      const int64_t k = b0 + c;
-      const bool ok = k < n;
-      const int32_t q0 = ok ? start[k] : 0, q1 = ok ? start[k + 1] : 0;
-      const int b = ok ? bank[k] : 0;
-      int32_t sum = 0;
-      for (int32_t q = q0; q < q1; ++q) sum += L[cgroups[q] * 16 + t];
-      const int32_t sb = __shfl_sync(0xffffffffu, sum, b, 16);
-      // move delta of sum L^2 (exact up to repeated groups): 2 (S_t - S_b) + 2 m
-      int32_t d = (t == b || !ok || q1 == q0) ? 0 : 2 * (sum - sb) + 2 * (q1 - q0);
-      int bt = t;
-      for (int o = 8; o > 0; o >>= 1) {  // argmin over the 16 targets, ties -> lower bank
-        const int32_t d2 = __shfl_xor_sync(0xffffffffu, d, o, 16);
-        const int bt2 = __shfl_xor_sync(0xffffffffu, bt, o, 16);
-        if (d2 < d || (d2 == d && bt2 < bt)) {
-          d = d2;
-          bt = bt2;
-        }
+  // Batches run strictly one after another (each sees the loads the previous one
+  // left), so a batch's global reads -- its columns' list bounds, banks and
+  // group lists -- are a chain of L2 round trips on the critical path.  They
+  // are software-pipelined: while batch i is evaluated from shared memory,
+  // every thread holds batch i + 1's values in registers (the next lists start
+  // where this batch's end, so their address needs no lookup) and parks them in
+  // the other buffer before the closing barrier.
+  const int64_t nbp = (n + kRelabelBatch - 1) / kRelabelBatch;  // batches per pass
+  const int64_t nbt = nbp * passes;
+  const bool pipelined = nbp > 1;  // one batch per pass: the next batch re-reads what this one writes
+  const int32_t total = start[n];
+  if (tid <= kRelabelBatch) sstart[0][tid] = start[tid < n ? tid : n];
+  if (tid < kRelabelBatch) sbk[0][tid] = tid < n ? bank[tid] : 0;
+  for (int32_t q = tid; q < kRelabelStage && q < total; q += blockDim.x) stage[0][q] = cgroups[q];
+  __syncthreads();
+  for (int64_t it = 0; it < nbt; ++it) {
+    const int cur = int(it & 1);
+    const int64_t b0 = (it % nbp) * kRelabelBatch;
+    const int64_t k = b0 + c;
+    const bool ok = k < n;
+    const int32_t q0 = ok ? sstart[cur][c] : 0, q1 = ok ? sstart[cur][c + 1] : 0;
+    const int b = ok ? sbk[cur][c] : 0;
+    const int64_t kcnt = n - b0 < kRelabelBatch ? n - b0 : kRelabelBatch;
+    const int32_t s0 = sstart[cur][0], s1 = sstart[cur][kcnt];  // the batch's lists: cgroups[s0, s1)
+    // ---- prefetch of the next batch (registers) ----
+    const bool more = it + 1 < nbt;
+    const int64_t nb0 = more ? ((it + 1) % nbp) * kRelabelBatch : 0;
+    const int32_t ns0 = nb0 == 0 ? 0 : s1;
+    int32_t pre[kRelabelStage / 1024];
+    int32_t pstart = 0, pbank = 0;
+    if (more && pipelined) {
+#pragma unroll
+      for (int u = 0; u < kRelabelStage / 1024; ++u) {
+        const int32_t q = ns0 + tid + u * 1024;
+        pre[u] = q < total ? cgroups[q] : 0;
       }
+      if (tid <= kRelabelBatch) pstart = start[nb0 + tid < n ? nb0 + tid : n];
+      if (tid < kRelabelBatch) pbank = nb0 + tid < n ? bank[nb0 + tid] : 0;
+    }
+    // ---- evaluate the batch ----
+    const bool staged = s1 - s0 <= kRelabelStage;  // block-uniform
+    const int32_t* __restrict__ cg = staged ? stage[cur] : cgroups;  // entry q of the lists at cg[q - cofs]
+    const int32_t cofs = staged ? s0 : 0;
+    int32_t sum = 0;
+    for (int32_t q = q0; q < q1; ++q) sum += L[cg[q - cofs] * 16 + t];
+    const int32_t sb = __shfl_sync(0xffffffffu, sum, b, 16);
+    // move delta of sum L^2 (exact up to repeated groups): 2 (S_t - S_b) + 2 m
+    int32_t d = (t == b || !ok || q1 == q0) ? 0 : 2 * (sum - sb) + 2 * (q1 - q0);
+    int bt = t;
+    for (int o = 8; o > 0; o >>= 1) {  // argmin over the 16 targets, ties -> lower bank
+      const int32_t d2 = __shfl_xor_sync(0xffffffffu, d, o, 16);
+      const int bt2 = __shfl_xor_sync(0xffffffffu, bt, o, 16);
+      if (d2 < d || (d2 == d && bt2 < bt)) {
+        d = d2;
+        bt = bt2;
+      }
+    }
+    if (t == 0) {
+      prop[c] = d < 0 ? bt : -1;
+      oldb[c] = b;
+    }
+    __syncthreads();
+    {  // capacity, in column order, against the sizes before the batch: the 16
+       // threads of a column count the earlier columns proposing the same bank
+      const int a0 = prop[c];
+      int ahead = 0;
+      for (int c2 = t; c2 < c; c2 += 16) ahead += (a0 >= 0 && prop[c2] == a0) ? 1 : 0;
+      for (int o = 8; o > 0; o >>= 1) ahead += __shfl_xor_sync(0xffffffffu, ahead, o, 16);
       if (t == 0) {
-        prop[c] = d < 0 ? bt : -1;
-        oldb[c] = b;
-      }
-      __syncthreads();
-      if (t == 0) {  // capacity, in column order, against the sizes before the batch
-        int a = prop[c];
-        if (a >= 0) {
-          int ahead = 0;
-          for (int c2 = 0; c2 < c; ++c2) ahead += prop[c2] == a ? 1 : 0;
-          if (size[a] + ahead >= cap) a = -2;
-        }
+        int a = a0;
+        if (a >= 0 && size[a] + ahead >= cap) a = -2;
         acc[c] = a;
       }
-      __syncthreads();
-      const int nb = acc[c];
-      if (nb >= 0) {
-        for (int32_t q = q0 + t; q < q1; q += 16) {
-          const int32_t g = cgroups[q];
-          atomicSub(&L[g * 16 + oldb[c]], 1);
-          atomicAdd(&L[g * 16 + nb], 1);
-        }
-        if (t == 0) {
-          atomicSub(&size[oldb[c]], 1);
-          atomicAdd(&size[nb], 1);
-          bank[k] = nb;
-        }
+    }
+    __syncthreads();
+    const int nb = acc[c];
+    if (nb >= 0) {
+      for (int32_t q = q0 + t; q < q1; q += 16) {
+        const int32_t g = cg[q - cofs];
+        atomicSub(&L[g * 16 + oldb[c]], 1);
+        atomicAdd(&L[g * 16 + nb], 1);
       }
+      if (t == 0) {
+        atomicSub(&size[oldb[c]], 1);
+        atomicAdd(&size[nb], 1);
+        bank[k] = nb;
+      }
+    }
+    if (more && pipelined) {  // park the prefetched batch in the other buffer
+#pragma unroll
+      for (int u = 0; u < kRelabelStage / 1024; ++u) stage[cur ^ 1][tid + u * 1024] = pre[u];
+      if (tid <= kRelabelBatch) sstart[cur ^ 1][tid] = pstart;
+      if (tid < kRelabelBatch) sbk[cur ^ 1][tid] = pbank;
+    }
+    __syncthreads();
+    if (more && !pipelined) {  // n <= 64: the same columns again, reloaded after this batch's writes
+      if (tid <= kRelabelBatch) sstart[cur ^ 1][tid] = start[tid < n ? tid : n];
+      if (tid < kRelabelBatch) sbk[cur ^ 1][tid] = tid < n ? bank[tid] : 0;
+      for (int32_t q = tid; q < kRelabelStage && q < total; q += blockDim.x) stage[cur ^ 1][q] = cgroups[q];
       __syncthreads();
     }
   }
@@ -477,7 +567,7 @@ cudaError_t launch_sell_pack(const int32_t* s_cols, const int64_t* off, int64_t 
   return cudaGetLastError();
 }
 
-size_t relabel_smem_bytes(int64_t nslices) { return size_t(2 * nslices) * 16 * 4; }
+size_t relabel_smem_bytes(int64_t nslices) { return size_t(2 * nslices) * 16 * 4 + 2 * kRelabelStage * 4 + 2048; }  // dynamic L + static stages
 
 cudaError_t launch_relabel(const int64_t* rp, const int32_t* cl, int64_t n, int64_t nnz, int64_t nslices,
                            const int64_t* slot_of, int cap, int passes, int32_t* scratch, int32_t* bank, int32_t* pos,
@@ -493,9 +583,9 @@ cudaError_t launch_relabel(const int64_t* rp, const int32_t* cl, int64_t n, int6
   relabel_count_kernel<<<blocks, 256, 0, st>>>(rp, cl, n, ccount);
   relabel_scan_kernel<<<1, 1024, 0, st>>>(ccount, n, start);
   relabel_fill_kernel<<<blocks, 256, 0, st>>>(rp, cl, n, slot_of, start, cfill, cgroups);
-  const size_t smem = relabel_smem_bytes(nslices);
+  const size_t smem = size_t(2 * nslices) * 16 * 4;  // L only: the stage is static
   static DeviceAttrOnce attr;
-  attr([] { cudaFuncSetAttribute(relabel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024); });
+  attr([] { cudaFuncSetAttribute(relabel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 188 * 1024); });  // + ~35 KB static
   relabel_kernel<<<1, 1024, smem, st>>>(start, cgroups, n, int(2 * nslices), cap, passes, bank, pos, inv, npad_alloc,
                                         npad_out);
   (void)nnz;

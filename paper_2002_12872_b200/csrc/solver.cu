@@ -701,8 +701,14 @@ void build_sell_device(DevProblem& dp, cudaStream_t st, dpt_error_info* err) {
     dalloc(bankb, size_t(n) * 4, err);
     dalloc(dp.s_perm, size_t(n) * 4, err);
     dalloc(dp.s_inv, size_t(16 * cap) * 4, err);
+    // Local-search passes of the relabelling (DPT_SELL_PASSES = 1..9).  One pass
+    // brings c3's image from 14 384 to 12 500 steps; passes 2 and 3 reach 12 448
+    // and 12 440 (K2 1.5734 vs 1.5688 ms per step) at 0.65 ms each -- more than
+    // an 18-iteration solve gets back, so the default is one.
+    const char* ps_env = std::getenv("DPT_SELL_PASSES");
+    const int rl_passes = (ps_env && ps_env[0] >= '1' && ps_env[0] <= '9') ? ps_env[0] - '0' : 1;
     CK(launch_relabel(dp.rowptr.as<int64_t>(), dp.cols.as<int32_t>(), n, dp.nnz, ns, dp.s_pos.as<int64_t>(), int(cap),
-                      3, scratch.as<int32_t>(), bankb.as<int32_t>(), dp.s_perm.as<int32_t>(), dp.s_inv.as<int32_t>(),
+                      rl_passes, scratch.as<int32_t>(), bankb.as<int32_t>(), dp.s_perm.as<int32_t>(), dp.s_inv.as<int32_t>(),
                       16 * cap, tot.as<int32_t>() + 2, st));
   }
   CK(launch_sell_widths(dp.rowptr.as<int64_t>(), dp.cols.as<int32_t>(), ns, dp.s_lcol.as<int32_t>(), G, sched,
