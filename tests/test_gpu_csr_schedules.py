@@ -1,6 +1,7 @@
 """GPU: K2's SELL image under every schedule (0 dense packing, 1 CSR-order bank
 greedy, 2 free-order bank auction -- the default) with and without the
-bank-balancing column relabelling, on patterns that stress them: a uniform
+bank-balancing column relabelling (one and three local-search passes), on
+patterns that stress them: a uniform
 random pattern, ragged rows (empty rows, a few rows 30x longer than the rest,
 a length that is not a multiple of 32), and a pattern whose columns all fall
 into a few banks.  Each run must meet the parity bar against the reference's
@@ -91,6 +92,13 @@ def test_schedules_and_relabelling_match_reference(tmp_path, kind):
             if int(g["iterations"]) == ref.iterations and ref.status != 2:
                 assert np.max(np.abs(g["a"] - ref.a)) < 1e-9, (sched, relabel)
                 assert eig_rel_err(g["eig"], ref.eig) < 1e-10, (sched, relabel)
+    # three local-search passes of the relabelling instead of the default one (DPT_SELL_PASSES)
+    o = str(tmp_path / "s2r1p3.npz")
+    env = dict(os.environ, DPT_SELL_SCHED="2", DPT_SELL_RELABEL="1", DPT_SELL_PASSES="3")
+    subprocess.run([sys.executable, "-c", SCRIPT, f, o], cwd=ROOT, env=env, check=True, timeout=300)
+    g = np.load(o)
+    outs[("2", "1p3")] = g
+    assert int(g["status"]) == ref.status and abs(int(g["iterations"]) - ref.iterations) <= 1
     base = outs[("2", "1")]
     for key, g in outs.items():
         if int(g["iterations"]) == int(base["iterations"]) and int(base["status"]) != 2:
