@@ -1,9 +1,7 @@
 """Per-iteration device time of the row-map solve (c4 / c4b) through the
-public call with device-resident inputs, with the fold fused into K3's last
-block (default) and as a separate launch (DPT_FOLD_SPLIT=1, set by the caller),
-plus the plan-step time (K3) for reference."""
+public call with device-resident inputs, next to the plan-step time (K3 alone):
+the difference is the fold / decision / cycle pre-check of the device loop."""
 import json
-import os
 import sys
 
 sys.path.insert(0, ".")
@@ -30,6 +28,5 @@ for name in ("c4", "c4b"):
     torch.cuda.synchronize()
     kms = plan.steps(20, time_kernel=True) / 20
     plan.close()
-    print(json.dumps({"config": name, "fold_split": os.environ.get("DPT_FOLD_SPLIT", "0"),
-                      "status": P.to_string(r.status), "iterations": r.iterations, "solve_device_ms_best5": best,
+    print(json.dumps({"config": name, "status": P.to_string(r.status), "iterations": r.iterations, "solve_device_ms_best5": best,
                       "per_iteration_us": best * 1e3 / r.iterations, "plan_step_kernel_us": kms * 1e3}), flush=True)
