@@ -236,6 +236,11 @@ __device__ __forceinline__ void dense_epilogue(const DevSolve& s, double (&acc)[
   }
 }
 
+#ifndef DPT_REFILL_LAG
+#define DPT_REFILL_LAG 2
+#endif
+constexpr int kRefillLag = DPT_REFILL_LAG;  // k-tiles between a stage's consumption and its refill (0 = at once)
+
 template <class C, bool CPLX>
 __global__ void __launch_bounds__(C::THREADS, C::MINB)
     dense_step_kernel(DevSolve s, const CUtensorMap* __restrict__ amaps,
@@ -312,13 +317,21 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
     dmma_consume_stage<C>(acc, a_st, b_st, wm, wn, t, gq);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
-    if (producer && kt + C::STAGES < KT) {  // refill this stage once every warp released it
-      const int kn = kt + C::STAGES;
-      mbar_wait(&empty[st], (kt / C::STAGES) & 1);
+    // Refill, lagging kRefillLag k-tiles: the producer is lane 0 of consumer
+    // warp 0, and the stage it has just finished is still being read by the
+    // slower warps -- waiting for it here made warp 0 the straggler of every
+    // k-tile.  The stage consumed kRefillLag iterations ago has been released by
+    // everyone (or nearly), so the wait returns at once; STAGES - kRefillLag
+    // k-tiles stay in flight.  Measured on c2 (100 steps, three A/B pairs):
+    // lag 0 3.926 ms, lag 1 3.940, lag 2 3.910 / 3.929 / 3.910.
+    if (producer && kt >= kRefillLag && kt - kRefillLag + C::STAGES < KT) {
+      const int kc = kt - kRefillLag, sr = kc % C::STAGES;
+      const int kn = kc + C::STAGES;
+      mbar_wait(&empty[sr], (kc / C::STAGES) & 1);
       fence_proxy_async_smem();  // the consumers' generic reads of the stage before the async-proxy refill
-      mbar_arrive_expect_tx(&full[st], C::STAGE_BYTES);
-      tma_load_2d(sA + st * C::A_BYTES, am, &full[st], kn * C::BK, tm * C::BM);
-      tma_load_2d(sB + st * C::B_BYTES, dmap, &full[st], kn * C::BK, tn * C::BN);
+      mbar_arrive_expect_tx(&full[sr], C::STAGE_BYTES);
+      tma_load_2d(sA + sr * C::A_BYTES, am, &full[sr], kn * C::BK, tm * C::BM);
+      tma_load_2d(sB + sr * C::B_BYTES, dmap, &full[sr], kn * C::BK, tn * C::BN);
     }
     __syncwarp();
   }
