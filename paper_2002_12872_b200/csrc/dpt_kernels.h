@@ -50,6 +50,8 @@ struct DevSell {
 int csr_step_ntiles(int64_t rows, int64_t n);
 int csr_ntn(int64_t n);
 cudaError_t launch_csr_step(const DevSolve& s, const DevSell& d, cudaStream_t st);
+// launch 1 from A_0 = I without the product (sparse_step.cu); scratch >= (rows + 4) * 8 bytes; the fold reads 1 tile
+cudaError_t launch_csr_init(const DevSolve& s, const DevCsr& c, const DevSell& d, void* scratch, cudaStream_t st);
 
 // row map (single vector): z slots are [nslots][n]
 int single_mode(int dense, int uniform16);
@@ -139,6 +141,7 @@ size_t relabel_smem_bytes(int64_t nslices);
 cudaError_t launch_sell_pack(const int32_t* s_cols, const int64_t* off, int64_t nslices, const int32_t* lane_col,
                              const int32_t* perm, const double* theta, uint16_t* cols16, int32_t* lane_pos,
                              double* lane_theta, cudaStream_t st);
+cudaError_t launch_csr_order_check(const int64_t* rp, const int32_t* cl, int64_t n, int32_t* flag, cudaStream_t st);
 cudaError_t launch_relabel(const int64_t* rp, const int32_t* cl, int64_t n, int64_t nnz, int64_t nslices,
                            const int64_t* slot_of, int cap, int passes, int32_t* scratch, int32_t* bank, int32_t* pos,
                            int32_t* inv, int64_t npad_alloc, int32_t* npad_out, cudaStream_t st);

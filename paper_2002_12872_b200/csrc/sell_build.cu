@@ -557,6 +557,21 @@ __global__ void __launch_bounds__(256)
 
 }  // namespace
 
+// *flag = 1 if some row's columns are not strictly increasing (a repeated or
+// out-of-order (row, column) pair): K2 handles both, the launch-1 shortcut
+// (launch_csr_init) assumes one entry per pair.
+__global__ void csr_order_kernel(const int64_t* __restrict__ rp, const int32_t* __restrict__ cl, int64_t n, int32_t* flag) {
+  for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < n; j += int64_t(gridDim.x) * blockDim.x)
+    for (int64_t q = rp[j] + 1; q < rp[j + 1]; ++q)
+      if (cl[q] <= cl[q - 1]) *flag = 1;
+}
+
+cudaError_t launch_csr_order_check(const int64_t* rp, const int32_t* cl, int64_t n, int32_t* flag, cudaStream_t st) {
+  const int64_t b = (n + 255) / 256;
+  if (b > 0) csr_order_kernel<<<unsigned(b > 1184 ? 1184 : b), 256, 0, st>>>(rp, cl, n, flag);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_sell_pack(const int32_t* s_cols, const int64_t* off, int64_t nslices, const int32_t* lane_col,
                              const int32_t* perm, const double* theta, uint16_t* cols16, int32_t* lane_pos,
                              double* lane_theta, cudaStream_t st) {

@@ -658,6 +658,7 @@ struct DevProblem {
   DBuf s_perm, s_inv;                                 // column relabelling (bank balance), empty = identity
   DBuf s_cols16, s_lpos, s_ltheta;                    // packed copy for K2's shared-memory kernel (launch_sell_pack)
   int64_t nslices = 0, s_npad = 0;
+  int csr_strict = 0;  // every CSR row's columns strictly increase (no repeated pair): launch_csr_init applies
   DevCsr csr() const { return DevCsr{rowptr.as<int64_t>(), cols.as<int32_t>(), vals.as<double>(), nnz}; }
   DevSell sell() const {
     return DevSell{s_cols.as<int32_t>(), s_vals.as<double>(), s_off.as<int64_t>(), s_lcol.as<int32_t>(),
@@ -689,6 +690,8 @@ void build_sell_device(DevProblem& dp, cudaStream_t st, dpt_error_info* err) {
   // row then has npad >= n positions, at most what keeps K2's natural R.
   DBuf tot;
   dalloc(tot, 16, err);
+  CK(cudaMemsetAsync(tot.p, 0, 16, st));
+  CK(launch_csr_order_check(dp.rowptr.as<int64_t>(), dp.cols.as<int32_t>(), n, tot.as<int32_t>() + 3, st));
   const int64_t per_bank = (n + 15) / 16;
   const int64_t cap = std::min<int64_t>(per_bank + 16, csr_staged_cols_max(n) / 16);
   const char* rl_env = std::getenv("DPT_SELL_RELABEL");
@@ -718,7 +721,10 @@ void build_sell_device(DevProblem& dp, cudaStream_t st, dpt_error_info* err) {
   int32_t npad = 0;
   CK(cudaMemcpyAsync(&total, tot.p, 8, cudaMemcpyDeviceToHost, st));
   if (relabel) CK(cudaMemcpyAsync(&npad, tot.as<int32_t>() + 2, 4, cudaMemcpyDeviceToHost, st));
+  int32_t disorder = 1;
+  CK(cudaMemcpyAsync(&disorder, tot.as<int32_t>() + 3, 4, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  dp.csr_strict = disorder == 0 ? 1 : 0;
   if (relabel) dp.s_npad = std::max<int64_t>(npad, n);
   if (std::getenv("DPT_SELL_DEBUG"))
     std::fprintf(stderr, "[dpt] SELL image: n=%lld slices=%lld steps=%lld sched=%d relabel=%d npad=%lld\n",
@@ -875,6 +881,7 @@ void upload(DevProblem& dp, dpt_ctx* ctx, const dpt_problem* p, dpt_error_info* 
 // ----------------------------------------------------------- workspace ----
 struct Work {
   DevSolve s{};
+  DBuf initpart;  // launch_csr_init scratch (CSR full map from the identity)
   DBuf slots, dvec, eps, res, rowpart, tilepart, blockpart, stats, state, trace, counter, cyclepart,
       amaps, lam_table, settled_table, sk_ws, sk_cnt;
   int ntiles_step = 0;
@@ -938,6 +945,7 @@ void make_work(Work& w, dpt_ctx* ctx, DevProblem& dp, Mode mode, int64_t row0, i
   dalloc(w.trace, size_t(w.max_trace) * 3 * 8, err);
   dalloc(w.counter, 16, err);
   dalloc(w.cyclepart, size_t(512) * DPT_MAX_WINDOW * 8, err);
+  if (mode == MODE_CSR_FULL) dalloc(w.initpart, size_t(rows + 4) * 8, err);
   s.theta = dp.theta.as<double>();
   s.slots = w.slots.as<double>();
   s.dvec[0] = w.dvec.as<double>();
@@ -1284,6 +1292,17 @@ void drive_graph(dpt_ctx* ctx, Work& w, DevProblem& dp, Mode mode, int64_t row, 
   replay_trace(w, w.h_state->trace_len, 0, trace, user, err);
 }
 
+// K2's launch 1 from the identity as three small kernels (sparse_step.cu,
+// launch_csr_init): real data, levels-generated gaps, the packed image built,
+// strictly increasing columns in every CSR row.  DPT_CSR_INIT=0: K2 as launch 1.
+bool csr_init_applies(const DevProblem& dp, const Work& w) {
+  static const bool off = [] {
+    const char* e = std::getenv("DPT_CSR_INIT");
+    return e && e[0] == '0';
+  }();
+  return !off && !dp.cplx && !w.s.gapmat && dp.s_cols16.p && dp.csr_strict && w.initpart.p;
+}
+
 // Runs launches 1 .. until the state machine terminates (or `total` launches).
 // Launch 1 is the special init (dense) or the generic step from slot 0.
 // Chunks are double-buffered: chunk c+1 is enqueued before the host waits for
@@ -1299,6 +1318,12 @@ void drive(dpt_ctx* ctx, Work& w, DevProblem& dp, Mode mode, int64_t row, int to
     CK(launch_dense_init(w.s, dp.delta.as<double>(), dp.big, st));
     ctx->launches += 1;
     post_step(ctx, w, dense_init_ntiles(w.s.rows, w.s.ntn, w.s.cplx), cycle_elems, err);
+    issued = 1;
+  } else if (mode == MODE_CSR_FULL && csr_init_applies(dp, w)) {
+    // CSR solves start from A_0 = I (put_identity): launch 1 without the product
+    CK(launch_csr_init(w.s, dp.csr(), dp.sell(), w.initpart.p, st));
+    ctx->launches += 3;
+    post_step(ctx, w, 1, cycle_elems, err);
     issued = 1;
   }
   // With a TraceSink the host chunk driver runs instead of the device loop: the

@@ -343,6 +343,166 @@ cudaError_t launch_csr_step(const DevSolve& s, const DevSell& d, cudaStream_t st
   return cudaGetLastError();
 }
 
+// ------------------------------------------------- K2, launch 1 from A_0 = I ----
+// The first application of the map starts from the identity, where the product
+// is known: P(I)(i,j) = Delta(j,i).  Running K2 on it costs a full step (c3:
+// 1.57 ms of a 30 ms solve) for n^2 outputs of which nnz are not signed zeros
+// -- the dense path's launch 1 is an elementwise kernel for the same reason
+// (the reference's matmul skips a(i,k) == 0, matrix.cpp:150).  Three small
+// kernels produce exactly what K2's launch 1 writes -- A_1, the step / max /
+// nonfinite statistics, the residual partials of A_0 and the lagged diagonal
+// d_1 -- with K2's own expressions, so every value is bit-identical to K2's:
+//   fill     A_1(i,j) = 1 (i = j), else (lam_1 g(i,j)) * (p - d_0(i) A_0(i,j))
+//            with p = +0, A_0(i,j) = 0 (a signed zero; NaN if lam_1 g overflows)
+//   scatter  one warp per row j of Delta: entry (j,k,v) is P(I)(k,j) = v, i.e.
+//            output (k,j); the maxima go through atomicMax on the bit patterns
+//            of non-negative doubles (order-preserving; NaNs skipped as fmax
+//            skips them) -- maxima do not depend on the order
+//   finish   d_1(i) with K2's lane partition over the SELL image, the diagonal
+//            column's residual term, rowpart / tilepart in K2's layout
+// Not used with an explicit gap matrix, complex data, rows that do not fit
+// shared memory, or a CSR with repeated (row, column) pairs (their sum would
+// follow the schedule's order).
+struct CsrInitScratch {
+  unsigned long long* rownum;  // [rows] max |residual term| of the entries of A_0's row i (bit pattern)
+  unsigned long long* stats;   // [0] max step, [1] max |A_1| (bit patterns), [2] nonfinite count (may wrap below
+                               //     zero transiently: two's complement), [3] spare
+};
+
+__device__ __forceinline__ void atomic_max_nonneg(unsigned long long* slot, double v) {
+  if (v == v) atomicMax(slot, (unsigned long long)__double_as_longlong(v));  // v >= 0; NaN skipped like fmax
+}
+
+__global__ void __launch_bounds__(256) csr_init_fill_kernel(DevSolve s, CsrInitScratch sc) {
+  if (s.state->done) return;
+  const int jl = launch_index(s);
+  double* a_out = s.slots + size_t(jl % s.nslots) * size_t(s.slot_elems);
+  const double lam_k = lam_of(s, jl);
+  const double* d_in = s.dvec[(jl - 1) & 1];
+  unsigned long long bad = 0;
+  for (int64_t il = blockIdx.y; il < s.rows; il += gridDim.y) {
+    const int64_t gi = s.row0 + il;
+    const double ti = s.theta[gi];
+    const double z = __dsub_rn(0.0, __dmul_rn(d_in[il], 0.0));  // p - d A_0(i,j) with p = +0, A_0(i,j) = 0
+    double* orow = a_out + size_t(il) * size_t(s.ld);
+    for (int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; j < s.n; j += int64_t(gridDim.x) * blockDim.x) {
+      double val = 1.0;
+      if (gi != j) {
+        val = __dmul_rn(__dmul_rn(lam_k, 1.0 / __dsub_rn(ti, s.theta[j])), z);
+        bad += isfinite(val) ? 0 : 1;
+      }
+      orow[j] = val;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+  if ((threadIdx.x & 31) == 0 && bad) atomicAdd(&sc.stats[2], bad);
+}
+
+__global__ void __launch_bounds__(256) csr_init_scatter_kernel(DevSolve s, DevCsr D, CsrInitScratch sc) {
+  if (s.state->done) return;
+  const int jl = launch_index(s);
+  double* a_out = s.slots + size_t(jl % s.nslots) * size_t(s.slot_elems);
+  const double lam_k = lam_of(s, jl), lam = s.lambda;
+  const double* d_in = s.dvec[(jl - 1) & 1];
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  double t_step = 0.0, t_max = 0.0;
+  long long bad = 0;  // nonfinite entries minus the nonfinite fills they replace
+  for (int64_t j = wid; j < s.n; j += nw) {
+    const double tj = s.theta[j];
+    for (int64_t q = D.rowptr[j] + lane; q < D.rowptr[j + 1]; q += 32) {
+      const int64_t k = D.cols[q];
+      const int64_t il = k - s.row0;
+      if (k == j || il < 0 || il >= s.rows) continue;  // the diagonal entry only feeds d_0; other ranks' rows
+      const double v = D.vals[q];
+      const double tk = s.theta[k], dk = d_in[il];
+      const double eps_k = __dadd_rn(tk, __dmul_rn(lam, dk));
+      const double t = __dmul_rn(lam_k, 1.0 / __dsub_rn(tk, tj));
+      const double dz = __dmul_rn(dk, 0.0);
+      const double val = __dmul_rn(t, __dsub_rn(v, dz));
+      const double fill = __dmul_rn(t, __dsub_rn(0.0, dz));
+      a_out[size_t(il) * size_t(s.ld) + size_t(j)] = val;
+      t_step = fmax(t_step, fabs(__dsub_rn(val, 0.0)));
+      t_max = fmax(t_max, fabs(val));
+      bad += (isfinite(val) ? 0 : 1) - (isfinite(fill) ? 0 : 1);
+      const double rr = __dadd_rn(__dmul_rn(__dsub_rn(tj, eps_k), 0.0), __dmul_rn(lam, v));
+      atomic_max_nonneg(&sc.rownum[il], fabs(rr));
+    }
+  }
+  t_step = warp_max(t_step);
+  t_max = warp_max(t_max);
+  for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+  if (lane == 0) {
+    atomic_max_nonneg(&sc.stats[0], t_step);
+    atomic_max_nonneg(&sc.stats[1], t_max);
+    if (bad) atomicAdd(&sc.stats[2], (unsigned long long)bad);
+  }
+}
+
+__global__ void __launch_bounds__(256) csr_init_finish_kernel(DevSolve s, DevSell S, CsrInitScratch sc) {
+  if (s.state->done) return;
+  const int jl = launch_index(s);
+  const double* a_out = s.slots + size_t(jl % s.nslots) * size_t(s.slot_elems);
+  const double lam = s.lambda;
+  const double* d_in = s.dvec[(jl - 1) & 1];
+  const int32_t* __restrict__ inv = S.inv;
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const int64_t rows = s.rows;
+  for (int64_t il = wid; il < rows; il += nw) {
+    // d_1(i) = P(A_1)(i,i): K2's tail (lanes split the row's SELL entries, one shuffle tree)
+    const int64_t gi = s.row0 + il;
+    const int64_t t = S.pos_of[gi];
+    const int L = int(t & 31);
+    const int64_t off = S.slice_off[t >> 5];
+    const int32_t width = int32_t((S.slice_off[(t >> 5) + 1] - off) >> 5);
+    const double* arow_new = a_out + size_t(il) * size_t(s.ld);
+    double part = 0.0;
+    for (int32_t q = lane; q < width; q += 32) {
+      const int64_t idx = off + int64_t(q) * 32 + L;
+      const int32_t c = __ldg(S.cols + idx);
+      if (c >= 0) part = __fma_rn(__ldg(S.vals + idx), arow_new[inv ? __ldg(inv + c) : c], part);
+    }
+    part = warp_sum(part);
+    if (lane == 0) {
+      // the diagonal column of A_0's row: a_ii = 1, p = P(I)(i,i) = d_0(i)
+      const double ti = s.theta[gi], di = d_in[il];
+      const double eps_i = __dadd_rn(ti, __dmul_rn(lam, di));
+      const double rr = __dadd_rn(__dmul_rn(__dsub_rn(ti, eps_i), 1.0), __dmul_rn(lam, di));
+      const double nu = fmax(__longlong_as_double((long long)sc.rownum[il]), fabs(rr));
+      s.rowpart[rp_index(0, il, 0, rows, 1)] = part;
+      s.rowpart[rp_index(1, il, 0, rows, 1)] = nu;
+      s.rowpart[rp_index(2, il, 0, rows, 1)] = 1.0;  // max_j |A_0(i,j)|
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    double* tp = s.tilepart;  // one tile: the fold of this launch reads tile 0 only
+    tp[0] = __longlong_as_double((long long)sc.stats[0]);
+    tp[1] = fmax(__longlong_as_double((long long)sc.stats[1]), 1.0);  // the unit diagonal
+    tp[2] = double((long long)sc.stats[2]);
+    tp[3] = 0.0;
+  }
+}
+
+// scratch: (rows + 4) * 8 bytes, zeroed here.  Tiles of the following fold: 1.
+cudaError_t launch_csr_init(const DevSolve& s, const DevCsr& c, const DevSell& d, void* scratch, cudaStream_t st) {
+  CsrInitScratch sc;
+  sc.rownum = static_cast<unsigned long long*>(scratch);
+  sc.stats = sc.rownum + s.rows;
+  cudaError_t e = cudaMemsetAsync(scratch, 0, size_t(s.rows + 4) * 8, st);
+  if (e != cudaSuccess) return e;
+  const int64_t cb = (s.n + 1023) / 1024 > 0 ? (s.n + 1023) / 1024 : 1;  // 4 columns per thread
+  const dim3 fgrid(unsigned(cb > 64 ? 64 : cb), unsigned(s.rows > 4096 ? 4096 : (s.rows > 0 ? s.rows : 1)));
+  csr_init_fill_kernel<<<fgrid, 256, 0, st>>>(s, sc);
+  const int64_t wb = (s.n + 7) / 8;
+  csr_init_scatter_kernel<<<unsigned(wb > 1184 ? 1184 : (wb > 0 ? wb : 1)), 256, 0, st>>>(s, c, sc);
+  const int64_t fb = (s.rows + 7) / 8;
+  csr_init_finish_kernel<<<unsigned(fb > 1184 ? 1184 : (fb > 0 ? fb : 1)), 256, 0, st>>>(s, d, sc);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ K3 ----
 // Row-dot "groups": G lanes cooperate on one row m of Delta.
 //   MODE 0  CSR with exactly 16 nonzeros per row (BASELINE c4): G = 4, each
