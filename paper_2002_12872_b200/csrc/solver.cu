@@ -1485,14 +1485,16 @@ void put_slot(Work& w, const DevProblem& dp, int slot, const double* a, int mem,
 }
 
 // A_0 = I in slot 0 and d_0 = diag(Delta) = P(I)(i,i).
-void put_identity(dpt_ctx* ctx, Work& w, DevProblem& dp, dpt_error_info* err) {
-  CK(launch_identity(w.s, ctx->stream));
+// matrix = false: only d_0 (the CSR launch-1 shortcut never reads A_0, and without
+// a cycle window nothing else does: every reported iterate has index >= 1).
+void put_identity(dpt_ctx* ctx, Work& w, DevProblem& dp, dpt_error_info* err, bool matrix = true) {
+  if (matrix) CK(launch_identity(w.s, ctx->stream));
   DevCsr c = dp.csr();
   if (dp.kind == DPT_DELTA_DENSE)
     CK(launch_set_diag_delta(w.s, dp.delta.as<double>(), nullptr, ctx->stream));
   else
     CK(launch_set_diag_delta(w.s, nullptr, &c, ctx->stream));
-  ctx->launches += 2;
+  ctx->launches += matrix ? 2 : 1;
 }
 
 void gather_rows(dpt_ctx* ctx, const Work& w, const DevProblem& dp, int slot, double* dst, int out_mem,
@@ -1726,7 +1728,7 @@ int run_full(dpt_ctx* ctx, const dpt_problem* p, const dpt_options* opts_in, boo
     if (fixed_k == 0) {
       put_identity(ctx, w, dp, err);
     } else {
-      if (!dense) put_identity(ctx, w, dp, err);
+      if (!dense) put_identity(ctx, w, dp, err, !csr_init_applies(dp, w));
       drive(ctx, w, dp, mode, 0, total, dense, nullptr, nullptr, err);
     }
     final_iter = fixed_k;
@@ -1739,7 +1741,8 @@ int run_full(dpt_ctx* ctx, const dpt_problem* p, const dpt_options* opts_in, boo
     post_step(ctx, w, w.ntiles_step, 0, err);
     final_iter = 0;
   } else {
-    if (!dense || win > 0) put_identity(ctx, w, dp, err);  // A_0 = I (CSR start / window entry)
+    // A_0 = I (CSR start / window entry); the CSR shortcut without a window needs d_0 only
+    if (!dense || win > 0) put_identity(ctx, w, dp, err, dense || win > 0 || !csr_init_applies(dp, w));
     drive(ctx, w, dp, mode, 0, total, dense, trace, user, err);
     if (!w.h_state->done) {
       set_err(err, DPT_ERR_CUDA, "internal: iteration budget consumed without a terminal status");

@@ -60,3 +60,57 @@ def test_staging_variants_agree_with_reference(tmp_path, cplx):
     if r.iterations == int(base["iterations"]) and r.status != 2:
         assert np.max(np.abs(base["a"] - r.a)) < 1e-9
         assert np.max(np.abs(base["eig"] - r.eig) / np.maximum(1.0, np.abs(r.eig))) < 1e-10
+
+
+INIT_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, ".")
+import paper_2002_12872_b200 as P
+from paper_2002_12872_b200 import problems as pr
+from paper_2002_12872_b200.dpt import CsrMatrix, PartitionedProblem
+out = {}
+def put(tag, r, tr=None):
+    out[tag + ".a"] = r.state.a; out[tag + ".eig"] = r.eigenvalues; out[tag + ".res"] = r.residuals
+    out[tag + ".meta"] = np.array([int(r.status), r.iterations, r.step_norm])
+    if tr is not None: out[tag + ".trace"] = np.array(tr, dtype=float)
+# 1. c3-like (no window: n > 1414), trace on
+n = 1600
+c = pr.csr_sym_bernoulli(n, 5, 0.01)
+p = PartitionedProblem(np.arange(n, dtype=float), c, 0.05)
+tr = []
+put("plain", P.iterate_full(p, P.IterationOptions(), trace=lambda k, s, m: tr.append((k, s, m))), tr)
+# 2. window on (n <= 1414), unsymmetric pattern with explicit diagonal entries of Delta
+n = 400
+rng = np.random.default_rng(3)
+rows = [sorted(set(rng.choice(n, 9, replace=False).tolist()) | ({i} if i % 3 == 0 else set())) for i in range(n)]
+rowptr = np.zeros(n + 1, dtype=np.int64); rowptr[1:] = np.cumsum([len(r) for r in rows])
+cols = np.concatenate([np.array(r, dtype=np.int32) for r in rows]); vals = rng.standard_normal(len(cols))
+c2 = CsrMatrix(n, rowptr, cols, vals)
+put("window", P.iterate_full(PartitionedProblem(np.arange(n, dtype=float) * 1.5, c2, 0.03)))
+# 3. ramped coupling, 4. exactly two applications, 5. a coupling that diverges, 6. one iteration allowed
+put("ramped", P.iterate_ramped(PartitionedProblem(np.arange(n, dtype=float) * 1.5, c2, 0.03), 0.5))
+fx = P.iterate_fixed(PartitionedProblem(np.arange(n, dtype=float) * 1.5, c2, 0.03), 2, 0.03)
+out["fixed.a"] = np.asarray(fx.a if hasattr(fx, "a") else fx)
+put("diverged", P.iterate_full(PartitionedProblem(np.arange(n, dtype=float) * 1.5, c2, 40.0)))
+put("budget", P.iterate_full(PartitionedProblem(np.arange(n, dtype=float) * 1.5, c2, 0.03), P.IterationOptions(max_iter=1)))
+np.savez(sys.argv[1], **out)
+"""
+
+
+def test_identity_start_shortcut_is_bit_identical(tmp_path):
+    """Launch 1 of a CSR solve starts from A_0 = I; launch_csr_init writes A_1, the
+    statistics, the residual partials and d_1 without the product.  Every
+    output of the solve (iterate, eigenvalues, residuals, status, iterations,
+    step norm, trace) must equal, bit for bit, the solve whose launch 1 is K2
+    itself (DPT_CSR_INIT=0): full map, trace, window, ramped, fixed, Diverged,
+    a one-iteration budget; explicit diagonal entries of Delta."""
+    outs = {}
+    for init in ("0", "1"):
+        f = str(tmp_path / f"init{init}.npz")
+        env = dict(os.environ, DPT_CSR_INIT=init)
+        subprocess.run([sys.executable, "-c", INIT_SCRIPT, f], cwd=ROOT, env=env, check=True, timeout=600)
+        outs[init] = np.load(f)
+    assert sorted(outs["0"].files) == sorted(outs["1"].files) and len(outs["0"].files) >= 18
+    for k in outs["0"].files:
+        assert np.array_equal(outs["0"][k], outs["1"][k], equal_nan=True), k
+    assert int(outs["1"]["plain.meta"][0]) == 0 and int(outs["1"]["diverged.meta"][0]) == 2  # Converged / Diverged
