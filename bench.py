@@ -417,10 +417,23 @@ def other_configs(P, torch, ctx, local, fp64_peak):
             byts = 12 * p.delta.nnz + 8 * (n + 1) + 24 * n
             rec.update(kernel="single_u16w_kernel (K3)", bound="hbm", gbs=byts / (kms * 1e-3) / 1e9,
                        frac=byts / (kms * 1e-3) / 1e9 / hbm, algorithmic_bytes=byts)
+            # what binds it (K3): one random 32-byte sector per SM clock on the miss path to L2;
+            # sectors per step = nnz gathers + the streamed bytes / 32
+            sm, ghz = 148, 1.965
+            sectors = p.delta.nnz + byts / 32.0
+            floor_ms = sectors / sm / (ghz * 1e9) * 1e3
+            rec.update(binding="SM miss path to L2 (one sector per SM clock)", sector_floor_ms=floor_ms,
+                       frac_of_sector_floor=floor_ms / kms)
         elif hasattr(p.delta, "rowptr"):
             byts = 16 * n * n + 12 * p.delta.nnz + 8 * (n + 1) + 8 * n
             rec.update(kernel="csr_step_kernel (K2)", bound="hbm", gbs=byts / (kms * 1e-3) / 1e9,
                        frac=byts / (kms * 1e-3) / 1e9 / hbm, algorithmic_bytes=byts)
+            # what binds it (K2): n * nnz random 8-byte shared-memory gathers through the
+            # 128 B/clk L1 data pipe of each SM
+            sm, ghz = 148, 1.965
+            floor_ms = float(n) * p.delta.nnz * 8.0 / (sm * 128.0 * ghz * 1e9) * 1e3
+            rec.update(binding="L1 data pipe (shared-memory gathers)", smem_gather_floor_ms=floor_ms,
+                       frac_of_gather_floor=floor_ms / kms)
         else:
             tf = 2.0 * n ** 3 / (kms * 1e-3) / 1e12
             rec.update(kernel="dense_step_kernel (K1)", bound="tensor", tflops=tf, frac=tf / fp64_peak)
