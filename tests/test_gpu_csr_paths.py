@@ -114,3 +114,40 @@ def test_identity_start_shortcut_is_bit_identical(tmp_path):
     for k in outs["0"].files:
         assert np.array_equal(outs["0"][k], outs["1"][k], equal_nan=True), k
     assert int(outs["1"]["plain.meta"][0]) == 0 and int(outs["1"]["diverged.meta"][0]) == 2  # Converged / Diverged
+
+
+def test_unsorted_and_repeated_pairs_take_the_product_path():
+    """A CSR whose rows list their columns out of order, or repeat a (row, column)
+    pair, is still a valid operator for K2 (a repeated pair adds up).  The
+    launch-1 shortcut assumes one entry per pair in increasing order, so the
+    upload's order check must route such inputs to K2 as launch 1: results equal
+    the canonical CSR's to rounding."""
+    import paper_2002_12872_b200 as P
+    from paper_2002_12872_b200 import problems as pr
+    from paper_2002_12872_b200.dpt import CsrMatrix, PartitionedProblem
+    n = 320
+    c = pr.csr_sym_bernoulli(n, 4, 0.03)
+    d = np.arange(n, dtype=float)
+    base = P.iterate_full(PartitionedProblem(d, c, 0.02))
+    rp, cols, vals = np.asarray(c.rowptr), np.asarray(c.cols), np.asarray(c.vals)
+    # 1. every row's entries reversed
+    rc, rv = cols.copy(), vals.copy()
+    for i in range(n):
+        rc[rp[i]:rp[i + 1]] = cols[rp[i]:rp[i + 1]][::-1]
+        rv[rp[i]:rp[i + 1]] = vals[rp[i]:rp[i + 1]][::-1]
+    r1 = P.iterate_full(PartitionedProblem(d, CsrMatrix(n, rp, rc, rv), 0.02))
+    # 2. the first entry of every non-empty row split into two halves (a repeated pair)
+    nrp, ncols, nvals = [0], [], []
+    for i in range(n):
+        cs, vs = cols[rp[i]:rp[i + 1]].tolist(), vals[rp[i]:rp[i + 1]].tolist()
+        if cs:
+            cs, vs = [cs[0]] + cs, [vs[0] * 0.5, vs[0] * 0.5] + vs[1:]
+        ncols += cs
+        nvals += vs
+        nrp.append(len(ncols))
+    r2 = P.iterate_full(PartitionedProblem(d, CsrMatrix(n, np.array(nrp, dtype=np.int64), np.array(ncols, dtype=np.int32),
+                                                        np.array(nvals)), 0.02))
+    for r in (r1, r2):
+        assert r.status == base.status and r.iterations == base.iterations
+        assert np.max(np.abs(r.state.a - base.state.a)) < 1e-12
+        assert np.max(np.abs(r.eigenvalues - base.eigenvalues)) < 1e-10
