@@ -237,7 +237,7 @@ __device__ __forceinline__ void dense_epilogue(const DevSolve& s, double (&acc)[
 }
 
 #ifndef DPT_REFILL_LAG
-#define DPT_REFILL_LAG 2
+#define DPT_REFILL_LAG 0
 #endif
 constexpr int kRefillLag = DPT_REFILL_LAG;  // k-tiles between a stage's consumption and its refill (0 = at once)
 
@@ -317,13 +317,13 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB)
     dmma_consume_stage<C>(acc, a_st, b_st, wm, wn, t, gq);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
-    // Refill, lagging kRefillLag k-tiles: the producer is lane 0 of consumer
-    // warp 0, and the stage it has just finished is still being read by the
-    // slower warps -- waiting for it here made warp 0 the straggler of every
-    // k-tile.  The stage consumed kRefillLag iterations ago has been released by
-    // everyone (or nearly), so the wait returns at once; STAGES - kRefillLag
-    // k-tiles stay in flight.  Measured on c2 (100 steps, three A/B pairs):
-    // lag 0 3.926 ms, lag 1 3.940, lag 2 3.910 / 3.929 / 3.910.
+    // Refill kRefillLag k-tiles after the consumption (compile-time, default 0 =
+    // at once).  The producer is lane 0 of consumer warp 0; refilling the stage
+    // it has just finished means waiting for the slower warps of this k-tile,
+    // while the stage consumed earlier is already free.  Measured, lag 0 / 1 / 2:
+    // c2 3.926 / 3.940 / 3.910 ms (3.929 in one of three runs); c5 shards w = 8
+    // 241.9 / - / 242.6 ms, w = 4 498.6 / - / 501.1 ms (two pairs each): within
+    // half a percent either way, so the simplest order stays.
     if (producer && kt >= kRefillLag && kt - kRefillLag + C::STAGES < KT) {
       const int kc = kt - kRefillLag, sr = kc % C::STAGES;
       const int kn = kc + C::STAGES;
