@@ -64,14 +64,15 @@ int csr_step_ntiles(int64_t rows, int64_t n) {
   return int((rows + R - 1) / R);
 }
 
-// K2 works on a SELL-32 image of Delta built once per problem on the host
-// (build_sell in solver.cu): rows of Delta are grouped 32 to a slice (after a
-// by-length sort inside windows of 256 rows, so slices have little padding),
-// and entry q of slice lane L is stored at slice_off + 32 q + L.  A warp then
-// takes one slice, lane L owns one output column j of P (one row of Delta):
-// every column / value load is one coalesced 128 / 256-byte access, the dot
-// P(i, j) = sum_q val * A(i, col) accumulates sequentially in CSR order in one
-// lane (no shuffle trees).  The next launch's diagonal d(i) = P(A')(i,i) is
+// K2 works on a SELL-32 image of Delta built once per problem on the device
+// (sell_build.cu, driven by build_sell_device in solver.cu): rows of Delta are
+// grouped 32 to a slice (after a by-length sort inside windows of 256 rows, so
+// slices have little padding), and entry q of slice lane L is stored at
+// slice_off + 32 q + L (values; the shared-memory kernel reads the columns
+// from the packed 16-bit copy, four steps per 8-byte load).  A warp takes one
+// slice, lane L owns one output column j of P (one row of Delta): every image
+// load is coalesced, the dot P(i, j) = sum_q val * A(i, col) accumulates
+// sequentially in the schedule's order in one lane (no shuffle trees).  The next launch's diagonal d(i) = P(A')(i,i) is
 // formed at the end by one warp per owned row (lagged, like K1).
 //
 // Shared-memory layout: the R staged rows are interleaved, element (k, r) at
