@@ -103,3 +103,31 @@ def test_schedules_and_relabelling_match_reference(tmp_path, kind):
     for key, g in outs.items():
         if int(g["iterations"]) == int(base["iterations"]) and int(base["status"]) != 2:
             assert np.max(np.abs(g["a"] - base["a"])) < 1e-12, key
+
+
+RELABEL_EDGE = r"""
+import sys, numpy as np
+sys.path.insert(0, ".")
+import paper_2002_12872_b200 as P
+from paper_2002_12872_b200 import problems as pr
+from paper_2002_12872_b200.dpt import PartitionedProblem
+from oracle.bind import Checker
+for n in (64, 65, 96, 127, 128, 129, 200, 257):
+    c = pr.csr_sym_bernoulli(n, 100 + n, 0.08)
+    p = PartitionedProblem(np.arange(n, dtype=float), c, 0.02)
+    g = P.iterate_full(p)
+    r = Checker("oracle").iterate_full(p, {})
+    assert int(g.status) == r.status and abs(g.iterations - r.iterations) <= 1, n
+    assert np.max(np.abs(g.state.a - r.a)) < 1e-9, n
+"""
+
+
+@pytest.mark.parametrize("passes", ["1", "3"])
+def test_relabel_batch_boundaries(passes):
+    """The relabelling walks the columns in batches of 64, software-pipelined
+    (the next batch prefetched while the current one is evaluated): sizes of
+    exactly one batch (n = 64: the next batch is the same columns, re-read after
+    this batch's writes), one column more, a partial last batch, several
+    batches -- each against the oracle, with one and three passes."""
+    env = dict(os.environ, DPT_SELL_PASSES=passes)
+    subprocess.run([sys.executable, "-c", RELABEL_EDGE], cwd=ROOT, env=env, check=True, timeout=300)
