@@ -59,6 +59,8 @@ int single_ntn(int64_t n, int mode);
 int single_ntiles(int64_t n, int mode);
 cudaError_t launch_single_step(const DevSolve& s, const DevCsr& d, const double* dense, int64_t row, int mode,
                                cudaStream_t st);
+// uniform-16 CSR row map, launch 1 from z_0 = e_row without the gathers (single_u16.cu)
+cudaError_t launch_single_u16_init(const DevSolve& s, const DevCsr& d, int64_t row, cudaStream_t st);
 
 // complex_steps.cu (complex K2 / K3)
 int csr_cplx_ntiles(int64_t rows, int64_t n);

@@ -443,6 +443,110 @@ static cudaError_t launch_u16(const DevSolve& s, const DevCsr& d, int64_t row, c
   return cudaGetLastError();
 }
 
+// ---------------------------------------------- launch 1 from z_0 = e_row ----
+// The row-map solve starts from z_0 = e_row, where w = Delta z_0 is column
+// `row` of Delta: w[m] is the entry (m, row) or +0, and no gather is needed to
+// know it -- only the row's 16 columns.  This kernel writes what K3's launch 1
+// writes (z_1, the step / max / nonfinite and residual partials per block, w[row]
+// for the fold's eps) from the columns alone (67 MB instead of 235 MB and 16.8 M
+// gathers at c4: ~15 us instead of 83), with K3's own expressions: the FMA
+// chain visits the row's entries in K3's order (rotated chunks when the
+// variant rotates) and adds v * 1 for a match -- a skipped entry would add
+// fma(v, 0, w) = w for every finite v -- so z_1 and every statistic are
+// bit-identical to K3's for finite Delta.  One thread per row; the grid and the
+// per-block partial layout are K3's (the fold is unchanged).
+__device__ __forceinline__ double u16_dot_unit(const int32_t* __restrict__ cols, const double* __restrict__ vals,
+                                               int64_t m, int rot, bool rotate, int64_t row) {
+  const int4* crow = reinterpret_cast<const int4*>(cols + 16 * m);
+  const double* vrow = vals + 16 * m;
+  double w = 0.0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int k = rotate ? (q + (rot >> 1)) & 3 : q;
+    const int4 c = __ldg(crow + k);
+    if (c.x == row) w = __fma_rn(vrow[4 * k + 0], 1.0, w);
+    if (c.y == row) w = __fma_rn(vrow[4 * k + 1], 1.0, w);
+    if (c.z == row) w = __fma_rn(vrow[4 * k + 2], 1.0, w);
+    if (c.w == row) w = __fma_rn(vrow[4 * k + 3], 1.0, w);
+  }
+  return w;
+}
+
+constexpr int kU16InitThreads = 1024;  // one block per SM (the grid is K3's): all the warps it can hold
+
+__global__ void __launch_bounds__(kU16InitThreads)
+    single_u16_init_kernel(DevSolve s, DevCsr D, int64_t row, int rotate) {
+  if (s.state->done) return;
+  __shared__ double red[kU16InitThreads / 32][5];
+  const int jl = launch_index(s);
+  const int64_t n = s.n;
+  double* __restrict__ zo = s.slots + size_t(jl % s.nslots) * size_t(s.slot_elems);
+  const double lam_k = lam_of(s, jl), lam = s.lambda;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double wr = u16_dot_unit(D.cols, D.vals, row, int(row & 31), rotate != 0, row);
+  if (blockIdx.x == 0 && threadIdx.x == 0) s.dvec[(jl - 1) & 1][0] = wr;  // for the fold's eps
+  const double trow = s.theta[row];
+  const double eps = __dadd_rn(trow, __dmul_rn(lam, wr));
+  double num = 0.0, den = 0.0, t_step = 0.0, t_max = 0.0, t_nonfin = 0.0;
+  for (int64_t m = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; m < n; m += int64_t(gridDim.x) * blockDim.x) {
+    const double zm = m == row ? 1.0 : 0.0;  // z_0
+    const double tm = s.theta[m];
+    const double w = u16_dot_unit(D.cols, D.vals, m, int(m & 31), rotate != 0, row);
+    double val;
+    if (m == row) {
+      val = 1.0;
+    } else {
+      const double g = 1.0 / __dsub_rn(trow, tm);
+      val = __dmul_rn(__dmul_rn(lam_k, g), __dsub_rn(w, __dmul_rn(wr, zm)));
+    }
+    zo[m] = val;
+    t_step = fmax(t_step, fabs(__dsub_rn(val, zm)));
+    t_max = fmax(t_max, fabs(val));
+    t_nonfin += isfinite(val) ? 0.0 : 1.0;
+    const double r = __dadd_rn(__dmul_rn(__dsub_rn(tm, eps), zm), __dmul_rn(lam, w));
+    num = fmax(num, fabs(r));
+    den = fmax(den, fabs(zm));
+  }
+  num = warp_max(num);
+  den = warp_max(den);
+  t_step = warp_max(t_step);
+  t_max = warp_max(t_max);
+  t_nonfin = warp_sum(t_nonfin);
+  if (lane == 0) {
+    red[warp][0] = num;
+    red[warp][1] = den;
+    red[warp][2] = t_step;
+    red[warp][3] = t_max;
+    red[warp][4] = t_nonfin;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a[5] = {0, 0, 0, 0, 0};
+    for (int ww = 0; ww < kU16InitThreads / 32; ++ww) {
+      a[0] = fmax(a[0], red[ww][0]);
+      a[1] = fmax(a[1], red[ww][1]);
+      a[2] = fmax(a[2], red[ww][2]);
+      a[3] = fmax(a[3], red[ww][3]);
+      a[4] += red[ww][4];
+    }
+    const int tn = blockIdx.x, ntn = s.ntn;
+    s.rowpart[rp_index(0, 0, tn, 1, ntn)] = 0.0;
+    s.rowpart[rp_index(1, 0, tn, 1, ntn)] = a[0];
+    s.rowpart[rp_index(2, 0, tn, 1, ntn)] = a[1];
+    double* tp = s.tilepart + size_t(tn) * 4;
+    tp[0] = a[2];
+    tp[1] = a[3];
+    tp[2] = a[4];
+    tp[3] = 0.0;
+  }
+}
+
+// Launch 1 of the uniform-16 row map from z_0 = e_row (real data, gaps from the levels).
+cudaError_t launch_single_u16_init(const DevSolve& s, const DevCsr& d, int64_t row, cudaStream_t st) {
+  single_u16_init_kernel<<<u16_grid(s.n), kU16InitThreads, 0, st>>>(s, d, row, kU16Var[u16_variant()].rot);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_single_u16(const DevSolve& s, const DevCsr& d, int64_t row, cudaStream_t st) {
   switch (u16_variant()) {
     case 1: return launch_u16<256, 2, true>(s, d, row, st);

@@ -1303,6 +1303,15 @@ bool csr_init_applies(const DevProblem& dp, const Work& w) {
   return !off && !dp.cplx && !w.s.gapmat && dp.s_cols16.p && dp.csr_strict && w.initpart.p;
 }
 
+// K3's launch 1 from z_0 = e_row without the gathers (single_u16.cu,
+// launch_single_u16_init): the uniform-16 CSR row map on real data with gaps from
+// the levels.  DPT_U16_INIT=0: K3 as launch 1.
+bool u16_init_applies(const DevProblem& dp, const Work& w) {
+  const char* e = std::getenv("DPT_U16_INIT");  // read per call: tests switch it in-process
+  const bool off = e && e[0] == '0';
+  return !off && !dp.cplx && !w.s.gapmat && dp.kind == DPT_DELTA_CSR && dp.uniform16;
+}
+
 // Runs launches 1 .. until the state machine terminates (or `total` launches).
 // Launch 1 is the special init (dense) or the generic step from slot 0.
 // Chunks are double-buffered: chunk c+1 is enqueued before the host waits for
@@ -1318,6 +1327,12 @@ void drive(dpt_ctx* ctx, Work& w, DevProblem& dp, Mode mode, int64_t row, int to
     CK(launch_dense_init(w.s, dp.delta.as<double>(), dp.big, st));
     ctx->launches += 1;
     post_step(ctx, w, dense_init_ntiles(w.s.rows, w.s.ntn, w.s.cplx), cycle_elems, err);
+    issued = 1;
+  } else if (mode == MODE_SINGLE && u16_init_applies(dp, w)) {
+    // the row map starts from z_0 = e_row (run_single): launch 1 from the columns alone
+    CK(launch_single_u16_init(w.s, dp.csr(), row, st));
+    ctx->launches += 1;
+    post_step(ctx, w, w.ntiles_step, cycle_elems, err);
     issued = 1;
   } else if (mode == MODE_CSR_FULL && csr_init_applies(dp, w)) {
     // CSR solves start from A_0 = I (put_identity): launch 1 without the product

@@ -98,3 +98,36 @@ def test_complex_u16_graph_cache_churn():
     assert a.eigenvalue == b.eigenvalue
     assert torch.equal(a.z_chart, b.z_chart)  # device-resident inputs -> device-resident outputs
     ctx.close()
+
+
+@pytest.mark.parametrize("n", [20, 1000, 70001])
+def test_unit_start_shortcut_is_bit_identical(variant_env, n):
+    """Launch 1 of the row map starts from z_0 = e_row; launch_single_u16_init
+    writes z_1 and the partials from the columns alone.  Every output of the
+    solve (chart vector, unit vector, eigenvalue, residual, status, iterations,
+    trace) equals, bit for bit, the solve whose launch 1 is K3 itself
+    (DPT_U16_INIT=0) -- for a rotated and an unrotated K3 variant, the
+    dominant pair, a row in the middle of the chart with a trace, and a ramped
+    coupling."""
+    p, o, _ = pr.config("c4b", n)
+    try:
+        for v in (16, 0):
+            os.environ["DPT_U16_VARIANT"] = str(v)
+            outs = {}
+            for flag in ("0", "1"):
+                os.environ["DPT_U16_INIT"] = flag
+                tr = []
+                d = P.dominant_eigenpair(p, P.IterationOptions(**o))
+                s1 = P.iterate_single(p, n // 2, P.IterationOptions(**o), trace=lambda k, s, m: tr.append((k, s, m)))
+                s2 = P.iterate_single(p, n - 1, P.IterationOptions(**o), ramp_alpha=0.5)
+                outs[flag] = (d, s1, s2, tr)
+            a, b = outs["0"], outs["1"]
+            assert a[0].status == b[0].status and a[0].iterations == b[0].iterations, v
+            assert a[0].eigenvalue == b[0].eigenvalue and a[0].residual == b[0].residual, v
+            assert np.array_equal(a[0].z_chart, b[0].z_chart) and np.array_equal(a[0].z_unit, b[0].z_unit), v
+            for q in (1, 2):
+                assert a[q].status == b[q].status and a[q].iterations == b[q].iterations, (v, q)
+                assert a[q].eigenvalue == b[q].eigenvalue and np.array_equal(a[q].z, b[q].z), (v, q)
+            assert a[3] == b[3] and len(a[3]) >= 1, v
+    finally:
+        os.environ.pop("DPT_U16_INIT", None)
