@@ -121,11 +121,21 @@ __device__ __forceinline__ void dense_epilogue(const DevSolve& s, double (&acc)[
       }
     }
   } else {
+  const double* __restrict__ gap = s.gapmat;
+  int n_nonfin = 0;
+  // fmax(acc, x) for an accumulator that is never NaN: a NaN x compares false and
+  // is skipped, exactly as fmax skips it
+  auto max_keep = [](double acc, double x) { return x > acc ? x : acc; };
+  // Interior tiles (every row and column pair in range: all tiles when n is a
+  // multiple of the tile) run the same code with the range guards compiled out.
+  auto elements = [&](auto full_tag) {
+  constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
   for (int a = 0; a < C::MB; ++a) {
     const int il = tm * C::BM + wm * C::WTM + a * 8 + gq;  // local row
-    const bool row_ok = il < rows;
+    const bool row_ok = FULL || il < rows;
     const int64_t gi = s.row0 + il;
+    const int gi32 = int(gi);  // n < 2^31: the diagonal test in 32 bits
     double num = 0.0, den = 0.0, dsum = 0.0;
     if (row_ok) {
       const double ti = theta[gi];
@@ -137,8 +147,8 @@ __device__ __forceinline__ void dense_epilogue(const DevSolve& s, double (&acc)[
 #pragma unroll
       for (int b = 0; b < C::NB; ++b) {
         const int c = colbase + b * 8;
-        if (c >= n) continue;
-        const bool pair = c + 1 < n;
+        if (!FULL && c >= n) continue;
+        const bool pair = FULL || c + 1 < n;
         double2 av, dv;
         if (pair) {
           av = *reinterpret_cast<const double2*>(arow + c);
@@ -155,21 +165,25 @@ __device__ __forceinline__ void dense_epilogue(const DevSolve& s, double (&acc)[
           const double aij = e ? av.y : av.x;
           const double dij = e ? dv.y : dv.x;
           const double p = acc[a][b][e];
-          double v;
-          if (gi == c + e) {
-            v = 1.0;  // exact unit diagonal (test_dpt.cpp:45-53)
-          } else {
-            const double g = s.gapmat ? s.gapmat[size_t(il) * size_t(s.ld) + size_t(c + e)]
-                                      : 1.0 / __dsub_rn(ti, e ? tc.y : tc.x);  // IEEE division = build_theta
-            v = __dmul_rn(__dmul_rn(lam_k, g), __dsub_rn(p, __dmul_rn(di, aij)));
-          }
+          // Branch-free: the off-diagonal value is formed for every element (on the
+          // diagonal 1 / 0 = inf, discarded by the select).  The epilogue is bound
+          // by instruction issue (per-CTA timestamps on c1: 4.8 us of element work
+          // per 64 x 64 tile, 10 us when both CTAs of an SM reach it together; the
+          // operands' loads are not what it waits for -- staging them through the
+          // TMA pipeline or hoisting them changed nothing), so the divergent
+          // diagonal branch, the 64-bit index compare, the library fmax sequences
+          // and the FP64 nonfinite counter are replaced by cheaper equivalents.
+          const double g = gap ? gap[size_t(il) * size_t(s.ld) + size_t(c + e)]
+                               : 1.0 / __dsub_rn(ti, e ? tc.y : tc.x);  // IEEE division = build_theta
+          const double voff = __dmul_rn(__dmul_rn(lam_k, g), __dsub_rn(p, __dmul_rn(di, aij)));
+          const double v = (gi32 == c + e) ? 1.0 : voff;  // exact unit diagonal (test_dpt.cpp:45-53)
           out[e] = v;
-          t_step = fmax(t_step, fabs(__dsub_rn(v, aij)));
-          t_max = fmax(t_max, fabs(v));
-          t_nonfin += isfinite(v) ? 0.0 : 1.0;
+          t_step = max_keep(t_step, fabs(__dsub_rn(v, aij)));
+          t_max = max_keep(t_max, fabs(v));
+          n_nonfin += isfinite(v) ? 0 : 1;
           const double r = __dadd_rn(__dmul_rn(__dsub_rn(e ? tc.y : tc.x, eps_i), aij), __dmul_rn(lam, p));
-          num = fmax(num, fabs(r));
-          den = fmax(den, fabs(aij));
+          num = max_keep(num, fabs(r));
+          den = max_keep(den, fabs(aij));
           dsum = __fma_rn(v, dij, dsum);
         }
         if (pair)
@@ -178,12 +192,12 @@ __device__ __forceinline__ void dense_epilogue(const DevSolve& s, double (&acc)[
           orow[c] = out[0];
       }
     }
-    // fold the 4 lanes that share this row (t = 0..3)
-    num = fmax(num, __shfl_xor_sync(0xffffffffu, num, 1));
-    den = fmax(den, __shfl_xor_sync(0xffffffffu, den, 1));
+    // fold the 4 lanes that share this row (t = 0..3); the maxima are never NaN
+    num = max_keep(num, __shfl_xor_sync(0xffffffffu, num, 1));
+    den = max_keep(den, __shfl_xor_sync(0xffffffffu, den, 1));
     dsum += __shfl_xor_sync(0xffffffffu, dsum, 1);
-    num = fmax(num, __shfl_xor_sync(0xffffffffu, num, 2));
-    den = fmax(den, __shfl_xor_sync(0xffffffffu, den, 2));
+    num = max_keep(num, __shfl_xor_sync(0xffffffffu, num, 2));
+    den = max_keep(den, __shfl_xor_sync(0xffffffffu, den, 2));
     dsum += __shfl_xor_sync(0xffffffffu, dsum, 2);
     if (t == 0) {
       const int rt = wm * C::WTM + a * 8 + gq;  // row within tile
@@ -193,6 +207,13 @@ __device__ __forceinline__ void dense_epilogue(const DevSolve& s, double (&acc)[
       red[(wn * C::BM + rt) * 4 + 3] = 0.0;
     }
   }
+  };
+  const bool full_tile = int64_t(tm + 1) * C::BM <= rows && int64_t(tn + 1) * C::BN <= n;  // CTA-uniform
+  if (full_tile)
+    elements(std::true_type{});
+  else
+    elements(std::false_type{});
+  t_nonfin += double(n_nonfin);
   }
   t_step = warp_max(t_step);
   t_max = warp_max(t_max);
